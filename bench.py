@@ -1,0 +1,363 @@
+#!/usr/bin/env python
+"""Decode-step benchmark: disaggregated-EP MoE layer with ping-pong micro-batches.
+
+Metric (BASELINE.json): "decode tokens/s/GPU (MoE layer, ping-pong); M2N
+dispatch+combine p50 us".  One step = one decode iteration of the MoE layer
+over L_sim layers (one layer's weights reused) for m
+micro-batches of b_a tokens per attention GPU, on synthetic random-init
+weights and activations.  ``value`` = whole-job layer-tokens/s
+= n_a * m * b_a * L_sim / step time (``value_per_gpu`` divides by N).
+
+Workloads (config 3 of BASELINE.json, Mixtral-8x22B-shaped, b_a = 1024, m = 3):
+  N=1 co-located (both roles on one GPU, M2N local); N=2 1+1; N=4 3+1; N=8 6+2.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SPLITS = {1: (1, 1, True), 2: (1, 1, False), 4: (3, 1, False), 8: (6, 2, False),
+          3: (2, 1, False), 5: (4, 1, False), 6: (4, 2, False), 7: (5, 2, False)}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--shape", default="mixtral-8x22b")
+    ap.add_argument("--b-a", type=int, default=1024)
+    ap.add_argument("--m", type=int, default=3)
+    ap.add_argument("--layers", type=int, default=4, help="L_sim layers per step")
+    ap.add_argument("--attn", default="standin", choices=["standin", "none"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
+# --------------------------------------------------------------- CPU leg ----
+def cpu_sample(model, b_a: int, threads: int) -> dict:
+    """The oracle (CPU restatement, oracle/) on a bounded sample of one
+    micro-batch of the workload: router over all b_a tokens, one expert's
+    SwiGLU FFN over its share of rows (b_a*K/E), combine over b_a tokens; the
+    layer time is projected as router + E x expert + combine."""
+    import numpy as np
+    from oracle import oracle as O
+
+    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
+    H, Hp, E, K = model.hidden, model.intermediate, model.experts, model.topk
+    x = O.synth_tokens(b_a, H, seed=1)
+    wts = O.synth_weights(H, Hp, E, seed=0, experts=[0])
+    t0 = time.perf_counter()
+    idx, w = O.router(x, wts.wg, K)
+    cnt, slot = O.place(idx, E)
+    t_router = time.perf_counter() - t0
+    rows = max(1, b_a * K // E)
+    t0 = time.perf_counter()
+    O.expert_ffn(x[:rows], wts.w_gate[0], wts.w_up[0], wts.w_down[0])
+    t_expert = time.perf_counter() - t0
+    y = np.zeros((b_a, K, H), np.uint16)
+    t0 = time.perf_counter()
+    O.combine(y, w, x)
+    t_comb = time.perf_counter() - t0
+    t_layer = t_router + E * t_expert + t_comb
+    return {"tokens_per_s": b_a / t_layer, "t_router_s": t_router, "t_expert_s": t_expert,
+            "t_combine_s": t_comb, "t_layer_s": t_layer,
+            "sample": f"1 micro-batch of {b_a} tokens: router+placement (all tokens), SwiGLU FFN of 1 of {E} experts "
+                      f"({rows} rows) x{E}, combine; numpy/OpenBLAS fp32 + C oracle"}
+
+
+def cpu_model_name() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    """--impl reference: the reference ships no implementation of this path
+    (SURVEY.md §0); its CPU restatement (oracle/) is timed on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2504_02263_b200.config import as_model_spec
+    import numpy as np  # noqa: F401
+
+    model = as_model_spec(args.shape)
+    threads = len(os.sched_getaffinity(0))
+    n_a, n_e, colo = SPLITS.get(args.gpus, (1, 1, True))
+    vals = []
+    info = None
+    for i in range(args.warmup + args.steps):
+        info = cpu_sample(model, min(args.b_a, 256), threads)
+        if i >= args.warmup:
+            vals.append(info["tokens_per_s"])
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": "decode tokens/s/GPU (MoE layer, ping-pong); M2N dispatch+combine p50 µs",
+            "value": v, "unit": "layer-tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * min(args.b_a, 256) / v, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"{model.name} MoE layer, CPU oracle (reference has no implementation)",
+                       "hidden": model.hidden, "intermediate": model.intermediate, "experts": model.experts,
+                       "topk": model.topk, "b_a": args.b_a, "m": args.m},
+            "cpu_baseline": {"value": v, "unit": "layer-tokens/s", "cores": threads, "kind": "port",
+                             "sample": info["sample"], "cpu": cpu_model_name()},
+            "e2e": {"value": v, "unit": "layer-tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- GPU leg ----
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_2504_02263_b200 import runtime
+    from paper_2504_02263_b200.config import DeploymentPlan, WorkloadSpec, as_model_spec
+
+    rank, world, local = runtime.init_distributed_from_env("nccl")
+    if world != args.gpus:
+        if rank == 0:
+            print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}))
+        sys.exit(2)
+    n_a, n_e, colo = SPLITS[world]
+    model = as_model_spec(args.shape)
+    plan = DeploymentPlan(n_a=n_a, n_e=n_e, m=args.m, b_a=args.b_a, colocated=colo)
+    dev = torch.device(f"cuda:{local}")
+    g = runtime.M2NGroup(model, plan, rank=rank, device=dev)
+    wg, w13, w2 = runtime.synth_device_weights(model, runtime.local_experts(g), seed=0, device=dev)
+    layer = runtime.MoEDecodeLayer(g, wg=wg if g.is_attention else None,
+                                   w13=w13 if g.is_expert else None, w2=w2 if g.is_expert else None)
+    wl = WorkloadSpec()
+    kv_bytes = 0
+    if args.attn == "standin" and g.is_attention:
+        # decode-attention HBM load of one micro-batch: b_a tokens x s x (K,V) x h/g x bf16
+        kv_bytes = args.b_a * wl.avg_seq_len * 2 * (model.hidden // model.gqa_group) * 2
+    runner = runtime.PingPongRunner(layer, layers=args.layers, kv_bytes=kv_bytes, chain=False)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1 + rank)
+    xs = [torch.randn((args.b_a, model.hidden), generator=gen, device=dev).to(torch.bfloat16)
+          for _ in range(plan.m)] if g.is_attention else None
+    x0 = [x.clone() for x in xs] if xs else None
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # expert-FFN timing inside the timed region (events on the launching stream)
+    ffn_events = []
+    orig_step = layer.expert_step
+
+    def timed_expert_step(mb=0, stream=None):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        r = orig_step(mb, stream)
+        e.record()
+        ffn_events.append((s, e))
+        return r
+
+    for _ in range(args.warmup):
+        runner.run(xs)
+    torch.cuda.synchronize()
+    barrier()
+    if g.is_expert:
+        rows0, calls0 = g.stats()
+    layer.expert_step = timed_expert_step
+    clk = ClockSampler(local)
+    clk.start()
+    torch.cuda.synchronize()
+    barrier()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_start.record()
+    for _ in range(args.steps):
+        runner.run(xs)
+    t_end.record()
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop()
+    layer.expert_step = orig_step
+    elapsed_ms = t_start.elapsed_time(t_end)
+    st = g.status()
+    if st != 0:
+        raise RuntimeError(f"device status {st} (timeout in a device-side wait)")
+    ffn_ms = [s.elapsed_time(e) for s, e in ffn_events]
+    rows = calls = 0
+    if g.is_expert:
+        rows1, calls1 = g.stats()
+        rows, calls = rows1 - rows0, calls1 - calls0
+    # reductions over ranks: step time = max; FFN stats from expert ranks
+    t = torch.tensor([elapsed_ms, sum(ffn_ms), len(ffn_ms), rows], dtype=torch.float64, device=dev)
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(tmax[1:], op=dist.ReduceOp.SUM)
+        t = tmax
+    elapsed_ms, ffn_total_ms, ffn_n, rows_total = t.tolist()
+
+    # ---- e2e through the public API with host buffers -------------------
+    e2e = None
+    if not args.no_e2e:
+        host_in = [x.cpu().pin_memory() for x in x0] if xs else None
+        host_out = [torch.empty_like(h).pin_memory() for h in host_in] if xs else None
+        barrier()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(args.steps):
+            if xs:
+                for x, h in zip(xs, host_in):
+                    x.copy_(h, non_blocking=True)
+            runner.run(xs)
+            if xs:
+                for x, h in zip(xs, host_out):
+                    h.copy_(x, non_blocking=True)
+        e.record()
+        torch.cuda.synchronize()
+        barrier()
+        e2e_ms = torch.tensor([s.elapsed_time(e)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+        bytes_io = plan.m * args.b_a * model.hidden * 2 if xs else 0
+        tok = n_a * plan.m * args.b_a * args.layers * args.steps
+        e2e = {"value": tok / (e2e_ms.item() / 1e3), "unit": "layer-tokens/s",
+               "h2d_bytes_per_step": bytes_io, "d2h_bytes_per_step": bytes_io,
+               "note": "per attention rank: m micro-batch inputs H2D from pinned memory, outputs D2H, every step"}
+
+    if rank != 0:
+        g.close()
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks = measured_peaks()
+    tokens = n_a * plan.m * args.b_a * args.layers * args.steps
+    value = tokens / (elapsed_ms / 1e3)
+    ffn_avg_s = (ffn_total_ms / max(ffn_n, 1)) / 1e3
+    flops_per_call = 6.0 * (rows_total / max(ffn_n, 1)) * model.hidden * model.intermediate
+    achieved = flops_per_call / ffn_avg_s / 1e12 if ffn_n else None
+    peak = peaks.get("bf16_tflops_sustained") or 1404.8
+    launches_per_mbl = (1 if kv_bytes else 0) + 1 + 1 + 2 + 1  # attn, router, dispatch, 2 GEMMs, combine
+    line = {
+        "metric": "decode tokens/s/GPU (MoE layer, ping-pong); M2N dispatch+combine p50 µs",
+        "value": value, "unit": "layer-tokens/s", "value_per_gpu": value / world,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights seed 0, N(0,1) tokens)",
+        "config": {"workload": f"{model.name}-shaped MoE layer, " +
+                   ("co-located 1 GPU" if colo else f"{n_a} attention + {n_e} expert GPUs"),
+                   "hidden": model.hidden, "intermediate": model.intermediate, "experts": model.experts,
+                   "topk": model.topk, "n_a": n_a, "n_e": n_e, "m": plan.m, "b_a": args.b_a,
+                   "L_sim": args.layers, "attention_stage": args.attn,
+                   "l2": "working set (weights 4.8 GB + KV stand-in) >> 126 MB L2; no flush needed",
+                   "parallelism": f"dp{n_a}-ep{n_e}"},
+        "roofline": {"bound": "tensor", "kernel": "expert FFN (grouped_gemm_kernel x2: gate/up+SiLU, down+N2M)",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": None,
+                     "flops_per_launch_pair": flops_per_call, "avg_launch_pair_ms": ffn_avg_s * 1e3,
+                     "peak_kind": "measured bf16_tflops_sustained (MEASURED_PEAKS.json)"},
+        "e2e": e2e,
+        "gpu_launches": None,
+        "clocks": clocks,
+    }
+    # our kernels inside the timed region (per rank, summed over roles)
+    per_step = plan.m * args.layers * (launches_per_mbl if colo else 0)
+    if not colo:
+        per_step = plan.m * args.layers * (n_a * ((1 if kv_bytes else 0) + 3) + n_e * 2)
+    line["gpu_launches"] = per_step * args.steps
+    if not args.no_cpu:
+        threads = len(os.sched_getaffinity(0))
+        cs = cpu_sample(model, args.b_a, threads)
+        line["cpu_baseline"] = {"value": cs["tokens_per_s"], "unit": "layer-tokens/s", "cores": threads,
+                                "kind": "port", "sample": cs["sample"], "cpu": cpu_model_name(),
+                                "t_router_s": cs["t_router_s"], "t_expert_s": cs["t_expert_s"]}
+    print(json.dumps(line), flush=True)
+    g.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

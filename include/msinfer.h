@@ -1,0 +1,164 @@
+/*
+ * msinfer.h -- C ABI of libmsinfer.so, the B200 (sm_100a) implementation of
+ * MegaScale-Infer's disaggregated expert-parallel MoE decode step
+ * (arXiv 2504.02263).
+ *
+ * The reference ships no native entry points for this path (SURVEY.md §0,
+ * §8b): its only code is the Python config layer
+ * (/root/reference/pkg/src/moeplan/catalog.py), mirrored by
+ * paper_2504_02263_b200/config.py.  Each entry point below replaces one
+ * operation the paper describes; the citation says which.
+ *
+ * Conventions (all functions):
+ *   - plain pointers and sizes, no C++ or torch types;
+ *   - device pointers unless stated; bf16 tensors are passed as void*;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default);
+ *   - every call is asynchronous on `stream` and never synchronizes the host;
+ *   - return 0 on success, > 0 = cudaError_t, < 0 = MSI_E* below; the text
+ *     of the last error of the calling thread is msi_last_error();
+ *   - the caller owns every tensor it passes; the library owns (and frees in
+ *     msi_ctx_destroy) the symmetric heap it allocates in msi_ctx_create;
+ *   - one host thread per process and per GPU; a context is not re-entrant.
+ */
+#ifndef MSINFER_H_
+#define MSINFER_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MSI_MAX_RANKS 8
+#define MSI_IPC_HANDLE_BYTES 64
+#define MSI_ROW_ALIGN 128 /* per-expert receive segment alignment (rows) */
+
+enum {
+  MSI_EINVAL = -1,      /* bad argument / shape */
+  MSI_EARCH = -2,       /* device is not sm_100 */
+  MSI_ESTATE = -3,      /* context not finalized / peer missing */
+  MSI_ETIMEOUT = -4,    /* a device-side wait exceeded its bound (see msi_poll_status) */
+  MSI_EDRIVER = -5      /* CUDA driver entry point unavailable */
+};
+
+/* Buffer ids for msi_ctx_buffer (inspection by tests / benches). */
+enum {
+  MSI_BUF_RECV = 0,   /* expert GPU: received token rows  [cap][H] bf16 per slot */
+  MSI_BUF_META = 1,   /* expert GPU: (sender, t*K+k) per received row, int32x2 */
+  MSI_BUF_YBUF = 2,   /* attention GPU: expert outputs [max_tokens*K][H] bf16 per slot */
+  MSI_BUF_HBUF = 3,   /* expert GPU: SwiGLU activations [cap][H'] bf16 (one, shared) */
+  MSI_BUF_CNTAB = 4   /* count table [n_a][E] of (epoch<<32 | count) per slot */
+};
+
+/* Deployment plan.  Vocabulary of SPEC.md:311 (n_a, m) plus n_e; tp = 1.
+ * Expert e lives on expert index e / (experts / n_e) (contiguous blocks). */
+typedef struct {
+  int32_t world;                         /* ranks (GPUs) in the deployment        */
+  int32_t n_a;                           /* attention GPUs (DP replicas)          */
+  int32_t n_e;                           /* expert GPUs (EP group)                */
+  int32_t attn_ranks[MSI_MAX_RANKS];     /* global rank of attention index s     */
+  int32_t expert_ranks[MSI_MAX_RANKS];   /* global rank of expert index q        */
+  int32_t hidden;                        /* h   (MoeModelSpec.hidden)             */
+  int32_t inter;                         /* h'  (MoeModelSpec.intermediate)       */
+  int32_t experts;                       /* E   (MoeModelSpec.experts)            */
+  int32_t topk;                          /* K   (MoeModelSpec.topk)               */
+  int32_t max_tokens;                    /* b_a: tokens per attention GPU per mb  */
+  int32_t slots;                         /* m:   micro-batch slots (ping-pong)    */
+} msi_plan;
+
+typedef struct msi_ctx msi_ctx;
+
+typedef struct {
+  unsigned char bytes[MSI_IPC_HANDLE_BYTES];
+} msi_ipc_handle;
+
+/* ---- library ------------------------------------------------------------ */
+int msi_version(void);
+const char* msi_last_error(void);
+/* 0 if the current device is sm_100 (B200) and the library's kernels load. */
+int msi_check_device(void);
+
+/* ---- context: symmetric heap + peer mapping ("pre-registered
+ * tensor"; the M2N library's registration step, here CUDA IPC over NVLink) -- */
+int msi_ctx_create(const msi_plan* plan, int rank, msi_ctx** out);
+int msi_ctx_destroy(msi_ctx* ctx);
+/* IPC handle of this rank's heap, to be exchanged out of band. */
+int msi_ctx_export(msi_ctx* ctx, msi_ipc_handle* out);
+/* Map peer `peer_rank`'s heap (no-op for own rank). */
+int msi_ctx_import(msi_ctx* ctx, int peer_rank, const msi_ipc_handle* handle);
+/* After every peer is imported; zeroes the control words (call, then barrier
+ * across ranks, before the first dispatch). */
+int msi_ctx_finalize(msi_ctx* ctx);
+int msi_ctx_buffer(msi_ctx* ctx, int which, int slot, void** ptr, size_t* bytes);
+/* Device status word: 0 = ok, else a MSI_E* code set by a device-side wait. */
+int msi_poll_status(msi_ctx* ctx, int32_t* status);
+/* Expert-role counters: rows through msi_expert_ffn and number of calls since
+ * msi_ctx_finalize (device-side, exact; read synchronously). */
+int msi_ctx_stats(msi_ctx* ctx, uint64_t* rows, uint64_t* calls);
+/* Bound on device-side spin waits, in nanoseconds (default 20 s). */
+int msi_set_wait_timeout(msi_ctx* ctx, uint64_t ns);
+int msi_ctx_workspace(msi_ctx* ctx, void** ptr, size_t* bytes);
+
+/* ---- (1) gate + top-K router, fused with per-expert counts, normalized
+ * weights and slot placement -------------
+ * x [T,H] bf16, wg [E,H] bf16 (row-major).  Outputs idx [T,K] int32 (descending
+ * logit, ties -> lower expert), w [T,K] fp32 (softmax over the K chosen
+ * logits), cnt [E] int32, slot [T,K] int32 = rank of token t among this
+ * sender's tokens routed to idx[t,k] (ascending token order).  Bit-exact with
+ * oracle/msi_oracle.c (pinned fp32 reduction order, deterministic exp).
+ * workspace: msi_gate_topk_workspace(T, E) bytes, zero-filled once before the
+ * first call (the kernel leaves it zeroed).  H % 256 == 0, 1 <= K <= min(E,32). */
+size_t msi_gate_topk_workspace(int T, int E);
+int msi_gate_topk(const void* x, const void* wg, int T, int H, int E, int K,
+                  int32_t* idx, float* w, int32_t* cnt, int32_t* slot,
+                  void* workspace, void* stream);
+
+/* ---- (1) M2N dispatch (sender; receiver PAPER.md:408-411)
+ * Publishes cnt to every rank, waits for all senders' counts, then stores each
+ * row x[t] into the expert GPUs' receive buffers over NVLink peer memory at
+ * row seg_start[e] + sum_{s'<s} cnt[s'][e] + slot[t,k], with its (s, t*K+k)
+ * metadata, and releases the receivers' arrival counters.  `epoch` counts the
+ * uses of `mb_slot` from 1. */
+int msi_dispatch(msi_ctx* ctx, const void* x, const int32_t* cnt,
+                 const int32_t* idx, const int32_t* slot, int T, int mb_slot,
+                 uint32_t epoch, void* stream);
+
+/* ---- (2) expert FFN (SwiGLU): waits for all senders'
+ * rows, then two tcgen05/TMEM/TMA grouped GEMMs over the local experts:
+ *   H = bf16(silu(X W_gate^T) * (X W_up^T)),  Y = bf16(H W_down^T)
+ * whose epilogue stores every Y row straight into its attention GPU's
+ * combine buffer (N2M leg) and releases its arrival counter.
+ * w13: msi_pack_w13 layout [E_l][2H'][H]; w2: [E_l][H][H'] (natural). */
+int msi_expert_ffn(msi_ctx* ctx, const void* w13, const void* w2, int mb_slot,
+                   uint32_t epoch, void* stream);
+
+/* ---- (3) combine: waits for all expert GPUs, then
+ * out[t] = bf16(resid[t] + sum_k w[t,k] * y[t,k]) (fp32 fmaf, ascending k;
+ * resid may be NULL). */
+int msi_combine(msi_ctx* ctx, void* out, const float* w, const void* resid,
+                int T, int mb_slot, uint32_t epoch, void* stream);
+
+/* ---- building blocks (also used by tests) -------------------------------- */
+/* w13[e] rows interleaved in 128-row blocks: [gate 128 | up 128] per 256. */
+int msi_pack_w13(const void* w_gate, const void* w_up, void* w13, int E_l,
+                 int inter, int hidden, void* stream);
+/* Stand-alone grouped SwiGLU FFN on compact rows: x [rows][H] where local
+ * expert e owns rows [seg_start[e], seg_start[e]+total[e]) with seg_start a
+ * MSI_ROW_ALIGN-aligned prefix of total; y [rows][H].  hbuf >= rows x H'. */
+int msi_grouped_ffn(const void* x, const int32_t* total, int E_l, int rows,
+                    const void* w13, const void* w2, void* hbuf, void* y,
+                    int hidden, int inter, void* stream);
+/* Stand-alone combine on a local [T,K,H] buffer (no waits). */
+int msi_combine_local(const void* y, const float* w, const void* resid,
+                      void* out, int T, int K, int H, void* stream);
+/* Attention-stage stand-in: streams `kv_bytes` of a KV buffer per call and
+ * folds them into a checksum (the decode-attention HBM load of one
+ * micro-batch; out of scope as a kernel). */
+int msi_attn_standin(const void* kv, size_t kv_bytes, float* checksum,
+                     void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MSINFER_H_ */

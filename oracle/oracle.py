@@ -1,0 +1,276 @@
+"""CPU oracle for the disaggregated-EP MoE decode step (numpy + liboracle.so).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and the
+cpu_baseline / ``--impl reference`` legs of bench.py, as the checker.  The
+product path never imports it.
+
+PARITY UNPINNED BY THE REFERENCE.  The reference (/root/reference) ships no
+implementation, tests or golden vectors for this path; this
+oracle restates the paper's semantics with the build's precision contract:
+
+* router   PAPER.md:83 (gate = x . W_g, top-K), PAPER.md:444-447 (fused top-K,
+           per-expert counts, normalized weights, scatter) -> ``router``,
+           ``place`` (bit-exact contract: idx, counts, slots, and weights via
+           the deterministic exp in msi_oracle.c)
+* dispatch PAPER.md:396-411 (M2N sender/receiver), per-pair bytes
+           PAPER.md:632 -> ``dispatch_layout`` (bit-exact row placement)
+* expert   PAPER.md:285-286 (FFN in/out GEMMs) + SwiGLU per BASELINE
+           north_star -> ``expert_ffn`` (fp32 accumulate; bf16 rounding at
+           X, H, Y; tolerance-checked)
+* combine  PAPER.md:83, 97 -> ``combine`` (fp32 fmaf, ascending k; bit-exact
+           given identical expert outputs)
+* pipeline SPEC.md:237-272 -> paper_2504_02263_b200.pipeline (closed forms)
+
+What *is* pinned by the reference -- the sizing numbers it states -- is
+checked in tests/test_oracle.py (196,608 B per pair PAPER.md:632; gemm_flops
+SPEC.md:127; P_e SPEC.md:153).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+
+ROW_ALIGN = 128  # per-expert segment alignment in the receive buffer (GEMM M tile)
+
+
+def build() -> str:
+    path = os.path.join(_HERE, "liboracle.so")
+    src = os.path.join(_HERE, "msi_oracle.c")
+    if not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(src):
+        subprocess.run(["make", "-C", _HERE], check=True, capture_output=True)
+    return path
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        L = ctypes.CDLL(build())
+        P = ctypes.c_void_p
+        i = ctypes.c_int
+        L.orc_router.argtypes = [P, P, i, i, i, i, P, P, P]
+        L.orc_place.argtypes = [P, i, i, i, P, P]
+        L.orc_combine.argtypes = [P, P, P, i, i, i, P]
+        L.orc_combine.restype = None
+        L.orc_bf16_round.argtypes = [P, P, ctypes.c_size_t]
+        L.orc_bf16_round.restype = None
+        L.orc_swiglu.argtypes = [P, P, P, ctypes.c_size_t]
+        L.orc_swiglu.restype = None
+        L.msi_det_expf.argtypes = [ctypes.c_float]
+        L.msi_det_expf.restype = ctypes.c_float
+        _LIB = L
+    return _LIB
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+# ----------------------------------------------------------------- bf16 ---- #
+def bf16_round(x: np.ndarray) -> np.ndarray:
+    """fp32 -> bf16 bit patterns (uint16), round-to-nearest-even."""
+    src = np.ascontiguousarray(x, dtype=np.float32)
+    out = np.empty(src.shape, dtype=np.uint16)
+    lib().orc_bf16_round(_p(src), _p(out), src.size)
+    return out
+
+
+def bf16_to_f32(b: np.ndarray) -> np.ndarray:
+    return (np.ascontiguousarray(b, dtype=np.uint16).astype(np.uint32) << 16).view(np.float32)
+
+
+def det_expf(d: float) -> float:
+    return float(lib().msi_det_expf(float(d)))
+
+
+# ------------------------------------------------------------- synthetic --- #
+@dataclass
+class LayerWeights:
+    """Natural-layout bf16 weights (uint16 bit patterns)."""
+
+    wg: np.ndarray      # [E, H]        gate (router) weights
+    w_gate: np.ndarray  # [E, Hp, H]    FFN gate projection
+    w_up: np.ndarray    # [E, Hp, H]    FFN up projection
+    w_down: np.ndarray  # [E, H, Hp]    FFN down projection
+
+
+def synth_weights(H: int, Hp: int, E: int, seed: int = 0, experts=None) -> LayerWeights:
+    """SURVEY.md §8(d) init: W_g, W_gate, W_up ~ N(0, 1/H), W_down ~ N(0, 1/Hp),
+    rounded to bf16.  ``experts`` limits the FFN weights to a subset (the CPU
+    baseline samples)."""
+    rng = np.random.default_rng(seed)
+    wg = bf16_round(rng.standard_normal((E, H), dtype=np.float32) / np.sqrt(H))
+    ids = range(E) if experts is None else experts
+    n = len(list(ids))
+    wgate = np.empty((n, Hp, H), np.uint16)
+    wup = np.empty((n, Hp, H), np.uint16)
+    wdown = np.empty((n, H, Hp), np.uint16)
+    for j in range(n):
+        wgate[j] = bf16_round(rng.standard_normal((Hp, H), dtype=np.float32) / np.sqrt(H))
+        wup[j] = bf16_round(rng.standard_normal((Hp, H), dtype=np.float32) / np.sqrt(H))
+        wdown[j] = bf16_round(rng.standard_normal((H, Hp), dtype=np.float32) / np.sqrt(Hp))
+    return LayerWeights(wg, wgate, wup, wdown)
+
+
+def synth_tokens(T: int, H: int, seed: int) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    return bf16_round(rng.standard_normal((T, H), dtype=np.float32))
+
+
+# ---------------------------------------------------------------- router --- #
+def router(x: np.ndarray, wg: np.ndarray, K: int, want_logits: bool = False):
+    """x [T,H] bf16, wg [E,H] bf16 -> idx [T,K] int32, w [T,K] fp32 (and logits)."""
+    x = np.ascontiguousarray(x, np.uint16)
+    wg = np.ascontiguousarray(wg, np.uint16)
+    T, H = x.shape
+    E = wg.shape[0]
+    idx = np.empty((T, K), np.int32)
+    w = np.empty((T, K), np.float32)
+    lg = np.empty((T, E), np.float32) if want_logits else None
+    rc = lib().orc_router(_p(x), _p(wg), T, H, E, K, _p(idx), _p(w),
+                          _p(lg) if lg is not None else None)
+    if rc:
+        raise ValueError(f"orc_router: bad shape (rc={rc}); H must be a multiple of 256")
+    return (idx, w, lg) if want_logits else (idx, w)
+
+
+def place(idx: np.ndarray, E: int):
+    """-> cnt [E] int32, slot [T,K] int32 (ascending token order per expert)."""
+    idx = np.ascontiguousarray(idx, np.int32)
+    T, K = idx.shape
+    cnt = np.empty(E, np.int32)
+    slot = np.empty((T, K), np.int32)
+    if lib().orc_place(_p(idx), T, K, E, _p(cnt), _p(slot)):
+        raise ValueError("orc_place: expert index out of range")
+    return cnt, slot
+
+
+# -------------------------------------------------------------- dispatch --- #
+def segment_starts(total: np.ndarray, align: int = ROW_ALIGN) -> np.ndarray:
+    """Start row of each local expert's segment: segments are packed in expert
+    order, each start aligned to ``align`` rows (the GEMM M tile)."""
+    padded = (np.asarray(total, np.int64) + align - 1) // align * align
+    return np.concatenate([[0], np.cumsum(padded)[:-1]]).astype(np.int64)
+
+
+def dispatch_layout(cnt_all: np.ndarray, E_l: int):
+    """cnt_all [n_a, E] -> per expert GPU q: (total [E_l], seg_start [E_l],
+    base [n_a, E_l]) with row(s, t, k) = seg_start[e_l] + base[s, e_l] + slot."""
+    cnt_all = np.asarray(cnt_all, np.int64)
+    n_a, E = cnt_all.shape
+    out = []
+    for q in range(E // E_l):
+        c = cnt_all[:, q * E_l:(q + 1) * E_l]
+        total = c.sum(0)
+        base = np.cumsum(c, 0) - c
+        out.append((total, segment_starts(total), base))
+    return out
+
+
+def dispatch_rows(idx: np.ndarray, slot: np.ndarray, s: int, layout, E_l: int):
+    """Destination (expert GPU, row) of every (t, k) of sender s."""
+    q = idx // E_l
+    el = idx % E_l
+    rows = np.empty(idx.shape, np.int64)
+    for qq, (total, seg, base) in enumerate(layout):
+        m = q == qq
+        rows[m] = seg[el[m]] + base[s, el[m]] + slot[m]
+    return q.astype(np.int32), rows
+
+
+# ---------------------------------------------------------------- expert --- #
+def expert_ffn(xe: np.ndarray, w_gate: np.ndarray, w_up: np.ndarray,
+               w_down: np.ndarray) -> np.ndarray:
+    """One expert's SwiGLU FFN on its rows.  xe [t,H] bf16 -> y [t,H] bf16.
+    G, U fp32-accumulated; H = bf16(silu(G) * U); Y = bf16(H . W_down^T)."""
+    if xe.shape[0] == 0:
+        return np.zeros((0, w_down.shape[0]), np.uint16)
+    xf = bf16_to_f32(xe)
+    g = xf @ bf16_to_f32(w_gate).T
+    u = xf @ bf16_to_f32(w_up).T
+    h = np.empty(g.shape, np.uint16)
+    g = np.ascontiguousarray(g, np.float32)
+    u = np.ascontiguousarray(u, np.float32)
+    lib().orc_swiglu(_p(g), _p(u), _p(h), g.size)
+    y = bf16_to_f32(h) @ bf16_to_f32(w_down).T
+    return bf16_round(y)
+
+
+# --------------------------------------------------------------- combine --- #
+def combine(y: np.ndarray, w: np.ndarray, resid: np.ndarray | None = None) -> np.ndarray:
+    """y [T,K,H] bf16, w [T,K] fp32 -> out [T,H] bf16 (optional residual)."""
+    y = np.ascontiguousarray(y, np.uint16)
+    w = np.ascontiguousarray(w, np.float32)
+    T, K, H = y.shape
+    out = np.empty((T, H), np.uint16)
+    r = None if resid is None else np.ascontiguousarray(resid, np.uint16)
+    lib().orc_combine(_p(y), _p(w), _p(r) if r is not None else None, T, K, H, _p(out))
+    return out
+
+
+# ------------------------------------------------------------ full layer --- #
+@dataclass
+class LayerResult:
+    idx: list      # per sender [T,K]
+    w: list        # per sender [T,K]
+    cnt: np.ndarray  # [n_a, E]
+    slot: list     # per sender [T,K]
+    layout: list   # per expert GPU (total, seg_start, base)
+    y: list        # per sender [T,K,H] expert outputs (unweighted)
+    out: list      # per sender [T,H]
+
+
+def moe_layer(xs: list, wts: LayerWeights, K: int, n_e: int, resid: bool = False) -> LayerResult:
+    """Full MoE layer step for n_a senders (one micro-batch): route, place,
+    dispatch, SwiGLU experts, combine."""
+    E = wts.wg.shape[0]
+    E_l = E // n_e
+    H = wts.wg.shape[1]
+    idxs, ws, slots, cnts = [], [], [], []
+    for x in xs:
+        i, w = router(x, wts.wg, K)
+        c, s = place(i, E)
+        idxs.append(i), ws.append(w), slots.append(s), cnts.append(c)
+    cnt = np.stack(cnts)
+    layout = dispatch_layout(cnt, E_l)
+    # gather each expert's rows in receive order, run it, scatter back
+    ys = [np.empty((x.shape[0], K, H), np.uint16) for x in xs]
+    for e in range(E):
+        srcs = []
+        for s_, (i, sl) in enumerate(zip(idxs, slots)):
+            t, k = np.nonzero(i == e)
+            order = np.argsort(sl[t, k], kind="stable")
+            srcs.append((s_, t[order], k[order]))
+        rows = np.concatenate([xs[s_][t] for s_, t, _ in srcs]) if srcs else np.zeros((0, H), np.uint16)
+        y = expert_ffn(rows, wts.w_gate[e], wts.w_up[e], wts.w_down[e])
+        off = 0
+        for s_, t, k in srcs:
+            ys[s_][t, k] = y[off:off + len(t)]
+            off += len(t)
+    outs = [combine(y, w, x if resid else None) for y, w, x in zip(ys, ws, xs)]
+    return LayerResult(idxs, ws, cnt, slots, layout, ys, outs)
+
+
+# -------------------------------------------------------- sizing (pins) ---- #
+def pair_payload_bytes(b: int, K: int, E: int, h: int, tp_a: int = 1, bytes_per=2) -> float:
+    """Average sender->receiver bytes (PAPER.md:632 example)."""
+    return b * K / E * h * bytes_per / tp_a
+
+
+def gemm_flops(b: int, h_in: int, h_out: int) -> int:
+    """2 * b * h_in * h_out."""
+    if min(b, h_in, h_out) <= 0:
+        raise ValueError("gemm_flops: all dimensions must be > 0")
+    return 2 * b * h_in * h_out
+
+
+def expert_param_bytes(layers: int, h: int, hp: int, bytes_per: int = 2, swiglu: bool = False) -> int:
+    """P_e: L * 2 * h * h' * bytes (3 matrices with SwiGLU)."""
+    return layers * (3 if swiglu else 2) * h * hp * bytes_per

@@ -1,0 +1,419 @@
+// expert_gemm.cu -- expert FFN as two grouped GEMMs on tcgen05 / TMEM / TMA.
+//
+// PAPER.md:285-286 (FFN Input (b_e,h)x(h,h'), FFN Output (b_e,h')x(h',h)),
+// SwiGLU per BASELINE north_star.  Rows of local expert e are a contiguous
+// segment of the receive buffer starting at a 128-row aligned seg_start[e]
+// (written there by the dispatch kernel), so every 128-row M tile belongs to
+// exactly one expert.
+//
+//   GEMM1  A = X [rows][H], B = W13[e] [2H'][H] (gate/up interleaved in
+//          128-row blocks)  ->  epilogue H = bf16(silu(G) * U) into hbuf
+//   GEMM2  A = hbuf [rows][H'], B = W2[e] [H][H']  ->  epilogue stores every
+//          Y row straight to its attention GPU's combine buffer at
+//          (sender, t*K+k) from the row metadata (N2M leg over NVLink), then
+//          the last CTA releases the attention GPUs' arrival counters.
+//
+// Kernel shape: persistent, one CTA per SM, 256 threads, warp-specialized:
+//   warp 0  TMA producer (1 thread): A 128x64 + B 256x64 bf16 per stage,
+//           128B swizzle, 4-stage mbarrier ring (48 KB / stage)
+//   warp 1  MMA issuer (1 thread): tcgen05.mma.cta_group::1.kind::f16
+//           M=128 N=256 K=16, fp32 accumulators in TMEM, 2 accumulator
+//           buffers (512 TMEM columns) so the epilogue of tile i overlaps the
+//           MMAs of tile i+1
+//   warp 2  TMEM allocator
+//   warps 4-7 epilogue: tcgen05.ld 32x32b -> registers -> swizzled smem
+//           staging -> coalesced 256 B row stores (local or NVLink peer)
+// Tile order: expert-major, then N tile, then M tile (fastest), so CTAs that
+// run concurrently share one expert's B tiles and its A rows stay in L2.
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+#include "gemm.h"
+
+namespace msi {
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;
+constexpr int B_BYTES = BN * BK * 2;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int EPI_WARP_BYTES = 32 * 256;  // 32 rows x 128 bf16
+constexpr int kThreads = 256;
+constexpr int TMEM_COLS = 512;
+constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 4 * EPI_WARP_BYTES + 256;
+
+struct SegInfo {
+  int total[MSI_MAX_LOCAL_EXPERTS];
+  int start[MSI_MAX_LOCAL_EXPERTS];
+  int tile0[MSI_MAX_LOCAL_EXPERTS + 1];  // first tile of expert e
+  int mtiles[MSI_MAX_LOCAL_EXPERTS];
+};
+
+__device__ __forceinline__ void decode_tile(const SegInfo& s, int E_l, int nt, int tau, int& e,
+                                            int& n, int& m) {
+  e = 0;
+  while (e + 1 < E_l && tau >= s.tile0[e + 1]) ++e;
+  const int local = tau - s.tile0[e];
+  n = local / s.mtiles[e];
+  m = local - n * s.mtiles[e];
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;                                  // STAGES x 16 KB (per-stage stride STAGE_BYTES)
+  uint8_t* sEpi = smem + STAGES * STAGE_BYTES;         // 4 x 8 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + 4 * EPI_WARP_BYTES);
+  uint64_t* full = bars;                 // [STAGES]
+  uint64_t* empty = bars + STAGES;       // [STAGES]
+  uint64_t* tfull = bars + 2 * STAGES;   // [2]
+  uint64_t* tempty = bars + 2 * STAGES + 2;  // [2]
+  __shared__ uint32_t s_tmem;
+  __shared__ SegInfo seg;
+  __shared__ int s_last;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // ---- wait for the senders' rows (GEMM1 on an expert GPU) ----------------
+  if (threadIdx.x == 0) {
+    bool ok = true;
+    if (p.wait_ctr) ok = wait_geq(p.wait_ctr, p.wait_target, p.timeout_ns, p.status);
+    if (!ok) p.status[1] = 1;
+    fence_proxy_async_global();  // rows written by peers are read by TMA (async proxy)
+  }
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128); }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<TMEM_COLS>(&s_tmem);
+  __syncthreads();
+  if (p.status && p.status[1]) {  // a wait timed out: skip the work, keep the GPU usable
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) tmem_dealloc<TMEM_COLS>(s_tmem);
+    return;
+  }
+
+  // ---- segment table (all threads compute the same) -----------------------
+  if (threadIdx.x == 0) {
+    int run_start = 0, run_tile = 0;
+    for (int e = 0; e < p.E_l; ++e) {
+      int tot;
+      if (p.totals) {
+        tot = p.totals[e];
+      } else {
+        tot = 0;
+        for (int s = 0; s < p.n_a; ++s)
+          tot += (int)(uint32_t)ld_relaxed_sys64(p.cntab + (size_t)s * p.E + p.e0 + e);
+      }
+      const int mt = (tot + BM - 1) / BM;
+      seg.total[e] = tot;
+      seg.start[e] = run_start;
+      seg.mtiles[e] = mt;
+      seg.tile0[e] = run_tile;
+      run_start += mt * BM;
+      run_tile += mt * p.nt;
+    }
+    seg.tile0[p.E_l] = run_tile;
+    if (p.stats && blockIdx.x == 0) {
+      unsigned long long rows = 0;
+      for (int e = 0; e < p.E_l; ++e) rows += seg.total[e];
+      atomicAdd(p.stats, rows);
+      atomicAdd(p.stats + 1, 1ull);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = s_tmem;
+  const int ntiles = seg.tile0[p.E_l];
+  const int kblocks = p.kdim / BK;
+
+  if (warp == 0 && lane == 0) {
+    // ===================== TMA producer =====================
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tau = blockIdx.x; tau < ntiles; tau += gridDim.x) {
+      int e, n, m;
+      decode_tile(seg, p.E_l, p.nt, tau, e, n, m);
+      const int rowA = seg.start[e] + m * BM;
+      const int rowB = e * p.n_total + n * BN;
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_expect_tx(&full[stage], STAGE_BYTES);
+        uint8_t* st = sA + stage * STAGE_BYTES;
+        tma_load_2d(st, &tmA, kb * BK, rowA, &full[stage]);
+        tma_load_2d(st + A_BYTES, &tmB, kb * BK, rowB, &full[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ===================== MMA issuer =====================
+    constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int tau = blockIdx.x; tau < ntiles; tau += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const uint32_t aph = (it >> 1) & 1;
+      mbar_wait(&tempty[acc], aph ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + acc * BN;
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        uint8_t* st = sA + stage * STAGE_BYTES;
+        const uint64_t ad = umma_desc_sw128(st);
+        const uint64_t bd = umma_desc_sw128(st + A_BYTES);
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)  // +32 B along K inside the 128 B swizzle atom
+          mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+        mma_commit(&empty[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      mma_commit(&tfull[acc]);
+    }
+  } else if (warp >= 4) {
+    // ===================== epilogue =====================
+    const int q = warp & 3;  // TMEM lanes [32q, 32q+32)
+    uint8_t* stg = sEpi + q * EPI_WARP_BYTES;
+    int it = 0;
+    for (int tau = blockIdx.x; tau < ntiles; tau += gridDim.x, ++it) {
+      int e, n, m;
+      decode_tile(seg, p.E_l, p.nt, tau, e, n, m);
+      const int acc = it & 1;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      const int row_in_tile = q * 32 + lane;                    // this thread's TMEM lane
+      const int row_local = m * BM + row_in_tile;               // row within expert segment
+      const int row_global = seg.start[e] + row_local;          // row in recv / hbuf
+      const int valid_rows = min(32, max(0, seg.total[e] - (m * BM + q * 32)));
+
+      // Destination of this thread's row (used by the store loop via shuffles).
+      char* rowdst = nullptr;
+      if (p.mode == 0) {
+        rowdst = reinterpret_cast<char*>(p.out) + ((size_t)row_global * p.out_ld + (size_t)n * (BN / 2)) * 2;
+      } else if (row_local < seg.total[e]) {
+        if (p.meta) {
+          const int2 md = p.meta[row_global];
+          rowdst = p.dst[md.x] + ((size_t)md.y * p.out_ld + (size_t)n * BN) * 2;
+        } else {
+          rowdst = reinterpret_cast<char*>(p.out) + ((size_t)row_global * p.out_ld + (size_t)n * BN) * 2;
+        }
+      }
+      const int halves = (p.mode == 0) ? 1 : 2;
+      for (int half = 0; half < halves; ++half) {
+        // ---- TMEM -> registers -> swizzled staging (16 B units, unit u of
+        //      row r lives at r*256 + ((u ^ (r & 15)) * 16)) ----
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t packed[16];
+          if (p.mode == 0) {
+            uint32_t g[32], u[32];
+            tmem_ld32(tbase + c * 32, g);
+            tmem_ld32(tbase + 128 + c * 32, u);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              float g0 = __uint_as_float(g[2 * j]), g1 = __uint_as_float(g[2 * j + 1]);
+              float u0 = __uint_as_float(u[2 * j]), u1 = __uint_as_float(u[2 * j + 1]);
+              float h0 = g0 / (1.0f + __expf(-g0)) * u0;
+              float h1 = g1 / (1.0f + __expf(-g1)) * u1;
+              packed[j] = pack_bf16x2(h0, h1);
+            }
+          } else {
+            uint32_t v[32];
+            tmem_ld32(tbase + half * 128 + c * 32, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              packed[j] = pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int u = c * 4 + j;
+            uint4 val = make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
+            *reinterpret_cast<uint4*>(stg + lane * 256 + ((u ^ (lane & 15)) * 16)) = val;
+          }
+        }
+        if (half == halves - 1) {
+          // accumulator fully read: hand the TMEM buffer back to the MMA warp
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+        }
+        __syncwarp();
+        // ---- coalesced row stores: 2 rows per instruction, 256 B per row ----
+        const int u = lane & 15;
+        for (int r0 = 0; r0 < valid_rows; r0 += 2) {
+          const int r = r0 + (lane >> 4);
+          char* dst = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(rowdst), r & 31));
+          if (r < valid_rows) {
+            uint4 val = *reinterpret_cast<const uint4*>(stg + r * 256 + ((u ^ (r & 15)) * 16));
+            st_v4(dst + half * 256 + u * 16, val);
+          }
+        }
+        __syncwarp();
+      }
+      (void)row_in_tile;
+    }
+  }
+
+  // ---- teardown + completion signal --------------------------------------
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<TMEM_COLS>(tmem_base);
+  if (p.n_sig > 0 && threadIdx.x == 0) {
+    __threadfence_system();
+    s_last = (atomicAdd(p.ticket, 1u) == gridDim.x - 1);
+    if (s_last) {
+      *p.ticket = 0;
+      fence_sys();
+      for (int i = 0; i < p.n_sig; ++i) red_release_sys_add(p.sig[i], 1u);
+    }
+  }
+}
+
+// ---------------------------------------------------------- tensor maps ----
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+int make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
+              uint32_t box_outer) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return MSI_EDRIVER;
+  }
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d): inner=%llu outer=%llu", (int)r,
+              (unsigned long long)inner, (unsigned long long)outer);
+    return MSI_EDRIVER;
+  }
+  return 0;
+}
+
+__global__ void pack_w13_kernel(const uint4* __restrict__ gate, const uint4* __restrict__ up,
+                                uint4* __restrict__ out, int E_l, int inter, int hidden) {
+  // out[e][256 j + i] = gate[e][128 j + i] (i < 128), up[e][128 j + i - 128] otherwise
+  const size_t row_vec = (size_t)hidden / 8;
+  const size_t total = (size_t)E_l * 2 * inter * row_vec;
+  for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < total; v += (size_t)gridDim.x * blockDim.x) {
+    const size_t row = v / row_vec, col = v % row_vec;
+    const size_t e = row / (2 * inter), r = row % (2 * inter);
+    const size_t blk = r / 256, i = r % 256;
+    const uint4* src = (i < 128) ? gate : up;
+    const size_t srow = e * inter + blk * 128 + (i & 127);
+    out[v] = src[srow * row_vec + col];
+  }
+}
+
+}  // namespace
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+int grouped_gemm_launch(const GemmLaunch& L, cudaStream_t st) {
+  MSI_REQUIRE(L.p.E_l >= 1 && L.p.E_l <= MSI_MAX_LOCAL_EXPERTS, "grouped_gemm: E_l out of range");
+  MSI_REQUIRE(L.p.kdim % BK == 0 && L.p.n_total % BN == 0, "grouped_gemm: K %% 64 and N %% 256 required");
+  CUtensorMap ta, tb;
+  int rc = make_tmap(&ta, L.a, (uint64_t)L.p.kdim, (uint64_t)L.a_rows, BK, BM);
+  if (rc) return rc;
+  rc = make_tmap(&tb, L.b, (uint64_t)L.p.kdim, (uint64_t)L.p.E_l * L.p.n_total, BK, BN);
+  if (rc) return rc;
+  static bool attr = false;
+  if (!attr) {
+    MSI_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+    attr = true;
+  }
+  const int grid = L.grid > 0 ? L.grid : num_sms();
+  grouped_gemm_kernel<<<grid, kThreads, SMEM_BYTES, st>>>(ta, tb, L.p);
+  return check_launch("grouped_gemm_kernel");
+}
+
+int pack_w13(const void* gate, const void* up, void* out, int E_l, int inter, int hidden, cudaStream_t st) {
+  MSI_REQUIRE(inter % 128 == 0 && hidden % 8 == 0, "pack_w13: inter %% 128 and hidden %% 8 required");
+  pack_w13_kernel<<<4 * num_sms(), 256, 0, st>>>(reinterpret_cast<const uint4*>(gate),
+                                                 reinterpret_cast<const uint4*>(up),
+                                                 reinterpret_cast<uint4*>(out), E_l, inter, hidden);
+  return check_launch("pack_w13_kernel");
+}
+
+int grouped_ffn_local(const void* x, const int32_t* total, int E_l, int rows, const void* w13,
+                      const void* w2, void* hbuf, void* y, int hidden, int inter, cudaStream_t st) {
+  MSI_REQUIRE(hidden % 256 == 0 && inter % 128 == 0, "grouped_ffn: hidden %% 256 and inter %% 128 required");
+  GemmLaunch g1{};
+  g1.a = x;
+  g1.a_rows = rows;
+  g1.b = w13;
+  g1.p.E_l = E_l;
+  g1.p.n_total = 2 * inter;
+  g1.p.nt = 2 * inter / BN;
+  g1.p.kdim = hidden;
+  g1.p.totals = total;
+  g1.p.mode = 0;
+  g1.p.out = reinterpret_cast<__nv_bfloat16*>(hbuf);
+  g1.p.out_ld = inter;
+  int rc = grouped_gemm_launch(g1, st);
+  if (rc) return rc;
+  GemmLaunch g2{};
+  g2.a = hbuf;
+  g2.a_rows = rows;
+  g2.b = w2;
+  g2.p.E_l = E_l;
+  g2.p.n_total = hidden;
+  g2.p.nt = hidden / BN;
+  g2.p.kdim = inter;
+  g2.p.totals = total;
+  g2.p.mode = 1;
+  g2.p.out = reinterpret_cast<__nv_bfloat16*>(y);
+  g2.p.out_ld = hidden;
+  return grouped_gemm_launch(g2, st);
+}
+
+}  // namespace msi
+
+extern "C" int msi_pack_w13(const void* w_gate, const void* w_up, void* w13, int E_l, int inter,
+                            int hidden, void* stream) {
+  return msi::pack_w13(w_gate, w_up, w13, E_l, inter, hidden, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int msi_grouped_ffn(const void* x, const int32_t* total, int E_l, int rows, const void* w13,
+                               const void* w2, void* hbuf, void* y, int hidden, int inter, void* stream) {
+  return msi::grouped_ffn_local(x, total, E_l, rows, w13, w2, hbuf, y, hidden, inter,
+                                reinterpret_cast<cudaStream_t>(stream));
+}

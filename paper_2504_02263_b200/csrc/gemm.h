@@ -1,0 +1,52 @@
+// gemm.h -- launch interface of the grouped expert GEMM (expert_gemm.cu).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/msinfer.h"
+
+#define MSI_MAX_LOCAL_EXPERTS 64
+
+namespace msi {
+
+struct GemmParams {
+  int E_l;        // local experts
+  int n_total;    // B rows per expert (2H' for GEMM1, H for GEMM2)
+  int nt;         // N tiles per expert (n_total / 256)
+  int kdim;       // reduction dim (H for GEMM1, H' for GEMM2)
+  // segment sizes: explicit device array, or summed from the count table
+  const int32_t* totals;    // [E_l] or null
+  const uint64_t* cntab;    // [n_a][E] of (epoch << 32 | count), used when totals == null
+  int n_a, E, e0;           // e0 = first global expert of this GPU
+  // optional wait before any load (GEMM1 on an expert GPU)
+  const uint32_t* wait_ctr;
+  uint32_t wait_target;
+  uint64_t timeout_ns;
+  int32_t* status;          // [0] = error code, [1] = abort flag
+  unsigned long long* stats;  // optional: [0] += rows processed, [1] += 1 (one CTA)
+  // epilogue
+  int mode;                 // 0: SwiGLU -> out[row][out_ld]; 1: plain -> rows by meta
+  __nv_bfloat16* out;       // mode 0: hbuf; mode 1 with meta == null: y
+  int out_ld;               // elements per output row (H' or H)
+  const int2* meta;         // mode 1: (sender, t*K+k) per row
+  char* dst[MSI_MAX_RANKS]; // mode 1: combine buffer base per sender index
+  // completion signal (last CTA): red.release.sys +1 on each sig[i]
+  uint32_t* ticket;
+  uint32_t* sig[MSI_MAX_RANKS];
+  int n_sig;
+};
+
+struct GemmLaunch {
+  const void* a;   // [a_rows][kdim] bf16
+  int64_t a_rows;
+  const void* b;   // [E_l * n_total][kdim] bf16
+  int grid;        // 0 = one CTA per SM
+  GemmParams p;
+};
+
+int grouped_gemm_launch(const GemmLaunch& L, cudaStream_t st);
+int num_sms();
+
+}  // namespace msi

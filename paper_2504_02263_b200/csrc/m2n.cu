@@ -1,0 +1,615 @@
+// m2n.cu -- M2N dispatch / N2M combine over NVLink peer memory, the symmetric
+// heap and its IPC registration, and the expert-step driver.
+//
+// The paper's M2N library moves tokens with CPU-driven
+// RDMA: the sender waits on a CUDA event, blocks its stream with a driver op,
+// has a CPU "core sender" post RDMA writes-with-immediate and poll the CQ,
+// then unblocks the stream; the receiver polls its CQ, flushes
+// with GDRCopy and unblocks.  On one NVSwitch box none of
+// that machinery is needed: every GPU maps every peer's receive buffers once
+// (CUDA IPC, the "pre-registered tensor"), SMs store rows straight into peer
+// HBM with 16 B vector stores, and readiness is a monotone epoch counter
+// bumped with red.release.sys and polled with ld.acquire.sys -- no host in the
+// loop, no per-step setup.
+//
+// Heap layout of one rank (offsets identical on every rank of the same role):
+//   ctrl   : per-slot counters, one 128 B line each
+//            arrive[slot]  (expert role)    dispatch arrivals, +1 per sender
+//            comb[slot]    (attention role) combine arrivals, +1 per expert GPU
+//            dticket[slot], fticket[slot]   last-CTA tickets (local)
+//            status[2]                      device error word + abort flag
+//            stats[2] u64                   rows through the expert FFN, FFN calls
+//            cntab[slot][n_a][E] u64        (epoch << 32 | count), all-gathered
+//   ybuf   : (attention role) [slot][max_tokens * K][H] bf16 expert outputs
+//   recv   : (expert role)    [slot][cap][H] bf16 received rows
+//   meta   : (expert role)    [slot][cap] int2 (sender, t*K + k)
+//   cap = n_a * max_tokens * min(K, E_l) + E_l * (ROW_ALIGN - 1), rounded to 128.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "gemm.h"
+
+namespace msi {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s launch: %s", what, cudaGetErrorString(e));
+    return (int)e;
+  }
+  return 0;
+}
+
+namespace {
+
+constexpr int CTR_STRIDE = 32;  // u32 per counter line (128 B)
+constexpr size_t ALIGN = 4096;
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct Layout {
+  size_t arrive, comb, dticket, fticket, status, stats, cntab, ctrl_bytes;
+  size_t ybuf, ybuf_slot;
+  size_t recv, recv_slot, meta, meta_slot;
+  size_t total;
+  int64_t cap;
+};
+
+Layout make_layout(const msi_plan& p, bool attn, bool expert) {
+  Layout L{};
+  const size_t line = CTR_STRIDE * 4;
+  size_t off = 0;
+  L.arrive = off; off += p.slots * line;
+  L.comb = off; off += p.slots * line;
+  L.dticket = off; off += p.slots * line;
+  L.fticket = off; off += p.slots * line;
+  L.status = off; off += line;
+  L.stats = off; off += line;
+  L.cntab = off; off += (size_t)p.slots * p.n_a * p.experts * 8;
+  L.ctrl_bytes = align_up(off, ALIGN);
+  off = L.ctrl_bytes;
+  const int E_l = p.experts / p.n_e;
+  const int per_tok = p.topk < E_l ? p.topk : E_l;
+  int64_t cap = (int64_t)p.n_a * p.max_tokens * per_tok + (int64_t)E_l * (MSI_ROW_ALIGN - 1);
+  L.cap = (cap + 127) / 128 * 128;
+  L.ybuf_slot = (size_t)p.max_tokens * p.topk * p.hidden * 2;
+  L.ybuf = off;
+  if (attn) off += align_up(L.ybuf_slot * p.slots, ALIGN);
+  L.recv_slot = (size_t)L.cap * p.hidden * 2;
+  L.recv = off;
+  if (expert) off += align_up(L.recv_slot * p.slots, ALIGN);
+  L.meta_slot = (size_t)L.cap * 8;
+  L.meta = off;
+  if (expert) off += align_up(L.meta_slot * p.slots, ALIGN);
+  L.total = off;
+  return L;
+}
+
+// Everything a device kernel needs, by value (kernel parameter space).
+struct DevCtx {
+  int n_a, n_e, n_world, E, K, H, Hp, E_l, slots, max_tokens;
+  int my_a, my_e;
+  long long cap;
+  uint64_t timeout_ns;
+  uint64_t* cntab_of[MSI_MAX_RANKS];   // count table on every rank of the world
+  uint32_t* arrive_of[MSI_MAX_RANKS];  // per expert index q
+  char* recv_of[MSI_MAX_RANKS];        // per expert index q
+  int2* meta_of[MSI_MAX_RANKS];        // per expert index q
+  uint32_t* comb_of[MSI_MAX_RANKS];    // per attention index s
+  char* ybuf_of[MSI_MAX_RANKS];        // per attention index s
+  uint64_t* my_cntab;
+  uint32_t *my_arrive, *my_comb, *my_dticket, *my_fticket;
+  int32_t* my_status;
+};
+
+}  // namespace
+}  // namespace msi
+
+struct msi_ctx {
+  msi_plan plan;
+  int rank;
+  bool attn, expert;
+  int my_a, my_e;
+  char* heap = nullptr;
+  char* hbuf = nullptr;       // expert role: SwiGLU activations [cap][H']
+  void* workspace = nullptr;  // router workspace for the runtime (zeroed)
+  size_t ws_bytes = 0;
+  size_t heap_bytes = 0;
+  char* peer[MSI_MAX_RANKS] = {nullptr};
+  bool opened[MSI_MAX_RANKS] = {false};
+  bool finalized = false;
+  uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
+  msi::Layout my_layout;
+  msi::DevCtx dev;
+};
+
+namespace msi {
+namespace {
+
+bool role_attn(const msi_plan& p, int r) {
+  for (int i = 0; i < p.n_a; ++i) if (p.attn_ranks[i] == r) return true;
+  return false;
+}
+bool role_expert(const msi_plan& p, int r) {
+  for (int i = 0; i < p.n_e; ++i) if (p.expert_ranks[i] == r) return true;
+  return false;
+}
+
+int validate(const msi_plan& p) {
+  MSI_REQUIRE(p.world >= 1 && p.world <= MSI_MAX_RANKS, "plan: world must be in [1, %d]", MSI_MAX_RANKS);
+  MSI_REQUIRE(p.n_a >= 1 && p.n_a <= p.world && p.n_e >= 1 && p.n_e <= p.world, "plan: bad n_a/n_e");
+  MSI_REQUIRE(p.experts >= 1 && p.experts % p.n_e == 0, "plan: experts must divide over n_e");
+  MSI_REQUIRE(p.experts / p.n_e <= MSI_MAX_LOCAL_EXPERTS, "plan: at most %d experts per GPU", MSI_MAX_LOCAL_EXPERTS);
+  MSI_REQUIRE(p.topk >= 1 && p.topk <= p.experts && p.topk <= 32, "plan: bad topk");
+  MSI_REQUIRE(p.hidden % 256 == 0 && p.inter % 128 == 0, "plan: hidden %% 256 and inter %% 128 required");
+  MSI_REQUIRE(p.max_tokens >= 1 && p.slots >= 1 && p.slots <= 16, "plan: bad max_tokens/slots");
+  for (int i = 0; i < p.n_a; ++i) MSI_REQUIRE(p.attn_ranks[i] >= 0 && p.attn_ranks[i] < p.world, "plan: attn rank out of range");
+  for (int i = 0; i < p.n_e; ++i) MSI_REQUIRE(p.expert_ranks[i] >= 0 && p.expert_ranks[i] < p.world, "plan: expert rank out of range");
+  return 0;
+}
+
+// ------------------------------------------------------------ dispatch ----
+constexpr int kDispThreads = 512;
+
+__global__ void __launch_bounds__(kDispThreads)
+dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ cnt,
+                const int32_t* __restrict__ idx, const int32_t* __restrict__ slot, int T, int mb,
+                uint32_t epoch) {
+  extern __shared__ long long s_rowbase[];  // [E] first row of this sender in expert e's segment
+  __shared__ int s_abort;
+  const int tid = threadIdx.x;
+  const int s = c.my_a;
+  const size_t tab = (size_t)mb * c.n_a * c.E;
+
+  // ---- publish this sender's counts to every rank (tagged with the epoch)
+  if (blockIdx.x == 0)
+    for (int i = tid; i < c.n_world * c.E; i += blockDim.x) {
+      const int r = i / c.E, e = i - r * c.E;
+      st_relaxed_sys64(c.cntab_of[r] + tab + (size_t)s * c.E + e,
+                       ((uint64_t)epoch << 32) | (uint32_t)cnt[e]);
+    }
+  // ---- wait for every sender's counts (local table)
+  if (tid == 0) s_abort = 0;
+  __syncthreads();
+  for (int i = tid; i < c.n_a * c.E; i += blockDim.x) {
+    const uint64_t* p = c.my_cntab + tab + i;
+    uint64_t t0 = 0;
+    uint32_t spins = 0;
+    while ((uint32_t)(ld_acquire_sys64(p) >> 32) != epoch) {
+      if ((++spins & 1023u) == 0) {
+        uint64_t now = globaltimer();
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > c.timeout_ns) { atomicExch(c.my_status, MSI_ETIMEOUT); s_abort = 1; break; }
+      }
+      __nanosleep(32);
+    }
+  }
+  __syncthreads();
+  if (s_abort) return;
+  // ---- row base per expert: 128-aligned segment start + rows of senders < s
+  for (int q = tid; q < c.n_e; q += blockDim.x) {
+    long long run = 0;
+    for (int el = 0; el < c.E_l; ++el) {
+      const int e = q * c.E_l + el;
+      long long total = 0, before = 0;
+      for (int s2 = 0; s2 < c.n_a; ++s2) {
+        const long long v = (uint32_t)ld_relaxed_sys64(c.my_cntab + tab + (size_t)s2 * c.E + e);
+        total += v;
+        if (s2 < s) before += v;
+      }
+      s_rowbase[e] = run + before;
+      run += (total + MSI_ROW_ALIGN - 1) / MSI_ROW_ALIGN * MSI_ROW_ALIGN;
+    }
+  }
+  __syncthreads();
+
+  // ---- copy rows: one warp per token, x[t] read once, written K times
+  const int lane = tid & 31;
+  const int gwarp = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  const int nchunk = c.H >> 8;  // 512 B per warp-chunk (16 B per lane)
+  const size_t row_bytes = (size_t)c.H * 2;
+  for (int t = gwarp; t < T; t += nwarps) {
+    // lane k (< K) resolves destination k
+    char* my_dst = nullptr;
+    if (lane < c.K) {
+      const int e = idx[(size_t)t * c.K + lane];
+      const int q = e / c.E_l;
+      const long long row = s_rowbase[e] + slot[(size_t)t * c.K + lane];
+      my_dst = c.recv_of[q] + ((size_t)mb * c.cap + row) * row_bytes;
+      c.meta_of[q][(size_t)mb * c.cap + row] = make_int2(s, t * c.K + lane);
+    }
+    const char* src = reinterpret_cast<const char*>(x + (size_t)t * c.H) + lane * 16;
+    constexpr int U = 8;
+    for (int j0 = 0; j0 < nchunk; j0 += U) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (j0 + u < nchunk) v[u] = ld_nc_v4(src + (size_t)(j0 + u) * 512);
+      for (int k = 0; k < c.K; ++k) {
+        char* d = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(my_dst), k)) + lane * 16;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (j0 + u < nchunk) st_v4(d + (size_t)(j0 + u) * 512, v[u]);
+      }
+    }
+  }
+
+  // ---- release: the last CTA bumps every expert GPU's arrival counter
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence_system();
+    const uint32_t old = atomicAdd(c.my_dticket + mb * CTR_STRIDE, 1u);
+    if (old == gridDim.x - 1) {
+      c.my_dticket[mb * CTR_STRIDE] = 0;
+      fence_sys();
+      for (int q = 0; q < c.n_e; ++q) red_release_sys_add(c.arrive_of[q] + mb * CTR_STRIDE, 1u);
+    }
+  }
+}
+
+// ------------------------------------------------------------- combine ----
+__device__ __forceinline__ void combine_row8(const char* ybase, const float* w, const uint16_t* resid,
+                                             uint16_t* out, int t, int col8, int K, int H) {
+  float acc[8];
+  if (resid) {
+    uint4 r = *reinterpret_cast<const uint4*>(resid + (size_t)t * H + col8 * 8);
+    acc[0] = bf16lo(r.x); acc[1] = bf16hi(r.x); acc[2] = bf16lo(r.y); acc[3] = bf16hi(r.y);
+    acc[4] = bf16lo(r.z); acc[5] = bf16hi(r.z); acc[6] = bf16lo(r.w); acc[7] = bf16hi(r.w);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+  }
+  for (int k = 0; k < K; ++k) {
+    const float wk = w[(size_t)t * K + k];
+    uint4 y = __ldcg(reinterpret_cast<const uint4*>(ybase + (((size_t)t * K + k) * H + col8 * 8) * 2));
+    acc[0] = __fmaf_rn(wk, bf16lo(y.x), acc[0]); acc[1] = __fmaf_rn(wk, bf16hi(y.x), acc[1]);
+    acc[2] = __fmaf_rn(wk, bf16lo(y.y), acc[2]); acc[3] = __fmaf_rn(wk, bf16hi(y.y), acc[3]);
+    acc[4] = __fmaf_rn(wk, bf16lo(y.z), acc[4]); acc[5] = __fmaf_rn(wk, bf16hi(y.z), acc[5]);
+    acc[6] = __fmaf_rn(wk, bf16lo(y.w), acc[6]); acc[7] = __fmaf_rn(wk, bf16hi(y.w), acc[7]);
+  }
+  uint4 o = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
+                       pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
+  *reinterpret_cast<uint4*>(out + (size_t)t * H + col8 * 8) = o;
+}
+
+__global__ void __launch_bounds__(256)
+combine_kernel(const char* __restrict__ ybase, const float* __restrict__ w, const uint16_t* __restrict__ resid,
+               uint16_t* __restrict__ out, int T, int K, int H, const uint32_t* wait_ctr,
+               uint32_t target, uint64_t timeout_ns, int32_t* status) {
+  __shared__ int s_ok;
+  if (wait_ctr) {
+    if (threadIdx.x == 0) s_ok = wait_geq(wait_ctr, target, timeout_ns, status);
+    __syncthreads();
+    if (!s_ok) return;
+  }
+  const int per_row = H / 8;
+  const size_t n = (size_t)T * per_row;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int t = (int)(i / per_row), c8 = (int)(i % per_row);
+    combine_row8(ybase, w, resid, out, t, c8, K, H);
+  }
+}
+
+// -------------------------------------------------- attention stand-in ----
+__global__ void attn_standin_kernel(const uint4* __restrict__ kv, size_t n16, float* checksum) {
+  float s = 0.0f;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x) {
+    uint4 v = ld_nc_v4(kv + i);
+    s += bf16lo(v.x) + bf16hi(v.w);
+  }
+  for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if ((threadIdx.x & 31) == 0 && s == 1234.5f) atomicAdd(checksum, s);  // keeps the loads live
+}
+
+}  // namespace
+}  // namespace msi
+
+using namespace msi;
+
+// =============================================================== C ABI ====
+extern "C" int msi_version(void) { return 1; }
+extern "C" const char* msi_last_error(void) { return msi::g_err; }
+
+extern "C" int msi_check_device(void) {
+  int dev = 0, major = 0, minor = 0;
+  MSI_CUDA(cudaGetDevice(&dev));
+  MSI_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  MSI_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
+  if (major != 10 || minor != 0) {
+    set_error("libmsinfer is built for sm_100a (B200); device is sm_%d%d", major, minor);
+    return MSI_EARCH;
+  }
+  return 0;
+}
+
+extern "C" int msi_ctx_create(const msi_plan* plan, int rank, msi_ctx** out) {
+  if (!plan || !out) { set_error("msi_ctx_create: null argument"); return MSI_EINVAL; }
+  int rc = validate(*plan);
+  if (rc) return rc;
+  if (rank < 0 || rank >= plan->world) { set_error("msi_ctx_create: rank out of range"); return MSI_EINVAL; }
+  rc = msi_check_device();
+  if (rc) return rc;
+  msi_ctx* c = new msi_ctx();
+  c->plan = *plan;
+  c->rank = rank;
+  c->attn = role_attn(*plan, rank);
+  c->expert = role_expert(*plan, rank);
+  c->my_a = c->my_e = -1;
+  for (int i = 0; i < plan->n_a; ++i) if (plan->attn_ranks[i] == rank) c->my_a = i;
+  for (int i = 0; i < plan->n_e; ++i) if (plan->expert_ranks[i] == rank) c->my_e = i;
+  c->my_layout = make_layout(*plan, c->attn, c->expert);
+  c->heap_bytes = c->my_layout.total;
+  cudaError_t e = cudaMalloc(&c->heap, c->heap_bytes);
+  if (e != cudaSuccess) { set_error("heap cudaMalloc(%zu): %s", c->heap_bytes, cudaGetErrorString(e)); delete c; return (int)e; }
+  cudaMemset(c->heap, 0, c->my_layout.ctrl_bytes);
+  if (c->expert) {
+    e = cudaMalloc(&c->hbuf, (size_t)c->my_layout.cap * plan->inter * 2);
+    if (e != cudaSuccess) { set_error("hbuf cudaMalloc: %s", cudaGetErrorString(e)); cudaFree(c->heap); delete c; return (int)e; }
+  }
+  c->ws_bytes = msi_gate_topk_workspace(plan->max_tokens, plan->experts);
+  e = cudaMalloc(&c->workspace, c->ws_bytes);
+  if (e != cudaSuccess) { set_error("workspace cudaMalloc: %s", cudaGetErrorString(e)); return (int)e; }
+  cudaMemset(c->workspace, 0, c->ws_bytes);
+  c->peer[rank] = c->heap;
+  c->opened[rank] = true;
+  *out = c;
+  return 0;
+}
+
+extern "C" int msi_ctx_destroy(msi_ctx* c) {
+  if (!c) return 0;
+  cudaDeviceSynchronize();
+  for (int r = 0; r < c->plan.world; ++r)
+    if (r != c->rank && c->opened[r] && c->peer[r]) cudaIpcCloseMemHandle(c->peer[r]);
+  if (c->heap) cudaFree(c->heap);
+  if (c->hbuf) cudaFree(c->hbuf);
+  if (c->workspace) cudaFree(c->workspace);
+  delete c;
+  return 0;
+}
+
+extern "C" int msi_ctx_export(msi_ctx* c, msi_ipc_handle* out) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == MSI_IPC_HANDLE_BYTES, "ipc handle size");
+  if (!c || !out) { set_error("msi_ctx_export: null argument"); return MSI_EINVAL; }
+  cudaIpcMemHandle_t h;
+  MSI_CUDA(cudaIpcGetMemHandle(&h, c->heap));
+  memcpy(out->bytes, &h, sizeof(h));
+  return 0;
+}
+
+extern "C" int msi_ctx_import(msi_ctx* c, int peer, const msi_ipc_handle* handle) {
+  if (!c || !handle || peer < 0 || peer >= c->plan.world) { set_error("msi_ctx_import: bad argument"); return MSI_EINVAL; }
+  if (peer == c->rank) return 0;
+  if (c->opened[peer]) return 0;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle->bytes, sizeof(h));
+  void* p = nullptr;
+  MSI_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  c->peer[peer] = reinterpret_cast<char*>(p);
+  c->opened[peer] = true;
+  return 0;
+}
+
+extern "C" int msi_ctx_finalize(msi_ctx* c) {
+  if (!c) { set_error("msi_ctx_finalize: null"); return MSI_EINVAL; }
+  const msi_plan& p = c->plan;
+  for (int r = 0; r < p.world; ++r)
+    if (!c->opened[r]) { set_error("msi_ctx_finalize: peer %d not imported", r); return MSI_ESTATE; }
+  DevCtx& d = c->dev;
+  memset(&d, 0, sizeof(d));
+  d.n_a = p.n_a; d.n_e = p.n_e; d.n_world = p.world; d.E = p.experts; d.K = p.topk;
+  d.H = p.hidden; d.Hp = p.inter; d.E_l = p.experts / p.n_e; d.slots = p.slots;
+  d.max_tokens = p.max_tokens; d.my_a = c->my_a; d.my_e = c->my_e;
+  d.cap = c->my_layout.cap;
+  d.timeout_ns = c->timeout_ns;
+  for (int r = 0; r < p.world; ++r) {
+    Layout L = make_layout(p, role_attn(p, r), role_expert(p, r));
+    d.cntab_of[r] = reinterpret_cast<uint64_t*>(c->peer[r] + L.cntab);
+  }
+  for (int q = 0; q < p.n_e; ++q) {
+    const int r = p.expert_ranks[q];
+    Layout L = make_layout(p, role_attn(p, r), true);
+    d.arrive_of[q] = reinterpret_cast<uint32_t*>(c->peer[r] + L.arrive);
+    d.recv_of[q] = c->peer[r] + L.recv;
+    d.meta_of[q] = reinterpret_cast<int2*>(c->peer[r] + L.meta);
+  }
+  for (int s = 0; s < p.n_a; ++s) {
+    const int r = p.attn_ranks[s];
+    Layout L = make_layout(p, true, role_expert(p, r));
+    d.comb_of[s] = reinterpret_cast<uint32_t*>(c->peer[r] + L.comb);
+    d.ybuf_of[s] = c->peer[r] + L.ybuf;
+  }
+  const Layout& M = c->my_layout;
+  d.my_cntab = reinterpret_cast<uint64_t*>(c->heap + M.cntab);
+  d.my_arrive = reinterpret_cast<uint32_t*>(c->heap + M.arrive);
+  d.my_comb = reinterpret_cast<uint32_t*>(c->heap + M.comb);
+  d.my_dticket = reinterpret_cast<uint32_t*>(c->heap + M.dticket);
+  d.my_fticket = reinterpret_cast<uint32_t*>(c->heap + M.fticket);
+  d.my_status = reinterpret_cast<int32_t*>(c->heap + M.status);
+  MSI_CUDA(cudaMemset(c->heap, 0, M.ctrl_bytes));
+  MSI_CUDA(cudaDeviceSynchronize());
+  c->finalized = true;
+  return 0;
+}
+
+extern "C" int msi_ctx_buffer(msi_ctx* c, int which, int slot, void** ptr, size_t* bytes) {
+  if (!c || !ptr || !bytes || slot < 0 || slot >= c->plan.slots) { set_error("msi_ctx_buffer: bad argument"); return MSI_EINVAL; }
+  const Layout& L = c->my_layout;
+  switch (which) {
+    case MSI_BUF_RECV:
+      if (!c->expert) break;
+      *ptr = c->heap + L.recv + slot * L.recv_slot; *bytes = L.recv_slot; return 0;
+    case MSI_BUF_META:
+      if (!c->expert) break;
+      *ptr = c->heap + L.meta + slot * L.meta_slot; *bytes = L.meta_slot; return 0;
+    case MSI_BUF_YBUF:
+      if (!c->attn) break;
+      *ptr = c->heap + L.ybuf + slot * L.ybuf_slot; *bytes = L.ybuf_slot; return 0;
+    case MSI_BUF_HBUF:
+      if (!c->expert) break;
+      *ptr = c->hbuf; *bytes = (size_t)L.cap * c->plan.inter * 2; return 0;
+    case MSI_BUF_CNTAB: {
+      const size_t per = (size_t)c->plan.n_a * c->plan.experts * 8;
+      *ptr = c->heap + L.cntab + slot * per; *bytes = per; return 0;
+    }
+  }
+  set_error("msi_ctx_buffer: buffer %d not present for this rank's role", which);
+  return MSI_EINVAL;
+}
+
+extern "C" int msi_ctx_workspace(msi_ctx* c, void** ptr, size_t* bytes) {
+  if (!c || !ptr || !bytes) { set_error("msi_ctx_workspace: null"); return MSI_EINVAL; }
+  *ptr = c->workspace;
+  *bytes = c->ws_bytes;
+  return 0;
+}
+
+extern "C" int msi_poll_status(msi_ctx* c, int32_t* status) {
+  if (!c || !status) { set_error("msi_poll_status: null"); return MSI_EINVAL; }
+  MSI_CUDA(cudaMemcpy(status, c->heap + c->my_layout.status, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+extern "C" int msi_ctx_stats(msi_ctx* c, uint64_t* rows, uint64_t* calls) {
+  if (!c || !rows || !calls) { set_error("msi_ctx_stats: null"); return MSI_EINVAL; }
+  uint64_t v[2];
+  MSI_CUDA(cudaMemcpy(v, c->heap + c->my_layout.stats, sizeof(v), cudaMemcpyDeviceToHost));
+  *rows = v[0];
+  *calls = v[1];
+  return 0;
+}
+
+extern "C" int msi_set_wait_timeout(msi_ctx* c, uint64_t ns) {
+  if (!c) { set_error("msi_set_wait_timeout: null"); return MSI_EINVAL; }
+  c->timeout_ns = ns;
+  c->dev.timeout_ns = ns;
+  return 0;
+}
+
+extern "C" int msi_dispatch(msi_ctx* c, const void* x, const int32_t* cnt, const int32_t* idx,
+                            const int32_t* slot, int T, int mb_slot, uint32_t epoch, void* stream) {
+  if (!c || !c->finalized) { set_error("msi_dispatch: context not finalized"); return MSI_ESTATE; }
+  if (!c->attn) { set_error("msi_dispatch: rank %d has no attention role", c->rank); return MSI_EINVAL; }
+  MSI_REQUIRE(T >= 0 && T <= c->plan.max_tokens, "msi_dispatch: T=%d exceeds max_tokens=%d", T, c->plan.max_tokens);
+  MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots && epoch >= 1, "msi_dispatch: bad slot/epoch");
+  MSI_REQUIRE(x && cnt && idx && slot, "msi_dispatch: null pointer");
+  const size_t smem = sizeof(long long) * c->plan.experts;
+  // enough warps to keep ~4 rows in flight per SM, at most one CTA per SM
+  int grid = (T + (kDispThreads / 32) - 1) / (kDispThreads / 32);
+  grid = grid < 1 ? 1 : (grid > num_sms() ? num_sms() : grid);
+  dispatch_kernel<<<grid, kDispThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
+      c->dev, reinterpret_cast<const __nv_bfloat16*>(x), cnt, idx, slot, T, mb_slot, epoch);
+  return check_launch("dispatch_kernel");
+}
+
+extern "C" int msi_expert_ffn(msi_ctx* c, const void* w13, const void* w2, int mb_slot,
+                              uint32_t epoch, void* stream) {
+  if (!c || !c->finalized) { set_error("msi_expert_ffn: context not finalized"); return MSI_ESTATE; }
+  if (!c->expert) { set_error("msi_expert_ffn: rank %d has no expert role", c->rank); return MSI_EINVAL; }
+  MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots && epoch >= 1, "msi_expert_ffn: bad slot/epoch");
+  MSI_REQUIRE(w13 && w2, "msi_expert_ffn: null weights");
+  const msi_plan& p = c->plan;
+  const DevCtx& d = c->dev;
+  const Layout& L = c->my_layout;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t tab = (size_t)mb_slot * p.n_a * p.experts;
+
+  GemmLaunch g1{};
+  g1.a = c->heap + L.recv + mb_slot * L.recv_slot;
+  g1.a_rows = L.cap;
+  g1.b = w13;
+  g1.p.E_l = d.E_l;
+  g1.p.n_total = 2 * p.inter;
+  g1.p.nt = 2 * p.inter / 256;
+  g1.p.kdim = p.hidden;
+  g1.p.cntab = d.my_cntab + tab;
+  g1.p.n_a = p.n_a;
+  g1.p.E = p.experts;
+  g1.p.e0 = c->my_e * d.E_l;
+  g1.p.wait_ctr = d.my_arrive + mb_slot * CTR_STRIDE;
+  g1.p.wait_target = epoch * (uint32_t)p.n_a;
+  g1.p.timeout_ns = c->timeout_ns;
+  g1.p.status = d.my_status;
+  g1.p.stats = reinterpret_cast<unsigned long long*>(c->heap + L.stats);
+  g1.p.mode = 0;
+  g1.p.out = reinterpret_cast<__nv_bfloat16*>(c->hbuf);
+  g1.p.out_ld = p.inter;
+  int rc = grouped_gemm_launch(g1, st);
+  if (rc) return rc;
+
+  GemmLaunch g2{};
+  g2.a = c->hbuf;
+  g2.a_rows = L.cap;
+  g2.b = w2;
+  g2.p.E_l = d.E_l;
+  g2.p.n_total = p.hidden;
+  g2.p.nt = p.hidden / 256;
+  g2.p.kdim = p.inter;
+  g2.p.cntab = d.my_cntab + tab;
+  g2.p.n_a = p.n_a;
+  g2.p.E = p.experts;
+  g2.p.e0 = c->my_e * d.E_l;
+  g2.p.status = d.my_status;
+  g2.p.mode = 1;
+  g2.p.out_ld = p.hidden;
+  g2.p.meta = reinterpret_cast<const int2*>(c->heap + L.meta + mb_slot * L.meta_slot);
+  for (int s = 0; s < p.n_a; ++s) g2.p.dst[s] = d.ybuf_of[s] + mb_slot * L.ybuf_slot;
+  g2.p.ticket = d.my_fticket + mb_slot * CTR_STRIDE;
+  for (int s = 0; s < p.n_a; ++s) g2.p.sig[s] = d.comb_of[s] + mb_slot * CTR_STRIDE;
+  g2.p.n_sig = p.n_a;
+  return grouped_gemm_launch(g2, st);
+}
+
+extern "C" int msi_combine(msi_ctx* c, void* out, const float* w, const void* resid, int T, int mb_slot,
+                           uint32_t epoch, void* stream) {
+  if (!c || !c->finalized) { set_error("msi_combine: context not finalized"); return MSI_ESTATE; }
+  if (!c->attn) { set_error("msi_combine: rank %d has no attention role", c->rank); return MSI_EINVAL; }
+  MSI_REQUIRE(T >= 0 && T <= c->plan.max_tokens, "msi_combine: T out of range");
+  MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots && epoch >= 1, "msi_combine: bad slot/epoch");
+  MSI_REQUIRE(out && w, "msi_combine: null pointer");
+  const msi_plan& p = c->plan;
+  const Layout& L = c->my_layout;
+  const size_t n = (size_t)T * p.hidden / 8;
+  int grid = (int)((n + 255) / 256);
+  grid = grid < 1 ? 1 : (grid > 4 * num_sms() ? 4 * num_sms() : grid);
+  combine_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      c->heap + L.ybuf + mb_slot * L.ybuf_slot, w, reinterpret_cast<const uint16_t*>(resid),
+      reinterpret_cast<uint16_t*>(out), T, p.topk, p.hidden, c->dev.my_comb + mb_slot * CTR_STRIDE,
+      epoch * (uint32_t)p.n_e, c->timeout_ns, c->dev.my_status);
+  return check_launch("combine_kernel");
+}
+
+extern "C" int msi_combine_local(const void* y, const float* w, const void* resid, void* out, int T, int K,
+                                 int H, void* stream) {
+  MSI_REQUIRE(y && w && out && T >= 0 && K >= 1 && H % 8 == 0, "msi_combine_local: bad argument");
+  if (T == 0) return 0;
+  const size_t n = (size_t)T * H / 8;
+  int grid = (int)((n + 255) / 256);
+  grid = grid > 4 * num_sms() ? 4 * num_sms() : grid;
+  combine_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const char*>(y), w, reinterpret_cast<const uint16_t*>(resid),
+      reinterpret_cast<uint16_t*>(out), T, K, H, nullptr, 0, 0, nullptr);
+  return check_launch("combine_kernel");
+}
+
+extern "C" int msi_attn_standin(const void* kv, size_t kv_bytes, float* checksum, void* stream) {
+  MSI_REQUIRE(kv && checksum && kv_bytes % 16 == 0, "msi_attn_standin: bad argument");
+  if (kv_bytes == 0) return 0;
+  attn_standin_kernel<<<2 * num_sms(), 512, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const uint4*>(kv), kv_bytes / 16, checksum);
+  return check_launch("attn_standin_kernel");
+}

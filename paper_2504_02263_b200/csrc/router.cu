@@ -1,0 +1,229 @@
+// router.cu -- fused gate GEMM + top-K + normalized weights + per-expert
+// counts + slot placement.
+//
+// One kernel launch.  Each CTA owns BT consecutive tokens:
+//   1. logits[t,e] in the pinned fp32 order (lane l accumulates elements
+//      256j + 8l + c with fmaf, then an xor butterfly 16,8,4,2,1) -- the
+//      order oracle/msi_oracle.c restates, so routing is bit-exact;
+//   2. top-K per token (warp arg-max, ties to the lower expert), weights =
+//      softmax of the K chosen logits with det_expf (bit-exact as well);
+//   3. per-CTA histogram and in-CTA ranks with a warp ballot/popc prefix
+//      (bit t of mask[e] = token t routed to e; rank = popc(mask & lanes_below));
+//   4. the last CTA to finish (ticket) scans the per-CTA histograms into
+//      per-CTA bases, writes cnt[E], and adds the bases to every slot.
+// HBM-bound for small E (reads x once); FMA-bound for E = 256 (logits on
+// CUDA cores because the fixed reduction order is the bit-exactness contract).
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace msi {
+namespace {
+
+constexpr int kWarps = 8;
+constexpr uint32_t kTaken = 0x7fc0dead;  // NaN payload marking an already-selected expert
+
+template <int TT, int TE>
+__global__ void __launch_bounds__(kWarps * 32)
+gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
+                 int T, int H, int E, int K, int BT, int32_t* __restrict__ idx_out,
+                 float* __restrict__ w_out, int32_t* __restrict__ cnt_out,
+                 int32_t* __restrict__ slot_out, int32_t* __restrict__ ws) {
+  extern __shared__ float s_logit[];                       // [BT][E]
+  uint32_t* s_mask = reinterpret_cast<uint32_t*>(s_logit + BT * E);  // [E]
+  __shared__ int s_last;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t0 = blockIdx.x * BT;
+  const int nchunk = H >> 8;
+
+  for (int e = threadIdx.x; e < E; e += blockDim.x) s_mask[e] = 0u;
+
+  // ---- 1. logits ---------------------------------------------------------
+  const int tgroups = BT / TT, egroups = E / TE;
+  for (int tile = warp; tile < tgroups * egroups; tile += kWarps) {
+    const int tg = tile % tgroups, eg = tile / tgroups;
+    float acc[TT][TE];
+#pragma unroll
+    for (int i = 0; i < TT; ++i)
+#pragma unroll
+      for (int j = 0; j < TE; ++j) acc[i][j] = 0.0f;
+    const __nv_bfloat16* xr[TT];
+    bool tv[TT];
+#pragma unroll
+    for (int i = 0; i < TT; ++i) {
+      int t = t0 + tg * TT + i;
+      tv[i] = t < T;
+      xr[i] = x + (size_t)(tv[i] ? t : 0) * H + 8 * lane;
+    }
+    const __nv_bfloat16* wr = wg + (size_t)(eg * TE) * H + 8 * lane;
+    for (int j = 0; j < nchunk; ++j) {
+      float xv[TT][8];
+#pragma unroll
+      for (int i = 0; i < TT; ++i) {
+        uint4 v = tv[i] ? __ldg(reinterpret_cast<const uint4*>(xr[i] + 256 * j)) : make_uint4(0, 0, 0, 0);
+        xv[i][0] = bf16lo(v.x); xv[i][1] = bf16hi(v.x);
+        xv[i][2] = bf16lo(v.y); xv[i][3] = bf16hi(v.y);
+        xv[i][4] = bf16lo(v.z); xv[i][5] = bf16hi(v.z);
+        xv[i][6] = bf16lo(v.w); xv[i][7] = bf16hi(v.w);
+      }
+#pragma unroll
+      for (int e = 0; e < TE; ++e) {
+        uint4 v = __ldg(reinterpret_cast<const uint4*>(wr + (size_t)e * H + 256 * j));
+        float wv[8] = {bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y),
+                       bf16lo(v.z), bf16hi(v.z), bf16lo(v.w), bf16hi(v.w)};
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+#pragma unroll
+          for (int i = 0; i < TT; ++i) acc[i][e] = __fmaf_rn(xv[i][c], wv[c], acc[i][e]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < TT; ++i)
+#pragma unroll
+      for (int e = 0; e < TE; ++e) {
+        float v = acc[i][e];
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+        v = (v != v) ? -INFINITY : v;  // NaN logits rank as -inf (the oracle does the same)
+        if (lane == ((i * TE + e) & 31)) s_logit[(tg * TT + i) * E + eg * TE + e] = v;
+      }
+  }
+  __syncthreads();
+
+  // ---- 2. top-K + weights (one warp per token) ----------------------------
+  for (int lt = warp; lt < BT; lt += kWarps) {
+    const int t = t0 + lt;
+    if (t >= T) break;
+    float* lg = s_logit + lt * E;
+    float selv[32];
+    int seli[32];
+    for (int k = 0; k < K; ++k) {
+      float bv = -INFINITY;
+      int bi = 0x7fffffff;
+      for (int e = lane; e < E; e += 32) {
+        float v = lg[e];
+        if (__float_as_uint(v) == kTaken) continue;
+        if (v > bv || (v == bv && e < bi)) { bv = v; bi = e; }
+      }
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) {
+        float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+      }
+      selv[k] = bv;
+      seli[k] = bi;
+      __syncwarp();
+      if (lane == 0) lg[bi] = __uint_as_float(kTaken);  // exclude from later rounds
+      __syncwarp();
+    }
+    if (lane == 0) {
+      float ex[32], s = 0.0f;
+      for (int k = 0; k < K; ++k) {
+        ex[k] = det_expf(__fsub_rn(selv[k], selv[0]));
+        s = (k == 0) ? ex[0] : __fadd_rn(s, ex[k]);
+      }
+      for (int k = 0; k < K; ++k) {
+        idx_out[(size_t)t * K + k] = seli[k];
+        w_out[(size_t)t * K + k] = __fdiv_rn(ex[k], s);
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- 3. per-CTA histogram + in-CTA ranks (warp 0, lane = token) ----------
+  int32_t* blk_hist = ws + 4;  // ws[0] = ticket
+  if (warp == 0) {
+    const int t = t0 + lane;
+    const bool valid = lane < BT && t < T;
+    int myE[32];
+    for (int k = 0; k < K; ++k) {
+      myE[k] = valid ? idx_out[(size_t)t * K + k] : 0;
+      if (valid) atomicOr(&s_mask[myE[k]], 1u << lane);
+    }
+    __syncwarp();
+    const uint32_t below = (1u << lane) - 1u;
+    if (valid)
+      for (int k = 0; k < K; ++k)
+        slot_out[(size_t)t * K + k] = __popc(s_mask[myE[k]] & below);
+    __syncwarp();
+    for (int e = lane; e < E; e += 32) blk_hist[(size_t)blockIdx.x * E + e] = __popc(s_mask[e]);
+  }
+
+  // ---- 4. last CTA: scan histograms, finalize counts and slots ------------
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(&ws[0], 1) == (int)gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int nblk = gridDim.x;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int run = 0;
+    for (int b = 0; b < nblk; ++b) {
+      int c = __ldcg(&blk_hist[(size_t)b * E + e]);
+      blk_hist[(size_t)b * E + e] = run;
+      run += c;
+    }
+    cnt_out[e] = run;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < T * K; i += blockDim.x) {
+    const int b = (i / K) / BT;
+    const int e = __ldcg(&idx_out[i]);
+    slot_out[i] = __ldcg(&slot_out[i]) + blk_hist[(size_t)b * E + e];
+  }
+  if (threadIdx.x == 0) ws[0] = 0;  // ticket ready for the next launch
+}
+
+template <int TT, int TE>
+int launch(const void* x, const void* wg, int T, int H, int E, int K, int BT, int32_t* idx,
+           float* w, int32_t* cnt, int32_t* slot, void* ws, cudaStream_t st) {
+  const int nblk = (T + BT - 1) / BT;
+  const size_t smem = (size_t)BT * E * sizeof(float) + (size_t)E * sizeof(uint32_t);
+  auto kern = gate_topk_kernel<TT, TE>;
+  if (smem > 48 * 1024) MSI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<nblk, kWarps * 32, smem, st>>>(reinterpret_cast<const __nv_bfloat16*>(x),
+                                        reinterpret_cast<const __nv_bfloat16*>(wg), T, H, E, K, BT,
+                                        idx, w, cnt, slot, reinterpret_cast<int32_t*>(ws));
+  return check_launch("gate_topk_kernel");
+}
+
+}  // namespace
+
+int gate_topk(const void* x, const void* wg, int T, int H, int E, int K, int32_t* idx, float* w,
+              int32_t* cnt, int32_t* slot, void* ws, cudaStream_t st) {
+  MSI_REQUIRE(T >= 0 && H > 0 && H % 256 == 0, "gate_topk: H must be a positive multiple of 256 (got %d)", H);
+  MSI_REQUIRE(E >= 1 && E <= 1024 && K >= 1 && K <= E && K <= 32, "gate_topk: need 1 <= K <= min(E, 32), E <= 1024");
+  MSI_REQUIRE(x && wg && idx && w && cnt && slot && ws, "gate_topk: null pointer");
+  if (T == 0) {
+    MSI_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * E, st));
+    return 0;
+  }
+  // Tile shapes: TE experts x TT tokens per warp; BT tokens per CTA.  Small E
+  // is HBM-bound (want many CTAs); large E is FMA-bound (want token reuse).
+  if (E % 16 == 0 && E > 16)  // fine-grained MoE: FMA-bound, BT=4 keeps >=148 CTAs busy at small T
+    return launch<4, 16>(x, wg, T, H, E, K, T >= 148 * 16 ? 16 : 4, idx, w, cnt, slot, ws, st);
+  if (E % 16 == 0) return launch<1, 16>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, st);
+  if (E % 8 == 0) return launch<1, 8>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, st);
+  if (E % 4 == 0) return launch<1, 4>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, st);
+  if (E % 2 == 0) return launch<1, 2>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, st);
+  return launch<1, 1>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, st);
+}
+
+size_t gate_topk_workspace(int T, int E) {
+  const int nblk = (T + 3) / 4;  // smallest BT used above
+  return 16 + (size_t)nblk * E * sizeof(int32_t);
+}
+
+}  // namespace msi
+
+extern "C" size_t msi_gate_topk_workspace(int T, int E) { return msi::gate_topk_workspace(T, E); }
+
+extern "C" int msi_gate_topk(const void* x, const void* wg, int T, int H, int E, int K,
+                             int32_t* idx, float* w, int32_t* cnt, int32_t* slot, void* workspace,
+                             void* stream) {
+  return msi::gate_topk(x, wg, T, H, E, K, idx, w, cnt, slot, workspace,
+                        reinterpret_cast<cudaStream_t>(stream));
+}

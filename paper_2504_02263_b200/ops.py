@@ -1,0 +1,120 @@
+"""Stateless building blocks of the decode step on torch CUDA tensors.
+
+Each function is a thin wrapper over one libmsinfer entry point
+(include/msinfer.h); tensors are passed by data pointer on the current torch
+stream.  No CPU or PyTorch fallback exists: on a non-B200 device or without
+the built library every call raises ``MsiError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+
+ROW_ALIGN = _lib.ROW_ALIGN
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check_bf16(name, t, ndim=None):
+    if t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous():
+        raise ValueError(f"{name}: expected a contiguous CUDA bfloat16 tensor")
+    if ndim is not None and t.dim() != ndim:
+        raise ValueError(f"{name}: expected {ndim} dims, got {tuple(t.shape)}")
+
+
+class RouterWorkspace:
+    """Zero-initialised scratch for gate_topk (the kernel leaves it zeroed)."""
+
+    def __init__(self, max_tokens: int, experts: int, device=None):
+        n = _lib.load().msi_gate_topk_workspace(max_tokens, experts)
+        self.buf = torch.zeros(n, dtype=torch.uint8, device=device or "cuda")
+        self.max_tokens = max_tokens
+
+
+def gate_topk(x: torch.Tensor, wg: torch.Tensor, topk: int, ws: RouterWorkspace | None = None,
+              out=None, stream=None):
+    """Router: -> idx [T,K] i32, w [T,K] f32, cnt [E] i32,
+    slot [T,K] i32.  Bit-exact with the oracle."""
+    _check_bf16("x", x, 2)
+    _check_bf16("wg", wg, 2)
+    T, H = x.shape
+    E = wg.shape[0]
+    if wg.shape[1] != H:
+        raise ValueError("wg must be [E, H]")
+    if ws is None or ws.max_tokens < T:
+        ws = RouterWorkspace(max(T, 1), E, x.device)
+    if out is None:
+        idx = torch.empty((T, topk), dtype=torch.int32, device=x.device)
+        w = torch.empty((T, topk), dtype=torch.float32, device=x.device)
+        cnt = torch.empty((E,), dtype=torch.int32, device=x.device)
+        slot = torch.empty((T, topk), dtype=torch.int32, device=x.device)
+    else:
+        idx, w, cnt, slot = out
+    _lib.call("msi_gate_topk", _ptr(x), _ptr(wg), T, H, E, topk, _ptr(idx), _ptr(w), _ptr(cnt),
+              _ptr(slot), _ptr(ws.buf), _stream(stream))
+    return idx, w, cnt, slot
+
+
+def pack_w13(w_gate: torch.Tensor, w_up: torch.Tensor, stream=None) -> torch.Tensor:
+    """[E_l, H', H] gate + up -> [E_l, 2H', H] interleaved in 128-row blocks."""
+    _check_bf16("w_gate", w_gate, 3)
+    _check_bf16("w_up", w_up, 3)
+    E_l, Hp, H = w_gate.shape
+    out = torch.empty((E_l, 2 * Hp, H), dtype=torch.bfloat16, device=w_gate.device)
+    _lib.call("msi_pack_w13", _ptr(w_gate), _ptr(w_up), _ptr(out), E_l, Hp, H, _stream(stream))
+    return out
+
+
+def segment_starts(total) -> list[int]:
+    starts, run = [], 0
+    for t in total:
+        starts.append(run)
+        run += (int(t) + ROW_ALIGN - 1) // ROW_ALIGN * ROW_ALIGN
+    return starts
+
+
+def grouped_ffn(x_rows: torch.Tensor, total: torch.Tensor, w13: torch.Tensor, w2: torch.Tensor,
+                hbuf: torch.Tensor | None = None, y: torch.Tensor | None = None, stream=None):
+    """Grouped SwiGLU FFN on the tcgen05 GEMM.  x_rows [rows, H] laid out in
+    128-row aligned per-expert segments (``segment_starts``); total [E_l] int32
+    on device.  Returns y [rows, H] (rows beyond each segment are untouched)."""
+    _check_bf16("x_rows", x_rows, 2)
+    rows, H = x_rows.shape
+    E_l, two_hp, _ = w13.shape
+    Hp = two_hp // 2
+    if hbuf is None:
+        hbuf = torch.empty((rows, Hp), dtype=torch.bfloat16, device=x_rows.device)
+    if y is None:
+        y = torch.zeros((rows, H), dtype=torch.bfloat16, device=x_rows.device)
+    total = total.to(device=x_rows.device, dtype=torch.int32).contiguous()
+    _lib.call("msi_grouped_ffn", _ptr(x_rows), _ptr(total), E_l, rows, _ptr(w13), _ptr(w2),
+              _ptr(hbuf), _ptr(y), H, Hp, _stream(stream))
+    return y
+
+
+def combine_local(y: torch.Tensor, w: torch.Tensor, resid: torch.Tensor | None = None,
+                  out: torch.Tensor | None = None, stream=None):
+    """out[t] = bf16(resid[t] + sum_k w[t,k] y[t,k])."""
+    _check_bf16("y", y, 3)
+    T, K, H = y.shape
+    if out is None:
+        out = torch.empty((T, H), dtype=torch.bfloat16, device=y.device)
+    _lib.call("msi_combine_local", _ptr(y), _ptr(w.contiguous()), _ptr(resid), _ptr(out), T, K, H,
+              _stream(stream))
+    return out
+
+
+def attn_standin(kv: torch.Tensor, checksum: torch.Tensor, stream=None):
+    _lib.call("msi_attn_standin", _ptr(kv), kv.numel() * kv.element_size(), _ptr(checksum),
+              _stream(stream))
