@@ -216,13 +216,18 @@ dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32
   }
   __syncthreads();
 
-  // ---- copy rows: one warp per token, x[t] read once, written K times
+  // ---- copy rows: a warp moves one part of one token row (x read once,
+  //      written K times with 16 B stores, 8 x 512 B in flight per warp)
   const int lane = tid & 31;
   const int gwarp = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
   const int nwarps = gridDim.x * (blockDim.x >> 5);
-  const int nchunk = c.H >> 8;  // 512 B per warp-chunk (16 B per lane)
+  const int nchunk = c.H >> 8;  // 512 B warp-chunks per row
+  int parts = T > 0 ? (nwarps + T - 1) / T : 1;
+  parts = parts < 1 ? 1 : (parts > nchunk ? nchunk : parts);
+  const int per_part = (nchunk + parts - 1) / parts;
   const size_t row_bytes = (size_t)c.H * 2;
-  for (int t = gwarp; t < T; t += nwarps) {
+  for (int item = gwarp; item < T * parts; item += nwarps) {
+    const int t = item / parts, part = item - t * parts;
     // lane k (< K) resolves destination k
     char* my_dst = nullptr;
     if (lane < c.K) {
@@ -230,20 +235,21 @@ dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32
       const int q = e / c.E_l;
       const long long row = s_rowbase[e] + slot[(size_t)t * c.K + lane];
       my_dst = c.recv_of[q] + ((size_t)mb * c.cap + row) * row_bytes;
-      c.meta_of[q][(size_t)mb * c.cap + row] = make_int2(s, t * c.K + lane);
+      if (part == 0) c.meta_of[q][(size_t)mb * c.cap + row] = make_int2(s, t * c.K + lane);
     }
     const char* src = reinterpret_cast<const char*>(x + (size_t)t * c.H) + lane * 16;
+    const int j_end = min(nchunk, (part + 1) * per_part);
     constexpr int U = 8;
-    for (int j0 = 0; j0 < nchunk; j0 += U) {
+    for (int j0 = part * per_part; j0 < j_end; j0 += U) {
       uint4 v[U];
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (j0 + u < nchunk) v[u] = ld_nc_v4(src + (size_t)(j0 + u) * 512);
+        if (j0 + u < j_end) v[u] = ld_nc_v4(src + (size_t)(j0 + u) * 512);
       for (int k = 0; k < c.K; ++k) {
         char* d = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(my_dst), k)) + lane * 16;
 #pragma unroll
         for (int u = 0; u < U; ++u)
-          if (j0 + u < nchunk) st_v4(d + (size_t)(j0 + u) * 512, v[u]);
+          if (j0 + u < j_end) st_v4(d + (size_t)(j0 + u) * 512, v[u]);
       }
     }
   }
@@ -508,9 +514,8 @@ extern "C" int msi_dispatch(msi_ctx* c, const void* x, const int32_t* cnt, const
   MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots && epoch >= 1, "msi_dispatch: bad slot/epoch");
   MSI_REQUIRE(x && cnt && idx && slot, "msi_dispatch: null pointer");
   const size_t smem = sizeof(long long) * c->plan.experts;
-  // enough warps to keep ~4 rows in flight per SM, at most one CTA per SM
-  int grid = (T + (kDispThreads / 32) - 1) / (kDispThreads / 32);
-  grid = grid < 1 ? 1 : (grid > num_sms() ? num_sms() : grid);
+  // one CTA per SM; rows are split into parts so every warp has work
+  const int grid = num_sms();
   dispatch_kernel<<<grid, kDispThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
       c->dev, reinterpret_cast<const __nv_bfloat16*>(x), cnt, idx, slot, T, mb_slot, epoch);
   return check_launch("dispatch_kernel");

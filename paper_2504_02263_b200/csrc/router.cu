@@ -7,10 +7,11 @@
 //      order oracle/msi_oracle.c restates, so routing is bit-exact;
 //   2. top-K per token (warp arg-max, ties to the lower expert), weights =
 //      softmax of the K chosen logits with det_expf (bit-exact as well);
-//   3. per-CTA histogram and in-CTA ranks with a warp ballot/popc prefix
-//      (bit t of mask[e] = token t routed to e; rank = popc(mask & lanes_below));
-//   4. the last CTA to finish (ticket) scans the per-CTA histograms into
-//      per-CTA bases, writes cnt[E], and adds the bases to every slot.
+//   3. the last CTA to finish (ticket) places every (t, k): warps own
+//      contiguous 32-token chunks; in a chunk bit `lane` of mask[e] marks
+//      "token lane chose e", so rank = popc(mask[e] & lanes_below); a count
+//      pass, a scan over warps and a second pass give the final slots and
+//      cnt[E] (warp ballot/popc prefix sums, no global scan).
 // HBM-bound for small E (reads x once); FMA-bound for E = 256 (logits on
 // CUDA cores because the fixed reduction order is the bit-exactness contract).
 #include <cstdio>
@@ -30,14 +31,11 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
                  float* __restrict__ w_out, int32_t* __restrict__ cnt_out,
                  int32_t* __restrict__ slot_out, int32_t* __restrict__ ws) {
   extern __shared__ float s_logit[];                       // [BT][E]
-  uint32_t* s_mask = reinterpret_cast<uint32_t*>(s_logit + BT * E);  // [E]
   __shared__ int s_last;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t0 = blockIdx.x * BT;
   const int nchunk = H >> 8;
-
-  for (int e = threadIdx.x; e < E; e += blockDim.x) s_mask[e] = 0u;
 
   // ---- 1. logits ---------------------------------------------------------
   const int tgroups = BT / TT, egroups = E / TE;
@@ -132,47 +130,64 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
   }
   __syncthreads();
 
-  // ---- 3. per-CTA histogram + in-CTA ranks (warp 0, lane = token) ----------
-  int32_t* blk_hist = ws + 4;  // ws[0] = ticket
-  if (warp == 0) {
-    const int t = t0 + lane;
-    const bool valid = lane < BT && t < T;
-    int myE[32];
-    for (int k = 0; k < K; ++k) {
-      myE[k] = valid ? idx_out[(size_t)t * K + k] : 0;
-      if (valid) atomicOr(&s_mask[myE[k]], 1u << lane);
-    }
-    __syncwarp();
-    const uint32_t below = (1u << lane) - 1u;
-    if (valid)
-      for (int k = 0; k < K; ++k)
-        slot_out[(size_t)t * K + k] = __popc(s_mask[myE[k]] & below);
-    __syncwarp();
-    for (int e = lane; e < E; e += 32) blk_hist[(size_t)blockIdx.x * E + e] = __popc(s_mask[e]);
-  }
-
-  // ---- 4. last CTA: scan histograms, finalize counts and slots ------------
+  // ---- 3. the last CTA to finish places every (t, k) ----------------------
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) s_last = (atomicAdd(&ws[0], 1) == (int)gridDim.x - 1);
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  const int nblk = gridDim.x;
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    int run = 0;
-    for (int b = 0; b < nblk; ++b) {
-      int c = __ldcg(&blk_hist[(size_t)b * E + e]);
-      blk_hist[(size_t)b * E + e] = run;
-      run += c;
+  // Warp w owns a contiguous range of 32-token chunks.  Inside a chunk,
+  // lane = token and bit `lane` of mask[e] says "this token chose e", so the
+  // rank of (t,k) among earlier tokens of the chunk is popc(mask & lanes_below).
+  // Pass 1 counts per (warp, expert); a scan over warps gives each warp its
+  // starting rank; pass 2 walks the chunks again and emits final slots.
+  uint32_t* wmask = reinterpret_cast<uint32_t*>(s_logit) + warp * E;            // [8][E]
+  int32_t* wcnt = reinterpret_cast<int32_t*>(s_logit) + kWarps * E + warp * E;  // [8][E]
+  for (int e = lane; e < E; e += 32) { wmask[e] = 0u; wcnt[e] = 0; }
+  __syncwarp();
+  const int nchunk_t = (T + 31) >> 5;
+  const int c_lo = (nchunk_t * warp) / kWarps, c_hi = (nchunk_t * (warp + 1)) / kWarps;
+  const uint32_t below = (1u << lane) - 1u;
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int ch = c_lo; ch < c_hi; ++ch) {
+      const int t = ch * 32 + lane;
+      const bool valid = t < T;
+      int myE[32];
+      for (int k = 0; k < K; ++k) {
+        myE[k] = valid ? __ldcg(&idx_out[(size_t)t * K + k]) : 0;
+        if (valid) atomicOr(&wmask[myE[k]], 1u << lane);
+      }
+      __syncwarp();
+      if (valid && pass == 1)
+        for (int k = 0; k < K; ++k)
+          slot_out[(size_t)t * K + k] = wcnt[myE[k]] + __popc(wmask[myE[k]] & below);
+      __syncwarp();
+      if (valid)
+        for (int k = 0; k < K; ++k) {
+          const uint32_t mk = wmask[myE[k]];
+          if ((mk >> lane) == 1u) wcnt[myE[k]] += __popc(mk);  // highest lane of e: once per chunk
+        }
+      __syncwarp();
+      if (valid)
+        for (int k = 0; k < K; ++k) wmask[myE[k]] = 0u;
+      __syncwarp();
     }
-    cnt_out[e] = run;
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < T * K; i += blockDim.x) {
-    const int b = (i / K) / BT;
-    const int e = __ldcg(&idx_out[i]);
-    slot_out[i] = __ldcg(&slot_out[i]) + blk_hist[(size_t)b * E + e];
+    __syncthreads();
+    if (pass == 0) {
+      // exclusive scan over warps per expert; totals are the sender's counts
+      int32_t* all = reinterpret_cast<int32_t*>(s_logit) + kWarps * E;
+      for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        int run = 0;
+        for (int w = 0; w < kWarps; ++w) {
+          const int c = all[w * E + e];
+          all[w * E + e] = run;
+          run += c;
+        }
+        cnt_out[e] = run;
+      }
+      __syncthreads();
+    }
   }
   if (threadIdx.x == 0) ws[0] = 0;  // ticket ready for the next launch
 }
@@ -181,7 +196,8 @@ template <int TT, int TE>
 int launch(const void* x, const void* wg, int T, int H, int E, int K, int BT, int32_t* idx,
            float* w, int32_t* cnt, int32_t* slot, void* ws, cudaStream_t st) {
   const int nblk = (T + BT - 1) / BT;
-  const size_t smem = (size_t)BT * E * sizeof(float) + (size_t)E * sizeof(uint32_t);
+  // logits [BT][E] during routing; [8][E] masks + [8][E] counts in the last CTA
+  const size_t smem = (size_t)(BT > 2 * kWarps ? BT : 2 * kWarps) * E * sizeof(float) + (size_t)E * sizeof(uint32_t);
   auto kern = gate_topk_kernel<TT, TE>;
   if (smem > 48 * 1024) MSI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<nblk, kWarps * 32, smem, st>>>(reinterpret_cast<const __nv_bfloat16*>(x),
@@ -213,8 +229,9 @@ int gate_topk(const void* x, const void* wg, int T, int H, int E, int K, int32_t
 }
 
 size_t gate_topk_workspace(int T, int E) {
-  const int nblk = (T + 3) / 4;  // smallest BT used above
-  return 16 + (size_t)nblk * E * sizeof(int32_t);
+  (void)T;
+  (void)E;
+  return 16;  // the last-CTA ticket
 }
 
 }  // namespace msi

@@ -1,0 +1,137 @@
+"""Multi-GPU parity: n_a attention GPUs -> n_e expert GPUs over NVLink peer
+memory (one process per GPU), checked against the oracle's multi-sender
+layer: routing / counts / placement bit-exact on every rank, expert outputs
+and layer outputs within tolerance, combine bit-exact given the GPU's own
+expert outputs.  Skipped when the box has fewer GPUs than the plan needs.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n_a, n_e, shape, tokens, m, layers, outdir):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    from oracle import oracle as O
+    from paper_2504_02263_b200 import ops, runtime
+    from paper_2504_02263_b200.config import DeploymentPlan, as_model_spec
+
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    model = as_model_spec(shape)
+    plan = DeploymentPlan(n_a=n_a, n_e=n_e, m=m, b_a=max(tokens))
+    g = runtime.M2NGroup(model, plan, rank=rank, device=f"cuda:{rank}", timeout_s=30)
+    wts = O.synth_weights(model.hidden, model.intermediate, model.experts, seed=0)
+
+    def dev(a):
+        return torch.from_numpy(np.ascontiguousarray(a).view(np.int16).copy()).view(torch.bfloat16).cuda()
+
+    w13 = w2 = wg = None
+    if g.is_expert:
+        ex = list(runtime.local_experts(g))
+        w13 = ops.pack_w13(dev(wts.w_gate[ex]), dev(wts.w_up[ex]))
+        w2 = dev(wts.w_down[ex])
+    if g.is_attention:
+        wg = dev(wts.wg)
+    layer = runtime.MoEDecodeLayer(g, wg=wg, w13=w13, w2=w2)
+    res = {}
+    for l in range(layers):
+        for j in range(m):
+            if g.is_attention:
+                s = g.attn_index
+                x = O.synth_tokens(tokens[s], model.hidden, seed=1000 * l + 10 * j + s)
+                xd = dev(x)
+                r = layer.router(xd, j)
+                layer.dispatch(xd, r, j)
+            if g.is_expert:
+                layer.expert_step(j)
+            if g.is_attention:
+                out = layer.combine(r, resid=xd)
+                torch.cuda.synchronize()
+                T = tokens[s]
+                res[f"idx_{l}_{j}"] = r.idx[:T].cpu().numpy()
+                res[f"w_{l}_{j}"] = r.w[:T].cpu().numpy()
+                res[f"cnt_{l}_{j}"] = r.cnt.cpu().numpy()
+                res[f"slot_{l}_{j}"] = r.slot[:T].cpu().numpy()
+                res[f"out_{l}_{j}"] = out.view(torch.int16).cpu().numpy().view(np.uint16)
+                res[f"y_{l}_{j}"] = g.ybuf_view(j)[:T].contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+            if g.is_expert:
+                torch.cuda.synchronize()
+                res[f"recv_{l}_{j}"] = g.recv_view(j).view(torch.int16).cpu().numpy().view(np.uint16)
+                res[f"meta_{l}_{j}"] = g.meta_view(j).cpu().numpy()
+            dist.barrier()
+    res["status"] = np.array([g.status()])
+    np.savez(os.path.join(outdir, f"rank{rank}.npz"), **res)
+    dist.barrier()
+    g.close()
+    dist.destroy_process_group()
+
+
+PLANS = [
+    # (n_a, n_e, shape, tokens per attention rank, m, layers)
+    (1, 1, "tiny", [64], 2, 2),
+    (3, 1, "tiny", [64, 40, 17], 2, 2),
+    (2, 2, "tiny", [48, 64], 2, 2),
+    (6, 2, "tiny", [64, 64, 33, 64, 1, 50], 3, 2),
+]
+
+
+@pytest.mark.parametrize("n_a,n_e,shape,tokens,m,layers", PLANS)
+def test_m2n_multi_gpu(lib, tmp_path, n_a, n_e, shape, tokens, m, layers):
+    import torch.multiprocessing as mp
+
+    from oracle import oracle as O
+    from paper_2504_02263_b200.config import as_model_spec
+
+    world = n_a + n_e
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs, box has {torch.cuda.device_count()}")
+    port = _free_port()
+    mp.spawn(_worker, args=(world, port, n_a, n_e, shape, tokens, m, layers, str(tmp_path)), nprocs=world, join=True)
+    model = as_model_spec(shape)
+    wts = O.synth_weights(model.hidden, model.intermediate, model.experts, seed=0)
+    got = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(world)]
+    for r in range(world):
+        assert got[r]["status"][0] == 0, f"rank {r} device status {got[r]['status']}"
+    E_l = model.experts // n_e
+    from tests.test_gpu_parity import assert_close_bf16
+    for l in range(layers):
+        for j in range(m):
+            xs = [O.synth_tokens(tokens[s], model.hidden, seed=1000 * l + 10 * j + s) for s in range(n_a)]
+            ref = O.moe_layer(xs, wts, model.topk, n_e=n_e, resid=True)
+            for s in range(n_a):
+                a = got[s]
+                np.testing.assert_array_equal(a[f"idx_{l}_{j}"], ref.idx[s])
+                np.testing.assert_array_equal(a[f"w_{l}_{j}"].view(np.uint32), ref.w[s].view(np.uint32))
+                np.testing.assert_array_equal(a[f"cnt_{l}_{j}"], ref.cnt[s])
+                np.testing.assert_array_equal(a[f"slot_{l}_{j}"], ref.slot[s])
+                assert_close_bf16(a[f"y_{l}_{j}"], ref.y[s], f"expert outputs s={s} l={l} j={j}")
+                np.testing.assert_array_equal(a[f"out_{l}_{j}"], O.combine(a[f"y_{l}_{j}"], a[f"w_{l}_{j}"], xs[s]))
+                assert_close_bf16(a[f"out_{l}_{j}"], ref.out[s], f"layer output s={s}")
+                # placement: every (t, k) row landed at the oracle's row on the right GPU
+                q, rows = O.dispatch_rows(ref.idx[s], ref.slot[s], s, ref.layout, E_l)
+                T = tokens[s]
+                for t in range(T):
+                    for k in range(model.topk):
+                        er = got[n_a + q[t, k]]
+                        np.testing.assert_array_equal(er[f"recv_{l}_{j}"][rows[t, k]], xs[s][t])
+                        np.testing.assert_array_equal(er[f"meta_{l}_{j}"][rows[t, k]], [s, t * model.topk + k])
