@@ -1,0 +1,167 @@
+#!/usr/bin/env python
+"""M2N dispatch + combine latency / bandwidth vs NCCL (BASELINE config 4).
+
+DBRX-shaped layer (h = 6144, E = 16, K = 4); splits 1 = co-located loopback,
+2 = 1+1, 4 = 2+2, 8 = 4+4 (n_a attention -> n_e expert GPUs).  For each
+micro-batch size b_a the round trip dispatch -> identity expert -> combine
+(msi_dispatch, msi_expert_echo, msi_combine) is timed per iteration with CUDA
+events on every attention GPU (max over them), after a host barrier, for
+--iters iterations; NCCL all_to_all_single moves the identical bytes
+(attention -> expert rows, then the same rows back) under the same protocol.
+This is the paper's M2N comparison on one NVSwitch box.
+
+  torchrun --nproc-per-node N --master-addr 127.0.0.1 bench_m2n.py [--iters 1000]
+Prints one JSON line per size and a summary line (rank 0).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SPLITS = {1: (1, 1, True), 2: (1, 1, False), 4: (2, 2, False), 8: (4, 4, False)}
+
+
+def pct(v, q):
+    v = sorted(v)
+    return v[min(len(v) - 1, int(q * len(v)))]
+
+
+def peer_copy_gbps(dev0: int, dev1: int, nbytes: int = 1 << 30) -> float:
+    import torch
+    a = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{dev0}")
+    b = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{dev1}")
+    for _ in range(3):
+        b.copy_(a)
+    torch.cuda.synchronize(dev0)
+    torch.cuda.synchronize(dev1)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.device(dev0):
+        s.record()
+        for _ in range(10):
+            b.copy_(a)
+        e.record()
+    torch.cuda.synchronize(dev0)
+    torch.cuda.synchronize(dev1)
+    return 10 * nbytes / (s.elapsed_time(e) / 1e3) / 1e9
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--shape", default="dbrx")
+    ap.add_argument("--sizes", default="1,2,4,8,16,32,64,128,256,512,1024")
+    ap.add_argument("--iters", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--no-nccl", action="store_true")
+    args = ap.parse_args()
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2504_02263_b200 import runtime
+    from paper_2504_02263_b200.config import DeploymentPlan, as_model_spec
+
+    rank, world, local = runtime.init_distributed_from_env("nccl")
+    n_a, n_e, colo = SPLITS[world]
+    model = as_model_spec(args.shape)
+    H, K, E = model.hidden, model.topk, model.experts
+    sizes = [int(s) for s in args.sizes.split(",")]
+    plan = DeploymentPlan(n_a=n_a, n_e=n_e, m=1, b_a=max(sizes), colocated=colo)
+    dev = torch.device(f"cuda:{local}")
+    g = runtime.M2NGroup(model, plan, rank=rank, device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(7)
+    wg = (torch.randn((E, H), generator=gen, device=dev) / H ** 0.5).to(torch.bfloat16) if g.is_attention else None
+    layer = runtime.MoEDecodeLayer(g, wg=wg)
+    peak = None
+    if rank == 0 and world > 1:
+        peak = peer_copy_gbps(local, (local + 1) % torch.cuda.device_count())
+    results = []
+    for T in sizes:
+        x = torch.randn((T, H), generator=gen, device=dev).to(torch.bfloat16) if g.is_attention else None
+        route = layer.router(x, 0) if g.is_attention else None
+        # rows this attention GPU sends to each expert GPU (for NCCL splits / bytes)
+        cnt_q = torch.zeros(world, dtype=torch.int64, device=dev)
+        if g.is_attention:
+            per_e = route.cnt.to(torch.int64)
+            for q, r in enumerate(plan.expert_ranks()):
+                cnt_q[r] += per_e[q * g.E_l:(q + 1) * g.E_l].sum()
+        all_cnt = [torch.zeros_like(cnt_q) for _ in range(world)] if world > 1 else [cnt_q]
+        if world > 1:
+            dist.all_gather(all_cnt, cnt_q)
+        mat = torch.stack(all_cnt).cpu()  # [src, dst] rows
+        ingress = int(mat.sum(0).max()) * H * 2  # busiest receiver, one way
+        out = torch.empty((T, H), dtype=torch.bfloat16, device=dev) if g.is_attention else None
+
+        def ours():
+            if g.is_attention:
+                layer.dispatch(x, route, 0)
+            if g.is_expert:
+                layer.expert_echo(0)
+            if g.is_attention:
+                layer.combine(route, out=out)
+
+        def bench(fn, iters, warm):
+            lat = []
+            for i in range(warm + iters):
+                if world > 1:
+                    dist.barrier()
+                torch.cuda.synchronize()
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                fn()
+                e.record()
+                torch.cuda.synchronize()
+                if i >= warm:
+                    lat.append(s.elapsed_time(e) * 1e3 if g.is_attention else 0.0)
+            t = torch.tensor(lat, dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return t.cpu().tolist()
+
+        lat = bench(ours, args.iters, args.warmup)
+        rec = {"T": T, "pair_bytes_avg": T * K / n_e * H * 2 if not colo else T * K * H * 2,
+               "ingress_bytes_busiest": ingress,
+               "ours_p50_us": pct(lat, 0.5), "ours_p99_us": pct(lat, 0.99)}
+        rec["ours_gbps_one_way"] = ingress / (rec["ours_p50_us"] / 2 * 1e-6) / 1e9
+        if not args.no_nccl and world > 1:
+            send_split = [int(mat[rank, d]) * H for d in range(world)]
+            recv_split = [int(mat[s_, rank]) * H for s_ in range(world)]
+            sbuf = torch.randn(max(sum(send_split), 1), device=dev).to(torch.bfloat16)
+            rbuf = torch.empty(max(sum(recv_split), 1), dtype=torch.bfloat16, device=dev)
+            back = torch.empty_like(sbuf)
+
+            def nccl():
+                dist.all_to_all_single(rbuf[:sum(recv_split)], sbuf[:sum(send_split)], recv_split, send_split)
+                dist.all_to_all_single(back[:sum(send_split)], rbuf[:sum(recv_split)], send_split, recv_split)
+
+            nl = bench(nccl, min(args.iters, 500), 20)
+            rec["nccl_p50_us"] = pct(nl, 0.5)
+            rec["nccl_p99_us"] = pct(nl, 0.99)
+            rec["speedup_p50"] = rec["nccl_p50_us"] / rec["ours_p50_us"]
+        results.append(rec)
+        if rank == 0:
+            print(json.dumps(rec), flush=True)
+    st = g.status()
+    if rank == 0:
+        summary = {"metric": "M2N dispatch+combine p50 µs", "n_gpus": world, "split": f"{n_a}+{n_e}" if not colo else "co-located",
+                   "shape": model.name, "hidden": H, "experts": E, "topk": K,
+                   "peer_copy_gbps_measured": peak, "nvlink_nominal_gbps": 900.0,
+                   "status": st, "sizes": results}
+        big = results[-1]
+        summary["largest"] = {"T": big["T"], "gbps_one_way": big["ours_gbps_one_way"],
+                              "frac_nvlink_nominal": big["ours_gbps_one_way"] / 900.0,
+                              "frac_peer_copy": (big["ours_gbps_one_way"] / peak) if peak else None}
+        print(json.dumps(summary), flush=True)
+    g.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

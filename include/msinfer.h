@@ -133,6 +133,12 @@ int msi_dispatch(msi_ctx* ctx, const void* x, const int32_t* cnt,
 int msi_expert_ffn(msi_ctx* ctx, const void* w13, const void* w2, int mb_slot,
                    uint32_t epoch, void* stream);
 
+/* Identity expert (M2N measurement): waits like msi_expert_ffn, then returns
+ * every received row unchanged to its sender's combine buffer (the N2M leg
+ * without the FFN), and releases the same counters.  dispatch + echo + combine
+ * is the pure M2N round trip of PAPER.md §5's latency/throughput figures. */
+int msi_expert_echo(msi_ctx* ctx, int mb_slot, uint32_t epoch, void* stream);
+
 /* ---- (3) combine: waits for all expert GPUs, then
  * out[t] = bf16(resid[t] + sum_k w[t,k] * y[t,k]) (fp32 fmaf, ascending k;
  * resid may be NULL). */

@@ -267,6 +267,71 @@ dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32
   }
 }
 
+// ---------------------------------------------------------------- echo ----
+// Identity expert: returns every received row to its sender's combine buffer
+// (the N2M leg without the FFN), so dispatch + echo + combine times the pure
+// M2N round trip.  Same waits, metadata, segment layout and signals as the
+// real expert step.
+constexpr int kEchoThreads = 512;
+
+__global__ void __launch_bounds__(kEchoThreads)
+echo_kernel(const DevCtx c, int mb, uint32_t epoch) {
+  __shared__ int s_ok, s_last;
+  __shared__ long long s_start[MSI_MAX_LOCAL_EXPERTS], s_total[MSI_MAX_LOCAL_EXPERTS];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t* arrive = c.my_arrive + mb * CTR_STRIDE;
+  if (tid == 0) s_ok = wait_geq(arrive, epoch * (uint32_t)c.n_a, c.timeout_ns, c.my_status);
+  __syncthreads();
+  if (!s_ok) return;
+  const size_t tab = (size_t)mb * c.n_a * c.E;
+  if (tid < c.E_l) {  // segment table: total[e] and the 128-aligned start[e]
+    long long tot = 0;
+    for (int s = 0; s < c.n_a; ++s)
+      tot += (uint32_t)ld_relaxed_sys64(c.my_cntab + tab + (size_t)s * c.E + c.my_e * c.E_l + tid);
+    s_total[tid] = tot;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    long long run = 0;
+    for (int el = 0; el < c.E_l; ++el) {
+      s_start[el] = run;
+      run += (s_total[el] + MSI_ROW_ALIGN - 1) / MSI_ROW_ALIGN * MSI_ROW_ALIGN;
+    }
+  }
+  __syncthreads();
+  const int gwarp = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  const size_t row_bytes = (size_t)c.H * 2;
+  const int nchunk = c.H >> 8;
+  for (int el = 0; el < c.E_l; ++el) {
+    for (long long r = gwarp; r < s_total[el]; r += nwarps) {
+      const long long row = s_start[el] + r;
+      const int2 md = c.meta_of[c.my_e][(size_t)mb * c.cap + row];
+      const char* src = c.recv_of[c.my_e] + ((size_t)mb * c.cap + row) * row_bytes + lane * 16;
+      char* dst = c.ybuf_of[md.x] + (size_t)mb * c.max_tokens * c.K * row_bytes + (size_t)md.y * row_bytes + lane * 16;
+      for (int j = 0; j < nchunk; j += 8) {
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (j + u < nchunk) v[u] = __ldcg(reinterpret_cast<const uint4*>(src + (size_t)(j + u) * 512));
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (j + u < nchunk) st_v4(dst + (size_t)(j + u) * 512, v[u]);
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence_system();
+    s_last = atomicAdd(c.my_fticket + mb * CTR_STRIDE, 1u) == gridDim.x - 1;
+    if (s_last) {
+      c.my_fticket[mb * CTR_STRIDE] = 0;
+      fence_sys();
+      for (int s = 0; s < c.n_a; ++s) red_release_sys_add(c.comb_of[s] + mb * CTR_STRIDE, 1u);
+    }
+  }
+}
+
 // ------------------------------------------------------------- combine ----
 __device__ __forceinline__ void combine_row8(const char* ybase, const float* w, const uint16_t* resid,
                                              uint16_t* out, int t, int col8, int K, int H) {
@@ -577,6 +642,14 @@ extern "C" int msi_expert_ffn(msi_ctx* c, const void* w13, const void* w2, int m
   for (int s = 0; s < p.n_a; ++s) g2.p.sig[s] = d.comb_of[s] + mb_slot * CTR_STRIDE;
   g2.p.n_sig = p.n_a;
   return grouped_gemm_launch(g2, st);
+}
+
+extern "C" int msi_expert_echo(msi_ctx* c, int mb_slot, uint32_t epoch, void* stream) {
+  if (!c || !c->finalized) { set_error("msi_expert_echo: context not finalized"); return MSI_ESTATE; }
+  if (!c->expert) { set_error("msi_expert_echo: rank %d has no expert role", c->rank); return MSI_EINVAL; }
+  MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots && epoch >= 1, "msi_expert_echo: bad slot/epoch");
+  echo_kernel<<<num_sms(), kEchoThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(c->dev, mb_slot, epoch);
+  return check_launch("echo_kernel");
 }
 
 extern "C" int msi_combine(msi_ctx* c, void* out, const float* w, const void* resid, int T, int mb_slot,

@@ -189,7 +189,8 @@ class MoEDecodeLayer:
         if group.is_attention:
             if wg is None or tuple(wg.shape) != (m.experts, m.hidden):
                 raise ValueError("attention ranks need wg [E, H]")
-        if group.is_expert:
+        if group.is_expert and (w13 is not None or w2 is not None):
+            # (weights may be omitted on an expert rank that only runs expert_echo)
             E_l = group.E_l
             if w13 is None or tuple(w13.shape) != (E_l, 2 * m.intermediate, m.hidden):
                 raise ValueError(f"expert ranks need w13 [{E_l}, {2 * m.intermediate}, {m.hidden}]")
@@ -232,9 +233,17 @@ class MoEDecodeLayer:
 
     # -- (2) expert FFN -------------------------------------------------------
     def expert_step(self, mb: int = 0, stream=None) -> int:
+        if self.w13 is None or self.w2 is None:
+            raise ValueError("expert_step needs w13/w2 on this expert rank")
         self.epoch_e[mb] += 1
         _lib.call("msi_expert_ffn", self.g.ctx, ops._ptr(self.w13), ops._ptr(self.w2), mb,
                   self.epoch_e[mb], ops._stream(stream))
+        return self.epoch_e[mb]
+
+    def expert_echo(self, mb: int = 0, stream=None) -> int:
+        """Identity expert: the N2M leg without the FFN (M2N measurements)."""
+        self.epoch_e[mb] += 1
+        _lib.call("msi_expert_echo", self.g.ctx, mb, self.epoch_e[mb], ops._stream(stream))
         return self.epoch_e[mb]
 
     # -- (3) N2M combine ------------------------------------------------------

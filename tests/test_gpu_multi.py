@@ -113,7 +113,7 @@ def test_m2n_multi_gpu(lib, tmp_path, n_a, n_e, shape, tokens, m, layers):
     for r in range(world):
         assert got[r]["status"][0] == 0, f"rank {r} device status {got[r]['status']}"
     E_l = model.experts // n_e
-    from tests.test_gpu_parity import assert_close_bf16
+    from _util import assert_close_bf16
     for l in range(layers):
         for j in range(m):
             xs = [O.synth_tokens(tokens[s], model.hidden, seed=1000 * l + 10 * j + s) for s in range(n_a)]

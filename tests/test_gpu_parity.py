@@ -16,8 +16,7 @@ torch = pytest.importorskip("torch")
 
 from oracle import oracle as O  # noqa: E402
 
-REL_L2 = 5e-3
-MAX_ABS_FRAC = 2.0 ** -7
+from _util import assert_close_bf16  # noqa: E402
 
 
 def to_dev(a_u16: np.ndarray) -> "torch.Tensor":
@@ -26,16 +25,6 @@ def to_dev(a_u16: np.ndarray) -> "torch.Tensor":
 
 def to_host(t) -> np.ndarray:
     return t.detach().contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
-
-
-def assert_close_bf16(got_u16, ref_u16, what=""):
-    g = O.bf16_to_f32(got_u16).astype(np.float64)
-    r = O.bf16_to_f32(ref_u16).astype(np.float64)
-    assert np.isfinite(g).all(), f"{what}: non-finite output"
-    rel = np.linalg.norm(g - r) / max(np.linalg.norm(r), 1e-30)
-    mx = np.abs(g - r).max() if g.size else 0.0
-    assert rel <= REL_L2, f"{what}: rel-L2 {rel:.3e} > {REL_L2}"
-    assert mx <= MAX_ABS_FRAC * max(np.abs(r).max(), 1e-30), f"{what}: max-abs {mx:.3e}"
 
 
 # ------------------------------------------------------------------ router --
@@ -269,4 +258,29 @@ def test_pingpong_runner_colocated(lib):
         for _ in range(3):
             cur = O.moe_layer([cur], wts, model.topk, n_e=1, resid=True).out[0]
         assert_close_bf16(to_host(xs[j]), cur, f"mb {j} after 3 layers")
+    g.close()
+
+
+def test_echo_round_trip_bit_exact(lib):
+    """dispatch -> identity expert -> combine returns every row to its (t, k)
+    slot: out = combine(y = x per k) exactly (pure M2N path)."""
+    from paper_2504_02263_b200 import runtime
+    from paper_2504_02263_b200.config import DeploymentPlan, as_model_spec
+
+    model = as_model_spec("dbrx")
+    g = runtime.M2NGroup(model, DeploymentPlan(n_a=1, n_e=1, m=2, b_a=40, colocated=True), rank=0)
+    wg = O.synth_weights(model.hidden, 128, model.experts, experts=[]).wg
+    layer = runtime.MoEDecodeLayer(g, wg=to_dev(wg))
+    for j, T in enumerate((40, 13)):
+        x = O.synth_tokens(T, model.hidden, seed=30 + j)
+        xd = to_dev(x)
+        r = layer.router(xd, j)
+        layer.dispatch(xd, r, j)
+        layer.expert_echo(j)
+        out = layer.combine(r)
+        torch.cuda.synchronize()
+        y = np.repeat(x[:, None, :], model.topk, axis=1)
+        np.testing.assert_array_equal(to_host(g.ybuf_view(j)[:T]), y)
+        np.testing.assert_array_equal(to_host(out), O.combine(y, r.w[:T].cpu().numpy()))
+    assert g.status() == 0
     g.close()
