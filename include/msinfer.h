@@ -119,7 +119,11 @@ int msi_gate_topk(const void* x, const void* wg, int T, int H, int E, int K,
  * row x[t] into the expert GPUs' receive buffers over NVLink peer memory at
  * row seg_start[e] + sum_{s'<s} cnt[s'][e] + slot[t,k], with its (s, t*K+k)
  * metadata, and releases the receivers' arrival counters.  `epoch` counts the
- * uses of `mb_slot` from 1. */
+ * uses of `mb_slot` from 1; epoch 0 means "the slot's next use" as counted on
+ * the device (msi_dispatch/msi_combine: attention side; msi_expert_ffn /
+ * msi_expert_echo: expert side), which makes a whole step capturable in a CUDA
+ * graph.  Explicit and device epochs may be mixed: every call records the
+ * epoch it used. */
 int msi_dispatch(msi_ctx* ctx, const void* x, const int32_t* cnt,
                  const int32_t* idx, const int32_t* slot, int T, int mb_slot,
                  uint32_t epoch, void* stream);

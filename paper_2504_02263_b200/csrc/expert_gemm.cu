@@ -76,11 +76,13 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   __shared__ int s_last;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t epoch = p.epoch;
+  if (epoch == 0 && p.epoch_src) epoch = *(volatile const uint32_t*)p.epoch_src + 1u;
 
   // ---- wait for the senders' rows (GEMM1 on an expert GPU) ----------------
   if (threadIdx.x == 0) {
     bool ok = true;
-    if (p.wait_ctr) ok = wait_geq(p.wait_ctr, p.wait_target, p.timeout_ns, p.status);
+    if (p.wait_ctr) ok = wait_geq(p.wait_ctr, epoch * p.wait_mul, p.timeout_ns, p.status);
     if (!ok) p.status[1] = 1;
     fence_proxy_async_global();  // rows written by peers are read by TMA (async proxy)
   }
@@ -274,6 +276,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     s_last = (atomicAdd(p.ticket, 1u) == gridDim.x - 1);
     if (s_last) {
       *p.ticket = 0;
+      if (p.epoch_store) *p.epoch_store = epoch;
       fence_sys();
       for (int i = 0; i < p.n_sig; ++i) red_release_sys_add(p.sig[i], 1u);
     }

@@ -22,7 +22,10 @@ struct GemmParams {
   int n_a, E, e0;           // e0 = first global expert of this GPU
   // optional wait before any load (GEMM1 on an expert GPU)
   const uint32_t* wait_ctr;
-  uint32_t wait_target;
+  uint32_t epoch;             // 0: read *epoch_src + 1 on the device
+  const uint32_t* epoch_src;  // this slot's expert-side use counter
+  uint32_t wait_mul;          // wait for *wait_ctr >= epoch * wait_mul
+  uint32_t* epoch_store;      // optional: last CTA stores the epoch (use done)
   uint64_t timeout_ns;
   int32_t* status;          // [0] = error code, [1] = abort flag
   unsigned long long* stats;  // optional: [0] += rows processed, [1] += 1 (one CTA)

@@ -17,6 +17,10 @@
 //            arrive[slot]  (expert role)    dispatch arrivals, +1 per sender
 //            comb[slot]    (attention role) combine arrivals, +1 per expert GPU
 //            dticket[slot], fticket[slot]   last-CTA tickets (local)
+//            ause[slot], euse[slot]         uses of each slot so far (attention /
+//                                           expert side): epoch 0 in the ABI means
+//                                           "next use", read on the device, so a
+//                                           whole step can be captured in a CUDA graph
 //            status[2]                      device error word + abort flag
 //            stats[2] u64                   rows through the expert FFN, FFN calls
 //            cntab[slot][n_a][E] u64        (epoch << 32 | count), all-gathered
@@ -61,7 +65,7 @@ constexpr size_t ALIGN = 4096;
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Layout {
-  size_t arrive, comb, dticket, fticket, status, stats, cntab, ctrl_bytes;
+  size_t arrive, comb, dticket, fticket, ause, euse, status, stats, cntab, ctrl_bytes;
   size_t ybuf, ybuf_slot;
   size_t recv, recv_slot, meta, meta_slot;
   size_t total;
@@ -76,6 +80,8 @@ Layout make_layout(const msi_plan& p, bool attn, bool expert) {
   L.comb = off; off += p.slots * line;
   L.dticket = off; off += p.slots * line;
   L.fticket = off; off += p.slots * line;
+  L.ause = off; off += p.slots * line;
+  L.euse = off; off += p.slots * line;
   L.status = off; off += line;
   L.stats = off; off += line;
   L.cntab = off; off += (size_t)p.slots * p.n_a * p.experts * 8;
@@ -111,7 +117,7 @@ struct DevCtx {
   uint32_t* comb_of[MSI_MAX_RANKS];    // per attention index s
   char* ybuf_of[MSI_MAX_RANKS];        // per attention index s
   uint64_t* my_cntab;
-  uint32_t *my_arrive, *my_comb, *my_dticket, *my_fticket;
+  uint32_t *my_arrive, *my_comb, *my_dticket, *my_fticket, *my_ause, *my_euse;
   int32_t* my_status;
 };
 
@@ -171,6 +177,7 @@ dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32
   extern __shared__ long long s_rowbase[];  // [E] first row of this sender in expert e's segment
   __shared__ int s_abort;
   const int tid = threadIdx.x;
+  if (epoch == 0) epoch = *(volatile uint32_t*)(c.my_ause + mb * CTR_STRIDE) + 1u;  // device-tracked
   const int s = c.my_a;
   const size_t tab = (size_t)mb * c.n_a * c.E;
 
@@ -261,6 +268,7 @@ dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32
     const uint32_t old = atomicAdd(c.my_dticket + mb * CTR_STRIDE, 1u);
     if (old == gridDim.x - 1) {
       c.my_dticket[mb * CTR_STRIDE] = 0;
+      c.my_ause[mb * CTR_STRIDE] = epoch;  // every CTA has read the old value
       fence_sys();
       for (int q = 0; q < c.n_e; ++q) red_release_sys_add(c.arrive_of[q] + mb * CTR_STRIDE, 1u);
     }
@@ -280,6 +288,7 @@ echo_kernel(const DevCtx c, int mb, uint32_t epoch) {
   __shared__ long long s_start[MSI_MAX_LOCAL_EXPERTS], s_total[MSI_MAX_LOCAL_EXPERTS];
   const int tid = threadIdx.x, lane = tid & 31;
   const uint32_t* arrive = c.my_arrive + mb * CTR_STRIDE;
+  if (epoch == 0) epoch = *(volatile uint32_t*)(c.my_euse + mb * CTR_STRIDE) + 1u;
   if (tid == 0) s_ok = wait_geq(arrive, epoch * (uint32_t)c.n_a, c.timeout_ns, c.my_status);
   __syncthreads();
   if (!s_ok) return;
@@ -326,6 +335,7 @@ echo_kernel(const DevCtx c, int mb, uint32_t epoch) {
     s_last = atomicAdd(c.my_fticket + mb * CTR_STRIDE, 1u) == gridDim.x - 1;
     if (s_last) {
       c.my_fticket[mb * CTR_STRIDE] = 0;
+      c.my_euse[mb * CTR_STRIDE] = epoch;
       fence_sys();
       for (int s = 0; s < c.n_a; ++s) red_release_sys_add(c.comb_of[s] + mb * CTR_STRIDE, 1u);
     }
@@ -360,10 +370,12 @@ __device__ __forceinline__ void combine_row8(const char* ybase, const float* w, 
 __global__ void __launch_bounds__(256)
 combine_kernel(const char* __restrict__ ybase, const float* __restrict__ w, const uint16_t* __restrict__ resid,
                uint16_t* __restrict__ out, int T, int K, int H, const uint32_t* wait_ctr,
-               uint32_t target, uint64_t timeout_ns, int32_t* status) {
+               uint32_t epoch, uint32_t mul, const uint32_t* epoch_src, uint64_t timeout_ns,
+               int32_t* status) {
   __shared__ int s_ok;
   if (wait_ctr) {
-    if (threadIdx.x == 0) s_ok = wait_geq(wait_ctr, target, timeout_ns, status);
+    if (epoch == 0) epoch = *(volatile const uint32_t*)epoch_src;  // set by this slot's dispatch
+    if (threadIdx.x == 0) s_ok = wait_geq(wait_ctr, epoch * mul, timeout_ns, status);
     __syncthreads();
     if (!s_ok) return;
   }
@@ -510,6 +522,8 @@ extern "C" int msi_ctx_finalize(msi_ctx* c) {
   d.my_comb = reinterpret_cast<uint32_t*>(c->heap + M.comb);
   d.my_dticket = reinterpret_cast<uint32_t*>(c->heap + M.dticket);
   d.my_fticket = reinterpret_cast<uint32_t*>(c->heap + M.fticket);
+  d.my_ause = reinterpret_cast<uint32_t*>(c->heap + M.ause);
+  d.my_euse = reinterpret_cast<uint32_t*>(c->heap + M.euse);
   d.my_status = reinterpret_cast<int32_t*>(c->heap + M.status);
   MSI_CUDA(cudaMemset(c->heap, 0, M.ctrl_bytes));
   MSI_CUDA(cudaDeviceSynchronize());
@@ -576,7 +590,7 @@ extern "C" int msi_dispatch(msi_ctx* c, const void* x, const int32_t* cnt, const
   if (!c || !c->finalized) { set_error("msi_dispatch: context not finalized"); return MSI_ESTATE; }
   if (!c->attn) { set_error("msi_dispatch: rank %d has no attention role", c->rank); return MSI_EINVAL; }
   MSI_REQUIRE(T >= 0 && T <= c->plan.max_tokens, "msi_dispatch: T=%d exceeds max_tokens=%d", T, c->plan.max_tokens);
-  MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots && epoch >= 1, "msi_dispatch: bad slot/epoch");
+  MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots && epoch != 0xffffffffu, "msi_dispatch: bad slot/epoch");
   MSI_REQUIRE(x && cnt && idx && slot, "msi_dispatch: null pointer");
   const size_t smem = sizeof(long long) * c->plan.experts;
   // one CTA per SM; rows are split into parts so every warp has work
@@ -590,7 +604,7 @@ extern "C" int msi_expert_ffn(msi_ctx* c, const void* w13, const void* w2, int m
                               uint32_t epoch, void* stream) {
   if (!c || !c->finalized) { set_error("msi_expert_ffn: context not finalized"); return MSI_ESTATE; }
   if (!c->expert) { set_error("msi_expert_ffn: rank %d has no expert role", c->rank); return MSI_EINVAL; }
-  MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots && epoch >= 1, "msi_expert_ffn: bad slot/epoch");
+  MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots , "msi_expert_ffn: bad slot");
   MSI_REQUIRE(w13 && w2, "msi_expert_ffn: null weights");
   const msi_plan& p = c->plan;
   const DevCtx& d = c->dev;
@@ -611,7 +625,9 @@ extern "C" int msi_expert_ffn(msi_ctx* c, const void* w13, const void* w2, int m
   g1.p.E = p.experts;
   g1.p.e0 = c->my_e * d.E_l;
   g1.p.wait_ctr = d.my_arrive + mb_slot * CTR_STRIDE;
-  g1.p.wait_target = epoch * (uint32_t)p.n_a;
+  g1.p.epoch = epoch;  // 0: device-tracked (euse + 1)
+  g1.p.epoch_src = d.my_euse + mb_slot * CTR_STRIDE;
+  g1.p.wait_mul = (uint32_t)p.n_a;
   g1.p.timeout_ns = c->timeout_ns;
   g1.p.status = d.my_status;
   g1.p.stats = reinterpret_cast<unsigned long long*>(c->heap + L.stats);
@@ -641,13 +657,16 @@ extern "C" int msi_expert_ffn(msi_ctx* c, const void* w13, const void* w2, int m
   g2.p.ticket = d.my_fticket + mb_slot * CTR_STRIDE;
   for (int s = 0; s < p.n_a; ++s) g2.p.sig[s] = d.comb_of[s] + mb_slot * CTR_STRIDE;
   g2.p.n_sig = p.n_a;
+  g2.p.epoch = epoch;
+  g2.p.epoch_src = d.my_euse + mb_slot * CTR_STRIDE;
+  g2.p.epoch_store = d.my_euse + mb_slot * CTR_STRIDE;  // last CTA: this use is done
   return grouped_gemm_launch(g2, st);
 }
 
 extern "C" int msi_expert_echo(msi_ctx* c, int mb_slot, uint32_t epoch, void* stream) {
   if (!c || !c->finalized) { set_error("msi_expert_echo: context not finalized"); return MSI_ESTATE; }
   if (!c->expert) { set_error("msi_expert_echo: rank %d has no expert role", c->rank); return MSI_EINVAL; }
-  MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots && epoch >= 1, "msi_expert_echo: bad slot/epoch");
+  MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots , "msi_expert_echo: bad slot");
   echo_kernel<<<num_sms(), kEchoThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(c->dev, mb_slot, epoch);
   return check_launch("echo_kernel");
 }
@@ -657,7 +676,7 @@ extern "C" int msi_combine(msi_ctx* c, void* out, const float* w, const void* re
   if (!c || !c->finalized) { set_error("msi_combine: context not finalized"); return MSI_ESTATE; }
   if (!c->attn) { set_error("msi_combine: rank %d has no attention role", c->rank); return MSI_EINVAL; }
   MSI_REQUIRE(T >= 0 && T <= c->plan.max_tokens, "msi_combine: T out of range");
-  MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots && epoch >= 1, "msi_combine: bad slot/epoch");
+  MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots , "msi_combine: bad slot");
   MSI_REQUIRE(out && w, "msi_combine: null pointer");
   const msi_plan& p = c->plan;
   const Layout& L = c->my_layout;
@@ -667,7 +686,7 @@ extern "C" int msi_combine(msi_ctx* c, void* out, const float* w, const void* re
   combine_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       c->heap + L.ybuf + mb_slot * L.ybuf_slot, w, reinterpret_cast<const uint16_t*>(resid),
       reinterpret_cast<uint16_t*>(out), T, p.topk, p.hidden, c->dev.my_comb + mb_slot * CTR_STRIDE,
-      epoch * (uint32_t)p.n_e, c->timeout_ns, c->dev.my_status);
+      epoch, (uint32_t)p.n_e, c->dev.my_ause + mb_slot * CTR_STRIDE, c->timeout_ns, c->dev.my_status);
   return check_launch("combine_kernel");
 }
 
@@ -680,7 +699,7 @@ extern "C" int msi_combine_local(const void* y, const float* w, const void* resi
   grid = grid > 4 * num_sms() ? 4 * num_sms() : grid;
   combine_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const char*>(y), w, reinterpret_cast<const uint16_t*>(resid),
-      reinterpret_cast<uint16_t*>(out), T, K, H, nullptr, 0, 0, nullptr);
+      reinterpret_cast<uint16_t*>(out), T, K, H, nullptr, 0, 0, nullptr, 0, nullptr);
   return check_launch("combine_kernel");
 }
 

@@ -197,6 +197,9 @@ class MoEDecodeLayer:
             if w2 is None or tuple(w2.shape) != (E_l, m.hidden, m.intermediate):
                 raise ValueError(f"expert ranks need w2 [{E_l}, {m.hidden}, {m.intermediate}]")
         self.wg, self.w13, self.w2 = wg, w13, w2
+        # epochs: host-counted uses of each slot (passed explicitly), or 0 =
+        # "next use" counted on the device (required inside CUDA graphs)
+        self.device_epochs = False
         self.epoch_a = [0] * group.plan.m   # uses of each slot (attention side)
         self.epoch_e = [0] * group.plan.m   # uses of each slot (expert side)
         self._routes = []
@@ -226,7 +229,7 @@ class MoEDecodeLayer:
     def dispatch(self, x: torch.Tensor, route: Route, mb: int | None = None, stream=None) -> Route:
         mb = route.mb if mb is None else mb
         self.epoch_a[mb] += 1
-        route.mb, route.epoch = mb, self.epoch_a[mb]
+        route.mb, route.epoch = mb, (0 if self.device_epochs else self.epoch_a[mb])
         _lib.call("msi_dispatch", self.g.ctx, ops._ptr(x), ops._ptr(route.cnt), ops._ptr(route.idx),
                   ops._ptr(route.slot), route.T, mb, route.epoch, ops._stream(stream))
         return route
@@ -237,13 +240,14 @@ class MoEDecodeLayer:
             raise ValueError("expert_step needs w13/w2 on this expert rank")
         self.epoch_e[mb] += 1
         _lib.call("msi_expert_ffn", self.g.ctx, ops._ptr(self.w13), ops._ptr(self.w2), mb,
-                  self.epoch_e[mb], ops._stream(stream))
+                  0 if self.device_epochs else self.epoch_e[mb], ops._stream(stream))
         return self.epoch_e[mb]
 
     def expert_echo(self, mb: int = 0, stream=None) -> int:
         """Identity expert: the N2M leg without the FFN (M2N measurements)."""
         self.epoch_e[mb] += 1
-        _lib.call("msi_expert_echo", self.g.ctx, mb, self.epoch_e[mb], ops._stream(stream))
+        _lib.call("msi_expert_echo", self.g.ctx, mb, 0 if self.device_epochs else self.epoch_e[mb],
+                  ops._stream(stream))
         return self.epoch_e[mb]
 
     # -- (3) N2M combine ------------------------------------------------------
@@ -346,6 +350,29 @@ class PingPongRunner:
                 for j in range(m):
                     self._ev(("ffn", j, l, 0)); lay.expert_step(j); self._ev(("ffn", j, l, 1))
         return xs
+
+    # -- CUDA graph: one whole step (m x L) captured per rank -----------------
+    def capture(self, xs: list | None):
+        """Capture one step into a CUDA graph.  Epochs switch to device-tracked
+        mode (epoch 0 in the ABI), so every replay is the next use of each slot
+        and peers stay in lock-step through their own graphs' device waits."""
+        if self.record:
+            raise ValueError("timeline recording is eager-only")
+        self.layer.device_epochs = True
+        side = torch.cuda.Stream(device=self.layer.g.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self.run(xs)  # eager step in device-epoch mode (first-use attribute setup)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=side):
+            self.run(xs)
+        torch.cuda.synchronize()
+        return self.graph
+
+    def replay(self):
+        self.graph.replay()
 
     def timeline(self):
         """Per-phase (phase, mb, layer, start_ms, end_ms) relative to the first

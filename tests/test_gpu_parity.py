@@ -284,3 +284,27 @@ def test_echo_round_trip_bit_exact(lib):
         np.testing.assert_array_equal(to_host(out), O.combine(y, r.w[:T].cpu().numpy()))
     assert g.status() == 0
     g.close()
+
+
+def test_graph_replay_device_epochs(lib):
+    """A captured step replays with device-tracked epochs: every replay is the
+    next use of each slot, results equal the eager (explicit-epoch) run."""
+    from paper_2504_02263_b200 import runtime
+
+    g, layer, wts, model = _colocated_layer("tiny", b_a=32, m=2)
+    xs0 = [O.synth_tokens(32, model.hidden, seed=70 + j) for j in range(2)]
+    xs = [to_dev(x) for x in xs0]
+    run = runtime.PingPongRunner(layer, layers=2, chain=False)
+    run.run(xs)                      # eager, explicit epochs
+    torch.cuda.synchronize()
+    eager = [to_host(o) for o in run.outs]
+    run.capture(xs)                  # switches to device epochs
+    for _ in range(3):
+        run.replay()
+    torch.cuda.synchronize()
+    assert g.status() == 0
+    for j in range(2):
+        np.testing.assert_array_equal(to_host(run.outs[j]), eager[j])
+        ref = O.moe_layer([xs0[j]], wts, model.topk, n_e=1, resid=True).out[0]
+        assert_close_bf16(to_host(run.outs[j]), ref, f"mb {j}")
+    g.close()
