@@ -593,8 +593,12 @@ extern "C" int msi_dispatch(msi_ctx* c, const void* x, const int32_t* cnt, const
   MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots && epoch != 0xffffffffu, "msi_dispatch: bad slot/epoch");
   MSI_REQUIRE(x && cnt && idx && slot, "msi_dispatch: null pointer");
   const size_t smem = sizeof(long long) * c->plan.experts;
-  // one CTA per SM; rows are split into parts so every warp has work
-  const int grid = num_sms();
+  // ~64 KB of row stores per CTA, at most one CTA per SM (rows are split into
+  // parts so every warp has work); small micro-batches use few CTAs, which keeps
+  // the last-CTA release cheap
+  const size_t bytes = (size_t)T * c->plan.topk * c->plan.hidden * 2;
+  int grid = (int)((bytes + 65535) / 65536);
+  grid = grid < 1 ? 1 : (grid > num_sms() ? num_sms() : grid);
   dispatch_kernel<<<grid, kDispThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
       c->dev, reinterpret_cast<const __nv_bfloat16*>(x), cnt, idx, slot, T, mb_slot, epoch);
   return check_launch("dispatch_kernel");
