@@ -239,7 +239,7 @@ def main():
     orig_step = layer.expert_step
 
     def timed_expert_step(mb=0, stream=None):
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s, e = torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True)
         s.record()
         r = orig_step(mb, stream)
         e.record()
