@@ -134,11 +134,22 @@ def main():
             return (t[:len(lat)], t[len(lat):]) if split else t[:len(lat)]
 
         def verify() -> bool:
-            """Every row came back byte-exact to its (t, k) slot (all ranks agree)."""
+            """One more round trip with fresh data (x negated, ybuf cleared):
+            every row must come back byte-exact to its (t, k) slot and no
+            device wait may have failed -- a round trip that raced its own
+            dispatch would return stale rows."""
             ok = torch.ones(1, device=dev)
+            if g.is_attention:
+                x.neg_()
+                g.ybuf_view(0)[:T].zero_()
+            if world > 1:
+                dist.barrier()
+            ours()
+            torch.cuda.synchronize()
             if g.is_attention:
                 y = g.ybuf_view(0)[:T]
                 ok[0] = float(torch.equal(y, x[:, None, :].expand(T, K, H)))
+            ok[0] *= float(g.status() == 0)
             if world > 1:
                 dist.all_reduce(ok, op=dist.ReduceOp.MIN)
             return bool(ok.item())
@@ -155,21 +166,12 @@ def main():
                 dist.barrier()
             return gr.replay
 
-        layer.device_epochs = False
-        with torch.no_grad():
-            out.zero_() if out is not None else None
-        if g.is_attention:
-            g.ybuf_view(0)[:T].zero_()
         lat, disp = bench(ours, args.iters, args.warmup, split=True)
         rec = {"T": T, "pair_bytes_avg": T * K / n_e * H * 2 if not colo else T * K * H * 2,
                "ingress_bytes_busiest": ingress,
                "ours_p50_us": pct(lat, 0.5), "ours_p99_us": pct(lat, 0.99),
                "dispatch_only_p50_us": pct(disp, 0.5), "verified": verify()}
-        layer.device_epochs = True
-        if g.is_attention:
-            g.ybuf_view(0)[:T].zero_()
         glat = bench(graphed(ours), args.iters, args.warmup)
-        layer.device_epochs = False
         rec["verified_graph"] = verify()
         rec["ours_graph_p50_us"] = pct(glat, 0.5)
         rec["ours_graph_p99_us"] = pct(glat, 0.99)

@@ -122,6 +122,22 @@ __device__ __forceinline__ bool wait_geq(const uint32_t* ctr, uint32_t target,
   return true;
 }
 
+// Epoch of this use of a micro-batch slot.  `use` is the slot's device-side
+// use counter (+`add` = 1 for the first kernel of a use).  epoch 0 = that
+// value; an explicit epoch must agree with it, because the arrival counters
+// are cumulative: a stale (too small) epoch would satisfy a wait early and
+// race with the producer.  Returns 0 on a mismatch (and sets *status).
+__device__ __forceinline__ uint32_t resolve_epoch(uint32_t epoch, const uint32_t* use, uint32_t add,
+                                                  int32_t* status) {
+  const uint32_t dev = *(volatile const uint32_t*)use + add;
+  if (epoch == 0) return dev;
+  if (epoch != dev) {
+    if (status) atomicExch(status, MSI_ESTATE);
+    return 0;
+  }
+  return epoch;
+}
+
 // 16-byte global accesses.
 __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
   uint4 r;

@@ -77,12 +77,12 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t epoch = p.epoch;
-  if (epoch == 0 && p.epoch_src) epoch = *(volatile const uint32_t*)p.epoch_src + 1u;
+  if (p.epoch_src) epoch = resolve_epoch(p.epoch, p.epoch_src, 1u, p.status);
 
   // ---- wait for the senders' rows (GEMM1 on an expert GPU) ----------------
   if (threadIdx.x == 0) {
-    bool ok = true;
-    if (p.wait_ctr) ok = wait_geq(p.wait_ctr, epoch * p.wait_mul, p.timeout_ns, p.status);
+    bool ok = !(p.epoch_src && epoch == 0);  // epoch mismatch: abort below
+    if (ok && p.wait_ctr) ok = wait_geq(p.wait_ctr, epoch * p.wait_mul, p.timeout_ns, p.status);
     if (!ok) p.status[1] = 1;
     fence_proxy_async_global();  // rows written by peers are read by TMA (async proxy)
   }

@@ -177,7 +177,8 @@ dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32
   extern __shared__ long long s_rowbase[];  // [E] first row of this sender in expert e's segment
   __shared__ int s_abort;
   const int tid = threadIdx.x;
-  if (epoch == 0) epoch = *(volatile uint32_t*)(c.my_ause + mb * CTR_STRIDE) + 1u;  // device-tracked
+  epoch = resolve_epoch(epoch, c.my_ause + mb * CTR_STRIDE, 1u, c.my_status);
+  if (epoch == 0) return;  // host/device epoch mismatch: status set, nothing sent
   const int s = c.my_a;
   const size_t tab = (size_t)mb * c.n_a * c.E;
 
@@ -288,7 +289,8 @@ echo_kernel(const DevCtx c, int mb, uint32_t epoch) {
   __shared__ long long s_start[MSI_MAX_LOCAL_EXPERTS], s_total[MSI_MAX_LOCAL_EXPERTS];
   const int tid = threadIdx.x, lane = tid & 31;
   const uint32_t* arrive = c.my_arrive + mb * CTR_STRIDE;
-  if (epoch == 0) epoch = *(volatile uint32_t*)(c.my_euse + mb * CTR_STRIDE) + 1u;
+  epoch = resolve_epoch(epoch, c.my_euse + mb * CTR_STRIDE, 1u, c.my_status);
+  if (epoch == 0) return;
   if (tid == 0) s_ok = wait_geq(arrive, epoch * (uint32_t)c.n_a, c.timeout_ns, c.my_status);
   __syncthreads();
   if (!s_ok) return;
@@ -374,7 +376,8 @@ combine_kernel(const char* __restrict__ ybase, const float* __restrict__ w, cons
                int32_t* status) {
   __shared__ int s_ok;
   if (wait_ctr) {
-    if (epoch == 0) epoch = *(volatile const uint32_t*)epoch_src;  // set by this slot's dispatch
+    epoch = resolve_epoch(epoch, epoch_src, 0u, status);  // set by this slot's dispatch
+    if (epoch == 0) return;
     if (threadIdx.x == 0) s_ok = wait_geq(wait_ctr, epoch * mul, timeout_ns, status);
     __syncthreads();
     if (!s_ok) return;

@@ -197,9 +197,12 @@ class MoEDecodeLayer:
             if w2 is None or tuple(w2.shape) != (E_l, m.hidden, m.intermediate):
                 raise ValueError(f"expert ranks need w2 [{E_l}, {m.hidden}, {m.intermediate}]")
         self.wg, self.w13, self.w2 = wg, w13, w2
-        # epochs: host-counted uses of each slot (passed explicitly), or 0 =
-        # "next use" counted on the device (required inside CUDA graphs)
-        self.device_epochs = False
+        # epochs: 0 = "next use of the slot" counted on the device (default;
+        # required inside CUDA graphs, whose replays the host cannot count).
+        # device_epochs=False passes the host count explicitly; the kernels
+        # check it against the device count and fail (status MSI_ESTATE) on a
+        # mismatch instead of racing.
+        self.device_epochs = True
         self.epoch_a = [0] * group.plan.m   # uses of each slot (attention side)
         self.epoch_e = [0] * group.plan.m   # uses of each slot (expert side)
         self._routes = []

@@ -308,3 +308,30 @@ def test_graph_replay_device_epochs(lib):
         ref = O.moe_layer([xs0[j]], wts, model.topk, n_e=1, resid=True).out[0]
         assert_close_bf16(to_host(run.outs[j]), ref, f"mb {j}")
     g.close()
+
+
+def test_stale_explicit_epoch_is_rejected(lib):
+    """An explicit epoch that disagrees with the device's use count must not
+    race (the arrival counters are cumulative): the dispatch refuses, sets
+    MSI_ESTATE, and sends nothing."""
+    from paper_2504_02263_b200 import runtime
+    from paper_2504_02263_b200.config import DeploymentPlan, as_model_spec
+
+    model = as_model_spec("tiny")
+    g = runtime.M2NGroup(model, DeploymentPlan(n_a=1, n_e=1, m=1, b_a=16, colocated=True), rank=0,
+                         timeout_s=0.5)
+    layer = runtime.MoEDecodeLayer(g, wg=to_dev(O.synth_weights(model.hidden, 128, 8, experts=[]).wg))
+    x = to_dev(O.synth_tokens(16, model.hidden, seed=3))
+    r = layer.router(x, 0)
+    layer.dispatch(x, r, 0)            # device epoch 1
+    layer.expert_echo(0)
+    layer.combine(r)
+    torch.cuda.synchronize()
+    assert g.status() == 0
+    layer.device_epochs = False         # host count says 1 again: stale
+    layer.epoch_a[0] = 0
+    r = layer.router(x, 0)
+    layer.dispatch(x, r, 0)
+    torch.cuda.synchronize()
+    assert g.status() == -3             # MSI_ESTATE
+    g.close()
