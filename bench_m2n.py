@@ -173,6 +173,22 @@ def main():
                "dispatch_only_p50_us": pct(disp, 0.5), "verified": verify()}
         glat = bench(graphed(ours), args.iters, args.warmup)
         rec["verified_graph"] = verify()
+        # one traced eager round trip: %globaltimer phase stamps of every rank,
+        # relative to attention rank 0's dispatch start (µs)
+        g.set_trace(True)
+        if world > 1:
+            dist.barrier()
+        ours()
+        torch.cuda.synchronize()
+        g.set_trace(False)
+        tr = {f"r{rank}_{k}": v for k, v in g.trace().items()}
+        if world > 1:
+            allt = [None] * world
+            dist.all_gather_object(allt, tr)
+            tr = {k: v for d in allt for k, v in d.items()}
+        t0 = tr.get("r0_disp_start")
+        if t0:
+            rec["trace_us"] = {k: round((v - t0) / 1e3, 2) for k, v in sorted(tr.items(), key=lambda kv: kv[1])}
         rec["ours_graph_p50_us"] = pct(glat, 0.5)
         rec["ours_graph_p99_us"] = pct(glat, 0.99)
         # one-way bandwidth from the dispatch leg alone (busiest receiver's bytes)

@@ -96,6 +96,14 @@ int msi_poll_status(msi_ctx* ctx, int32_t* status);
 /* Expert-role counters: rows through msi_expert_ffn and number of calls since
  * msi_ctx_finalize (device-side, exact; read synchronously). */
 int msi_ctx_stats(msi_ctx* ctx, uint64_t* rows, uint64_t* calls);
+/* Phase tracing (SPEC.md:232 timeline): when on, the kernels
+ * write %globaltimer stamps (ns) of this rank's phases into a 32-slot trace
+ * line: 0/1/2 dispatch start/counts ready/release, 3/4/5 echo start/rows
+ * arrived/release, 6/7/8 combine start/rows arrived/end, 9/10 expert FFN
+ * start/rows arrived, 13/14 GEMM2 start/release.  Takes effect for calls
+ * (and CUDA-graph captures) made after it. */
+int msi_set_trace(msi_ctx* ctx, int on);
+int msi_ctx_trace(msi_ctx* ctx, uint64_t* out, int n);
 /* Bound on device-side spin waits, in nanoseconds (default 20 s). */
 int msi_set_wait_timeout(msi_ctx* ctx, uint64_t ns);
 int msi_ctx_workspace(msi_ctx* ctx, void** ptr, size_t* bytes);

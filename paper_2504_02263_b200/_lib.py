@@ -55,6 +55,8 @@ SIGNATURES = {
     "msi_poll_status": (_I, [_P, ctypes.POINTER(ctypes.c_int32)]),
     "msi_set_wait_timeout": (_I, [_P, _U64]),
     "msi_ctx_stats": (_I, [_P, ctypes.POINTER(_U64), ctypes.POINTER(_U64)]),
+    "msi_set_trace": (_I, [_P, _I]),
+    "msi_ctx_trace": (_I, [_P, ctypes.POINTER(_U64), _I]),
     "msi_ctx_workspace": (_I, [_P, ctypes.POINTER(_P), ctypes.POINTER(_SZ)]),
     "msi_gate_topk_workspace": (_SZ, [_I, _I]),
     "msi_gate_topk": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P]),

@@ -102,6 +102,16 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
+// Phase tracing (SPEC.md:232 timeline): %globaltimer stamps written to a
+// per-rank trace line when tracing is on (trace != nullptr).  Slots:
+//   0 dispatch start  1 dispatch counts ready  2 dispatch release
+//   3 echo start      4 echo rows arrived      5 echo release
+//   6 combine start   7 combine rows arrived   8 combine end (CTA 0)
+//   9 ffn start      10 ffn rows arrived      13 GEMM2 start   14 ffn release
+__device__ __forceinline__ void trace_stamp(unsigned long long* tr, int i) {
+  if (tr) tr[i] = globaltimer();
+}
+
 // Spin until *ctr >= target (acquire, system scope).  Returns false (and sets
 // *status) if `timeout_ns` elapses: hangs surface as errors, not lost GPUs.
 __device__ __forceinline__ bool wait_geq(const uint32_t* ctr, uint32_t target,

@@ -81,6 +81,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 
   // ---- wait for the senders' rows (GEMM1 on an expert GPU) ----------------
   if (threadIdx.x == 0) {
+    if (blockIdx.x == 0 && p.trace && p.wait_ctr) p.trace[p.trace_slot] = globaltimer();
     bool ok = !(p.epoch_src && epoch == 0);  // epoch mismatch: abort below
     if (ok && p.wait_ctr) ok = wait_geq(p.wait_ctr, epoch * p.wait_mul, p.timeout_ns, p.status);
     if (!ok) p.status[1] = 1;
@@ -103,17 +104,24 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   }
 
   // ---- segment table (all threads compute the same) -----------------------
+  if (blockIdx.x == 0 && threadIdx.x == 0 && p.trace) p.trace[p.trace_slot + 1] = globaltimer();
+  // totals: every (sender, expert) count loaded in parallel (no serial chain
+  // of system-scope loads), summed in shared memory
+  for (int e = threadIdx.x; e < p.E_l; e += blockDim.x) seg.total[e] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < (p.totals ? p.E_l : p.n_a * p.E_l); i += blockDim.x) {
+    if (p.totals) {
+      seg.total[i] = p.totals[i];
+    } else {
+      const int s = i / p.E_l, e = i - s * p.E_l;
+      atomicAdd(&seg.total[e], (int)(uint32_t)ld_relaxed_sys64(p.cntab + (size_t)s * p.E + p.e0 + e));
+    }
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     int run_start = 0, run_tile = 0;
     for (int e = 0; e < p.E_l; ++e) {
-      int tot;
-      if (p.totals) {
-        tot = p.totals[e];
-      } else {
-        tot = 0;
-        for (int s = 0; s < p.n_a; ++s)
-          tot += (int)(uint32_t)ld_relaxed_sys64(p.cntab + (size_t)s * p.E + p.e0 + e);
-      }
+      const int tot = seg.total[e];
       const int mt = (tot + BM - 1) / BM;
       seg.total[e] = tot;
       seg.start[e] = run_start;
@@ -277,6 +285,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     if (s_last) {
       *p.ticket = 0;
       if (p.epoch_store) *p.epoch_store = epoch;
+      if (p.trace) p.trace[p.trace_slot + 2] = globaltimer();
       fence_sys();
       for (int i = 0; i < p.n_sig; ++i) red_release_sys_add(p.sig[i], 1u);
     }

@@ -29,6 +29,8 @@ struct GemmParams {
   uint64_t timeout_ns;
   int32_t* status;          // [0] = error code, [1] = abort flag
   unsigned long long* stats;  // optional: [0] += rows processed, [1] += 1 (one CTA)
+  unsigned long long* trace;  // optional %globaltimer stamps: [slot] start,
+  int trace_slot;             //   [slot+1] rows arrived, [slot+2] release
   // epilogue
   int mode;                 // 0: SwiGLU -> out[row][out_ld]; 1: plain -> rows by meta
   __nv_bfloat16* out;       // mode 0: hbuf; mode 1 with meta == null: y

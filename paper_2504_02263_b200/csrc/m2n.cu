@@ -65,7 +65,7 @@ constexpr size_t ALIGN = 4096;
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Layout {
-  size_t arrive, comb, dticket, fticket, ause, euse, status, stats, cntab, ctrl_bytes;
+  size_t arrive, comb, dticket, fticket, ause, euse, status, stats, trace, cntab, ctrl_bytes;
   size_t ybuf, ybuf_slot;
   size_t recv, recv_slot, meta, meta_slot;
   size_t total;
@@ -84,6 +84,7 @@ Layout make_layout(const msi_plan& p, bool attn, bool expert) {
   L.euse = off; off += p.slots * line;
   L.status = off; off += line;
   L.stats = off; off += line;
+  L.trace = off; off += 2 * line;  // 32 x u64 %globaltimer stamps
   L.cntab = off; off += (size_t)p.slots * p.n_a * p.experts * 8;
   L.ctrl_bytes = align_up(off, ALIGN);
   off = L.ctrl_bytes;
@@ -119,6 +120,7 @@ struct DevCtx {
   uint64_t* my_cntab;
   uint32_t *my_arrive, *my_comb, *my_dticket, *my_fticket, *my_ause, *my_euse;
   int32_t* my_status;
+  unsigned long long* trace;  // null = tracing off
 };
 
 }  // namespace
@@ -182,6 +184,7 @@ dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32
   const int s = c.my_a;
   const size_t tab = (size_t)mb * c.n_a * c.E;
 
+  if (blockIdx.x == 0 && tid == 0) trace_stamp(c.trace, 0);
   // ---- publish this sender's counts to every rank (tagged with the epoch)
   if (blockIdx.x == 0)
     for (int i = tid; i < c.n_world * c.E; i += blockDim.x) {
@@ -189,14 +192,16 @@ dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32
       st_relaxed_sys64(c.cntab_of[r] + tab + (size_t)s * c.E + e,
                        ((uint64_t)epoch << 32) | (uint32_t)cnt[e]);
     }
-  // ---- wait for every sender's counts (local table)
+  // ---- wait for every sender's counts (local table), keep them in smem
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_rowbase + c.E);  // [n_a][E]
   if (tid == 0) s_abort = 0;
   __syncthreads();
   for (int i = tid; i < c.n_a * c.E; i += blockDim.x) {
     const uint64_t* p = c.my_cntab + tab + i;
     uint64_t t0 = 0;
     uint32_t spins = 0;
-    while ((uint32_t)(ld_acquire_sys64(p) >> 32) != epoch) {
+    uint64_t v;
+    while ((uint32_t)((v = ld_acquire_sys64(p)) >> 32) != epoch) {
       if ((++spins & 1023u) == 0) {
         uint64_t now = globaltimer();
         if (t0 == 0) t0 = now;
@@ -204,9 +209,11 @@ dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32
       }
       __nanosleep(32);
     }
+    s_cnt[i] = (uint32_t)v;
   }
   __syncthreads();
   if (s_abort) return;
+  if (blockIdx.x == 0 && tid == 0) trace_stamp(c.trace, 1);
   // ---- row base per expert: 128-aligned segment start + rows of senders < s
   for (int q = tid; q < c.n_e; q += blockDim.x) {
     long long run = 0;
@@ -214,7 +221,7 @@ dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32
       const int e = q * c.E_l + el;
       long long total = 0, before = 0;
       for (int s2 = 0; s2 < c.n_a; ++s2) {
-        const long long v = (uint32_t)ld_relaxed_sys64(c.my_cntab + tab + (size_t)s2 * c.E + e);
+        const long long v = s_cnt[s2 * c.E + e];
         total += v;
         if (s2 < s) before += v;
       }
@@ -270,6 +277,7 @@ dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32
     if (old == gridDim.x - 1) {
       c.my_dticket[mb * CTR_STRIDE] = 0;
       c.my_ause[mb * CTR_STRIDE] = epoch;  // every CTA has read the old value
+      trace_stamp(c.trace, 2);
       fence_sys();
       for (int q = 0; q < c.n_e; ++q) red_release_sys_add(c.arrive_of[q] + mb * CTR_STRIDE, 1u);
     }
@@ -286,37 +294,45 @@ constexpr int kEchoThreads = 512;
 __global__ void __launch_bounds__(kEchoThreads)
 echo_kernel(const DevCtx c, int mb, uint32_t epoch) {
   __shared__ int s_ok, s_last;
-  __shared__ long long s_start[MSI_MAX_LOCAL_EXPERTS], s_total[MSI_MAX_LOCAL_EXPERTS];
+  __shared__ int s_start[MSI_MAX_LOCAL_EXPERTS], s_total[MSI_MAX_LOCAL_EXPERTS];
+  __shared__ int s_first[MSI_MAX_LOCAL_EXPERTS + 1];  // exclusive prefix of totals
   const int tid = threadIdx.x, lane = tid & 31;
   const uint32_t* arrive = c.my_arrive + mb * CTR_STRIDE;
   epoch = resolve_epoch(epoch, c.my_euse + mb * CTR_STRIDE, 1u, c.my_status);
   if (epoch == 0) return;
+  if (blockIdx.x == 0 && tid == 0) trace_stamp(c.trace, 3);
   if (tid == 0) s_ok = wait_geq(arrive, epoch * (uint32_t)c.n_a, c.timeout_ns, c.my_status);
+  if (tid < MSI_MAX_LOCAL_EXPERTS) s_total[tid] = 0;
   __syncthreads();
   if (!s_ok) return;
+  if (blockIdx.x == 0 && tid == 0) trace_stamp(c.trace, 4);
   const size_t tab = (size_t)mb * c.n_a * c.E;
-  if (tid < c.E_l) {  // segment table: total[e] and the 128-aligned start[e]
-    long long tot = 0;
-    for (int s = 0; s < c.n_a; ++s)
-      tot += (uint32_t)ld_relaxed_sys64(c.my_cntab + tab + (size_t)s * c.E + c.my_e * c.E_l + tid);
-    s_total[tid] = tot;
+  for (int i = tid; i < c.n_a * c.E_l; i += blockDim.x) {  // all entries in parallel
+    const int s = i / c.E_l, el = i - s * c.E_l;
+    atomicAdd(&s_total[el], (int)(uint32_t)ld_relaxed_sys64(c.my_cntab + tab + (size_t)s * c.E + c.my_e * c.E_l + el));
   }
   __syncthreads();
-  if (tid == 0) {
-    long long run = 0;
+  if (tid == 0) {  // 128-aligned segment starts and the flat row prefix
+    int run = 0, flat = 0;
     for (int el = 0; el < c.E_l; ++el) {
       s_start[el] = run;
+      s_first[el] = flat;
       run += (s_total[el] + MSI_ROW_ALIGN - 1) / MSI_ROW_ALIGN * MSI_ROW_ALIGN;
+      flat += s_total[el];
     }
+    s_first[c.E_l] = flat;
   }
   __syncthreads();
   const int gwarp = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
   const int nwarps = gridDim.x * (blockDim.x >> 5);
   const size_t row_bytes = (size_t)c.H * 2;
   const int nchunk = c.H >> 8;
-  for (int el = 0; el < c.E_l; ++el) {
-    for (long long r = gwarp; r < s_total[el]; r += nwarps) {
-      const long long row = s_start[el] + r;
+  {
+    // one flat row index over all local experts: every warp has work
+    for (int i = gwarp; i < s_first[c.E_l]; i += nwarps) {
+      int el = 0;
+      while (i >= s_first[el + 1]) ++el;
+      const long long row = s_start[el] + (i - s_first[el]);
       const int2 md = c.meta_of[c.my_e][(size_t)mb * c.cap + row];
       const char* src = c.recv_of[c.my_e] + ((size_t)mb * c.cap + row) * row_bytes + lane * 16;
       char* dst = c.ybuf_of[md.x] + (size_t)mb * c.max_tokens * c.K * row_bytes + (size_t)md.y * row_bytes + lane * 16;
@@ -338,6 +354,7 @@ echo_kernel(const DevCtx c, int mb, uint32_t epoch) {
     if (s_last) {
       c.my_fticket[mb * CTR_STRIDE] = 0;
       c.my_euse[mb * CTR_STRIDE] = epoch;
+      trace_stamp(c.trace, 5);
       fence_sys();
       for (int s = 0; s < c.n_a; ++s) red_release_sys_add(c.comb_of[s] + mb * CTR_STRIDE, 1u);
     }
@@ -373,14 +390,17 @@ __global__ void __launch_bounds__(256)
 combine_kernel(const char* __restrict__ ybase, const float* __restrict__ w, const uint16_t* __restrict__ resid,
                uint16_t* __restrict__ out, int T, int K, int H, const uint32_t* wait_ctr,
                uint32_t epoch, uint32_t mul, const uint32_t* epoch_src, uint64_t timeout_ns,
-               int32_t* status) {
+               int32_t* status, unsigned long long* trace) {
   __shared__ int s_ok;
+  const bool t0 = blockIdx.x == 0 && threadIdx.x == 0;
   if (wait_ctr) {
     epoch = resolve_epoch(epoch, epoch_src, 0u, status);  // set by this slot's dispatch
     if (epoch == 0) return;
+    if (t0) trace_stamp(trace, 6);
     if (threadIdx.x == 0) s_ok = wait_geq(wait_ctr, epoch * mul, timeout_ns, status);
     __syncthreads();
     if (!s_ok) return;
+    if (t0) trace_stamp(trace, 7);
   }
   const int per_row = H / 8;
   const size_t n = (size_t)T * per_row;
@@ -388,6 +408,7 @@ combine_kernel(const char* __restrict__ ybase, const float* __restrict__ w, cons
     const int t = (int)(i / per_row), c8 = (int)(i % per_row);
     combine_row8(ybase, w, resid, out, t, c8, K, H);
   }
+  if (t0) trace_stamp(trace, 8);
 }
 
 // -------------------------------------------------- attention stand-in ----
@@ -528,6 +549,7 @@ extern "C" int msi_ctx_finalize(msi_ctx* c) {
   d.my_ause = reinterpret_cast<uint32_t*>(c->heap + M.ause);
   d.my_euse = reinterpret_cast<uint32_t*>(c->heap + M.euse);
   d.my_status = reinterpret_cast<int32_t*>(c->heap + M.status);
+  d.trace = nullptr;
   MSI_CUDA(cudaMemset(c->heap, 0, M.ctrl_bytes));
   MSI_CUDA(cudaDeviceSynchronize());
   c->finalized = true;
@@ -581,6 +603,19 @@ extern "C" int msi_ctx_stats(msi_ctx* c, uint64_t* rows, uint64_t* calls) {
   return 0;
 }
 
+extern "C" int msi_set_trace(msi_ctx* c, int on) {
+  if (!c || !c->finalized) { set_error("msi_set_trace: context not finalized"); return MSI_ESTATE; }
+  c->dev.trace = on ? reinterpret_cast<unsigned long long*>(c->heap + c->my_layout.trace) : nullptr;
+  if (on) MSI_CUDA(cudaMemset(c->heap + c->my_layout.trace, 0, 32 * sizeof(unsigned long long)));
+  return 0;
+}
+
+extern "C" int msi_ctx_trace(msi_ctx* c, uint64_t* out, int n) {
+  if (!c || !out || n < 0 || n > 32) { set_error("msi_ctx_trace: bad argument"); return MSI_EINVAL; }
+  MSI_CUDA(cudaMemcpy(out, c->heap + c->my_layout.trace, n * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
 extern "C" int msi_set_wait_timeout(msi_ctx* c, uint64_t ns) {
   if (!c) { set_error("msi_set_wait_timeout: null"); return MSI_EINVAL; }
   c->timeout_ns = ns;
@@ -595,7 +630,8 @@ extern "C" int msi_dispatch(msi_ctx* c, const void* x, const int32_t* cnt, const
   MSI_REQUIRE(T >= 0 && T <= c->plan.max_tokens, "msi_dispatch: T=%d exceeds max_tokens=%d", T, c->plan.max_tokens);
   MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots && epoch != 0xffffffffu, "msi_dispatch: bad slot/epoch");
   MSI_REQUIRE(x && cnt && idx && slot, "msi_dispatch: null pointer");
-  const size_t smem = sizeof(long long) * c->plan.experts;
+  // row bases [E] (long long) + the all-gathered count table [n_a][E] (u32)
+  const size_t smem = sizeof(long long) * c->plan.experts + sizeof(uint32_t) * c->plan.n_a * c->plan.experts;
   // ~64 KB of row stores per CTA, at most one CTA per SM (rows are split into
   // parts so every warp has work); small micro-batches use few CTAs, which keeps
   // the last-CTA release cheap
@@ -638,6 +674,8 @@ extern "C" int msi_expert_ffn(msi_ctx* c, const void* w13, const void* w2, int m
   g1.p.timeout_ns = c->timeout_ns;
   g1.p.status = d.my_status;
   g1.p.stats = reinterpret_cast<unsigned long long*>(c->heap + L.stats);
+  g1.p.trace = d.trace;  // stamps 9 (start), 10 (rows arrived)
+  g1.p.trace_slot = 9;
   g1.p.mode = 0;
   g1.p.out = reinterpret_cast<__nv_bfloat16*>(c->hbuf);
   g1.p.out_ld = p.inter;
@@ -667,6 +705,8 @@ extern "C" int msi_expert_ffn(msi_ctx* c, const void* w13, const void* w2, int m
   g2.p.epoch = epoch;
   g2.p.epoch_src = d.my_euse + mb_slot * CTR_STRIDE;
   g2.p.epoch_store = d.my_euse + mb_slot * CTR_STRIDE;  // last CTA: this use is done
+  g2.p.trace = d.trace;  // stamps 13 (GEMM2 start), 14 (release to combine)
+  g2.p.trace_slot = 12;
   return grouped_gemm_launch(g2, st);
 }
 
@@ -693,7 +733,8 @@ extern "C" int msi_combine(msi_ctx* c, void* out, const float* w, const void* re
   combine_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       c->heap + L.ybuf + mb_slot * L.ybuf_slot, w, reinterpret_cast<const uint16_t*>(resid),
       reinterpret_cast<uint16_t*>(out), T, p.topk, p.hidden, c->dev.my_comb + mb_slot * CTR_STRIDE,
-      epoch, (uint32_t)p.n_e, c->dev.my_ause + mb_slot * CTR_STRIDE, c->timeout_ns, c->dev.my_status);
+      epoch, (uint32_t)p.n_e, c->dev.my_ause + mb_slot * CTR_STRIDE, c->timeout_ns, c->dev.my_status,
+      c->dev.trace);
   return check_launch("combine_kernel");
 }
 
@@ -706,7 +747,7 @@ extern "C" int msi_combine_local(const void* y, const float* w, const void* resi
   grid = grid > 4 * num_sms() ? 4 * num_sms() : grid;
   combine_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const char*>(y), w, reinterpret_cast<const uint16_t*>(resid),
-      reinterpret_cast<uint16_t*>(out), T, K, H, nullptr, 0, 0, nullptr, 0, nullptr);
+      reinterpret_cast<uint16_t*>(out), T, K, H, nullptr, 0, 0, nullptr, 0, nullptr, nullptr);
   return check_launch("combine_kernel");
 }
 

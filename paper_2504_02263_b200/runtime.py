@@ -149,6 +149,19 @@ class M2NGroup:
         _lib.call("msi_ctx_stats", self.ctx, ctypes.byref(r), ctypes.byref(c))
         return r.value, c.value
 
+    TRACE_SLOTS = {0: "disp_start", 1: "disp_counts", 2: "disp_release", 3: "echo_start",
+                   4: "echo_rows", 5: "echo_release", 6: "comb_start", 7: "comb_rows", 8: "comb_end",
+                   9: "ffn_start", 10: "ffn_rows", 13: "gemm2_start", 14: "ffn_release"}
+
+    def set_trace(self, on: bool = True):
+        _lib.call("msi_set_trace", self.ctx, int(on))
+
+    def trace(self) -> dict:
+        """%globaltimer stamps (ns) of this rank's last traced phases."""
+        buf = (ctypes.c_uint64 * 32)()
+        _lib.call("msi_ctx_trace", self.ctx, buf, 32)
+        return {name: buf[i] for i, name in self.TRACE_SLOTS.items() if buf[i]}
+
     def close(self):
         if getattr(self, "ctx", None):
             _lib.load().msi_ctx_destroy(self.ctx)
