@@ -412,9 +412,17 @@ combine_kernel(const char* __restrict__ ybase, const float* __restrict__ w, cons
 }
 
 // -------------------------------------------------- attention stand-in ----
-__global__ void attn_standin_kernel(const uint4* __restrict__ kv, size_t n16, float* checksum) {
+__global__ void __launch_bounds__(512) attn_standin_kernel(const uint4* __restrict__ kv, size_t n16, float* checksum) {
+  // 4 independent 16 B loads in flight per thread per iteration (HBM streaming)
   float s = 0.0f;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+    uint4 v0 = ld_nc_v4(kv + i), v1 = ld_nc_v4(kv + i + stride);
+    uint4 v2 = ld_nc_v4(kv + i + 2 * stride), v3 = ld_nc_v4(kv + i + 3 * stride);
+    s += bf16lo(v0.x) + bf16hi(v1.w) + bf16lo(v2.y) + bf16hi(v3.z);
+  }
+  for (; i < n16; i += stride) {
     uint4 v = ld_nc_v4(kv + i);
     s += bf16lo(v.x) + bf16hi(v.w);
   }
