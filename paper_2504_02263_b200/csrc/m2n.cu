@@ -762,7 +762,7 @@ extern "C" int msi_combine_local(const void* y, const float* w, const void* resi
 extern "C" int msi_attn_standin(const void* kv, size_t kv_bytes, float* checksum, void* stream) {
   MSI_REQUIRE(kv && checksum && kv_bytes % 16 == 0, "msi_attn_standin: bad argument");
   if (kv_bytes == 0) return 0;
-  attn_standin_kernel<<<2 * num_sms(), 512, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  attn_standin_kernel<<<4 * num_sms(), 512, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const uint4*>(kv), kv_bytes / 16, checksum);
   return check_launch("attn_standin_kernel");
 }
