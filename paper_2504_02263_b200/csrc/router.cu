@@ -55,25 +55,43 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
       xr[i] = x + (size_t)(tv[i] ? t : 0) * H + 8 * lane;
     }
     const __nv_bfloat16* wr = wg + (size_t)(eg * TE) * H + 8 * lane;
-    for (int j = 0; j < nchunk; ++j) {
-      float xv[TT][8];
+    // x chunks are prefetched PF iterations ahead (HBM latency), W_g rows are
+    // small and L1/L2-resident; the accumulation order per (token, expert)
+    // stays j-major, c-minor as pinned.
+    constexpr int PF = (TT * TE >= 32) ? 2 : 4;
+    uint4 xq[PF][TT];
 #pragma unroll
-      for (int i = 0; i < TT; ++i) {
-        uint4 v = tv[i] ? __ldg(reinterpret_cast<const uint4*>(xr[i] + 256 * j)) : make_uint4(0, 0, 0, 0);
-        xv[i][0] = bf16lo(v.x); xv[i][1] = bf16hi(v.x);
-        xv[i][2] = bf16lo(v.y); xv[i][3] = bf16hi(v.y);
-        xv[i][4] = bf16lo(v.z); xv[i][5] = bf16hi(v.z);
-        xv[i][6] = bf16lo(v.w); xv[i][7] = bf16hi(v.w);
-      }
+    for (int u = 0; u < PF; ++u)
 #pragma unroll
-      for (int e = 0; e < TE; ++e) {
-        uint4 v = __ldg(reinterpret_cast<const uint4*>(wr + (size_t)e * H + 256 * j));
-        float wv[8] = {bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y),
-                       bf16lo(v.z), bf16hi(v.z), bf16lo(v.w), bf16hi(v.w)};
+      for (int i = 0; i < TT; ++i)
+        xq[u][i] = (tv[i] && u < nchunk) ? __ldg(reinterpret_cast<const uint4*>(xr[i] + 256 * u)) : make_uint4(0, 0, 0, 0);
+    for (int j0 = 0; j0 < nchunk; j0 += PF) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
+      for (int u = 0; u < PF; ++u) {
+        const int j = j0 + u;
+        if (j >= nchunk) break;
+        float xv[TT][8];
 #pragma unroll
-          for (int i = 0; i < TT; ++i) acc[i][e] = __fmaf_rn(xv[i][c], wv[c], acc[i][e]);
+        for (int i = 0; i < TT; ++i) {
+          const uint4 v = xq[u][i];
+          xv[i][0] = bf16lo(v.x); xv[i][1] = bf16hi(v.x);
+          xv[i][2] = bf16lo(v.y); xv[i][3] = bf16hi(v.y);
+          xv[i][4] = bf16lo(v.z); xv[i][5] = bf16hi(v.z);
+          xv[i][6] = bf16lo(v.w); xv[i][7] = bf16hi(v.w);
+          // refill this slot with chunk j + PF
+          xq[u][i] = (tv[i] && j + PF < nchunk) ? __ldg(reinterpret_cast<const uint4*>(xr[i] + 256 * (j + PF)))
+                                               : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int e = 0; e < TE; ++e) {
+          uint4 v = __ldg(reinterpret_cast<const uint4*>(wr + (size_t)e * H + 256 * j));
+          float wv[8] = {bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y),
+                         bf16lo(v.z), bf16hi(v.z), bf16lo(v.w), bf16hi(v.w)};
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+#pragma unroll
+            for (int i = 0; i < TT; ++i) acc[i][e] = __fmaf_rn(xv[i][c], wv[c], acc[i][e]);
+        }
       }
     }
 #pragma unroll
