@@ -24,18 +24,33 @@ namespace {
 constexpr int kWarps = 8;
 constexpr uint32_t kTaken = 0x7fc0dead;  // NaN payload marking an already-selected expert
 
-template <int TT, int TE>
+// Shared memory: logits [max(BT,16)][E] fp32 (reused by the last CTA for
+// [8][E] masks + [8][E] counts), then -- when WS -- a copy of W_g [E][H] bf16
+// so the FMA loop reads the gate weights at shared-memory latency.
+__host__ __device__ inline size_t logit_smem_bytes(int BT, int E) {
+  return (size_t)(BT > 16 ? BT : 16) * E * sizeof(float) + (size_t)E * sizeof(uint32_t);
+}
+
+template <int TT, int TE, bool WS>
 __global__ void __launch_bounds__(kWarps * 32)
 gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
                  int T, int H, int E, int K, int BT, int32_t* __restrict__ idx_out,
                  float* __restrict__ w_out, int32_t* __restrict__ cnt_out,
                  int32_t* __restrict__ slot_out, int32_t* __restrict__ ws) {
-  extern __shared__ float s_logit[];                       // [BT][E]
+  extern __shared__ __align__(16) float s_logit[];         // [BT][E]
   __shared__ int s_last;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t0 = blockIdx.x * BT;
   const int nchunk = H >> 8;
+  if (WS) {  // stage W_g (E*H*2 bytes, 16 B vectors, coalesced)
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<char*>(s_logit) + ((logit_smem_bytes(BT, E) + 15) & ~size_t(15)));
+    const uint4* src = reinterpret_cast<const uint4*>(wg);
+    const int n16 = E * H / 8;
+    for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = __ldg(src + i);
+    wg = reinterpret_cast<const __nv_bfloat16*>(dst);
+    __syncthreads();
+  }
 
   // ---- 1. logits ---------------------------------------------------------
   const int tgroups = BT / TT, egroups = E / TE;
@@ -84,7 +99,8 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
         }
 #pragma unroll
         for (int e = 0; e < TE; ++e) {
-          uint4 v = __ldg(reinterpret_cast<const uint4*>(wr + (size_t)e * H + 256 * j));
+          const uint4* wp = reinterpret_cast<const uint4*>(wr + (size_t)e * H + 256 * j);
+          uint4 v = WS ? *wp : __ldg(wp);
           float wv[8] = {bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y),
                          bf16lo(v.z), bf16hi(v.z), bf16lo(v.w), bf16hi(v.w)};
 #pragma unroll
@@ -210,13 +226,16 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
   if (threadIdx.x == 0) ws[0] = 0;  // ticket ready for the next launch
 }
 
+constexpr size_t kMaxStagedW = 200 * 1024;  // W_g staged in smem up to this size
+
 template <int TT, int TE>
 int launch(const void* x, const void* wg, int T, int H, int E, int K, int BT, int32_t* idx,
            float* w, int32_t* cnt, int32_t* slot, void* ws, cudaStream_t st) {
   const int nblk = (T + BT - 1) / BT;
-  // logits [BT][E] during routing; [8][E] masks + [8][E] counts in the last CTA
-  const size_t smem = (size_t)(BT > 2 * kWarps ? BT : 2 * kWarps) * E * sizeof(float) + (size_t)E * sizeof(uint32_t);
-  auto kern = gate_topk_kernel<TT, TE>;
+  const size_t wbytes = (size_t)E * H * 2;
+  const bool stage = E <= 16 && wbytes <= kMaxStagedW;
+  const size_t smem = ((logit_smem_bytes(BT, E) + 15) & ~size_t(15)) + (stage ? wbytes : 0);
+  auto kern = stage ? gate_topk_kernel<TT, TE, true> : gate_topk_kernel<TT, TE, false>;
   if (smem > 48 * 1024) MSI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<nblk, kWarps * 32, smem, st>>>(reinterpret_cast<const __nv_bfloat16*>(x),
                                         reinterpret_cast<const __nv_bfloat16*>(wg), T, H, E, K, BT,
