@@ -1,0 +1,72 @@
+#!/usr/bin/env python
+"""Expert grouped-GEMM microbenchmark (msi_grouped_ffn: GEMM1 gate/up+SiLU and
+GEMM2 down) on a Mixtral-8x22B-shaped expert group, for a sweep of tokens per
+expert t_e.  Reports algorithmic TFLOP/s (6 * rows * h * h') against the
+measured bf16 peaks.  MSI_GEMM_CG=1|2 selects the CTA-group variant.
+
+  python bench_gemm.py [--experts 8] [--te 256,768,1536] [--iters 10]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--experts", type=int, default=8)
+    ap.add_argument("--hidden", type=int, default=6144)
+    ap.add_argument("--inter", type=int, default=16384)
+    ap.add_argument("--te", default="64,256,768,1536")
+    ap.add_argument("--iters", type=int, default=10)
+    args = ap.parse_args()
+
+    import torch
+
+    from paper_2504_02263_b200 import ops
+
+    torch.manual_seed(0)
+    E, H, Hp = args.experts, args.hidden, args.inter
+    dev = torch.device("cuda:0")
+    w13 = (torch.randn(E, 2 * Hp, H, device=dev) / H ** 0.5).to(torch.bfloat16)
+    w2 = (torch.randn(E, H, Hp, device=dev) / Hp ** 0.5).to(torch.bfloat16)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    out = []
+    for te in [int(v) for v in args.te.split(",")]:
+        # realistic ragged loads: +-5% around te
+        g = torch.Generator().manual_seed(te)
+        totals = [max(1, int(te * (0.95 + 0.1 * torch.rand(1, generator=g).item()))) for _ in range(E)]
+        rows = sum((t + 127) // 128 * 128 for t in totals)
+        x = torch.randn(rows, H, device=dev).to(torch.bfloat16)
+        tot = torch.tensor(totals, dtype=torch.int32, device=dev)
+        hbuf = torch.empty(rows, Hp, dtype=torch.bfloat16, device=dev)
+        y = torch.empty(rows, H, dtype=torch.bfloat16, device=dev)
+        for _ in range(3):
+            ops.grouped_ffn(x, tot, w13, w2, hbuf, y)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(args.iters):
+            ops.grouped_ffn(x, tot, w13, w2, hbuf, y)
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / args.iters
+        flops = 6.0 * sum(totals) * H * Hp
+        tf = flops / (ms / 1e3) / 1e12
+        rec = {"cg": os.environ.get("MSI_GEMM_CG", "default"), "te": te, "rows": sum(totals), "ms": ms,
+               "tflops": tf, "frac_burst": tf / peaks.get("bf16_tflops", 1677.4),
+               "frac_sustained": tf / peaks.get("bf16_tflops_sustained", 1404.8),
+               "weight_gbps": E * 3 * H * Hp * 2 / (ms / 1e3) / 1e9}
+        out.append(rec)
+        print(json.dumps(rec), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -26,6 +26,7 @@
 // Tile order: expert-major, then N tile, then M tile (fastest), so CTAs that
 // run concurrently share one expert's B tiles and its A rows stay in L2.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -34,24 +35,34 @@
 namespace msi {
 namespace {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
-constexpr int A_BYTES = BM * BK * 2;
-constexpr int B_BYTES = BN * BK * 2;
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int BM = 128, BN = 256, BK = 64;
 constexpr int EPI_WARP_BYTES = 32 * 256;  // 32 rows x 128 bf16
 constexpr int kThreads = 256;
 constexpr int TMEM_COLS = 512;
-constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 4 * EPI_WARP_BYTES + 256;
+
+// Per-CTA-group configuration.  CG=1: one CTA computes a 128x256 tile from
+// A 128x64 + B 256x64 per stage (48 KB).  CG=2: a CTA pair computes a 256x256
+// tile with tcgen05.mma.cta_group::2; each CTA stages its 128 A rows and half
+// of B (128 rows) -- 32 KB -- so per-SM shared-memory traffic per MAC is 2/3
+// of the CG=1 kernel's and 6 stages fit.
+template <int CG>
+struct Cfg {
+  static constexpr int STAGES = CG == 1 ? 4 : 6;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_ROWS = BN / CG;
+  static constexpr int B_BYTES = B_ROWS * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr size_t SMEM = 1024 /*align*/ + (size_t)STAGES * STAGE_BYTES + 4 * EPI_WARP_BYTES + 256;
+};
 
 struct SegInfo {
   int total[MSI_MAX_LOCAL_EXPERTS];
   int start[MSI_MAX_LOCAL_EXPERTS];
   int tile0[MSI_MAX_LOCAL_EXPERTS + 1];  // first tile of expert e
-  int mtiles[MSI_MAX_LOCAL_EXPERTS];
+  int mtiles[MSI_MAX_LOCAL_EXPERTS];     // M tiles (CG=1) or M-tile pairs (CG=2)
 };
 
-__device__ __forceinline__ void decode_tile(const SegInfo& s, int E_l, int nt, int tau, int& e,
-                                            int& n, int& m) {
+__device__ __forceinline__ void decode_tile(const SegInfo& s, int E_l, int tau, int& e, int& n, int& m) {
   e = 0;
   while (e + 1 < E_l && tau >= s.tile0[e + 1]) ++e;
   const int local = tau - s.tile0[e];
@@ -59,47 +70,75 @@ __device__ __forceinline__ void decode_tile(const SegInfo& s, int E_l, int nt, i
   m = local - n * s.mtiles[e];
 }
 
+template <int CG>
 __global__ void __launch_bounds__(kThreads, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const GemmParams p) {
+  using C = Cfg<CG>;
+  constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;                                  // STAGES x 16 KB (per-stage stride STAGE_BYTES)
-  uint8_t* sEpi = smem + STAGES * STAGE_BYTES;         // 4 x 8 KB
+  uint8_t* sA = smem;                                  // STAGES x (A | B) per stage
+  uint8_t* sEpi = smem + STAGES * C::STAGE_BYTES;      // 4 x 8 KB epilogue staging
   uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + 4 * EPI_WARP_BYTES);
-  uint64_t* full = bars;                 // [STAGES]
-  uint64_t* empty = bars + STAGES;       // [STAGES]
-  uint64_t* tfull = bars + 2 * STAGES;   // [2]
-  uint64_t* tempty = bars + 2 * STAGES + 2;  // [2]
+  uint64_t* full = bars;                     // [STAGES] (CG=2: the leader's is used)
+  uint64_t* empty = bars + STAGES;           // [STAGES]
+  uint64_t* tfull = bars + 2 * STAGES;       // [2]
+  uint64_t* tempty = bars + 2 * STAGES + 2;  // [2]   (CG=2: the leader's is used)
   __shared__ uint32_t s_tmem;
   __shared__ SegInfo seg;
-  __shared__ int s_last;
+  __shared__ int s_last, s_abort;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;  // CTA within the pair
+  const bool leader = rank == 0;
+  const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;  // pair / CTA index
+  const int nunits = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   uint32_t epoch = p.epoch;
   if (p.epoch_src) epoch = resolve_epoch(p.epoch, p.epoch_src, 1u, p.status);
 
-  // ---- wait for the senders' rows (GEMM1 on an expert GPU) ----------------
+  // ---- wait for the senders' rows (GEMM1 on an expert GPU); in a pair the
+  //      leader waits and both CTAs follow its decision ----------------------
   if (threadIdx.x == 0) {
-    if (blockIdx.x == 0 && p.trace && p.wait_ctr) p.trace[p.trace_slot] = globaltimer();
-    bool ok = !(p.epoch_src && epoch == 0);  // epoch mismatch: abort below
-    if (ok && p.wait_ctr) ok = wait_geq(p.wait_ctr, epoch * p.wait_mul, p.timeout_ns, p.status);
-    if (!ok) p.status[1] = 1;
-    fence_proxy_async_global();  // rows written by peers are read by TMA (async proxy)
-  }
-  if (threadIdx.x == 0) {
+    bool ok = true;
+    if (leader) {
+      if (blockIdx.x == 0 && p.trace && p.wait_ctr) p.trace[p.trace_slot] = globaltimer();
+      ok = !(p.epoch_src && epoch == 0);  // epoch mismatch: abort below
+      if (ok && p.wait_ctr) ok = wait_geq(p.wait_ctr, epoch * p.wait_mul, p.timeout_ns, p.status);
+      if (!ok) p.status[1] = 1;
+      if (ok && p.status && p.status[1]) ok = false;  // an earlier call failed
+    }
+    s_abort = ok ? 0 : 1;
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4 * CG); }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<TMEM_COLS>(&s_tmem);
-  __syncthreads();
-  if (p.status && p.status[1]) {  // a wait timed out: skip the work, keep the GPU usable
-    tc_fence_before();
+  if (warp == 2) {
+    if constexpr (CG == 2) tmem_alloc2<TMEM_COLS>(&s_tmem);
+    else tmem_alloc<TMEM_COLS>(&s_tmem);
+  }
+  tc_fence_before();
+  if constexpr (CG == 2) {
+    cluster_sync();  // barriers of both CTAs initialised, leader's wait done
+    if (!leader) {
+      if (threadIdx.x == 0) s_abort = (int)ld_shared_cluster_u32(mapa_shared(smem_u32(&s_abort), 0));
+      __syncthreads();
+    }
+  } else {
     __syncthreads();
-    if (warp == 2) tmem_dealloc<TMEM_COLS>(s_tmem);
+  }
+  tc_fence_after();
+  if (threadIdx.x == 0) fence_proxy_async_global();  // rows written by peers are read by TMA
+  const uint32_t tmem_base = s_tmem;
+  if (s_abort) {  // a wait timed out / epoch mismatch: skip the work, keep the GPU usable
+    if constexpr (CG == 2) cluster_sync();
+    else __syncthreads();
+    if (warp == 2) {
+      if constexpr (CG == 2) tmem_dealloc2<TMEM_COLS>(tmem_base);
+      else tmem_dealloc<TMEM_COLS>(tmem_base);
+    }
     return;
   }
 
@@ -123,12 +162,12 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     for (int e = 0; e < p.E_l; ++e) {
       const int tot = seg.total[e];
       const int mt = (tot + BM - 1) / BM;
-      seg.total[e] = tot;
+      const int units = (mt + CG - 1) / CG;  // M tiles per CTA or per pair
       seg.start[e] = run_start;
-      seg.mtiles[e] = mt;
+      seg.mtiles[e] = units;
       seg.tile0[e] = run_tile;
       run_start += mt * BM;
-      run_tile += mt * p.nt;
+      run_tile += units * p.nt;
     }
     seg.tile0[p.E_l] = run_tile;
     if (p.stats && blockIdx.x == 0) {
@@ -138,38 +177,41 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       atomicAdd(p.stats + 1, 1ull);
     }
   }
-  tc_fence_before();
   __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = s_tmem;
   const int ntiles = seg.tile0[p.E_l];
   const int kblocks = p.kdim / BK;
 
   if (warp == 0 && lane == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer (both CTAs of a pair) ==============
     int stage = 0;
     uint32_t phase = 0;
-    for (int tau = blockIdx.x; tau < ntiles; tau += gridDim.x) {
+    for (int tau = unit; tau < ntiles; tau += nunits) {
       int e, n, m;
-      decode_tile(seg, p.E_l, p.nt, tau, e, n, m);
-      const int rowA = seg.start[e] + m * BM;
-      const int rowB = e * p.n_total + n * BN;
+      decode_tile(seg, p.E_l, tau, e, n, m);
+      const int rowA = seg.start[e] + (m * CG + (int)rank) * BM;  // this CTA's 128 rows
+      const int rowB = e * p.n_total + n * BN + (int)rank * C::B_ROWS;
       for (int kb = 0; kb < kblocks; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
-        mbar_expect_tx(&full[stage], STAGE_BYTES);
-        uint8_t* st = sA + stage * STAGE_BYTES;
-        tma_load_2d(st, &tmA, kb * BK, rowA, &full[stage]);
-        tma_load_2d(st + A_BYTES, &tmB, kb * BK, rowB, &full[stage]);
+        uint8_t* st = sA + stage * C::STAGE_BYTES;
+        if constexpr (CG == 2) {
+          if (leader) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+          tma_load_2d_pair(st, &tmA, kb * BK, rowA, &full[stage]);
+          tma_load_2d_pair(st + C::A_BYTES, &tmB, kb * BK, rowB, &full[stage]);
+        } else {
+          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+          tma_load_2d(st, &tmA, kb * BK, rowA, &full[stage]);
+          tma_load_2d(st + C::A_BYTES, &tmB, kb * BK, rowB, &full[stage]);
+        }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ===================== MMA issuer =====================
-    constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+  } else if (warp == 1 && lane == 0 && leader) {
+    // ===================== MMA issuer (leader only) =====================
+    constexpr uint32_t idesc = umma_idesc_bf16(BM * CG, BN);
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int tau = blockIdx.x; tau < ntiles; tau += gridDim.x, ++it) {
+    for (int tau = unit; tau < ntiles; tau += nunits, ++it) {
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
       mbar_wait(&tempty[acc], aph ^ 1);
@@ -178,40 +220,44 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       for (int kb = 0; kb < kblocks; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
-        uint8_t* st = sA + stage * STAGE_BYTES;
+        uint8_t* st = sA + stage * C::STAGE_BYTES;
         const uint64_t ad = umma_desc_sw128(st);
-        const uint64_t bd = umma_desc_sw128(st + A_BYTES);
+        const uint64_t bd = umma_desc_sw128(st + C::A_BYTES);
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k)  // +32 B along K inside the 128 B swizzle atom
-          mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
-        mma_commit(&empty[stage]);
+        for (int k = 0; k < BK / 16; ++k) {  // +32 B along K inside the 128 B swizzle atom
+          if constexpr (CG == 2) mma_bf16_pair(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          else mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+        }
+        if constexpr (CG == 2) mma_commit_pair(&empty[stage]);
+        else mma_commit(&empty[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      mma_commit(&tfull[acc]);
+      if constexpr (CG == 2) mma_commit_pair(&tfull[acc]);
+      else mma_commit(&tfull[acc]);
     }
   } else if (warp >= 4) {
-    // ===================== epilogue =====================
+    // ===================== epilogue (both CTAs, own TMEM rows) ============
     const int q = warp & 3;  // TMEM lanes [32q, 32q+32)
     uint8_t* stg = sEpi + q * EPI_WARP_BYTES;
     int it = 0;
-    for (int tau = blockIdx.x; tau < ntiles; tau += gridDim.x, ++it) {
+    for (int tau = unit; tau < ntiles; tau += nunits, ++it) {
       int e, n, m;
-      decode_tile(seg, p.E_l, p.nt, tau, e, n, m);
+      decode_tile(seg, p.E_l, tau, e, n, m);
+      const int mtile = m * CG + (int)rank;
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-      const int row_in_tile = q * 32 + lane;                    // this thread's TMEM lane
-      const int row_local = m * BM + row_in_tile;               // row within expert segment
+      const int row_local = mtile * BM + q * 32 + lane;         // row within expert segment
       const int row_global = seg.start[e] + row_local;          // row in recv / hbuf
-      const int valid_rows = min(32, max(0, seg.total[e] - (m * BM + q * 32)));
+      const int valid_rows = min(32, max(0, seg.total[e] - (mtile * BM + q * 32)));
 
       // Destination of this thread's row (used by the store loop via shuffles).
       char* rowdst = nullptr;
-      if (p.mode == 0) {
-        rowdst = reinterpret_cast<char*>(p.out) + ((size_t)row_global * p.out_ld + (size_t)n * (BN / 2)) * 2;
-      } else if (row_local < seg.total[e]) {
-        if (p.meta) {
+      if (row_local < seg.total[e]) {
+        if (p.mode == 0) {
+          rowdst = reinterpret_cast<char*>(p.out) + ((size_t)row_global * p.out_ld + (size_t)n * (BN / 2)) * 2;
+        } else if (p.meta) {
           const int2 md = p.meta[row_global];
           rowdst = p.dst[md.x] + ((size_t)md.y * p.out_ld + (size_t)n * BN) * 2;
         } else {
@@ -222,41 +268,48 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       for (int half = 0; half < halves; ++half) {
         // ---- TMEM -> registers -> swizzled staging (16 B units, unit u of
         //      row r lives at r*256 + ((u ^ (r & 15)) * 16)) ----
+        if (valid_rows > 0) {
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t packed[16];
-          if (p.mode == 0) {
-            uint32_t g[32], u[32];
-            tmem_ld32(tbase + c * 32, g);
-            tmem_ld32(tbase + 128 + c * 32, u);
-            tmem_wait_ld();
+          for (int c = 0; c < 4; ++c) {
+            uint32_t packed[16];
+            if (p.mode == 0) {
+              uint32_t g[32], u[32];
+              tmem_ld32(tbase + c * 32, g);
+              tmem_ld32(tbase + 128 + c * 32, u);
+              tmem_wait_ld();
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              float g0 = __uint_as_float(g[2 * j]), g1 = __uint_as_float(g[2 * j + 1]);
-              float u0 = __uint_as_float(u[2 * j]), u1 = __uint_as_float(u[2 * j + 1]);
-              float h0 = g0 / (1.0f + __expf(-g0)) * u0;
-              float h1 = g1 / (1.0f + __expf(-g1)) * u1;
-              packed[j] = pack_bf16x2(h0, h1);
+              for (int j = 0; j < 16; ++j) {
+                float g0 = __uint_as_float(g[2 * j]), g1 = __uint_as_float(g[2 * j + 1]);
+                float u0 = __uint_as_float(u[2 * j]), u1 = __uint_as_float(u[2 * j + 1]);
+                float h0 = g0 / (1.0f + __expf(-g0)) * u0;
+                float h1 = g1 / (1.0f + __expf(-g1)) * u1;
+                packed[j] = pack_bf16x2(h0, h1);
+              }
+            } else {
+              uint32_t v[32];
+              tmem_ld32(tbase + half * 128 + c * 32, v);
+              tmem_wait_ld();
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                packed[j] = pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
             }
-          } else {
-            uint32_t v[32];
-            tmem_ld32(tbase + half * 128 + c * 32, v);
-            tmem_wait_ld();
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-              packed[j] = pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
-          }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int u = c * 4 + j;
-            uint4 val = make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
-            *reinterpret_cast<uint4*>(stg + lane * 256 + ((u ^ (lane & 15)) * 16)) = val;
+            for (int j = 0; j < 4; ++j) {
+              const int u = c * 4 + j;
+              uint4 val = make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
+              *reinterpret_cast<uint4*>(stg + lane * 256 + ((u ^ (lane & 15)) * 16)) = val;
+            }
           }
         }
         if (half == halves - 1) {
           // accumulator fully read: hand the TMEM buffer back to the MMA warp
+          // (one arrival per warp; a pair's peer arrives on the leader's barrier)
           tc_fence_before();
-          mbar_arrive(&tempty[acc]);
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+            else mbar_arrive(&tempty[acc]);
+          }
         }
         __syncwarp();
         // ---- coalesced row stores: 2 rows per instruction, 256 B per row ----
@@ -271,14 +324,17 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         }
         __syncwarp();
       }
-      (void)row_in_tile;
     }
   }
 
   // ---- teardown + completion signal --------------------------------------
   tc_fence_before();
-  __syncthreads();
-  if (warp == 2) tmem_dealloc<TMEM_COLS>(tmem_base);
+  if constexpr (CG == 2) cluster_sync();  // the leader's last commits target both CTAs
+  else __syncthreads();
+  if (warp == 2) {
+    if constexpr (CG == 2) tmem_dealloc2<TMEM_COLS>(tmem_base);
+    else tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
   if (p.n_sig > 0 && threadIdx.x == 0) {
     __threadfence_system();
     s_last = (atomicAdd(p.ticket, 1u) == gridDim.x - 1);
@@ -359,22 +415,52 @@ int num_sms() {
   return n;
 }
 
-int grouped_gemm_launch(const GemmLaunch& L, cudaStream_t st) {
-  MSI_REQUIRE(L.p.E_l >= 1 && L.p.E_l <= MSI_MAX_LOCAL_EXPERTS, "grouped_gemm: E_l out of range");
-  MSI_REQUIRE(L.p.kdim % BK == 0 && L.p.n_total % BN == 0, "grouped_gemm: K %% 64 and N %% 256 required");
+template <int CG>
+int launch_cg(const GemmLaunch& L, cudaStream_t st) {
+  using C = Cfg<CG>;
   CUtensorMap ta, tb;
   int rc = make_tmap(&ta, L.a, (uint64_t)L.p.kdim, (uint64_t)L.a_rows, BK, BM);
   if (rc) return rc;
-  rc = make_tmap(&tb, L.b, (uint64_t)L.p.kdim, (uint64_t)L.p.E_l * L.p.n_total, BK, BN);
+  rc = make_tmap(&tb, L.b, (uint64_t)L.p.kdim, (uint64_t)L.p.E_l * L.p.n_total, BK, C::B_ROWS);
   if (rc) return rc;
   static bool attr = false;
   if (!attr) {
-    MSI_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+    MSI_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     attr = true;
   }
-  const int grid = L.grid > 0 ? L.grid : num_sms();
-  grouped_gemm_kernel<<<grid, kThreads, SMEM_BYTES, st>>>(ta, tb, L.p);
+  int grid = L.grid > 0 ? L.grid : num_sms();
+  grid -= grid % CG;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = CG;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = CG == 2 ? 1 : 0;
+  MSI_CUDA(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<CG>, ta, tb, L.p));
   return check_launch("grouped_gemm_kernel");
+}
+
+// CTA-group selection: MSI_GEMM_CG=1|2 overrides; default = the pair kernel.
+int default_cg() {
+  static int cg = 0;
+  if (!cg) {
+    const char* v = getenv("MSI_GEMM_CG");
+    cg = (v && v[0] == '1') ? 1 : 2;
+  }
+  return cg;
+}
+
+int grouped_gemm_launch(const GemmLaunch& L, cudaStream_t st) {
+  MSI_REQUIRE(L.p.E_l >= 1 && L.p.E_l <= MSI_MAX_LOCAL_EXPERTS, "grouped_gemm: E_l out of range");
+  MSI_REQUIRE(L.p.kdim % BK == 0 && L.p.n_total % BN == 0, "grouped_gemm: K %% 64 and N %% 256 required");
+  const int cg = L.cta_group ? L.cta_group : default_cg();
+  return cg == 1 ? launch_cg<1>(L, st) : launch_cg<2>(L, st);
 }
 
 int pack_w13(const void* gate, const void* up, void* out, int E_l, int inter, int hidden, cudaStream_t st) {

@@ -48,6 +48,7 @@ struct GemmLaunch {
   int64_t a_rows;
   const void* b;   // [E_l * n_total][kdim] bf16
   int grid;        // 0 = one CTA per SM
+  int cta_group;   // 1: 128x256 tiles per CTA; 2: 256x256 tiles per CTA pair; 0 = default
   GemmParams p;
 };
 
