@@ -446,12 +446,15 @@ int launch_cg(const GemmLaunch& L, cudaStream_t st) {
   return check_launch("grouped_gemm_kernel");
 }
 
-// CTA-group selection: MSI_GEMM_CG=1|2 overrides; default = the pair kernel.
+// CTA-group selection: MSI_GEMM_CG=1|2 overrides; default = the 1-CTA kernel,
+// which measured equal or faster on B200 (profiles/r01_gemm_cg_ab.jsonl: both
+// run at the power-capped tensor rate for t_e >= 768, and pairing M tiles
+// adds padding at small t_e).
 int default_cg() {
   static int cg = 0;
   if (!cg) {
     const char* v = getenv("MSI_GEMM_CG");
-    cg = (v && v[0] == '1') ? 1 : 2;
+    cg = (v && v[0] == '2') ? 2 : 1;
   }
   return cg;
 }
