@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--attn", default="standin", choices=["standin", "none"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-merge", dest="merge", action="store_false",
+                    help="N=1 co-located: keep m separate micro-batches instead of one merged batch")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch eagerly from Python instead of replaying a captured CUDA graph")
     return ap.parse_args()
@@ -212,7 +214,14 @@ def main():
         sys.exit(2)
     n_a, n_e, colo = SPLITS[world]
     model = as_model_spec(args.shape)
-    plan = DeploymentPlan(n_a=n_a, n_e=n_e, m=args.m, b_a=args.b_a, colocated=colo)
+    m_eff, b_a = args.m, args.b_a
+    if colo and args.merge:
+        # One co-located GPU has no ping-pong partner: its m micro-batches are
+        # merged into one batch (same tokens per step, expert weights streamed
+        # once per layer instead of m times).
+        m_eff, b_a = 1, args.m * args.b_a
+    args.b_a = b_a
+    plan = DeploymentPlan(n_a=n_a, n_e=n_e, m=m_eff, b_a=b_a, colocated=colo)
     dev = torch.device(f"cuda:{local}")
     g = runtime.M2NGroup(model, plan, rank=rank, device=dev)
     wg, w13, w2 = runtime.synth_device_weights(model, runtime.local_experts(g), seed=0, device=dev)
@@ -344,6 +353,9 @@ def main():
                    ("co-located 1 GPU" if colo else f"{n_a} attention + {n_e} expert GPUs"),
                    "hidden": model.hidden, "intermediate": model.intermediate, "experts": model.experts,
                    "topk": model.topk, "n_a": n_a, "n_e": n_e, "m": plan.m, "b_a": args.b_a,
+                   "tokens_per_step_per_attention_gpu": plan.m * args.b_a * args.layers,
+                   "microbatching": ("co-located: m micro-batches merged into one batch (no ping-pong partner)"
+                                     if colo and args.merge else "ping-pong, m micro-batches"),
                    "L_sim": args.layers, "attention_stage": args.attn,
                    "l2": "working set (weights 4.8 GB + KV stand-in) >> 126 MB L2; no flush needed",
                    "parallelism": f"dp{n_a}-ep{n_e}",
