@@ -45,9 +45,12 @@ constexpr int TMEM_COLS = 512;
 // tile with tcgen05.mma.cta_group::2; each CTA stages its 128 A rows and half
 // of B (128 rows) -- 32 KB -- so per-SM shared-memory traffic per MAC is 2/3
 // of the CG=1 kernel's and 6 stages fit.
-template <int CG>
+// MAXE = capacity of the per-expert segment table in shared memory; the
+// 256-expert variant (fine-grained MoE on few GPUs) gives one pipeline stage
+// to the larger table.
+template <int CG, int MAXE>
 struct Cfg {
-  static constexpr int STAGES = CG == 1 ? 4 : 6;
+  static constexpr int STAGES = (CG == 1 ? 4 : 6) - (MAXE > MSI_SMALL_LOCAL_EXPERTS ? 1 : 0);
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_ROWS = BN / CG;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
@@ -55,26 +58,33 @@ struct Cfg {
   static constexpr size_t SMEM = 1024 /*align*/ + (size_t)STAGES * STAGE_BYTES + 4 * EPI_WARP_BYTES + 256;
 };
 
+template <int MAXE>
 struct SegInfo {
-  int total[MSI_MAX_LOCAL_EXPERTS];
-  int start[MSI_MAX_LOCAL_EXPERTS];
-  int tile0[MSI_MAX_LOCAL_EXPERTS + 1];  // first tile of expert e
-  int mtiles[MSI_MAX_LOCAL_EXPERTS];     // M tiles (CG=1) or M-tile pairs (CG=2)
+  int total[MAXE];
+  int start[MAXE];
+  int tile0[MAXE + 1];  // first tile of expert e
+  int mtiles[MAXE];     // M tiles (CG=1) or M-tile pairs (CG=2)
 };
 
-__device__ __forceinline__ void decode_tile(const SegInfo& s, int E_l, int tau, int& e, int& n, int& m) {
-  e = 0;
-  while (e + 1 < E_l && tau >= s.tile0[e + 1]) ++e;
+template <int MAXE>
+__device__ __forceinline__ void decode_tile(const SegInfo<MAXE>& s, int E_l, int tau, int& e, int& n, int& m) {
+  int lo = 0, hi = E_l - 1;  // last e with tile0[e] <= tau (binary search, E_l up to 256)
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (s.tile0[mid] <= tau) lo = mid;
+    else hi = mid - 1;
+  }
+  e = lo;
   const int local = tau - s.tile0[e];
   n = local / s.mtiles[e];
   m = local - n * s.mtiles[e];
 }
 
-template <int CG>
+template <int CG, int MAXE>
 __global__ void __launch_bounds__(kThreads, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const GemmParams p) {
-  using C = Cfg<CG>;
+  using C = Cfg<CG, MAXE>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -86,7 +96,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   uint64_t* tfull = bars + 2 * STAGES;       // [2]
   uint64_t* tempty = bars + 2 * STAGES + 2;  // [2]   (CG=2: the leader's is used)
   __shared__ uint32_t s_tmem;
-  __shared__ SegInfo seg;
+  __shared__ SegInfo<MAXE> seg;
   __shared__ int s_last, s_abort;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -415,9 +425,9 @@ int num_sms() {
   return n;
 }
 
-template <int CG>
+template <int CG, int MAXE>
 int launch_cg(const GemmLaunch& L, cudaStream_t st) {
-  using C = Cfg<CG>;
+  using C = Cfg<CG, MAXE>;
   CUtensorMap ta, tb;
   int rc = make_tmap(&ta, L.a, (uint64_t)L.p.kdim, (uint64_t)L.a_rows, BK, BM);
   if (rc) return rc;
@@ -425,7 +435,8 @@ int launch_cg(const GemmLaunch& L, cudaStream_t st) {
   if (rc) return rc;
   static bool attr = false;
   if (!attr) {
-    MSI_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    MSI_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<CG, MAXE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)C::SMEM));
     attr = true;
   }
   int grid = L.grid > 0 ? L.grid : num_sms();
@@ -442,7 +453,7 @@ int launch_cg(const GemmLaunch& L, cudaStream_t st) {
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = CG == 2 ? 1 : 0;
-  MSI_CUDA(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<CG>, ta, tb, L.p));
+  MSI_CUDA(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<CG, MAXE>, ta, tb, L.p));
   return check_launch("grouped_gemm_kernel");
 }
 
@@ -463,7 +474,9 @@ int grouped_gemm_launch(const GemmLaunch& L, cudaStream_t st) {
   MSI_REQUIRE(L.p.E_l >= 1 && L.p.E_l <= MSI_MAX_LOCAL_EXPERTS, "grouped_gemm: E_l out of range");
   MSI_REQUIRE(L.p.kdim % BK == 0 && L.p.n_total % BN == 0, "grouped_gemm: K %% 64 and N %% 256 required");
   const int cg = L.cta_group ? L.cta_group : default_cg();
-  return cg == 1 ? launch_cg<1>(L, st) : launch_cg<2>(L, st);
+  if (L.p.E_l > MSI_SMALL_LOCAL_EXPERTS)
+    return cg == 1 ? launch_cg<1, MSI_MAX_LOCAL_EXPERTS>(L, st) : launch_cg<2, MSI_MAX_LOCAL_EXPERTS>(L, st);
+  return cg == 1 ? launch_cg<1, MSI_SMALL_LOCAL_EXPERTS>(L, st) : launch_cg<2, MSI_SMALL_LOCAL_EXPERTS>(L, st);
 }
 
 int pack_w13(const void* gate, const void* up, void* out, int E_l, int inter, int hidden, cudaStream_t st) {

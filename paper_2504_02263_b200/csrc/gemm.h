@@ -7,7 +7,8 @@
 
 #include "../../include/msinfer.h"
 
-#define MSI_MAX_LOCAL_EXPERTS 64
+#define MSI_MAX_LOCAL_EXPERTS 256  /* DeepSeek-V3 shape on one GPU */
+#define MSI_SMALL_LOCAL_EXPERTS 64 /* GEMM variant with the deeper pipeline */
 
 namespace msi {
 

@@ -215,18 +215,25 @@ dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32
   if (s_abort) return;
   if (blockIdx.x == 0 && tid == 0) trace_stamp(c.trace, 1);
   // ---- row base per expert: 128-aligned segment start + rows of senders < s
+  //      (per expert in parallel, then a short prefix per expert GPU)
+  uint32_t* s_pad = s_cnt + c.n_a * c.E;  // [E] padded segment sizes
+  for (int e = tid; e < c.E; e += blockDim.x) {
+    long long total = 0, before = 0;
+    for (int s2 = 0; s2 < c.n_a; ++s2) {
+      const long long v = s_cnt[s2 * c.E + e];
+      total += v;
+      if (s2 < s) before += v;
+    }
+    s_rowbase[e] = before;
+    s_pad[e] = (uint32_t)((total + MSI_ROW_ALIGN - 1) / MSI_ROW_ALIGN * MSI_ROW_ALIGN);
+  }
+  __syncthreads();
   for (int q = tid; q < c.n_e; q += blockDim.x) {
     long long run = 0;
     for (int el = 0; el < c.E_l; ++el) {
       const int e = q * c.E_l + el;
-      long long total = 0, before = 0;
-      for (int s2 = 0; s2 < c.n_a; ++s2) {
-        const long long v = s_cnt[s2 * c.E + e];
-        total += v;
-        if (s2 < s) before += v;
-      }
-      s_rowbase[e] = run + before;
-      run += (total + MSI_ROW_ALIGN - 1) / MSI_ROW_ALIGN * MSI_ROW_ALIGN;
+      s_rowbase[e] += run;
+      run += s_pad[e];
     }
   }
   __syncthreads();
@@ -639,7 +646,8 @@ extern "C" int msi_dispatch(msi_ctx* c, const void* x, const int32_t* cnt, const
   MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots && epoch != 0xffffffffu, "msi_dispatch: bad slot/epoch");
   MSI_REQUIRE(x && cnt && idx && slot, "msi_dispatch: null pointer");
   // row bases [E] (long long) + the all-gathered count table [n_a][E] (u32)
-  const size_t smem = sizeof(long long) * c->plan.experts + sizeof(uint32_t) * c->plan.n_a * c->plan.experts;
+  const size_t smem = sizeof(long long) * c->plan.experts +
+                      sizeof(uint32_t) * (c->plan.n_a + 1) * c->plan.experts;  // + padded sizes
   // ~64 KB of row stores per CTA, at most one CTA per SM (rows are split into
   // parts so every warp has work); small micro-batches use few CTAs, which keeps
   // the last-CTA release cheap

@@ -26,7 +26,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, n_a, n_e, shape, tokens, m, layers, outdir):
+def _worker(rank, world, port, n_a, n_e, colo, shape, tokens, m, layers, outdir):
     import sys
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
@@ -38,7 +38,7 @@ def _worker(rank, world, port, n_a, n_e, shape, tokens, m, layers, outdir):
     torch.cuda.set_device(rank)
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     model = as_model_spec(shape)
-    plan = DeploymentPlan(n_a=n_a, n_e=n_e, m=m, b_a=max(tokens))
+    plan = DeploymentPlan(n_a=n_a, n_e=n_e, m=m, b_a=max(tokens), colocated=colo)
     g = runtime.M2NGroup(model, plan, rank=rank, device=f"cuda:{rank}", timeout_s=30)
     wts = O.synth_weights(model.hidden, model.intermediate, model.experts, seed=0)
 
@@ -86,27 +86,33 @@ def _worker(rank, world, port, n_a, n_e, shape, tokens, m, layers, outdir):
     dist.destroy_process_group()
 
 
+# fine-grained shape (DeepSeek-V3-like routing: many experts, top-8) small enough for the oracle
+FINE = {"name": "fine", "layers": 1, "hidden": 512, "intermediate": 256, "experts": 64, "topk": 8}
+
 PLANS = [
-    # (n_a, n_e, shape, tokens per attention rank, m, layers)
-    (1, 1, "tiny", [64], 2, 2),
-    (3, 1, "tiny", [64, 40, 17], 2, 2),
-    (2, 2, "tiny", [48, 64], 2, 2),
-    (6, 2, "tiny", [64, 64, 33, 64, 1, 50], 3, 2),
+    # (n_a, n_e, colocated, shape, tokens per attention rank, m, layers)
+    (1, 1, False, "tiny", [64], 2, 2),
+    (3, 1, False, "tiny", [64, 40, 17], 2, 2),
+    (2, 2, False, "tiny", [48, 64], 2, 2),
+    (6, 2, False, "tiny", [64, 64, 33, 64, 1, 50], 3, 2),
+    (2, 2, True, FINE, [64, 37], 2, 2),            # co-located 2 -> 2 (config 5 pattern)
+    (4, 4, True, FINE, [16, 64, 1, 40], 2, 1),      # co-located 4 -> 4, 16 experts per GPU
 ]
 
 
-@pytest.mark.parametrize("n_a,n_e,shape,tokens,m,layers", PLANS)
-def test_m2n_multi_gpu(lib, tmp_path, n_a, n_e, shape, tokens, m, layers):
+@pytest.mark.parametrize("n_a,n_e,colo,shape,tokens,m,layers", PLANS)
+def test_m2n_multi_gpu(lib, tmp_path, n_a, n_e, colo, shape, tokens, m, layers):
     import torch.multiprocessing as mp
 
     from oracle import oracle as O
     from paper_2504_02263_b200.config import as_model_spec
 
-    world = n_a + n_e
+    world = n_a if colo else n_a + n_e
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs, box has {torch.cuda.device_count()}")
     port = _free_port()
-    mp.spawn(_worker, args=(world, port, n_a, n_e, shape, tokens, m, layers, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, port, n_a, n_e, colo, shape, tokens, m, layers, str(tmp_path)), nprocs=world,
+             join=True)
     model = as_model_spec(shape)
     wts = O.synth_weights(model.hidden, model.intermediate, model.experts, seed=0)
     got = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(world)]
@@ -132,6 +138,6 @@ def test_m2n_multi_gpu(lib, tmp_path, n_a, n_e, shape, tokens, m, layers):
                 T = tokens[s]
                 for t in range(T):
                     for k in range(model.topk):
-                        er = got[n_a + q[t, k]]
+                        er = got[(0 if colo else n_a) + q[t, k]]
                         np.testing.assert_array_equal(er[f"recv_{l}_{j}"][rows[t, k]], xs[s][t])
                         np.testing.assert_array_equal(er[f"meta_{l}_{j}"][rows[t, k]], [s, t * model.topk + k])

@@ -335,3 +335,24 @@ def test_stale_explicit_epoch_is_rejected(lib):
     torch.cuda.synchronize()
     assert g.status() == -3             # MSI_ESTATE
     g.close()
+
+
+def test_colocated_layer_256_experts(lib):
+    """Fine-grained routing (E=256, top-8) with all 256 experts on one GPU:
+    exercises the large segment-table GEMM variant and the E=256 router."""
+    shape = {"name": "fine256", "layers": 1, "hidden": 512, "intermediate": 256, "experts": 256, "topk": 8}
+    g, layer, wts, model = _colocated_layer(shape, b_a=96)
+    x = O.synth_tokens(96, model.hidden, seed=12)
+    xd = to_dev(x)
+    r = layer.router(xd, 0)
+    layer.dispatch(xd, r, 0)
+    layer.expert_step(0)
+    out = layer.combine(r, resid=xd)
+    torch.cuda.synchronize()
+    assert g.status() == 0
+    ref = O.moe_layer([x], wts, model.topk, n_e=1, resid=True)
+    np.testing.assert_array_equal(r.idx.cpu().numpy(), ref.idx[0])
+    np.testing.assert_array_equal(r.slot.cpu().numpy(), ref.slot[0])
+    assert_close_bf16(to_host(g.ybuf_view(0)[:96]), ref.y[0], "expert outputs")
+    assert_close_bf16(to_host(out), ref.out[0], "layer output")
+    g.close()
