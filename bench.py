@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--attn", default="standin", choices=["standin", "none"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--colocated", action="store_true",
+                    help="every GPU is both an attention and an expert GPU (DeepSeek-V3-shaped config 5)")
     ap.add_argument("--no-merge", dest="merge", action="store_false",
                     help="N=1 co-located: keep m separate micro-batches instead of one merged batch")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
@@ -213,6 +215,8 @@ def main():
             print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}))
         sys.exit(2)
     n_a, n_e, colo = SPLITS[world]
+    if args.colocated:  # every GPU holds both roles (config 5: 8 -> 8, 32 experts per GPU)
+        n_a, n_e, colo = world, world, True
     model = as_model_spec(args.shape)
     m_eff, b_a = args.m, args.b_a
     if colo and args.merge:
@@ -357,7 +361,8 @@ def main():
                    "microbatching": ("co-located: m micro-batches merged into one batch (no ping-pong partner)"
                                      if colo and args.merge else "ping-pong, m micro-batches"),
                    "L_sim": args.layers, "attention_stage": args.attn,
-                   "l2": "working set (weights 4.8 GB + KV stand-in) >> 126 MB L2; no flush needed",
+                   "l2": (f"working set (expert weights {model.experts * 3 * model.hidden * model.intermediate * 2 / 1e9:.1f} GB"
+                          " + KV stand-in) >> 126 MB L2; no flush needed"),
                    "parallelism": f"dp{n_a}-ep{n_e}",
                    "launch": "CUDA graph per rank (device-tracked epochs)" if args.graph else "eager"},
         "roofline": {"bound": "tensor", "kernel": "expert FFN (grouped_gemm_kernel x2: gate/up+SiLU, down+N2M)",
