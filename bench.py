@@ -41,7 +41,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--shape", default="mixtral-8x22b")
     ap.add_argument("--b-a", type=int, default=1024)
-    ap.add_argument("--m", type=int, default=3)
+    # (not "--m": torchrun would take it as an abbreviation of its own options)
+    ap.add_argument("--micro-batches", dest="m", type=int, default=3, help="m, micro-batches per step")
     ap.add_argument("--layers", type=int, default=4, help="L_sim layers per step")
     ap.add_argument("--attn", default="standin", choices=["standin", "none"])
     ap.add_argument("--no-e2e", action="store_true")
