@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--attn", default="standin", choices=["standin", "none"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--timeline-csv", default="",
+                    help="write the SPEC timeline CSV of the last timed step ('{rank}' is substituted)")
     ap.add_argument("--colocated", action="store_true",
                     help="every GPU is both an attention and an expert GPU (DeepSeek-V3-shaped config 5)")
     ap.add_argument("--no-merge", dest="merge", action="store_false",
@@ -155,6 +157,31 @@ def cpu_sample(model, b_a: int, threads: int) -> dict:
                       f"({rows} rows) x{E}, combine; numpy/OpenBLAS fp32 + C oracle"}
 
 
+def eq5_report(all_stages: list, plan, L: int, ms_per_step: float, colocated: bool) -> dict:
+    """Measured T_a / T_e (medians over micro-batches and layers, max over the
+    GPUs of a role) against the reference's closed form Eq. 5 (PAPER.md:237,
+    SPEC.md:246-254): T_total = (T_a + T_e + 2 T_c) + T_f (m L - 1).  T_c is 0
+    here: dispatch and the N2M send run on SMs inside T_a and T_e."""
+    from paper_2504_02263_b200.pipeline import StageTimes, closed_form_total, simulate
+
+    t_a = max((s.get("T_a", 0.0) for s in all_stages), default=0.0)
+    t_e = max((s.get("T_e", 0.0) for s in all_stages), default=0.0)
+    comb = max((s.get("comb", 0.0) for s in all_stages), default=0.0)
+    rep = {"T_a_ms": t_a, "T_e_ms": t_e, "comb_ms": comb, "m": plan.m, "L": L, "T_c_ms": 0.0}
+    if colocated:
+        # both stages share one GPU: no overlap, the step is the sum
+        pred = plan.m * L * (t_a + t_e + comb)
+        rep.update(model="co-located sum m*L*(T_a+T_e+comb)", predicted_ms=pred)
+    else:
+        st = StageTimes(t_a, t_e, 0.0)
+        pred = closed_form_total(st, plan.m, L)
+        rep.update(model="Eq. 5 closed_form_total", predicted_ms=pred,
+                   simulated_ms=simulate(st, plan.m, L).total_latency)
+    rep["measured_ms"] = ms_per_step
+    rep["measured_over_predicted"] = ms_per_step / pred if pred else None
+    return rep
+
+
 def cpu_model_name() -> str:
     try:
         with open("/proc/cpuinfo") as fh:
@@ -237,7 +264,8 @@ def main():
     if args.attn == "standin" and g.is_attention:
         # decode-attention HBM load of one micro-batch: b_a tokens x s x (K,V) x h/g x bf16
         kv_bytes = args.b_a * wl.avg_seq_len * 2 * (model.hidden // model.gqa_group) * 2
-    runner = runtime.PingPongRunner(layer, layers=args.layers, kv_bytes=kv_bytes, chain=False)
+    runner = runtime.PingPongRunner(layer, layers=args.layers, kv_bytes=kv_bytes, chain=False,
+                                    record_timeline=True)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1 + rank)
     xs = [torch.randn((args.b_a, model.hidden), generator=gen, device=dev).to(torch.bfloat16)
@@ -304,6 +332,21 @@ def main():
         dist.all_reduce(tmax[1:], op=dist.ReduceOp.SUM)
         t = tmax
     elapsed_ms, ffn_total_ms, ffn_n, rows_total, calls_total = t.tolist()
+
+    # ---- measured stage times vs the reference's timing model (Eq. 5) ----
+    stages = runner.stage_times_ms()
+    all_stages = [stages]
+    if world > 1:
+        all_stages = [None] * world
+        dist.all_gather_object(all_stages, stages)
+    if args.timeline_csv:  # SPEC.md:232 schema, one file per rank (events are per-GPU clocks)
+        import csv as _csv
+        path = args.timeline_csv.replace("{rank}", str(rank))
+        with open(path, "w", newline="") as fh:
+            wcsv = _csv.writer(fh)
+            wcsv.writerow(["resource", "microbatch", "layer", "phase", "start_s", "end_s"])
+            for ph, j, l, s, e in runner.timeline():
+                wcsv.writerow([f"gpu{rank}:{g.role}", j, l, ph, s / 1e3, e / 1e3])
 
     # ---- e2e through the public API with host buffers -------------------
     e2e = None
@@ -374,6 +417,7 @@ def main():
         "e2e": e2e,
         "gpu_launches": None,
         "clocks": clocks,
+        "stage_times": eq5_report(all_stages, plan, args.layers, elapsed_ms / args.steps, colo),
     }
     # our kernels inside the timed region (per rank, summed over roles)
     per_step = plan.m * args.layers * (launches_per_mbl if colo else 0)

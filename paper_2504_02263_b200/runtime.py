@@ -325,7 +325,9 @@ class PingPongRunner:
 
     def _ev(self, tag):
         if self.record:
-            e = torch.cuda.Event(enable_timing=True)
+            # external: inside a CUDA-graph capture the record becomes a graph
+            # node, so every replay re-stamps it (read after the last replay)
+            e = torch.cuda.Event(enable_timing=True, external=True)
             e.record()
             self.events.append((tag, e))
 
@@ -372,8 +374,6 @@ class PingPongRunner:
         """Capture one step into a CUDA graph.  Epochs switch to device-tracked
         mode (epoch 0 in the ABI), so every replay is the next use of each slot
         and peers stay in lock-step through their own graphs' device waits."""
-        if self.record:
-            raise ValueError("timeline recording is eager-only")
         self.layer.device_epochs = True
         side = torch.cuda.Stream(device=self.layer.g.device)
         side.wait_stream(torch.cuda.current_stream())
@@ -405,6 +405,26 @@ class PingPongRunner:
                 s = opened.pop((ph, j, l))
                 rows.append((ph, j, l, t0.elapsed_time(s), t0.elapsed_time(ev)))
         return rows
+
+    def stage_times_ms(self) -> dict:
+        """Median per-(micro-batch, layer) duration of each phase (ms) from the
+        last recorded step: attention-side work T_a = attn + disp (router and
+        M2N send run on the attention GPU's SMs), expert T_e = ffn (both GEMMs,
+        N2M send in the GEMM2 epilogue), comb = the combine kernel including
+        its wait for the expert GPUs."""
+        import statistics
+
+        per = {}
+        for ph, j, l, s, e in self.timeline():
+            per.setdefault(ph, {})[(j, l)] = e - s
+        out = {ph: statistics.median(v.values()) for ph, v in per.items()}
+        if "attn" in per or "disp" in per:
+            keys = set(per.get("attn", {})) | set(per.get("disp", {}))
+            out["T_a"] = statistics.median(per.get("attn", {}).get(k, 0.0) + per.get("disp", {}).get(k, 0.0)
+                                           for k in keys)
+        if "ffn" in per:
+            out["T_e"] = out["ffn"]
+        return out
 
 
 def synth_device_weights(model: MoeModelSpec, experts, seed: int = 0, device="cuda"):
