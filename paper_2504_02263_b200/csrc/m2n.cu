@@ -29,6 +29,7 @@
 //   meta   : (expert role)    [slot][cap] int2 (sender, t*K + k)
 //   cap = n_a * max_tokens * min(K, E_l) + E_l * (ROW_ALIGN - 1), rounded to 128.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -172,11 +173,30 @@ int validate(const msi_plan& p) {
 // ------------------------------------------------------------ dispatch ----
 constexpr int kDispThreads = 512;
 
+// Dynamic smem of the dispatch kernel: row bases [E] (i64), counts [n_a][E]
+// and padded sizes [E] (u32); the TMA variant adds one row buffer + mbarrier
+// per warp after a 128-B aligned offset.
+__host__ __device__ inline size_t disp_table_bytes(int E, int n_a) {
+  return ((size_t)E * 8 + (size_t)(n_a + 1) * E * 4 + 127) & ~size_t(127);
+}
+
+// Copy engine of the dispatch: MSI_DISPATCH=tma selects TMA bulk copies
+// (cp.async.bulk global->smem->peer), otherwise SM 16-B vector stores.
+bool dispatch_uses_tma() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MSI_DISPATCH");
+    v = (e && e[0] == 't') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+template <bool TMA>
 __global__ void __launch_bounds__(kDispThreads)
 dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ cnt,
                 const int32_t* __restrict__ idx, const int32_t* __restrict__ slot, int T, int mb,
                 uint32_t epoch) {
-  extern __shared__ long long s_rowbase[];  // [E] first row of this sender in expert e's segment
+  extern __shared__ __align__(128) long long s_rowbase[];  // [E] first row of this sender in expert e's segment
   __shared__ int s_abort;
   const int tid = threadIdx.x;
   epoch = resolve_epoch(epoch, c.my_ause + mb * CTR_STRIDE, 1u, c.my_status);
@@ -238,16 +258,55 @@ dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32
   }
   __syncthreads();
 
-  // ---- copy rows: a warp moves one part of one token row (x read once,
-  //      written K times with 16 B stores, 8 x 512 B in flight per warp)
   const int lane = tid & 31;
   const int gwarp = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
   const int nwarps = gridDim.x * (blockDim.x >> 5);
+  const size_t row_bytes = (size_t)c.H * 2;
+  if constexpr (TMA) {
+    // ---- copy rows with the TMA engine: one bulk load of x[t] into this
+    //      warp's smem buffer, then K bulk stores straight into the expert
+    //      GPUs' receive rows (NVLink peer memory); one lane per warp drives it
+    char* buf = reinterpret_cast<char*>(s_rowbase) + disp_table_bytes(c.E, c.n_a) + (size_t)(tid >> 5) * row_bytes;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(s_rowbase) + disp_table_bytes(c.E, c.n_a) +
+                                                (size_t)(blockDim.x >> 5) * row_bytes) + (tid >> 5);
+    if (lane == 0) {
+      mbar_init(bar, 1);
+      fence_barrier_init();
+    }
+    __syncwarp();
+    uint32_t phase = 0;
+    for (int t = gwarp; t < T; t += nwarps) {
+      if (lane < c.K) {  // metadata of (t, lane)
+        const int e = idx[(size_t)t * c.K + lane];
+        const long long row = s_rowbase[e] + slot[(size_t)t * c.K + lane];
+        c.meta_of[e / c.E_l][(size_t)mb * c.cap + row] = make_int2(s, t * c.K + lane);
+      }
+      if (lane == 0) {
+        bulk_wait_read0();  // the previous token's stores have read the buffer
+        mbar_expect_tx(bar, (uint32_t)row_bytes);
+        bulk_g2s(buf, x + (size_t)t * c.H, (uint32_t)row_bytes, bar);
+        mbar_wait(bar, phase);
+        for (int k = 0; k < c.K; ++k) {
+          const int e = idx[(size_t)t * c.K + k];
+          const long long row = s_rowbase[e] + slot[(size_t)t * c.K + k];
+          bulk_s2g(c.recv_of[e / c.E_l] + ((size_t)mb * c.cap + row) * row_bytes, buf, (uint32_t)row_bytes);
+        }
+        bulk_commit();
+      }
+      phase ^= 1;
+      __syncwarp();
+    }
+    if (lane == 0) {
+      bulk_wait0();                // every bulk store has completed its writes
+      fence_proxy_async_global();  // order them before the generic-proxy release below
+    }
+  } else {
+  // ---- copy rows: a warp moves one part of one token row (x read once,
+  //      written K times with 16 B stores, 8 x 512 B in flight per warp)
   const int nchunk = c.H >> 8;  // 512 B warp-chunks per row
   int parts = T > 0 ? (nwarps + T - 1) / T : 1;
   parts = parts < 1 ? 1 : (parts > nchunk ? nchunk : parts);
   const int per_part = (nchunk + parts - 1) / parts;
-  const size_t row_bytes = (size_t)c.H * 2;
   for (int item = gwarp; item < T * parts; item += nwarps) {
     const int t = item / parts, part = item - t * parts;
     // lane k (< K) resolves destination k
@@ -275,6 +334,7 @@ dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32
       }
     }
   }
+  }  // copy variant
 
   // ---- release: the last CTA bumps every expert GPU's arrival counter
   __syncthreads();
@@ -645,16 +705,31 @@ extern "C" int msi_dispatch(msi_ctx* c, const void* x, const int32_t* cnt, const
   MSI_REQUIRE(T >= 0 && T <= c->plan.max_tokens, "msi_dispatch: T=%d exceeds max_tokens=%d", T, c->plan.max_tokens);
   MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots && epoch != 0xffffffffu, "msi_dispatch: bad slot/epoch");
   MSI_REQUIRE(x && cnt && idx && slot, "msi_dispatch: null pointer");
-  // row bases [E] (long long) + the all-gathered count table [n_a][E] (u32)
-  const size_t smem = sizeof(long long) * c->plan.experts +
-                      sizeof(uint32_t) * (c->plan.n_a + 1) * c->plan.experts;  // + padded sizes
-  // ~64 KB of row stores per CTA, at most one CTA per SM (rows are split into
-  // parts so every warp has work); small micro-batches use few CTAs, which keeps
-  // the last-CTA release cheap
+  // row bases [E] (long long) + the all-gathered count table [n_a][E] + padded sizes (u32)
+  const size_t table = disp_table_bytes(c->plan.experts, c->plan.n_a);
   const size_t bytes = (size_t)T * c->plan.topk * c->plan.hidden * 2;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (dispatch_uses_tma()) {
+    // TMA variant: 8 warps per CTA, one token row buffer each, a warp per token
+    constexpr int kThr = 256;
+    const size_t smem = table + (kThr / 32) * ((size_t)c->plan.hidden * 2 + 8);
+    static size_t attr = 0;
+    if (smem > attr) {
+      MSI_CUDA(cudaFuncSetAttribute(dispatch_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = smem;
+    }
+    int grid = (T + kThr / 32 - 1) / (kThr / 32);
+    grid = grid < 1 ? 1 : (grid > 2 * num_sms() ? 2 * num_sms() : grid);
+    dispatch_kernel<true><<<grid, kThr, smem, st>>>(c->dev, reinterpret_cast<const __nv_bfloat16*>(x), cnt, idx,
+                                                    slot, T, mb_slot, epoch);
+    return check_launch("dispatch_kernel<tma>");
+  }
+  // SM-store variant: ~64 KB of row stores per CTA, at most one CTA per SM
+  // (rows are split into parts so every warp has work); small micro-batches
+  // use few CTAs, which keeps the last-CTA release cheap
   int grid = (int)((bytes + 65535) / 65536);
   grid = grid < 1 ? 1 : (grid > num_sms() ? num_sms() : grid);
-  dispatch_kernel<<<grid, kDispThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
+  dispatch_kernel<false><<<grid, kDispThreads, table, st>>>(
       c->dev, reinterpret_cast<const __nv_bfloat16*>(x), cnt, idx, slot, T, mb_slot, epoch);
   return check_launch("dispatch_kernel");
 }
