@@ -43,13 +43,19 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t0 = blockIdx.x * BT;
   const int nchunk = H >> 8;
-  if (WS) {  // stage W_g (E*H*2 bytes, 16 B vectors, coalesced)
-    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<char*>(s_logit) + ((logit_smem_bytes(BT, E) + 15) & ~size_t(15)));
-    const uint4* src = reinterpret_cast<const uint4*>(wg);
-    const int n16 = E * H / 8;
-    for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = __ldg(src + i);
-    wg = reinterpret_cast<const __nv_bfloat16*>(dst);
+  if (WS) {  // stage W_g (E*H*2 bytes) with one TMA bulk copy
+    __shared__ __align__(8) uint64_t s_bar;
+    char* dst = reinterpret_cast<char*>(s_logit) + ((logit_smem_bytes(BT, E) + 15) & ~size_t(15));
+    const uint32_t bytes = (uint32_t)E * H * 2;
+    if (threadIdx.x == 0) {
+      mbar_init(&s_bar, 1);
+      fence_barrier_init();
+      mbar_expect_tx(&s_bar, bytes);
+      bulk_g2s(dst, wg, bytes, &s_bar);
+    }
     __syncthreads();
+    mbar_wait(&s_bar, 0);
+    wg = reinterpret_cast<const __nv_bfloat16*>(dst);
   }
 
   // ---- 1. logits ---------------------------------------------------------
@@ -258,8 +264,10 @@ int gate_topk(const void* x, const void* wg, int T, int H, int E, int K, int32_t
   // is HBM-bound (want many CTAs); large E is FMA-bound (want token reuse).
   if (E % 16 == 0 && E > 16)  // fine-grained MoE: FMA-bound, BT=4 keeps >=148 CTAs busy at small T
     return launch<4, 16>(x, wg, T, H, E, K, T >= 148 * 16 ? 16 : 4, idx, w, cnt, slot, ws, st);
-  if (E % 16 == 0) return launch<1, 16>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, st);
-  if (E % 8 == 0) return launch<1, 8>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, st);
+  // E = 8 / 16: W_g staged once per CTA (TMA bulk copy) and amortised over 32
+  // tokens (4 per warp); x is the only HBM stream
+  if (E % 16 == 0) return launch<4, 16>(x, wg, T, H, E, K, 32, idx, w, cnt, slot, ws, st);
+  if (E % 8 == 0) return launch<4, 8>(x, wg, T, H, E, K, 32, idx, w, cnt, slot, ws, st);
   if (E % 4 == 0) return launch<1, 4>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, st);
   if (E % 2 == 0) return launch<1, 2>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, st);
   return launch<1, 1>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, st);
