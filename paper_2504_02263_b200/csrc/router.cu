@@ -7,11 +7,12 @@
 //      order oracle/msi_oracle.c restates, so routing is bit-exact;
 //   2. top-K per token (warp arg-max, ties to the lower expert), weights =
 //      softmax of the K chosen logits with det_expf (bit-exact as well);
-//   3. the last CTA to finish (ticket) places every (t, k): warps own
-//      contiguous 32-token chunks; in a chunk bit `lane` of mask[e] marks
-//      "token lane chose e", so rank = popc(mask[e] & lanes_below); a count
-//      pass, a scan over warps and a second pass give the final slots and
-//      cnt[E] (warp ballot/popc prefix sums, no global scan).
+//   3. in-CTA ranks (BT <= 32 tokens, one warp): bit `lane` of mask[e] marks
+//      "token lane chose e", so rank = popc(mask[e] & lanes_below); the
+//      CTA's per-expert histogram goes to the workspace;
+//   4. the last CTA to finish (ticket) scans the histograms over CTAs
+//      (independent loads) into per-CTA bases, writes cnt[E] and adds the
+//      bases to every slot.
 // HBM-bound for small E (reads x once); FMA-bound for E = 256 (logits on
 // CUDA cores because the fixed reduction order is the bit-exactness contract).
 #include <cstdio>
@@ -170,64 +171,52 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
   }
   __syncthreads();
 
-  // ---- 3. the last CTA to finish places every (t, k) ----------------------
+  // ---- 3. in-CTA ranks (BT <= 32 tokens = one warp chunk): lane = token,
+  //      bit `lane` of mask[e] says "this token chose e", so the rank of (t,k)
+  //      among the CTA's earlier tokens is popc(mask[e] & lanes_below) -------
+  int32_t* hist = ws + 16;                                   // [nblk][E] CTA histograms
+  int32_t* base = hist + (size_t)gridDim.x * E;              // [nblk][E] CTA bases
+  uint32_t* mask = reinterpret_cast<uint32_t*>(s_logit);     // [E] (logits no longer needed)
+  for (int e = threadIdx.x; e < E; e += blockDim.x) mask[e] = 0u;
+  __syncthreads();
+  if (warp == 0) {
+    const int t = t0 + lane;
+    const bool valid = lane < BT && t < T;
+    if (valid)
+      for (int k = 0; k < K; ++k) atomicOr(&mask[idx_out[(size_t)t * K + k]], 1u << lane);
+    __syncwarp();
+    const uint32_t below = (1u << lane) - 1u;
+    if (valid)
+      for (int k = 0; k < K; ++k)
+        slot_out[(size_t)t * K + k] = __popc(mask[idx_out[(size_t)t * K + k]] & below);
+    __syncwarp();
+    for (int e = lane; e < E; e += 32) hist[(size_t)blockIdx.x * E + e] = __popc(mask[e]);
+  }
+
+  // ---- 4. the last CTA to finish turns CTA histograms into bases (exclusive
+  //      scan over CTAs per expert; independent loads, no serial L2 chain) and
+  //      adds them to every slot; its totals are this sender's counts --------
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) s_last = (atomicAdd(&ws[0], 1) == (int)gridDim.x - 1);
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  // Warp w owns a contiguous range of 32-token chunks.  Inside a chunk,
-  // lane = token and bit `lane` of mask[e] says "this token chose e", so the
-  // rank of (t,k) among earlier tokens of the chunk is popc(mask & lanes_below).
-  // Pass 1 counts per (warp, expert); a scan over warps gives each warp its
-  // starting rank; pass 2 walks the chunks again and emits final slots.
-  uint32_t* wmask = reinterpret_cast<uint32_t*>(s_logit) + warp * E;            // [8][E]
-  int32_t* wcnt = reinterpret_cast<int32_t*>(s_logit) + kWarps * E + warp * E;  // [8][E]
-  for (int e = lane; e < E; e += 32) { wmask[e] = 0u; wcnt[e] = 0; }
-  __syncwarp();
-  const int nchunk_t = (T + 31) >> 5;
-  const int c_lo = (nchunk_t * warp) / kWarps, c_hi = (nchunk_t * (warp + 1)) / kWarps;
-  const uint32_t below = (1u << lane) - 1u;
-  for (int pass = 0; pass < 2; ++pass) {
-    for (int ch = c_lo; ch < c_hi; ++ch) {
-      const int t = ch * 32 + lane;
-      const bool valid = t < T;
-      int myE[32];
-      for (int k = 0; k < K; ++k) {
-        myE[k] = valid ? __ldcg(&idx_out[(size_t)t * K + k]) : 0;
-        if (valid) atomicOr(&wmask[myE[k]], 1u << lane);
-      }
-      __syncwarp();
-      if (valid && pass == 1)
-        for (int k = 0; k < K; ++k)
-          slot_out[(size_t)t * K + k] = wcnt[myE[k]] + __popc(wmask[myE[k]] & below);
-      __syncwarp();
-      if (valid)
-        for (int k = 0; k < K; ++k) {
-          const uint32_t mk = wmask[myE[k]];
-          if ((mk >> lane) == 1u) wcnt[myE[k]] += __popc(mk);  // highest lane of e: once per chunk
-        }
-      __syncwarp();
-      if (valid)
-        for (int k = 0; k < K; ++k) wmask[myE[k]] = 0u;
-      __syncwarp();
+  const int nblk = gridDim.x;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int run = 0;
+#pragma unroll 8
+    for (int b = 0; b < nblk; ++b) {
+      const int c = __ldcg(&hist[(size_t)b * E + e]);
+      base[(size_t)b * E + e] = run;
+      run += c;
     }
-    __syncthreads();
-    if (pass == 0) {
-      // exclusive scan over warps per expert; totals are the sender's counts
-      int32_t* all = reinterpret_cast<int32_t*>(s_logit) + kWarps * E;
-      for (int e = threadIdx.x; e < E; e += blockDim.x) {
-        int run = 0;
-        for (int w = 0; w < kWarps; ++w) {
-          const int c = all[w * E + e];
-          all[w * E + e] = run;
-          run += c;
-        }
-        cnt_out[e] = run;
-      }
-      __syncthreads();
-    }
+    cnt_out[e] = run;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < T * K; i += blockDim.x) {
+    const int b = (i / K) / BT;
+    slot_out[i] = __ldcg(&slot_out[i]) + __ldcg(&base[(size_t)b * E + __ldcg(&idx_out[i])]);
   }
   if (threadIdx.x == 0) ws[0] = 0;  // ticket ready for the next launch
 }
@@ -274,9 +263,8 @@ int gate_topk(const void* x, const void* wg, int T, int H, int E, int K, int32_t
 }
 
 size_t gate_topk_workspace(int T, int E) {
-  (void)T;
-  (void)E;
-  return 16;  // the last-CTA ticket
+  const size_t nblk = ((size_t)T + 3) / 4;  // smallest BT used above
+  return 64 /* ticket + pad */ + 2 * nblk * (size_t)E * sizeof(int32_t);  // CTA histograms + bases
 }
 
 }  // namespace msi
