@@ -202,21 +202,46 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  // (loads are issued in batches of 8 ahead of the dependent stores: the last
+  //  CTA runs alone, so its L2 round trips must overlap)
   const int nblk = gridDim.x;
+  constexpr int U = 8;
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     int run = 0;
-#pragma unroll 8
-    for (int b = 0; b < nblk; ++b) {
-      const int c = __ldcg(&hist[(size_t)b * E + e]);
-      base[(size_t)b * E + e] = run;
-      run += c;
+    for (int b0 = 0; b0 < nblk; b0 += U) {
+      int c[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) c[u] = (b0 + u < nblk) ? __ldcg(&hist[(size_t)(b0 + u) * E + e]) : 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (b0 + u < nblk) {
+          base[(size_t)(b0 + u) * E + e] = run;
+          run += c[u];
+        }
     }
     cnt_out[e] = run;
   }
+  __threadfence_block();
   __syncthreads();
-  for (int i = threadIdx.x; i < T * K; i += blockDim.x) {
-    const int b = (i / K) / BT;
-    slot_out[i] = __ldcg(&slot_out[i]) + __ldcg(&base[(size_t)b * E + __ldcg(&idx_out[i])]);
+  const int TK = T * K, stride = blockDim.x;
+  for (int i0 = threadIdx.x; i0 < TK; i0 += stride * U) {
+    int ex[U], sl[U], bs[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * stride;
+      ex[u] = i < TK ? __ldcg(&idx_out[i]) : 0;
+      sl[u] = i < TK ? __ldcg(&slot_out[i]) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * stride;
+      bs[u] = i < TK ? base[(size_t)((i / K) / BT) * E + ex[u]] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * stride;
+      if (i < TK) slot_out[i] = sl[u] + bs[u];
+    }
   }
   if (threadIdx.x == 0) ws[0] = 0;  // ticket ready for the next launch
 }
