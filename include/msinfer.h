@@ -122,6 +122,17 @@ int msi_gate_topk(const void* x, const void* wg, int T, int H, int E, int K,
                   int32_t* idx, float* w, int32_t* cnt, int32_t* slot,
                   void* workspace, void* stream);
 
+/* Router with replicated experts (load balance; SPEC.md
+ * balance_experts): rep[e*(R+1)] = replica count of logical expert e,
+ * rep[e*(R+1)+1+r] = its r-th physical slot (0 <= slot < P).  Token t of
+ * sender `sender` routed to e goes to replica (t + sender) mod count; pidx
+ * [T,K] gets the physical slot, cnt [P] and slot [T,K] are per physical slot
+ * (idx and w stay logical).  workspace: msi_gate_topk_workspace(T, P). */
+int msi_gate_topk_placed(const void* x, const void* wg, int T, int H, int E, int K,
+                         const int32_t* rep, int R, int P, int sender, int32_t* idx,
+                         int32_t* pidx, float* w, int32_t* cnt, int32_t* slot,
+                         void* workspace, void* stream);
+
 /* ---- (1) M2N dispatch (sender; receiver PAPER.md:408-411)
  * Publishes cnt to every rank, waits for all senders' counts, then stores each
  * row x[t] into the expert GPUs' receive buffers over NVLink peer memory at

@@ -152,6 +152,16 @@ def place(idx: np.ndarray, E: int):
     return cnt, slot
 
 
+def physical_slots(idx: np.ndarray, rep: np.ndarray, sender: int) -> np.ndarray:
+    """Replicated experts: token t of sender s routed to
+    logical expert e goes to replica (t + s) mod rep[e, 0], i.e. physical slot
+    rep[e, 1 + r] -- the rule msi_gate_topk_placed implements."""
+    idx = np.asarray(idx, np.int64)
+    t = np.arange(idx.shape[0])[:, None]
+    r = (t + sender) % rep[idx, 0]
+    return rep[idx, 1 + r].astype(np.int32)
+
+
 # -------------------------------------------------------------- dispatch --- #
 def segment_starts(total: np.ndarray, align: int = ROW_ALIGN) -> np.ndarray:
     """Start row of each local expert's segment: segments are packed in expert
@@ -227,35 +237,46 @@ class LayerResult:
     out: list      # per sender [T,H]
 
 
-def moe_layer(xs: list, wts: LayerWeights, K: int, n_e: int, resid: bool = False) -> LayerResult:
+def moe_layer(xs: list, wts: LayerWeights, K: int, n_e: int, resid: bool = False,
+              rep: np.ndarray | None = None, phys2log: np.ndarray | None = None) -> LayerResult:
     """Full MoE layer step for n_a senders (one micro-batch): route, place,
-    dispatch, SwiGLU experts, combine."""
+    dispatch, SwiGLU experts, combine.  With a replica table ``rep`` [E, R+1]
+    and ``phys2log`` [P] the placement, counts and receive layout are per
+    physical slot (``idx`` stays logical; ``LayerResult.pidx`` holds the
+    slots); every slot runs its logical expert's weights."""
     E = wts.wg.shape[0]
-    E_l = E // n_e
+    P = E if rep is None else len(phys2log)
+    E_l = P // n_e
     H = wts.wg.shape[1]
-    idxs, ws, slots, cnts = [], [], [], []
-    for x in xs:
+    idxs, ws, slots, cnts, pidxs = [], [], [], [], []
+    for s_, x in enumerate(xs):
         i, w = router(x, wts.wg, K)
-        c, s = place(i, E)
-        idxs.append(i), ws.append(w), slots.append(s), cnts.append(c)
+        pi = i if rep is None else physical_slots(i, rep, s_)
+        c, s = place(pi, P)
+        idxs.append(i), ws.append(w), slots.append(s), cnts.append(c), pidxs.append(pi)
     cnt = np.stack(cnts)
     layout = dispatch_layout(cnt, E_l)
-    # gather each expert's rows in receive order, run it, scatter back
+    # gather each slot's rows in receive order, run its expert, scatter back
     ys = [np.empty((x.shape[0], K, H), np.uint16) for x in xs]
-    for e in range(E):
+    for p in range(P):
+        e = p if rep is None else int(phys2log[p])
         srcs = []
-        for s_, (i, sl) in enumerate(zip(idxs, slots)):
-            t, k = np.nonzero(i == e)
+        for s_, (pi, sl) in enumerate(zip(pidxs, slots)):
+            t, k = np.nonzero(pi == p)
             order = np.argsort(sl[t, k], kind="stable")
             srcs.append((s_, t[order], k[order]))
-        rows = np.concatenate([xs[s_][t] for s_, t, _ in srcs]) if srcs else np.zeros((0, H), np.uint16)
+        if e < 0 or not any(len(t) for _, t, _ in srcs):
+            continue
+        rows = np.concatenate([xs[s_][t] for s_, t, _ in srcs])
         y = expert_ffn(rows, wts.w_gate[e], wts.w_up[e], wts.w_down[e])
         off = 0
         for s_, t, k in srcs:
             ys[s_][t, k] = y[off:off + len(t)]
             off += len(t)
     outs = [combine(y, w, x if resid else None) for y, w, x in zip(ys, ws, xs)]
-    return LayerResult(idxs, ws, cnt, slots, layout, ys, outs)
+    res = LayerResult(idxs, ws, cnt, slots, layout, ys, outs)
+    res.pidx = pidxs
+    return res
 
 
 # -------------------------------------------------------- sizing (pins) ---- #

@@ -1,0 +1,164 @@
+"""Expert load balancing with replicated hot experts.
+
+The paper balances expert nodes by minimising the maximum node cost
+C_j = sum_i x_ij * max(a_i, K) with a greedy; the
+reference's SPEC fixes the greedy (module ``balance``):
+
+* ``node_cost(x, loads, k_cold)``
+* ``balance_experts(loads, n, k_cold, mode)`` SPEC.md:407-414 -- LPT; in
+  replicated mode experts whose effective cost exceeds the running average
+  Sum/N are split evenly across up to R replicas, the rest assigned LPT.
+
+``SlotPlacement`` turns a placement into what the B200 runtime executes:
+``P`` physical expert slots, ``P_l`` per expert GPU (contiguous), a
+logical->replica table consumed by ``msi_gate_topk_placed`` (token t of
+sender s goes to replica (t + s) mod nrep -- the even split the placement
+assumes) and the logical expert behind every slot (whose weights it holds).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+MODES = ("integral", "replicated", "fractional")
+
+
+def node_cost(x, loads, k_cold: float = 0.0) -> np.ndarray:
+    """C_j = sum_i x[i, j] * max(a_i, K_cold)."""
+    x = np.asarray(x, dtype=np.float64)
+    eff = np.maximum(np.asarray(loads, dtype=np.float64), k_cold)
+    return eff @ x
+
+
+def balance_experts(loads, n: int, k_cold: float = 0.0, mode: str = "integral",
+                    max_replicas: int = 2) -> np.ndarray:
+    """Greedy placement x[E, N] minimising max_j C_j approximately.
+
+    integral: LPT (largest effective cost first onto the least-loaded node,
+    ties to the lowest node).  replicated: experts above the running average
+    are split evenly over up to ``max_replicas`` distinct nodes (least loaded
+    first), the rest LPT.  fractional: exact water-filling (every node ends at
+    the average)."""
+    if mode not in MODES:
+        raise ValueError(f"mode must be one of {MODES}")
+    if n < 1:
+        raise ValueError("need at least one node")
+    a = np.maximum(np.asarray(loads, dtype=np.float64), k_cold)
+    E = a.size
+    if E == 0:
+        raise ValueError("loads must be non-empty")
+    x = np.zeros((E, n))
+    if mode == "fractional":
+        # water-filling: walk experts in order, pouring each into the nodes
+        # up to the common level avg (exact, every node ends at avg)
+        avg = a.sum() / n
+        j, room = 0, avg
+        for i in range(E):
+            left = a[i]
+            if left == 0:
+                x[i, min(j, n - 1)] = 1.0
+                continue
+            while left > 1e-15 * max(avg, 1.0) and j < n:
+                take = min(left, room)
+                x[i, j] += take / a[i]
+                left -= take
+                room -= take
+                if room <= 1e-15 * max(avg, 1.0):
+                    j, room = j + 1, avg
+            if left > 0 and j >= n:  # rounding remainder
+                x[i, n - 1] += left / a[i]
+        return x / x.sum(1, keepdims=True)
+    order = sorted(range(E), key=lambda i: (-a[i], i))
+    cost = np.zeros(n)
+    avg = a.sum() / n
+    for i in order:
+        split = 1
+        if mode == "replicated" and a[i] > avg and n > 1:
+            split = int(min(max_replicas, n, np.ceil(a[i] / avg)))
+        if split == 1:
+            j = int(np.argmin(cost))
+            x[i, j] = 1.0
+            cost[j] += a[i]
+        else:
+            nodes = sorted(range(n), key=lambda j: (cost[j], j))[:split]
+            for j in nodes:
+                x[i, j] = 1.0 / split
+                cost[j] += a[i] / split
+    return x
+
+
+@dataclass
+class SlotPlacement:
+    """Physical expert slots as the runtime executes them."""
+
+    E: int                 # logical experts
+    n_e: int               # expert GPUs
+    P_l: int               # slots per expert GPU (contiguous blocks)
+    phys2log: np.ndarray   # [P] logical expert of each slot (-1: empty slot)
+    rep: np.ndarray        # [E, R+1] int32: count, then physical slots
+    R: int
+
+    @property
+    def P(self) -> int:
+        return self.n_e * self.P_l
+
+    def gpu_of_slot(self, p: int) -> int:
+        return p // self.P_l
+
+    def logical_of_local(self, q: int) -> list:
+        """Logical expert held by each local slot of expert GPU q (-1 = empty)."""
+        return [int(v) for v in self.phys2log[q * self.P_l:(q + 1) * self.P_l]]
+
+    def expected_gpu_rows(self, loads) -> np.ndarray:
+        """Rows per expert GPU when expert e's rows split evenly over its replicas."""
+        out = np.zeros(self.n_e)
+        for e in range(self.E):
+            c = int(self.rep[e, 0])
+            for r in range(c):
+                out[self.gpu_of_slot(int(self.rep[e, 1 + r]))] += loads[e] / c
+        return out
+
+
+def identity_slots(E: int, n_e: int) -> SlotPlacement:
+    """No replication: slot p = logical expert p, contiguous blocks (the default layout)."""
+    if E % n_e:
+        raise ValueError("experts must divide over expert GPUs")
+    rep = np.zeros((E, 2), np.int32)
+    rep[:, 0] = 1
+    rep[:, 1] = np.arange(E)
+    return SlotPlacement(E, n_e, E // n_e, np.arange(E, dtype=np.int32), rep, 1)
+
+
+def slots_from_placement(x: np.ndarray, max_replicas: int | None = None) -> SlotPlacement:
+    """Integral / replicated placement x[E, N] -> physical slots.  Each nonzero
+    (expert, node) becomes a slot on that node; nodes are padded with empty
+    slots (never routed to) to a common P_l."""
+    x = np.asarray(x)
+    E, n = x.shape
+    per_node = [[i for i in range(E) if x[i, j] > 0] for j in range(n)]
+    P_l = max(1, max(len(v) for v in per_node))
+    phys2log = np.full(n * P_l, -1, np.int32)
+    slots_of = [[] for _ in range(E)]
+    for j, experts in enumerate(per_node):
+        for k, i in enumerate(experts):
+            p = j * P_l + k
+            phys2log[p] = i
+            slots_of[i].append(p)
+    R = max(len(v) for v in slots_of)
+    if max_replicas is not None and R > max_replicas:
+        raise ValueError("placement exceeds max_replicas")
+    rep = np.zeros((E, R + 1), np.int32)
+    for i, s in enumerate(slots_of):
+        if not s:
+            raise ValueError(f"expert {i} has no slot")
+        rep[i, 0] = len(s)
+        rep[i, 1:1 + len(s)] = s
+    return SlotPlacement(E, n, P_l, phys2log, rep, R)
+
+
+def balanced_slots(loads, n_e: int, max_replicas: int = 2, k_cold: float = 0.0) -> SlotPlacement:
+    """balance_experts(mode='replicated') followed by slots_from_placement."""
+    x = balance_experts(loads, n_e, k_cold=k_cold, mode="replicated", max_replicas=max_replicas)
+    return slots_from_placement(x, max_replicas)

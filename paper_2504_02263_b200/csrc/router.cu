@@ -32,12 +32,23 @@ __host__ __device__ inline size_t logit_smem_bytes(int BT, int E) {
   return (size_t)(BT > 16 ? BT : 16) * E * sizeof(float) + (size_t)E * sizeof(uint32_t);
 }
 
+// Replicated-expert placement: rep[e*(R+1)] = number of
+// replicas of logical expert e, rep[e*(R+1)+1+r] = physical slot of replica r.
+// Token t of sender s routed to e goes to replica (t + s) mod nrep[e]; counts
+// and slots are then per physical slot (P of them).  rep == nullptr: P = E,
+// physical = logical.
+struct Placement {
+  const int32_t* rep;
+  int R, P, sender;
+  int32_t* pidx;  // [T,K] physical slot per (t,k) (may alias idx when rep == nullptr)
+};
+
 template <int TT, int TE, bool WS>
 __global__ void __launch_bounds__(kWarps * 32)
 gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
                  int T, int H, int E, int K, int BT, int32_t* __restrict__ idx_out,
                  float* __restrict__ w_out, int32_t* __restrict__ cnt_out,
-                 int32_t* __restrict__ slot_out, int32_t* __restrict__ ws) {
+                 int32_t* __restrict__ slot_out, int32_t* __restrict__ ws, const Placement pl) {
   extern __shared__ __align__(16) float s_logit[];         // [BT][E]
   __shared__ int s_last;
 
@@ -166,31 +177,37 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
       for (int k = 0; k < K; ++k) {
         idx_out[(size_t)t * K + k] = seli[k];
         w_out[(size_t)t * K + k] = __fdiv_rn(ex[k], s);
+        if (pl.rep) {
+          const int32_t* re = pl.rep + (size_t)seli[k] * (pl.R + 1);
+          pl.pidx[(size_t)t * K + k] = re[1 + (t + pl.sender) % re[0]];
+        }
       }
     }
   }
   __syncthreads();
 
   // ---- 3. in-CTA ranks (BT <= 32 tokens = one warp chunk): lane = token,
-  //      bit `lane` of mask[e] says "this token chose e", so the rank of (t,k)
-  //      among the CTA's earlier tokens is popc(mask[e] & lanes_below) -------
-  int32_t* hist = ws + 16;                                   // [nblk][E] CTA histograms
-  int32_t* base = hist + (size_t)gridDim.x * E;              // [nblk][E] CTA bases
-  uint32_t* mask = reinterpret_cast<uint32_t*>(s_logit);     // [E] (logits no longer needed)
-  for (int e = threadIdx.x; e < E; e += blockDim.x) mask[e] = 0u;
+  //      bit `lane` of mask[p] says "this token chose physical slot p", so the
+  //      rank of (t,k) among the CTA's earlier tokens is popc(mask[p] & lanes_below)
+  const int P = pl.P;
+  const int32_t* pidx = pl.rep ? pl.pidx : idx_out;
+  int32_t* hist = ws + 16;                                   // [nblk][P] CTA histograms
+  int32_t* base = hist + (size_t)gridDim.x * P;              // [nblk][P] CTA bases
+  uint32_t* mask = reinterpret_cast<uint32_t*>(s_logit);     // [P] (logits no longer needed)
+  for (int e = threadIdx.x; e < P; e += blockDim.x) mask[e] = 0u;
   __syncthreads();
   if (warp == 0) {
     const int t = t0 + lane;
     const bool valid = lane < BT && t < T;
     if (valid)
-      for (int k = 0; k < K; ++k) atomicOr(&mask[idx_out[(size_t)t * K + k]], 1u << lane);
+      for (int k = 0; k < K; ++k) atomicOr(&mask[pidx[(size_t)t * K + k]], 1u << lane);
     __syncwarp();
     const uint32_t below = (1u << lane) - 1u;
     if (valid)
       for (int k = 0; k < K; ++k)
-        slot_out[(size_t)t * K + k] = __popc(mask[idx_out[(size_t)t * K + k]] & below);
+        slot_out[(size_t)t * K + k] = __popc(mask[pidx[(size_t)t * K + k]] & below);
     __syncwarp();
-    for (int e = lane; e < E; e += 32) hist[(size_t)blockIdx.x * E + e] = __popc(mask[e]);
+    for (int e = lane; e < P; e += 32) hist[(size_t)blockIdx.x * P + e] = __popc(mask[e]);
   }
 
   // ---- 4. the last CTA to finish turns CTA histograms into bases (exclusive
@@ -206,16 +223,16 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
   //  CTA runs alone, so its L2 round trips must overlap)
   const int nblk = gridDim.x;
   constexpr int U = 8;
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+  for (int e = threadIdx.x; e < P; e += blockDim.x) {
     int run = 0;
     for (int b0 = 0; b0 < nblk; b0 += U) {
       int c[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) c[u] = (b0 + u < nblk) ? __ldcg(&hist[(size_t)(b0 + u) * E + e]) : 0;
+      for (int u = 0; u < U; ++u) c[u] = (b0 + u < nblk) ? __ldcg(&hist[(size_t)(b0 + u) * P + e]) : 0;
 #pragma unroll
       for (int u = 0; u < U; ++u)
         if (b0 + u < nblk) {
-          base[(size_t)(b0 + u) * E + e] = run;
+          base[(size_t)(b0 + u) * P + e] = run;
           run += c[u];
         }
     }
@@ -229,13 +246,13 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = i0 + u * stride;
-      ex[u] = i < TK ? __ldcg(&idx_out[i]) : 0;
+      ex[u] = i < TK ? __ldcg(&pidx[i]) : 0;
       sl[u] = i < TK ? __ldcg(&slot_out[i]) : 0;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = i0 + u * stride;
-      bs[u] = i < TK ? base[(size_t)((i / K) / BT) * E + ex[u]] : 0;
+      bs[u] = i < TK ? base[(size_t)((i / K) / BT) * P + ex[u]] : 0;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -250,41 +267,47 @@ constexpr size_t kMaxStagedW = 200 * 1024;  // W_g staged in smem up to this siz
 
 template <int TT, int TE>
 int launch(const void* x, const void* wg, int T, int H, int E, int K, int BT, int32_t* idx,
-           float* w, int32_t* cnt, int32_t* slot, void* ws, cudaStream_t st) {
+           float* w, int32_t* cnt, int32_t* slot, void* ws, const Placement& pl, cudaStream_t st) {
   const int nblk = (T + BT - 1) / BT;
   const size_t wbytes = (size_t)E * H * 2;
   const bool stage = E <= 16 && wbytes <= kMaxStagedW;
-  const size_t smem = ((logit_smem_bytes(BT, E) + 15) & ~size_t(15)) + (stage ? wbytes : 0);
+  size_t head = logit_smem_bytes(BT, E);
+  if (head < (size_t)pl.P * 4) head = (size_t)pl.P * 4;  // the [P] slot masks reuse this space
+  const size_t smem = ((head + 15) & ~size_t(15)) + (stage ? wbytes : 0);
   auto kern = stage ? gate_topk_kernel<TT, TE, true> : gate_topk_kernel<TT, TE, false>;
   if (smem > 48 * 1024) MSI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<nblk, kWarps * 32, smem, st>>>(reinterpret_cast<const __nv_bfloat16*>(x),
                                         reinterpret_cast<const __nv_bfloat16*>(wg), T, H, E, K, BT,
-                                        idx, w, cnt, slot, reinterpret_cast<int32_t*>(ws));
+                                        idx, w, cnt, slot, reinterpret_cast<int32_t*>(ws), pl);
   return check_launch("gate_topk_kernel");
 }
 
 }  // namespace
 
 int gate_topk(const void* x, const void* wg, int T, int H, int E, int K, int32_t* idx, float* w,
-              int32_t* cnt, int32_t* slot, void* ws, cudaStream_t st) {
+              int32_t* cnt, int32_t* slot, void* ws, cudaStream_t st, const int32_t* rep = nullptr,
+              int R = 0, int P = 0, int sender = 0, int32_t* pidx = nullptr) {
   MSI_REQUIRE(T >= 0 && H > 0 && H % 256 == 0, "gate_topk: H must be a positive multiple of 256 (got %d)", H);
   MSI_REQUIRE(E >= 1 && E <= 1024 && K >= 1 && K <= E && K <= 32, "gate_topk: need 1 <= K <= min(E, 32), E <= 1024");
   MSI_REQUIRE(x && wg && idx && w && cnt && slot && ws, "gate_topk: null pointer");
+  MSI_REQUIRE(!rep || (R >= 1 && P >= E && P <= 4096 && pidx && sender >= 0),
+              "gate_topk: replica table needs R >= 1, E <= P <= 4096, pidx and sender >= 0");
+  const Placement pl{rep, R, rep ? P : E, sender, rep ? pidx : idx};
   if (T == 0) {
-    MSI_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * E, st));
+    MSI_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * pl.P, st));
     return 0;
   }
   // Tile shapes: TE experts x TT tokens per warp; BT tokens per CTA.  Small E
   // is HBM-bound (want many CTAs); large E is FMA-bound (want token reuse).
   if (E % 16 == 0 && E > 16)  // fine-grained MoE: FMA-bound, BT=4 keeps >=148 CTAs busy at small T
-    return launch<4, 16>(x, wg, T, H, E, K, T >= 148 * 16 ? 16 : 4, idx, w, cnt, slot, ws, st);
+    return launch<4, 16>(x, wg, T, H, E, K, T >= 148 * 16 ? 16 : 4, idx, w, cnt, slot, ws, pl, st);
   // E = 8 / 16: W_g staged once per CTA (TMA bulk copy) and amortised over 32
   // tokens (4 per warp); x is the only HBM stream
-  if (E % 16 == 0) return launch<4, 16>(x, wg, T, H, E, K, 32, idx, w, cnt, slot, ws, st);
-  if (E % 8 == 0) return launch<4, 8>(x, wg, T, H, E, K, 32, idx, w, cnt, slot, ws, st);
-  if (E % 4 == 0) return launch<1, 4>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, st);
-  if (E % 2 == 0) return launch<1, 2>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, st);
-  return launch<1, 1>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, st);
+  if (E % 16 == 0) return launch<4, 16>(x, wg, T, H, E, K, 32, idx, w, cnt, slot, ws, pl, st);
+  if (E % 8 == 0) return launch<4, 8>(x, wg, T, H, E, K, 32, idx, w, cnt, slot, ws, pl, st);
+  if (E % 4 == 0) return launch<1, 4>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, pl, st);
+  if (E % 2 == 0) return launch<1, 2>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, pl, st);
+  return launch<1, 1>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, pl, st);
 }
 
 size_t gate_topk_workspace(int T, int E) {
@@ -301,4 +324,12 @@ extern "C" int msi_gate_topk(const void* x, const void* wg, int T, int H, int E,
                              void* stream) {
   return msi::gate_topk(x, wg, T, H, E, K, idx, w, cnt, slot, workspace,
                         reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int msi_gate_topk_placed(const void* x, const void* wg, int T, int H, int E, int K,
+                                    const int32_t* rep, int R, int P, int sender, int32_t* idx,
+                                    int32_t* pidx, float* w, int32_t* cnt, int32_t* slot,
+                                    void* workspace, void* stream) {
+  return msi::gate_topk(x, wg, T, H, E, K, idx, w, cnt, slot, workspace,
+                        reinterpret_cast<cudaStream_t>(stream), rep, R, P, sender, pidx);
 }

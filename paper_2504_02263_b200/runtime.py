@@ -43,8 +43,13 @@ def device_view(ptr: int, shape, dtype: torch.dtype, device) -> torch.Tensor:
     return t.view(torch.bfloat16) if dtype == torch.bfloat16 else t
 
 
-def make_plan_struct(model: MoeModelSpec, plan: DeploymentPlan) -> _lib.Plan:
-    plan.check_model(model)
+def make_plan_struct(model: MoeModelSpec, plan: DeploymentPlan, slots=None) -> _lib.Plan:
+    """C plan for this deployment.  With a ``balance.SlotPlacement`` the M2N
+    layer works on its P physical expert slots instead of the E logical experts."""
+    if slots is None:
+        plan.check_model(model)
+    elif slots.E != model.experts or slots.n_e != plan.n_e:
+        raise ValueError("slot placement does not match the model / plan")
     if plan.world > _lib.MAX_RANKS:
         raise ValueError(f"plan needs {plan.world} ranks; at most {_lib.MAX_RANKS} per box")
     p = _lib.Plan()
@@ -55,7 +60,7 @@ def make_plan_struct(model: MoeModelSpec, plan: DeploymentPlan) -> _lib.Plan:
     for i, r in enumerate(plan.expert_ranks()):
         p.expert_ranks[i] = r
     p.hidden, p.inter = model.hidden, model.intermediate
-    p.experts, p.topk = model.experts, model.topk
+    p.experts, p.topk = (model.experts if slots is None else slots.P), model.topk
     p.max_tokens, p.slots = plan.b_a, plan.m
     return p
 
@@ -77,15 +82,16 @@ class M2NGroup:
     """This rank's M2N endpoint: context, peer mapping, role."""
 
     def __init__(self, model, plan: DeploymentPlan, rank: int = 0, device=None, group=None,
-                 timeout_s: float = 20.0):
+                 timeout_s: float = 20.0, slots=None):
         self.model = as_model_spec(model)
         self.plan = plan
         self.rank = rank
         self.role = plan.role_of(rank)
+        self.slots = slots  # balance.SlotPlacement (replicated experts) or None
         self.device = torch.device(device if device is not None else f"cuda:{torch.cuda.current_device()}")
         lib = _lib.load()
         _lib.call("msi_check_device")
-        self._pstruct = make_plan_struct(self.model, plan)
+        self._pstruct = make_plan_struct(self.model, plan, slots)
         ctx = ctypes.c_void_p()
         _lib.call("msi_ctx_create", ctypes.byref(self._pstruct), rank, ctypes.byref(ctx))
         self.ctx = ctx
@@ -108,7 +114,8 @@ class M2NGroup:
         self.is_expert = self.role in ("expert", "both")
         self.attn_index = plan.attention_ranks().index(rank) if self.is_attention else -1
         self.expert_index = plan.expert_ranks().index(rank) if self.is_expert else -1
-        self.E_l = plan.experts_per_gpu(self.model)
+        self.E_l = plan.experts_per_gpu(self.model) if slots is None else slots.P_l  # local (physical) slots
+        self.P = self.model.experts if slots is None else slots.P
         ws = ctypes.c_void_p()
         nb = ctypes.c_size_t()
         _lib.call("msi_ctx_workspace", ctx, ctypes.byref(ws), ctypes.byref(nb))
@@ -179,13 +186,19 @@ class M2NGroup:
 class Route:
     """Router output for one micro-batch on an attention GPU."""
 
-    idx: torch.Tensor
-    w: torch.Tensor
-    cnt: torch.Tensor
-    slot: torch.Tensor
+    idx: torch.Tensor   # [T,K] logical experts
+    w: torch.Tensor     # [T,K] combine weights
+    cnt: torch.Tensor   # [P] tokens per physical expert slot (= logical without replication)
+    slot: torch.Tensor  # [T,K] rank within the physical slot
     T: int
     mb: int = 0
     epoch: int = 0
+    pidx: torch.Tensor | None = None  # [T,K] physical slots (replicated experts) or None
+
+    @property
+    def dest(self) -> torch.Tensor:
+        """Physical slot of every (t, k): what the M2N dispatch routes by."""
+        return self.idx if self.pidx is None else self.pidx
 
 
 class MoEDecodeLayer:
@@ -219,13 +232,19 @@ class MoEDecodeLayer:
         self.epoch_a = [0] * group.plan.m   # uses of each slot (attention side)
         self.epoch_e = [0] * group.plan.m   # uses of each slot (expert side)
         self._routes = []
+        self._rep = None
         if group.is_attention:
             dev, K, T = group.device, m.topk, group.plan.b_a
+            sl = group.slots
+            if sl is not None:
+                self._rep = torch.from_numpy(sl.rep.astype("int32").ravel()).to(dev)
             for _ in range(group.plan.m):
                 self._routes.append(Route(torch.empty((T, K), dtype=torch.int32, device=dev),
                                           torch.empty((T, K), dtype=torch.float32, device=dev),
-                                          torch.empty((m.experts,), dtype=torch.int32, device=dev),
-                                          torch.empty((T, K), dtype=torch.int32, device=dev), T))
+                                          torch.empty((group.P,), dtype=torch.int32, device=dev),
+                                          torch.empty((T, K), dtype=torch.int32, device=dev), T,
+                                          pidx=None if sl is None else
+                                          torch.empty((T, K), dtype=torch.int32, device=dev)))
         self._ws = group.workspace_ptr
 
     # -- (1) router ---------------------------------------------------------
@@ -235,9 +254,16 @@ class MoEDecodeLayer:
         if T > self.g.plan.b_a:
             raise ValueError(f"micro-batch of {T} tokens exceeds plan.b_a={self.g.plan.b_a}")
         r = self._routes[mb]
-        _lib.call("msi_gate_topk", ops._ptr(x), ops._ptr(self.wg), T, m.hidden, m.experts, m.topk,
-                  ops._ptr(r.idx), ops._ptr(r.w), ops._ptr(r.cnt), ops._ptr(r.slot),
-                  ctypes.c_void_p(self._ws), ops._stream(stream))
+        if self._rep is None:
+            _lib.call("msi_gate_topk", ops._ptr(x), ops._ptr(self.wg), T, m.hidden, m.experts, m.topk,
+                      ops._ptr(r.idx), ops._ptr(r.w), ops._ptr(r.cnt), ops._ptr(r.slot),
+                      ctypes.c_void_p(self._ws), ops._stream(stream))
+        else:  # replicated experts: route to physical slots (balance.SlotPlacement)
+            sl = self.g.slots
+            _lib.call("msi_gate_topk_placed", ops._ptr(x), ops._ptr(self.wg), T, m.hidden, m.experts, m.topk,
+                      ops._ptr(self._rep), sl.R, sl.P, self.g.attn_index, ops._ptr(r.idx), ops._ptr(r.pidx),
+                      ops._ptr(r.w), ops._ptr(r.cnt), ops._ptr(r.slot), ctypes.c_void_p(self._ws),
+                      ops._stream(stream))
         r.T, r.mb = T, mb
         return r
 
@@ -246,7 +272,7 @@ class MoEDecodeLayer:
         mb = route.mb if mb is None else mb
         self.epoch_a[mb] += 1
         route.mb, route.epoch = mb, (0 if self.device_epochs else self.epoch_a[mb])
-        _lib.call("msi_dispatch", self.g.ctx, ops._ptr(x), ops._ptr(route.cnt), ops._ptr(route.idx),
+        _lib.call("msi_dispatch", self.g.ctx, ops._ptr(x), ops._ptr(route.cnt), ops._ptr(route.dest),
                   ops._ptr(route.slot), route.T, mb, route.epoch, ops._stream(stream))
         return route
 
@@ -439,6 +465,10 @@ def synth_device_weights(model: MoeModelSpec, experts, seed: int = 0, device="cu
     w13 = torch.empty((len(experts), 2 * Hp, H), dtype=torch.bfloat16, device=device)
     w2 = torch.empty((len(experts), H, Hp), dtype=torch.bfloat16, device=device)
     for i, e in enumerate(experts):
+        if e < 0:  # empty slot of a replicated placement: never routed to
+            w13[i].zero_()
+            w2[i].zero_()
+            continue
         gen.manual_seed(seed * 100003 + 1 + e)
         wgt = (torch.randn((1, Hp, H), generator=gen, device=device) / H ** 0.5).to(torch.bfloat16)
         wup = (torch.randn((1, Hp, H), generator=gen, device=device) / H ** 0.5).to(torch.bfloat16)
@@ -448,10 +478,14 @@ def synth_device_weights(model: MoeModelSpec, experts, seed: int = 0, device="cu
     return wg, w13, w2
 
 
-def local_experts(group: M2NGroup) -> range:
+def local_experts(group: M2NGroup) -> list:
+    """Logical expert behind each local (physical) slot of this expert GPU, in
+    slot order; -1 marks an empty slot of a replicated placement."""
     if not group.is_expert:
-        return range(0)
-    return range(group.expert_index * group.E_l, (group.expert_index + 1) * group.E_l)
+        return []
+    if group.slots is not None:
+        return group.slots.logical_of_local(group.expert_index)
+    return list(range(group.expert_index * group.E_l, (group.expert_index + 1) * group.E_l))
 
 
 def init_distributed_from_env(backend: str = "nccl"):

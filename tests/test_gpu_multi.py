@@ -26,7 +26,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, n_a, n_e, colo, shape, tokens, m, layers, outdir):
+def _worker(rank, world, port, n_a, n_e, colo, shape, tokens, m, layers, outdir, slots=None):
     import sys
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
@@ -39,7 +39,7 @@ def _worker(rank, world, port, n_a, n_e, colo, shape, tokens, m, layers, outdir)
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     model = as_model_spec(shape)
     plan = DeploymentPlan(n_a=n_a, n_e=n_e, m=m, b_a=max(tokens), colocated=colo)
-    g = runtime.M2NGroup(model, plan, rank=rank, device=f"cuda:{rank}", timeout_s=30)
+    g = runtime.M2NGroup(model, plan, rank=rank, device=f"cuda:{rank}", timeout_s=30, slots=slots)
     wts = O.synth_weights(model.hidden, model.intermediate, model.experts, seed=0)
 
     def dev(a):
@@ -47,7 +47,7 @@ def _worker(rank, world, port, n_a, n_e, colo, shape, tokens, m, layers, outdir)
 
     w13 = w2 = wg = None
     if g.is_expert:
-        ex = list(runtime.local_experts(g))
+        ex = [max(e, 0) for e in runtime.local_experts(g)]  # empty slots (-1) are never routed to
         w13 = ops.pack_w13(dev(wts.w_gate[ex]), dev(wts.w_up[ex]))
         w2 = dev(wts.w_down[ex])
     if g.is_attention:
@@ -72,6 +72,7 @@ def _worker(rank, world, port, n_a, n_e, colo, shape, tokens, m, layers, outdir)
                 res[f"w_{l}_{j}"] = r.w[:T].cpu().numpy()
                 res[f"cnt_{l}_{j}"] = r.cnt.cpu().numpy()
                 res[f"slot_{l}_{j}"] = r.slot[:T].cpu().numpy()
+                res[f"dest_{l}_{j}"] = r.dest[:T].cpu().numpy()
                 res[f"out_{l}_{j}"] = out.view(torch.int16).cpu().numpy().view(np.uint16)
                 res[f"y_{l}_{j}"] = g.ybuf_view(j)[:T].contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
             if g.is_expert:
@@ -97,11 +98,13 @@ PLANS = [
     (6, 2, False, "tiny", [64, 64, 33, 64, 1, 50], 3, 2),
     (2, 2, True, FINE, [64, 37], 2, 2),            # co-located 2 -> 2 (config 5 pattern)
     (4, 4, True, FINE, [16, 64, 1, 40], 2, 1),      # co-located 4 -> 4, 16 experts per GPU
+    (2, 2, False, "tiny", [64, 48], 2, 1, "skew"),  # replicated hot experts (load balancing)
 ]
 
 
-@pytest.mark.parametrize("n_a,n_e,colo,shape,tokens,m,layers", PLANS)
-def test_m2n_multi_gpu(lib, tmp_path, n_a, n_e, colo, shape, tokens, m, layers):
+@pytest.mark.parametrize("n_a,n_e,colo,shape,tokens,m,layers,balanced",
+                         [p if len(p) == 8 else p + (None,) for p in PLANS])
+def test_m2n_multi_gpu(lib, tmp_path, n_a, n_e, colo, shape, tokens, m, layers, balanced):
     import torch.multiprocessing as mp
 
     from oracle import oracle as O
@@ -110,20 +113,28 @@ def test_m2n_multi_gpu(lib, tmp_path, n_a, n_e, colo, shape, tokens, m, layers):
     world = n_a if colo else n_a + n_e
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs, box has {torch.cuda.device_count()}")
-    port = _free_port()
-    mp.spawn(_worker, args=(world, port, n_a, n_e, colo, shape, tokens, m, layers, str(tmp_path)), nprocs=world,
-             join=True)
     model = as_model_spec(shape)
+    slots = None
+    if balanced == "skew":  # experts 0 and 4 hot: replicated over both expert GPUs
+        from paper_2504_02263_b200.balance import balanced_slots
+        loads = np.ones(model.experts)
+        loads[0], loads[4] = 20.0, 15.0
+        slots = balanced_slots(loads, n_e, max_replicas=2)
+    port = _free_port()
+    mp.spawn(_worker, args=(world, port, n_a, n_e, colo, shape, tokens, m, layers, str(tmp_path), slots),
+             nprocs=world, join=True)
     wts = O.synth_weights(model.hidden, model.intermediate, model.experts, seed=0)
     got = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(world)]
     for r in range(world):
         assert got[r]["status"][0] == 0, f"rank {r} device status {got[r]['status']}"
-    E_l = model.experts // n_e
+    E_l = model.experts // n_e if slots is None else slots.P_l
     from _util import assert_close_bf16
     for l in range(layers):
         for j in range(m):
             xs = [O.synth_tokens(tokens[s], model.hidden, seed=1000 * l + 10 * j + s) for s in range(n_a)]
-            ref = O.moe_layer(xs, wts, model.topk, n_e=n_e, resid=True)
+            ref = O.moe_layer(xs, wts, model.topk, n_e=n_e, resid=True,
+                              rep=None if slots is None else slots.rep,
+                              phys2log=None if slots is None else slots.phys2log)
             for s in range(n_a):
                 a = got[s]
                 np.testing.assert_array_equal(a[f"idx_{l}_{j}"], ref.idx[s])
@@ -134,7 +145,8 @@ def test_m2n_multi_gpu(lib, tmp_path, n_a, n_e, colo, shape, tokens, m, layers):
                 np.testing.assert_array_equal(a[f"out_{l}_{j}"], O.combine(a[f"y_{l}_{j}"], a[f"w_{l}_{j}"], xs[s]))
                 assert_close_bf16(a[f"out_{l}_{j}"], ref.out[s], f"layer output s={s}")
                 # placement: every (t, k) row landed at the oracle's row on the right GPU
-                q, rows = O.dispatch_rows(ref.idx[s], ref.slot[s], s, ref.layout, E_l)
+                np.testing.assert_array_equal(a[f"dest_{l}_{j}"], ref.pidx[s])
+                q, rows = O.dispatch_rows(ref.pidx[s], ref.slot[s], s, ref.layout, E_l)
                 T = tokens[s]
                 for t in range(T):
                     for k in range(model.topk):

@@ -356,3 +356,50 @@ def test_colocated_layer_256_experts(lib):
     assert_close_bf16(to_host(g.ybuf_view(0)[:96]), ref.y[0], "expert outputs")
     assert_close_bf16(to_host(out), ref.out[0], "layer output")
     g.close()
+
+
+def _replicated_slots():
+    """Tiny model, one expert GPU, experts 0-3 replicated: 12 physical slots."""
+    from paper_2504_02263_b200.balance import SlotPlacement
+    phys2log = np.array([0, 1, 2, 3, 4, 5, 6, 7, 0, 1, 2, 3], np.int32)
+    rep = np.zeros((8, 3), np.int32)
+    for e in range(8):
+        ps = np.flatnonzero(phys2log == e)
+        rep[e, 0] = len(ps)
+        rep[e, 1:1 + len(ps)] = ps
+    return SlotPlacement(8, 1, 12, phys2log, rep, 2)
+
+
+def test_replicated_experts_bit_identical(lib):
+    """Routing to replicated expert slots (load balancing) changes placement but
+    not results: pidx / counts / slots bit-exact vs the oracle, layer output
+    bit-identical to the unreplicated GPU run."""
+    from paper_2504_02263_b200 import ops, runtime
+    from paper_2504_02263_b200.config import DeploymentPlan, as_model_spec
+
+    model = as_model_spec("tiny")
+    wts = O.synth_weights(model.hidden, model.intermediate, model.experts, seed=0)
+    x = O.synth_tokens(64, model.hidden, seed=41)
+    outs = {}
+    for name, sl in (("plain", None), ("rep", _replicated_slots())):
+        g = runtime.M2NGroup(model, DeploymentPlan(n_a=1, n_e=1, m=1, b_a=64, colocated=True), rank=0, slots=sl)
+        ex = runtime.local_experts(g)
+        w13 = ops.pack_w13(to_dev(wts.w_gate[ex]), to_dev(wts.w_up[ex]))
+        layer = runtime.MoEDecodeLayer(g, wg=to_dev(wts.wg), w13=w13, w2=to_dev(wts.w_down[ex]))
+        xd = to_dev(x)
+        r = layer.router(xd, 0)
+        layer.dispatch(xd, r, 0)
+        layer.expert_step(0)
+        out = layer.combine(r, resid=xd)
+        torch.cuda.synchronize()
+        assert g.status() == 0
+        outs[name] = to_host(out)
+        if sl is not None:
+            ref = O.moe_layer([x], wts, model.topk, n_e=1, resid=True, rep=sl.rep, phys2log=sl.phys2log)
+            np.testing.assert_array_equal(r.idx.cpu().numpy(), ref.idx[0])
+            np.testing.assert_array_equal(r.pidx.cpu().numpy(), ref.pidx[0])
+            np.testing.assert_array_equal(r.cnt.cpu().numpy(), ref.cnt[0])
+            np.testing.assert_array_equal(r.slot.cpu().numpy(), ref.slot[0])
+            assert (r.cnt.cpu().numpy()[8:] > 0).all()  # the replicas received tokens
+        g.close()
+    np.testing.assert_array_equal(outs["rep"], outs["plain"])
