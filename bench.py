@@ -47,6 +47,11 @@ def parse():
     ap.add_argument("--attn", default="standin", choices=["standin", "none"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--split", default="", help="attention+expert GPUs, e.g. 2+2 (default: config-3 ratio)")
+    ap.add_argument("--skew", type=float, default=0.0,
+                    help="make experts 0/1 hot (gate-logit bias); 0 = random-init routing")
+    ap.add_argument("--balance", action="store_true",
+                    help="replicate hot experts across expert GPUs (balance_experts, SPEC.md:407-414)")
     ap.add_argument("--timeline-csv", default="",
                     help="write the SPEC timeline CSV of the last timed step ('{rank}' is substituted)")
     ap.add_argument("--colocated", action="store_true",
@@ -243,6 +248,11 @@ def main():
             print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}))
         sys.exit(2)
     n_a, n_e, colo = SPLITS[world]
+    if args.split:  # e.g. "2+2"
+        n_a, n_e = (int(v) for v in args.split.split("+"))
+        colo = False
+        if n_a + n_e != world:
+            raise SystemExit(f"--split {args.split} needs {n_a + n_e} GPUs")
     if args.colocated:  # every GPU holds both roles (config 5: 8 -> 8, 32 experts per GPU)
         n_a, n_e, colo = world, world, True
     model = as_model_spec(args.shape)
@@ -255,8 +265,43 @@ def main():
     args.b_a = b_a
     plan = DeploymentPlan(n_a=n_a, n_e=n_e, m=m_eff, b_a=b_a, colocated=colo)
     dev = torch.device(f"cuda:{local}")
-    g = runtime.M2NGroup(model, plan, rank=rank, device=dev)
-    wg, w13, w2 = runtime.synth_device_weights(model, runtime.local_experts(g), seed=0, device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1 + rank)
+    is_attn_rank = rank in plan.attention_ranks()
+    wg = runtime.synth_device_weights(model, [], seed=0, device=dev)[0]
+    xs = [torch.randn((args.b_a, model.hidden), generator=gen, device=dev) for _ in range(plan.m)] if is_attn_rank else None
+    if args.skew > 0:
+        # hot experts: tokens share a direction u that the gate rows of experts
+        # 0 and 1 favour (logit bias ~ skew), the way real routing concentrates
+        gu = torch.Generator(device=dev)
+        gu.manual_seed(12345)
+        u = torch.randn(model.hidden, generator=gu, device=dev)
+        u = u / u.norm()
+        wgf = wg.float()
+        wgf[0] += args.skew * u
+        wgf[1] += 0.6 * args.skew * u
+        wg = wgf.to(torch.bfloat16)
+        if xs:
+            xs = [x + u * model.hidden ** 0.5 for x in xs]
+    if xs:
+        xs = [x.to(torch.bfloat16) for x in xs]
+    slots, loads = None, None
+    if args.balance or args.skew > 0:
+        # calibration: this step's routing counts (all attention ranks), placement
+        # by balance_experts(mode="replicated"), agreed by all ranks
+        cnt = torch.zeros(model.experts, dtype=torch.float64, device=dev)
+        if xs:
+            from paper_2504_02263_b200 import ops as _ops
+            for x in xs:
+                cnt += _ops.gate_topk(x, wg, model.topk)[2].double()
+        if world > 1:
+            dist.all_reduce(cnt)
+        loads = cnt.cpu().numpy()
+        if args.balance:
+            from paper_2504_02263_b200.balance import balanced_slots
+            slots = balanced_slots(loads, n_e, max_replicas=min(n_e, 2))
+    g = runtime.M2NGroup(model, plan, rank=rank, device=dev, slots=slots)
+    _, w13, w2 = runtime.synth_device_weights(model, runtime.local_experts(g), seed=0, device=dev)
     layer = runtime.MoEDecodeLayer(g, wg=wg if g.is_attention else None,
                                    w13=w13 if g.is_expert else None, w2=w2 if g.is_expert else None)
     wl = WorkloadSpec()
@@ -266,10 +311,6 @@ def main():
         kv_bytes = args.b_a * wl.avg_seq_len * 2 * (model.hidden // model.gqa_group) * 2
     runner = runtime.PingPongRunner(layer, layers=args.layers, kv_bytes=kv_bytes, chain=False,
                                     record_timeline=True)
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(1 + rank)
-    xs = [torch.randn((args.b_a, model.hidden), generator=gen, device=dev).to(torch.bfloat16)
-          for _ in range(plan.m)] if g.is_attention else None
     x0 = [x.clone() for x in xs] if xs else None
 
     def barrier():
@@ -332,6 +373,25 @@ def main():
         dist.all_reduce(tmax[1:], op=dist.ReduceOp.SUM)
         t = tmax
     elapsed_ms, ffn_total_ms, ffn_n, rows_total, calls_total = t.tolist()
+    # rows each expert GPU processed per FFN call (load balance evidence)
+    mine = (rows / calls) if (g.is_expert and calls) else None
+    per_gpu_rows = [mine]
+    if world > 1:
+        per_gpu_rows = [None] * world
+        dist.all_gather_object(per_gpu_rows, mine)
+    per_gpu_rows = [r for r in per_gpu_rows if r is not None]
+    lb_report = None
+    if loads is not None:
+        from paper_2504_02263_b200.balance import identity_slots
+        ident = identity_slots(model.experts, n_e)
+        lb_report = {"skew": args.skew, "balanced": bool(args.balance),
+                     "expert_loads": [int(v) for v in loads],
+                     "rows_per_expert_gpu_per_call": per_gpu_rows,
+                     "max_over_mean": (max(per_gpu_rows) / (sum(per_gpu_rows) / len(per_gpu_rows)))
+                     if per_gpu_rows else None,
+                     "expected_max_rows_unbalanced": float(ident.expected_gpu_rows(loads).max()),
+                     "expected_max_rows": float((slots or ident).expected_gpu_rows(loads).max()),
+                     "physical_slots": slots.P if slots else model.experts}
 
     # ---- measured stage times vs the reference's timing model (Eq. 5) ----
     stages = runner.stage_times_ms()
@@ -418,6 +478,7 @@ def main():
         "gpu_launches": None,
         "clocks": clocks,
         "stage_times": eq5_report(all_stages, plan, args.layers, elapsed_ms / args.steps, colo),
+        "load_balance": lb_report,
     }
     # our kernels inside the timed region (per rank, summed over roles)
     per_step = plan.m * args.layers * (launches_per_mbl if colo else 0)
