@@ -187,6 +187,37 @@ int msi_combine_local(const void* y, const float* w, const void* resid,
 int msi_attn_standin(const void* kv, size_t kv_bytes, float* checksum,
                      void* stream);
 
+/* ---- Attention stage: GQA decode over paged KV.
+ * The reference models it as T_a = k1*b_a + k2 with the KV traffic
+ * 2*b*s*h*bytes/g (Table 3).
+ *
+ * Paged KV cache (per layer): k_cache / v_cache bf16
+ *   [num_pages][n_kv][MSI_KV_PAGE][MSI_HEAD_DIM]
+ * block_table int32 [T][max_pages] (page ids of sequence t, in order).
+ * Query heads n_heads = G * n_kv, G <= 16; head h uses KV head h / G. */
+#define MSI_KV_PAGE 64
+#define MSI_HEAD_DIM 128
+
+/* RoPE (rotate-half, base theta) on the new token's q and k at position
+ * pos[t], then append k, v into the cache slot (page block_table[t][pos/64],
+ * row pos%64).  qkv bf16 [T][qkv_ld] holds q (n_heads*128) | k (n_kv*128) |
+ * v (n_kv*128); q_out bf16 [T][n_heads*128] receives the rotated q. */
+int msi_rope_append(const void* qkv, int64_t qkv_ld, const int32_t* pos, int T,
+                    int n_heads, int n_kv, float theta,
+                    const int32_t* block_table, int max_pages,
+                    void* k_cache, void* v_cache, int64_t num_pages,
+                    void* q_out, void* stream);
+/* Workspace bytes msi_decode_attention needs for T sequences (split-KV
+ * partials; 0 when no split is used). */
+size_t msi_decode_attention_workspace(int T, int n_heads, int n_kv, int max_pages);
+/* out[t][h*128 + d] = softmax(q[t,h] . K[t,kvh]^T * scale) V[t,kvh], over
+ * seq_lens[t] cached tokens; out bf16 [T][n_heads*128]. */
+int msi_decode_attention(const void* q, const void* k_cache, const void* v_cache,
+                         int64_t num_pages, const int32_t* block_table, int max_pages,
+                         const int32_t* seq_lens, int T, int n_heads, int n_kv,
+                         float scale, void* out, void* workspace, size_t ws_bytes,
+                         void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -295,3 +295,86 @@ def gemm_flops(b: int, h_in: int, h_out: int) -> int:
 def expert_param_bytes(layers: int, h: int, hp: int, bytes_per: int = 2, swiglu: bool = False) -> int:
     """P_e: L * 2 * h * h' * bytes (3 matrices with SwiGLU)."""
     return layers * (3 if swiglu else 2) * h * hp * bytes_per
+
+
+# ------------------------------------------------------- attention stage --- #
+# SURVEY.md §8(f) rank 3.  The reference only models this stage (T_a = k1 b_a
+# + k2, KV traffic 2 b s h bytes / g: SPEC.md:156-164, 186; Table 3 GEMMs
+# PAPER.md:283-284); the restatement below is the standard GQA decode layer
+# those formulas describe: QKV projection (h -> h (1 + 2/g)), RoPE, KV append,
+# softmax(q K^T / sqrt(d)) V over the cached tokens, output projection
+# (h -> h) plus residual.  fp32 math, bf16 rounding where the GPU path stores
+# (qkv, rotated q/k, attention output, stage output).
+KV_PAGE = 64
+HEAD_DIM = 128
+
+
+def rope(x: np.ndarray, pos: np.ndarray, theta: float) -> np.ndarray:
+    """Rotate-half RoPE.  x fp32 [T, heads, 128], pos int [T] -> fp32."""
+    d = x.shape[-1]
+    i = np.arange(d // 2, dtype=np.float32)
+    inv = (np.float32(1.0) / np.power(np.float32(theta), (2 * i) / np.float32(d))).astype(np.float32)
+    ang = (pos.astype(np.float32)[:, None] * inv[None, :]).astype(np.float32)
+    cs, sn = np.cos(ang)[:, None, :], np.sin(ang)[:, None, :]
+    lo, hi = x[..., : d // 2], x[..., d // 2:]
+    return np.concatenate([lo * cs - hi * sn, hi * cs + lo * sn], axis=-1).astype(np.float32)
+
+
+def paged_kv_gather(cache: np.ndarray, block_table: np.ndarray, t: int, n: int, kvh: int) -> np.ndarray:
+    """Rows 0..n-1 of sequence t's KV head kvh from a paged cache
+    [pages, n_kv, 64, 128] (bf16 bits) -> fp32 [n, 128]."""
+    pages = (n + KV_PAGE - 1) // KV_PAGE
+    rows = np.concatenate([cache[block_table[t, p], kvh] for p in range(pages)]) if pages else \
+        np.zeros((0, HEAD_DIM), np.uint16)
+    return bf16_to_f32(rows[:n])
+
+
+def decode_attention(q: np.ndarray, k_cache: np.ndarray, v_cache: np.ndarray, block_table: np.ndarray,
+                     seq_lens: np.ndarray, scale: float | None = None) -> np.ndarray:
+    """q bf16 [T, n_heads, 128]; caches bf16 [pages, n_kv, 64, 128] -> out bf16
+    [T, n_heads * 128].  An empty sequence yields zeros."""
+    T, nh, d = q.shape
+    n_kv = k_cache.shape[1]
+    G = nh // n_kv
+    scale = 1.0 / np.sqrt(d) if scale is None else scale
+    qf = bf16_to_f32(q)
+    out = np.zeros((T, nh, d), np.float32)
+    for t in range(T):
+        n = int(seq_lens[t])
+        if n == 0:
+            continue
+        for h in range(n_kv):
+            K = paged_kv_gather(k_cache, block_table, t, n, h)
+            V = paged_kv_gather(v_cache, block_table, t, n, h)
+            s = (qf[t, h * G:(h + 1) * G] @ K.T) * np.float32(scale)
+            s = s - s.max(axis=1, keepdims=True)
+            p = np.exp(s)
+            out[t, h * G:(h + 1) * G] = (p @ V) / p.sum(axis=1, keepdims=True)
+    return bf16_round(out.reshape(T, nh * d))
+
+
+def rope_append(qkv: np.ndarray, pos: np.ndarray, n_heads: int, n_kv: int, theta: float,
+                block_table: np.ndarray, k_cache: np.ndarray, v_cache: np.ndarray) -> np.ndarray:
+    """qkv bf16 [T, (n_heads + 2 n_kv) 128]; rotates q, k at pos and writes k, v
+    into the caches in place.  Returns rotated q bf16 [T, n_heads, 128]."""
+    T = qkv.shape[0]
+    f = bf16_to_f32(qkv)
+    q = rope(f[:, : n_heads * HEAD_DIM].reshape(T, n_heads, HEAD_DIM), pos, theta)
+    k = rope(f[:, n_heads * HEAD_DIM:(n_heads + n_kv) * HEAD_DIM].reshape(T, n_kv, HEAD_DIM), pos, theta)
+    v = qkv[:, (n_heads + n_kv) * HEAD_DIM:(n_heads + 2 * n_kv) * HEAD_DIM].reshape(T, n_kv, HEAD_DIM)
+    kb = bf16_round(k)
+    for t in range(T):
+        pg, r = block_table[t, pos[t] // KV_PAGE], pos[t] % KV_PAGE
+        k_cache[pg, :, r] = kb[t]
+        v_cache[pg, :, r] = v[t]
+    return bf16_round(q)
+
+
+def attention_stage(x: np.ndarray, wqkv: np.ndarray, wo: np.ndarray, pos: np.ndarray, n_heads: int, n_kv: int,
+                    theta: float, block_table: np.ndarray, k_cache: np.ndarray, v_cache: np.ndarray) -> np.ndarray:
+    """One decode attention layer on the attention GPU: x bf16 [T, h] ->
+    bf16(x + attn(x) W_o^T).  Appends the new token at pos (caches updated in place)."""
+    qkv = bf16_round(bf16_to_f32(x) @ bf16_to_f32(wqkv).T)
+    q = rope_append(qkv, pos, n_heads, n_kv, theta, block_table, k_cache, v_cache)
+    o = decode_attention(q, k_cache, v_cache, block_table, pos.astype(np.int64) + 1)
+    return bf16_round(bf16_to_f32(x) + bf16_to_f32(o) @ bf16_to_f32(wo).T)

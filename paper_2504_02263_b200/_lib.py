@@ -14,6 +14,8 @@ LIB_PATH = os.path.join(_PKG, "libmsinfer.so")
 MAX_RANKS = 8
 IPC_HANDLE_BYTES = 64
 ROW_ALIGN = 128
+KV_PAGE = 64     # MSI_KV_PAGE
+HEAD_DIM = 128   # MSI_HEAD_DIM
 
 BUF_RECV, BUF_META, BUF_YBUF, BUF_HBUF, BUF_CNTAB = range(5)
 ERRORS = {-1: "MSI_EINVAL", -2: "MSI_EARCH", -3: "MSI_ESTATE", -4: "MSI_ETIMEOUT", -5: "MSI_EDRIVER"}
@@ -69,6 +71,11 @@ SIGNATURES = {
     "msi_grouped_ffn": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _I, _I, _P]),
     "msi_combine_local": (_I, [_P, _P, _P, _P, _I, _I, _I, _P]),
     "msi_attn_standin": (_I, [_P, _SZ, _P, _P]),
+    "msi_rope_append": (_I, [_P, ctypes.c_int64, _P, _I, _I, _I, ctypes.c_float, _P, _I, _P, _P,
+                             ctypes.c_int64, _P, _P]),
+    "msi_decode_attention_workspace": (_SZ, [_I, _I, _I, _I]),
+    "msi_decode_attention": (_I, [_P, _P, _P, ctypes.c_int64, _P, _I, _P, _I, _I, _I, ctypes.c_float, _P, _P,
+                                  _SZ, _P]),
 }
 
 _lib = None

@@ -118,3 +118,55 @@ def combine_local(y: torch.Tensor, w: torch.Tensor, resid: torch.Tensor | None =
 def attn_standin(kv: torch.Tensor, checksum: torch.Tensor, stream=None):
     _lib.call("msi_attn_standin", _ptr(kv), kv.numel() * kv.element_size(), _ptr(checksum),
               _stream(stream))
+
+
+# ---------------------------------------------------------- attention ---- #
+def _check_i32(name, t):
+    if t.dtype != torch.int32 or not t.is_cuda or not t.is_contiguous():
+        raise ValueError(f"{name}: expected a contiguous CUDA int32 tensor")
+
+
+def rope_append(qkv: torch.Tensor, pos: torch.Tensor, n_heads: int, n_kv: int, theta: float,
+                block_table: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
+                q_out: torch.Tensor, stream=None) -> torch.Tensor:
+    """RoPE on the new token's q, k at ``pos`` + KV append (msi_rope_append).
+    qkv bf16 [T, >= (n_heads + 2 n_kv) 128] (row stride may exceed the width);
+    caches bf16 [pages, n_kv, 64, 128]; q_out bf16 [T, n_heads, 128]."""
+    if qkv.dtype != torch.bfloat16 or not qkv.is_cuda or qkv.stride(1) != 1:
+        raise ValueError("rope_append: qkv must be a row-major CUDA bfloat16 matrix")
+    _check_i32("pos", pos)
+    _check_i32("block_table", block_table)
+    for n, t in (("k_cache", k_cache), ("v_cache", v_cache), ("q_out", q_out)):
+        _check_bf16(n, t)
+    _lib.call("msi_rope_append", _ptr(qkv), qkv.stride(0), _ptr(pos), qkv.shape[0], n_heads, n_kv,
+              ctypes.c_float(theta), _ptr(block_table), block_table.shape[1], _ptr(k_cache), _ptr(v_cache),
+              k_cache.shape[0], _ptr(q_out), _stream(stream))
+    return q_out
+
+
+def decode_attention_workspace(T: int, n_heads: int, n_kv: int, max_pages: int, device=None) -> torch.Tensor | None:
+    n = _lib.load().msi_decode_attention_workspace(T, n_heads, n_kv, max_pages)
+    return torch.empty(n, dtype=torch.uint8, device=device) if n else None
+
+
+def decode_attention(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, block_table: torch.Tensor,
+                     seq_lens: torch.Tensor, out: torch.Tensor, workspace: torch.Tensor | None = None,
+                     scale: float | None = None, stream=None) -> torch.Tensor:
+    """GQA decode attention over the paged cache (msi_decode_attention).
+    q bf16 [T, n_heads, 128]; out bf16 [T, n_heads * 128]."""
+    for n, t in (("q", q), ("k_cache", k_cache), ("v_cache", v_cache), ("out", out)):
+        _check_bf16(n, t)
+    _check_i32("block_table", block_table)
+    _check_i32("seq_lens", seq_lens)
+    T, n_heads, d = q.shape
+    n_kv = k_cache.shape[1]
+    if k_cache.shape[2:] != (_lib.KV_PAGE, _lib.HEAD_DIM) or d != _lib.HEAD_DIM:
+        raise ValueError("decode_attention: caches must be [pages, n_kv, 64, 128], q [T, heads, 128]")
+    if workspace is None:
+        workspace = decode_attention_workspace(T, n_heads, n_kv, block_table.shape[1], q.device)
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    scale = d ** -0.5 if scale is None else scale
+    _lib.call("msi_decode_attention", _ptr(q), _ptr(k_cache), _ptr(v_cache), k_cache.shape[0], _ptr(block_table),
+              block_table.shape[1], _ptr(seq_lens), T, n_heads, n_kv, ctypes.c_float(scale), _ptr(out),
+              _ptr(workspace), ws_bytes, _stream(stream))
+    return out
