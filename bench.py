@@ -26,6 +26,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -44,7 +46,7 @@ def parse():
     # (not "--m": torchrun would take it as an abbreviation of its own options)
     ap.add_argument("--micro-batches", dest="m", type=int, default=3, help="m, micro-batches per step")
     ap.add_argument("--layers", type=int, default=4, help="L_sim layers per step")
-    ap.add_argument("--attn", default="standin", choices=["standin", "none"])
+    ap.add_argument("--attn", default="real", choices=["real", "standin", "none"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--split", default="", help="attention+expert GPUs, e.g. 2+2 (default: config-3 ratio)")
@@ -309,8 +311,15 @@ def main():
     if args.attn == "standin" and g.is_attention:
         # decode-attention HBM load of one micro-batch: b_a tokens x s x (K,V) x h/g x bf16
         kv_bytes = args.b_a * wl.avg_seq_len * 2 * (model.hidden // model.gqa_group) * 2
+    att_stages = None
+    if args.attn == "real" and g.is_attention:
+        # real decode attention layer per micro-batch (paged KV at s = avg_seq_len)
+        from paper_2504_02263_b200 import attention as attn_mod
+        w_att = attn_mod.AttentionWeights(model, dev, seed=0)
+        att_stages = [attn_mod.AttentionStage(model, args.b_a, args.layers, dev, weights=w_att,
+                                          avg_seq_len=wl.avg_seq_len, seed=1000 * rank + j) for j in range(plan.m)]
     runner = runtime.PingPongRunner(layer, layers=args.layers, kv_bytes=kv_bytes, chain=False,
-                                    record_timeline=True)
+                                    record_timeline=True, attn=att_stages)
     x0 = [x.clone() for x in xs] if xs else None
 
     def barrier():
@@ -337,6 +346,9 @@ def main():
     # replayed; the FFN timing events are captured with it, so the values read
     # after the loop are those of the last timed replay.
     layer.expert_step = timed_expert_step
+    attn_events = []
+    for stg in att_stages or []:
+        stg.timing = attn_events
     if args.graph:
         runner.capture(xs)
         barrier()
@@ -361,6 +373,22 @@ def main():
     if st != 0:
         raise RuntimeError(f"device status {st} (timeout in a device-side wait)")
     ffn_ms = [s.elapsed_time(e) for s, e in ffn_events]
+    attn_ms = [s.elapsed_time(e) for s, e in attn_events]
+    for stg in att_stages or []:
+        stg.timing = None
+    attn_report = None
+    if att_stages:
+        # decode_attn_kernel: algorithmic bytes (K/V rows read + q + o) per launch
+        by = sum(stg.attn_bytes() for stg in att_stages) * args.layers
+        ms = sum(attn_ms)
+        gbps = by / (ms / 1e3) / 1e9 if ms else None
+        hbm = measured_peaks().get("hbm_gbs") or 6546.6
+        attn_report = {"kernel": "decode_attn_kernel (paged GQA decode, TMA-streamed KV)", "bound": "hbm",
+                       "heads": att_stages[0].n_heads, "kv_heads": att_stages[0].n_kv, "page_tokens": 64,
+                       "mean_ctx": float(np.mean([stg.cache.ctx_host.mean() for stg in att_stages])),
+                       "bytes_per_launch": by / max(len(attn_ms), 1), "avg_launch_ms": ms / max(len(attn_ms), 1),
+                       "achieved": gbps, "peak": hbm, "unit": "GB/s", "frac": gbps / hbm if gbps else None,
+                       "peak_kind": "measured hbm_gbs (MEASURED_PEAKS.json, copy read+write)"}
     rows = calls = 0
     if g.is_expert:
         rows1, calls1 = g.stats()
@@ -450,7 +478,13 @@ def main():
     flops_per_call = 6.0 * (rows_total / max(calls_total, 1)) * model.hidden * model.intermediate
     achieved = flops_per_call / ffn_avg_s / 1e12 if ffn_n else None
     peak = peaks.get("bf16_tflops_sustained") or 1404.8
-    launches_per_mbl = (1 if kv_bytes else 0) + 1 + 1 + 2 + 1  # attn, router, dispatch, 2 GEMMs, combine
+    # our kernels per (micro-batch, layer): attention (stand-in 1; real: rope_append +
+    # decode_attn [+ split combine]; its two projections are cuBLAS), router,
+    # dispatch, 2 GEMMs, combine
+    attn_launches = (1 if kv_bytes else 0)
+    if att_stages:
+        attn_launches = 2 + (1 if att_stages[0].ws is not None else 0)
+    launches_per_mbl = attn_launches + 1 + 1 + 2 + 1
     line = {
         "metric": "decode tokens/s/GPU (MoE layer, ping-pong); M2N dispatch+combine p50 µs",
         "value": value, "unit": "layer-tokens/s", "value_per_gpu": value / world,
@@ -466,7 +500,7 @@ def main():
                                      if colo and args.merge else "ping-pong, m micro-batches"),
                    "L_sim": args.layers, "attention_stage": args.attn,
                    "l2": (f"working set (expert weights {model.experts * 3 * model.hidden * model.intermediate * 2 / 1e9:.1f} GB"
-                          " + KV stand-in) >> 126 MB L2; no flush needed"),
+                          " + KV cache) >> 126 MB L2; no flush needed"),
                    "parallelism": f"dp{n_a}-ep{n_e}",
                    "launch": "CUDA graph per rank (device-tracked epochs)" if args.graph else "eager"},
         "roofline": {"bound": "tensor", "kernel": "expert FFN (grouped_gemm_kernel x2: gate/up+SiLU, down+N2M)",
@@ -479,11 +513,12 @@ def main():
         "clocks": clocks,
         "stage_times": eq5_report(all_stages, plan, args.layers, elapsed_ms / args.steps, colo),
         "load_balance": lb_report,
+        "attention": attn_report,
     }
     # our kernels inside the timed region (per rank, summed over roles)
     per_step = plan.m * args.layers * (launches_per_mbl if colo else 0)
     if not colo:
-        per_step = plan.m * args.layers * (n_a * ((1 if kv_bytes else 0) + 3) + n_e * 2)
+        per_step = plan.m * args.layers * (n_a * (attn_launches + 3) + n_e * 2)
     line["gpu_launches"] = per_step * args.steps
     if not args.no_cpu:
         threads = len(os.sched_getaffinity(0))

@@ -151,6 +151,7 @@ class AttentionStage:
         self.o = torch.empty((T, self.n_heads * D), dtype=torch.bfloat16, device=device)
         self.y = torch.empty((T, model.hidden), dtype=torch.bfloat16, device=device)
         self.ws = ops.decode_attention_workspace(T, self.n_heads, self.n_kv, self.cache.max_pages, device)
+        self.timing = None  # set to a list to collect attention-kernel events
 
     def forward(self, x: torch.Tensor, layer: int, out: torch.Tensor | None = None) -> torch.Tensor:
         """x bf16 [T, h] -> x + Attn(x) W_o^T (bf16 [T, h]) on the current stream."""
@@ -159,7 +160,13 @@ class AttentionStage:
         torch.matmul(x, self.w.wqkv.t(), out=self.qkv)
         ops.rope_append(self.qkv, c.pos, self.n_heads, self.n_kv, self.theta, c.block_table, c.k[layer],
                         c.v[layer], self.q)
+        if self.timing is not None:  # (start, end) events around the attention kernel
+            e0, e1 = torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True)
+            e0.record()
         ops.decode_attention(self.q, c.k[layer], c.v[layer], c.block_table, c.lens, self.o, self.ws)
+        if self.timing is not None:
+            e1.record()
+            self.timing.append((e0, e1))
         torch.addmm(x, self.o, self.w.wo.t(), out=out)
         return out
 

@@ -321,10 +321,17 @@ class PingPongRunner:
     """
 
     def __init__(self, layer: MoEDecodeLayer, layers: int, kv_bytes: int = 0, record_timeline: bool = False,
-                 chain: bool = True):
+                 chain: bool = True, attn: list | None = None):
         self.layer = layer
         self.L = layers
         g = layer.g
+        # attn: one attention.AttentionStage per micro-batch (attention ranks):
+        # the real decode attention layer whose output feeds the MoE layer.
+        # Without it, kv_bytes > 0 runs the HBM stand-in and the MoE layer
+        # reads x directly.
+        self.attn = attn if g.is_attention else None
+        if self.attn is not None and len(self.attn) != g.plan.m:
+            raise ValueError("need one AttentionStage per micro-batch")
         # chain=False: every layer reads the same x and writes x + MoE(x) to a
         # separate buffer (benchmarks: random-init SwiGLU layers without a norm
         # grow |x| quadratically and overflow when chained; the cross-GPU
@@ -342,9 +349,13 @@ class PingPongRunner:
         self.record = record_timeline
         self.events = []
 
-    def _attn(self, j, l):
+    def _attn(self, j, l, x):
+        """Attention stage of micro-batch j, layer l -> the MoE layer's input."""
+        if self.attn is not None:
+            return self.attn[j].forward(x, l)
         if self.kv is not None:
             ops.attn_standin(self.kv, self.checksum)
+        return x
 
     def _out(self, xs, j):
         return xs[j] if self.chain else self.outs[j][: xs[j].shape[0]]
@@ -365,29 +376,29 @@ class PingPongRunner:
         if g.role == "both":
             for l in range(L):
                 for j in range(m):
-                    self._ev(("attn", j, l, 0)); self._attn(j, l); self._ev(("attn", j, l, 1))
+                    self._ev(("attn", j, l, 0)); h = self._attn(j, l, xs[j]); self._ev(("attn", j, l, 1))
                     self._ev(("disp", j, l, 0))
-                    r = lay.router(xs[j], j)
-                    lay.dispatch(xs[j], r, j)
+                    r = lay.router(h, j)
+                    lay.dispatch(h, r, j)
                     self._ev(("disp", j, l, 1))
                     self._ev(("ffn", j, l, 0)); lay.expert_step(j); self._ev(("ffn", j, l, 1))
-                    self._ev(("comb", j, l, 0)); lay.combine(r, resid=xs[j], out=self._out(xs, j)); self._ev(("comb", j, l, 1))
+                    self._ev(("comb", j, l, 0)); lay.combine(r, resid=h, out=self._out(xs, j)); self._ev(("comb", j, l, 1))
         elif g.role == "attention":
-            routes = [None] * m
+            routes, hs = [None] * m, [None] * m
             for i in range(m * L):
                 j, l = i % m, i // m
                 if l > 0:
                     self._ev(("comb", j, l - 1, 0))
-                    lay.combine(routes[j], resid=xs[j], out=self._out(xs, j))
+                    lay.combine(routes[j], resid=hs[j], out=self._out(xs, j))
                     self._ev(("comb", j, l - 1, 1))
-                self._ev(("attn", j, l, 0)); self._attn(j, l); self._ev(("attn", j, l, 1))
+                self._ev(("attn", j, l, 0)); hs[j] = self._attn(j, l, xs[j]); self._ev(("attn", j, l, 1))
                 self._ev(("disp", j, l, 0))
-                routes[j] = lay.router(xs[j], j)
-                lay.dispatch(xs[j], routes[j], j)
+                routes[j] = lay.router(hs[j], j)
+                lay.dispatch(hs[j], routes[j], j)
                 self._ev(("disp", j, l, 1))
             for j in range(m):
                 self._ev(("comb", j, L - 1, 0))
-                lay.combine(routes[j], resid=xs[j], out=self._out(xs, j))
+                lay.combine(routes[j], resid=hs[j], out=self._out(xs, j))
                 self._ev(("comb", j, L - 1, 1))
         else:
             for l in range(L):

@@ -182,3 +182,46 @@ def test_attention_stage_vs_oracle(lib):
         torch.cuda.synchronize()
         assert_close_bf16(to_host(y), ref, f"attention stage step {step}")
         c.advance()
+
+
+def test_pingpong_runner_with_attention_stage(lib):
+    """Co-located decode step through PingPongRunner with the real attention
+    stage feeding the MoE layer (m = 2 micro-batches, two consecutive decode
+    steps): attention output vs the oracle stage, then the MoE layer on that
+    output -- routing bit-exact, layer output within tolerance."""
+    from paper_2504_02263_b200 import attention as A
+    from paper_2504_02263_b200 import ops, runtime
+    from paper_2504_02263_b200.config import DeploymentPlan, as_model_spec
+
+    model = as_model_spec("tiny")
+    m, T = 2, 40
+    plan = DeploymentPlan(n_a=1, n_e=1, m=m, b_a=T, colocated=True)
+    g = runtime.M2NGroup(model, plan, rank=0)
+    wts = O.synth_weights(model.hidden, model.intermediate, model.experts, seed=0)
+    layer = runtime.MoEDecodeLayer(g, wg=to_dev(wts.wg), w13=ops.pack_w13(to_dev(wts.w_gate), to_dev(wts.w_up)),
+                                   w2=to_dev(wts.w_down))
+    w = A.AttentionWeights(model, "cuda", seed=3)
+    stages = [A.AttentionStage(model, T, 1, "cuda", weights=w, avg_seq_len=90, seed=j, headroom=64)
+              for j in range(m)]
+    runner = runtime.PingPongRunner(layer, layers=1, attn=stages, chain=True)
+    xs_host = [O.synth_tokens(T, model.hidden, seed=50 + j) for j in range(m)]
+    xs = [to_dev(x) for x in xs_host]
+    for step in range(2):
+        refs_h = []
+        for j, st in enumerate(stages):
+            c = st.cache
+            refs_h.append(O.attention_stage(xs_host[j], to_host(w.wqkv), to_host(w.wo), c.ctx_host.copy(),
+                                            st.n_heads, st.n_kv, st.theta, c.block_table_host, to_host(c.k[0]),
+                                            to_host(c.v[0])))
+        runner.run(xs)
+        torch.cuda.synchronize()
+        assert g.status() == 0
+        for j, st in enumerate(stages):
+            h = to_host(st.y)
+            assert_close_bf16(h, refs_h[j], f"attention output step {step} mb {j}")
+            ref = O.moe_layer([h], wts, model.topk, n_e=1, resid=True)
+            got = to_host(xs[j])
+            assert_close_bf16(got, ref.out[0], f"layer output step {step} mb {j}")
+            xs_host[j] = got
+            st.cache.advance()
+    g.close()
