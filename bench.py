@@ -60,6 +60,7 @@ def parse():
                     help="every GPU is both an attention and an expert GPU (DeepSeek-V3-shaped config 5)")
     ap.add_argument("--no-merge", dest="merge", action="store_false",
                     help="N=1 co-located: keep m separate micro-batches instead of one merged batch")
+    ap.add_argument("--no-m2n", action="store_true", help="skip the M2N round-trip p50 measurement")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch eagerly from Python instead of replaying a captured CUDA graph")
     return ap.parse_args()
@@ -117,6 +118,16 @@ class ClockSampler:
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
                 "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def ncu_traffic(name: str, b_a: int, n_a: int, n_e: int, colo: bool) -> dict | None:
+    """DRAM bytes per launch of the dominant kernels from the committed ncu
+    capture of this exact configuration (profiles/r01_ncu_traffic.json), or None."""
+    path = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    key = f"{name}|{b_a}|{n_a}+{n_e}|{'colo' if colo else 'disagg'}"
+    return json.load(open(path)).get(key)
 
 
 def measured_peaks() -> dict:
@@ -187,6 +198,62 @@ def eq5_report(all_stages: list, plan, L: int, ms_per_step: float, colocated: bo
     rep["measured_ms"] = ms_per_step
     rep["measured_over_predicted"] = ms_per_step / pred if pred else None
     return rep
+
+
+def m2n_latency(layer, g, x, world: int, iters: int = 1000, warm: int = 50) -> dict | None:
+    """The metric's second half: M2N dispatch + N2M combine round trip p50/p99
+    (µs) for this config's micro-batch (x = the MoE layer input of micro-batch
+    0 on attention ranks), with an identity expert step (msi_expert_echo) in
+    between so the expert GEMM is not counted.  One CUDA graph replay per
+    iteration, barrier + synchronize around each, max over ranks
+    (>= 1000 iterations after >= 50 warm-up)."""
+    import torch
+    import torch.distributed as dist
+
+    route = layer.router(x, 0) if g.is_attention else None
+    out = torch.empty_like(x) if g.is_attention else None
+
+    def trip():
+        if g.is_attention:
+            layer.dispatch(x, route, 0)
+        if g.is_expert:
+            layer.expert_echo(0)
+        if g.is_attention:
+            layer.combine(route, out=out)
+
+    for _ in range(3):
+        trip()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    gr = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream(device=x.device if x is not None else None)
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.graph(gr, stream=side):
+        trip()
+    torch.cuda.synchronize()
+    lat = []
+    for i in range(warm + iters):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        gr.replay()
+        e.record()
+        torch.cuda.synchronize()
+        if i >= warm:
+            lat.append(s.elapsed_time(e) * 1e3 if g.is_attention else 0.0)
+    t = torch.tensor(lat, dtype=torch.float64, device=torch.device("cuda", torch.cuda.current_device()))
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    v = sorted(t.cpu().tolist())
+    if g.status() != 0:
+        raise RuntimeError("device status after the M2N round trips")
+    T, H, K = (x.shape[0], x.shape[1], g.model.topk) if x is not None else (0, 0, 0)
+    return {"p50_us": v[len(v) // 2], "p99_us": v[min(len(v) - 1, int(0.99 * len(v)))], "iters": iters,
+            "tokens_per_attention_gpu": T, "dispatch_bytes_per_attention_gpu": T * K * H * 2,
+            "how": "graph replay of dispatch -> expert echo -> combine, barrier each, max over ranks"}
 
 
 def cpu_model_name() -> str:
@@ -379,7 +446,9 @@ def main():
     attn_report = None
     if att_stages:
         # decode_attn_kernel: algorithmic bytes (K/V rows read + q + o) per launch
-        by = sum(stg.attn_bytes() for stg in att_stages) * args.layers
+        # (the events list holds the eager capture-warmup step and the graph's
+        # last replay: per-launch averages are over whatever was recorded)
+        by = sum(stg.attn_bytes() for stg in att_stages) / len(att_stages) * len(attn_ms)
         ms = sum(attn_ms)
         gbps = by / (ms / 1e3) / 1e9 if ms else None
         hbm = measured_peaks().get("hbm_gbs") or 6546.6
@@ -465,6 +534,14 @@ def main():
                "h2d_bytes_per_step": bytes_io, "d2h_bytes_per_step": bytes_io,
                "note": "per attention rank: m micro-batch inputs H2D from pinned memory, outputs D2H, every step"}
 
+    # ---- the metric's M2N dispatch+combine p50 (this config's micro-batch) ----
+    m2n = None
+    if not args.no_m2n:
+        xm = None
+        if g.is_attention:
+            xm = att_stages[0].y if att_stages else xs[0]
+        m2n = m2n_latency(layer, g, xm, world)
+
     if rank != 0:
         g.close()
         if world > 1:
@@ -472,6 +549,9 @@ def main():
         return
 
     peaks = measured_peaks()
+    traffic = ncu_traffic(model.name, args.b_a, n_a, n_e, colo)
+    if attn_report is not None:
+        attn_report["traffic"] = traffic.get("decode_attn") if traffic else None
     tokens = n_a * plan.m * args.b_a * args.layers * args.steps
     value = tokens / (elapsed_ms / 1e3)
     ffn_avg_s = (ffn_total_ms / max(ffn_n, 1)) / 1e3
@@ -505,7 +585,10 @@ def main():
                    "launch": "CUDA graph per rank (device-tracked epochs)" if args.graph else "eager"},
         "roofline": {"bound": "tensor", "kernel": "expert FFN (grouped_gemm_kernel x2: gate/up+SiLU, down+N2M)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": (achieved / peak) if achieved else None, "traffic": None,
+                     "frac": (achieved / peak) if achieved else None,
+                     "traffic": traffic.get("ffn_pair") if traffic else None,
+                     "traffic_source": "profiles/r01_ncu_traffic.json (ncu --set full, dram read+write per launch pair)"
+                     if traffic else None,
                      "flops_per_launch_pair": flops_per_call, "avg_launch_pair_ms": ffn_avg_s * 1e3,
                      "peak_kind": "measured bf16_tflops_sustained (MEASURED_PEAKS.json)"},
         "e2e": e2e,
@@ -514,6 +597,7 @@ def main():
         "stage_times": eq5_report(all_stages, plan, args.layers, elapsed_ms / args.steps, colo),
         "load_balance": lb_report,
         "attention": attn_report,
+        "m2n": m2n,
     }
     # our kernels inside the timed region (per rank, summed over roles)
     per_step = plan.m * args.layers * (launches_per_mbl if colo else 0)
