@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--inter", type=int, default=16384)
     ap.add_argument("--te", default="64,256,768,1536")
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--exact", action="store_true", help="every expert gets exactly t_e rows (no raggedness)")
     args = ap.parse_args()
 
     import torch
@@ -42,7 +43,8 @@ def main():
     for te in [int(v) for v in args.te.split(",")]:
         # realistic ragged loads: +-5% around te
         g = torch.Generator().manual_seed(te)
-        totals = [max(1, int(te * (0.95 + 0.1 * torch.rand(1, generator=g).item()))) for _ in range(E)]
+        totals = [te if args.exact else max(1, int(te * (0.95 + 0.1 * torch.rand(1, generator=g).item())))
+                  for _ in range(E)]
         rows = sum((t + 127) // 128 * 128 for t in totals)
         x = torch.randn(rows, H, device=dev).to(torch.bfloat16)
         tot = torch.tensor(totals, dtype=torch.int32, device=dev)
@@ -60,7 +62,7 @@ def main():
         ms = s.elapsed_time(e) / args.iters
         flops = 6.0 * sum(totals) * H * Hp
         tf = flops / (ms / 1e3) / 1e12
-        rec = {"cg": os.environ.get("MSI_GEMM_CG", "default"), "te": te, "rows": sum(totals), "ms": ms,
+        rec = {"cg": os.environ.get("MSI_GEMM_CG", "default"), "te": te, "exact": args.exact, "rows": sum(totals), "ms": ms,
                "tflops": tf, "frac_burst": tf / peaks.get("bf16_tflops", 1677.4),
                "frac_sustained": tf / peaks.get("bf16_tflops_sustained", 1404.8),
                "weight_gbps": E * 3 * H * Hp * 2 / (ms / 1e3) / 1e9}

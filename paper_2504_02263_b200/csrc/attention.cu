@@ -293,42 +293,47 @@ __global__ void attn_split_combine_kernel(const float* __restrict__ part_o, cons
   out[hrow * kD + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
 }
 
-// One CTA per token: rotate q (n_heads) and k (n_kv) pairs (i, i+64) by
-// pos * theta^(-2i/128), write q to q_out and k, v into the cache slot.
+// One CTA per token: the token's 64 (cos, sin) pairs of pos * theta^(-2i/128)
+// once into shared memory, then q (n_heads) and k (n_kv) rotated 8 pairs per
+// thread with 16 B loads/stores (pairs (i, i+64)); q to q_out, k and v into
+// the cache slot.
 __global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld, const int* __restrict__ pos,
                                    int n_heads, int n_kv, float theta, const int* __restrict__ bt, int max_pages,
                                    __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
                                    __nv_bfloat16* __restrict__ q_out) {
+  __shared__ float s_cos[kD / 2], s_sin[kD / 2];
   const int t = blockIdx.x;
   const int p = pos[t];
+  if (threadIdx.x < kD / 2) {
+    const int i = threadIdx.x;
+    const float inv = 1.0f / powf(theta, (float)(2 * i) / (float)kD);
+    sincosf((float)p * inv, &s_sin[i], &s_cos[i]);
+  }
+  __syncthreads();
   const int page = bt[(size_t)t * max_pages + p / kPage];
   const int prow = p % kPage;
   const __nv_bfloat16* src = qkv + (size_t)t * ld;
-  const int nrot = (n_heads + n_kv) * 32;  // (head, pair-of-pairs) work items: 2 rotations each
+  const int nrot = (n_heads + n_kv) * 8;  // (head, 8-pair chunk)
   for (int w = threadIdx.x; w < nrot; w += blockDim.x) {
-    const int head = w / 32, j = w % 32;  // pairs i = 2j, 2j+1
+    const int head = w >> 3, c = w & 7;
     const __nv_bfloat16* hs = src + (size_t)head * kD;
-    const __nv_bfloat162 lo = *reinterpret_cast<const __nv_bfloat162*>(hs + 2 * j);
-    const __nv_bfloat162 hi = *reinterpret_cast<const __nv_bfloat162*>(hs + 64 + 2 * j);
-    float r_lo[2], r_hi[2];
+    const uint4 lo4 = *reinterpret_cast<const uint4*>(hs + 8 * c);
+    const uint4 hi4 = *reinterpret_cast<const uint4*>(hs + 64 + 8 * c);
+    const uint32_t lo[4] = {lo4.x, lo4.y, lo4.z, lo4.w}, hi[4] = {hi4.x, hi4.y, hi4.z, hi4.w};
+    uint32_t ro[4], rh[4];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int i = 2 * j + u;
-      const float inv = 1.0f / powf(theta, (float)(2 * i) / (float)kD);
-      float sn, cs;
-      sincosf((float)p * inv, &sn, &cs);
-      const float x0 = __bfloat162float(u ? lo.y : lo.x), x1 = __bfloat162float(u ? hi.y : hi.x);
-      r_lo[u] = x0 * cs - x1 * sn;
-      r_hi[u] = x1 * cs + x0 * sn;
+    for (int j = 0; j < 4; ++j) {
+      const int i0 = 8 * c + 2 * j;
+      const float x0a = bf16lo(lo[j]), x0b = bf16hi(lo[j]);
+      const float x1a = bf16lo(hi[j]), x1b = bf16hi(hi[j]);
+      const float ca = s_cos[i0], sa = s_sin[i0], cb = s_cos[i0 + 1], sb = s_sin[i0 + 1];
+      ro[j] = pack_bf16x2(x0a * ca - x1a * sa, x0b * cb - x1b * sb);
+      rh[j] = pack_bf16x2(x1a * ca + x0a * sa, x1b * cb + x0b * sb);
     }
-    __nv_bfloat16* dst;
-    if (head < n_heads) {
-      dst = q_out + ((size_t)t * n_heads + head) * kD;
-    } else {
-      dst = kc + (((size_t)page * n_kv + (head - n_heads)) * kPage + prow) * kD;
-    }
-    *reinterpret_cast<__nv_bfloat162*>(dst + 2 * j) = __floats2bfloat162_rn(r_lo[0], r_lo[1]);
-    *reinterpret_cast<__nv_bfloat162*>(dst + 64 + 2 * j) = __floats2bfloat162_rn(r_hi[0], r_hi[1]);
+    __nv_bfloat16* dst = head < n_heads ? q_out + ((size_t)t * n_heads + head) * kD
+                                        : kc + (((size_t)page * n_kv + (head - n_heads)) * kPage + prow) * kD;
+    *reinterpret_cast<uint4*>(dst + 8 * c) = make_uint4(ro[0], ro[1], ro[2], ro[3]);
+    *reinterpret_cast<uint4*>(dst + 64 + 8 * c) = make_uint4(rh[0], rh[1], rh[2], rh[3]);
   }
   // v: n_kv heads x 128 dims, 16B vectors
   const uint4* vs = reinterpret_cast<const uint4*>(src + (size_t)(n_heads + n_kv) * kD);
@@ -398,7 +403,7 @@ extern "C" int msi_rope_append(const void* qkv, int64_t qkv_ld, const int32_t* p
   MSI_REQUIRE(theta > 0.f && max_pages > 0 && num_pages > 0, "rope_append: bad theta / page counts");
   MSI_REQUIRE(qkv && pos && block_table && k_cache && v_cache && q_out, "rope_append: null pointer");
   if (T == 0) return 0;
-  rope_append_kernel<<<T, 256, 0, (cudaStream_t)stream>>>(
+  rope_append_kernel<<<T, 128, 0, (cudaStream_t)stream>>>(
       (const __nv_bfloat16*)qkv, qkv_ld, pos, n_heads, n_kv, theta, block_table, max_pages,
       (__nv_bfloat16*)k_cache, (__nv_bfloat16*)v_cache, (__nv_bfloat16*)q_out);
   return check_launch("rope_append_kernel");
