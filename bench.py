@@ -347,13 +347,24 @@ def main():
         u = torch.randn(model.hidden, generator=gu, device=dev)
         u = u / u.norm()
         wgf = wg.float()
-        wgf[0] += args.skew * u
-        wgf[1] += 0.6 * args.skew * u
+        # tokens share a component a*sqrt(H)*u (a = 0.3); experts 0 and 1 get
+        # logit shifts of skew and 0.6*skew along it (skew 0.5 -> max/mean load ~2)
+        a = 0.3
+        wgf[0] += args.skew * u / (a * model.hidden ** 0.5)
+        wgf[1] += 0.6 * args.skew * u / (a * model.hidden ** 0.5)
         wg = wgf.to(torch.bfloat16)
         if xs:
-            xs = [x + u * model.hidden ** 0.5 for x in xs]
+            xs = [x + a * u * model.hidden ** 0.5 for x in xs]
     if xs:
         xs = [x.to(torch.bfloat16) for x in xs]
+    wl = WorkloadSpec()
+    att_stages = None
+    if args.attn == "real" and is_attn_rank:
+        # real decode attention layer per micro-batch (paged KV at s = avg_seq_len)
+        from paper_2504_02263_b200 import attention as attn_mod
+        w_att = attn_mod.AttentionWeights(model, dev, seed=0)
+        att_stages = [attn_mod.AttentionStage(model, args.b_a, args.layers, dev, weights=w_att,
+                                          avg_seq_len=wl.avg_seq_len, seed=1000 * rank + j) for j in range(plan.m)]
     slots, loads = None, None
     if args.balance or args.skew > 0:
         # calibration: this step's routing counts (all attention ranks), placement
@@ -361,8 +372,9 @@ def main():
         cnt = torch.zeros(model.experts, dtype=torch.float64, device=dev)
         if xs:
             from paper_2504_02263_b200 import ops as _ops
-            for x in xs:
-                cnt += _ops.gate_topk(x, wg, model.topk)[2].double()
+            for j, x in enumerate(xs):  # routing of the MoE layer input (after attention)
+                h = att_stages[j].forward(x, 0) if att_stages else x
+                cnt += _ops.gate_topk(h, wg, model.topk)[2].double()
         if world > 1:
             dist.all_reduce(cnt)
         loads = cnt.cpu().numpy()
@@ -373,18 +385,10 @@ def main():
     _, w13, w2 = runtime.synth_device_weights(model, runtime.local_experts(g), seed=0, device=dev)
     layer = runtime.MoEDecodeLayer(g, wg=wg if g.is_attention else None,
                                    w13=w13 if g.is_expert else None, w2=w2 if g.is_expert else None)
-    wl = WorkloadSpec()
     kv_bytes = 0
     if args.attn == "standin" and g.is_attention:
         # decode-attention HBM load of one micro-batch: b_a tokens x s x (K,V) x h/g x bf16
         kv_bytes = args.b_a * wl.avg_seq_len * 2 * (model.hidden // model.gqa_group) * 2
-    att_stages = None
-    if args.attn == "real" and g.is_attention:
-        # real decode attention layer per micro-batch (paged KV at s = avg_seq_len)
-        from paper_2504_02263_b200 import attention as attn_mod
-        w_att = attn_mod.AttentionWeights(model, dev, seed=0)
-        att_stages = [attn_mod.AttentionStage(model, args.b_a, args.layers, dev, weights=w_att,
-                                          avg_seq_len=wl.avg_seq_len, seed=1000 * rank + j) for j in range(plan.m)]
     runner = runtime.PingPongRunner(layer, layers=args.layers, kv_bytes=kv_bytes, chain=False,
                                     record_timeline=True, attn=att_stages)
     x0 = [x.clone() for x in xs] if xs else None
