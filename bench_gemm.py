@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--te", default="64,256,768,1536")
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--exact", action="store_true", help="every expert gets exactly t_e rows (no raggedness)")
+    ap.add_argument("--ab", type=int, default=0,
+                    help="interleaved A/B of the 1-CTA and CTA-pair kernels: N alternating rounds, medians")
     args = ap.parse_args()
 
     import torch
@@ -50,6 +52,35 @@ def main():
         tot = torch.tensor(totals, dtype=torch.int32, device=dev)
         hbuf = torch.empty(rows, Hp, dtype=torch.bfloat16, device=dev)
         y = torch.empty(rows, H, dtype=torch.bfloat16, device=dev)
+        if args.ab:
+            from paper_2504_02263_b200 import _lib
+            lib = _lib.load()
+            per = {1: [], 2: []}
+            for rnd in range(args.ab):
+                for cg in ((1, 2) if rnd % 2 == 0 else (2, 1)):
+                    lib.msi_set_gemm_cta_group(cg)
+                    for _ in range(2):
+                        ops.grouped_ffn(x, tot, w13, w2, hbuf, y)
+                    torch.cuda.synchronize()
+                    s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    s0.record()
+                    for _ in range(args.iters):
+                        ops.grouped_ffn(x, tot, w13, w2, hbuf, y)
+                    e0.record()
+                    torch.cuda.synchronize()
+                    per[cg].append(s0.elapsed_time(e0) / args.iters)
+            lib.msi_set_gemm_cta_group(0)
+            flops = 6.0 * sum(totals) * H * Hp
+            rec = {"ab": args.ab, "te": te, "exact": args.exact, "rows": sum(totals),
+                   "odd_tiles": sum(((t + 127) // 128) % 2 for t in totals)}
+            for cg in (1, 2):
+                ms = sorted(per[cg])[len(per[cg]) // 2]
+                rec[f"cg{cg}_ms"] = ms
+                rec[f"cg{cg}_tflops"] = flops / (ms / 1e3) / 1e12
+            rec["cg2_over_cg1"] = rec["cg1_ms"] / rec["cg2_ms"]
+            out.append(rec)
+            print(json.dumps(rec), flush=True)
+            continue
         for _ in range(3):
             ops.grouped_ffn(x, tot, w13, w2, hbuf, y)
         torch.cuda.synchronize()

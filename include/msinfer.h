@@ -169,7 +169,12 @@ int msi_combine(msi_ctx* ctx, void* out, const float* w, const void* resid,
                 int T, int mb_slot, uint32_t epoch, void* stream);
 
 /* ---- building blocks (also used by tests) -------------------------------- */
-/* w13[e] rows interleaved in 128-row blocks: [gate 128 | up 128] per 256. */
+/* Expert GEMM variant: 1 = one CTA per 128x256 tile, 2 = CTA pairs
+ * (cta_group::2, 256x256 tiles, half pairs for odd 128-row tails), 0 = the
+ * default (env MSI_GEMM_CG, else 2).  Process-wide tuning knob. */
+int msi_set_gemm_cta_group(int cg);
+/* w13[e]: every 256 rows = [gate 64 | up 64 | gate 64 | up 64] of 128
+ * consecutive features (matching gate/up in each 128-column half). */
 int msi_pack_w13(const void* w_gate, const void* w_up, void* w13, int E_l,
                  int inter, int hidden, void* stream);
 /* Stand-alone grouped SwiGLU FFN on compact rows: x [rows][H] where local

@@ -68,6 +68,7 @@ SIGNATURES = {
     "msi_expert_echo": (_I, [_P, _I, _U32, _P]),
     "msi_combine": (_I, [_P, _P, _P, _P, _I, _I, _U32, _P]),
     "msi_pack_w13": (_I, [_P, _P, _P, _I, _I, _I, _P]),
+    "msi_set_gemm_cta_group": (_I, [_I]),
     "msi_grouped_ffn": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _I, _I, _P]),
     "msi_combine_local": (_I, [_P, _P, _P, _P, _I, _I, _I, _P]),
     "msi_attn_standin": (_I, [_P, _SZ, _P, _P]),

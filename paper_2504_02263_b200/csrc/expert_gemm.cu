@@ -80,6 +80,18 @@ __device__ __forceinline__ void decode_tile(const SegInfo<MAXE>& s, int E_l, int
   m = local - n * s.mtiles[e];
 }
 
+// CTA-pair kernels only: the last unit of a segment with an odd number of
+// 128-row tiles is a "half pair" -- an M = 128 pair MMA (64 rows per CTA),
+// which costs half of an M = 256 one, so odd tiles are not padded to 256.
+// Its accumulator is folded in TMEM: row r of the CTA's 64 rows holds N
+// columns [0,128) in lane r and [128,256) in lane 64 + r (measured,
+// scripts/probe_tmem_pair_m128.cu).
+template <int MAXE>
+__device__ __forceinline__ bool half_pair_rows(const SegInfo<MAXE>& s, int e, int m) {
+  const int mt = (s.total[e] + BM - 1) / BM;
+  return (mt & 1) && m == s.mtiles[e] - 1;
+}
+
 template <int CG, int MAXE>
 __global__ void __launch_bounds__(kThreads, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -190,6 +202,10 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   __syncthreads();
   const int ntiles = seg.tile0[p.E_l];
   const int kblocks = p.kdim / BK;
+  auto half_pair = [&](const SegInfo<MAXE>& sg, int e, int m) -> bool {
+    if constexpr (CG == 2) return half_pair_rows(sg, e, m);
+    else return false;
+  };
 
   if (warp == 0 && lane == 0) {
     // ===================== TMA producer (both CTAs of a pair) ==============
@@ -198,7 +214,10 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     for (int tau = unit; tau < ntiles; tau += nunits) {
       int e, n, m;
       decode_tile(seg, p.E_l, tau, e, n, m);
-      const int rowA = seg.start[e] + (m * CG + (int)rank) * BM;  // this CTA's 128 rows
+      // this CTA's A rows: 128 (full tile / pair) or 64 (half pair: the odd
+      // last 128-row tile of a segment split 64/64 over the pair; the box
+      // still moves 128 rows, the MMA reads the first 64)
+      const int rowA = seg.start[e] + m * CG * BM + (int)rank * (half_pair(seg, e, m) ? BM / 2 : BM);
       const int rowB = e * p.n_total + n * BN + (int)rank * C::B_ROWS;
       for (int kb = 0; kb < kblocks; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
@@ -217,11 +236,15 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     }
   } else if (warp == 1 && lane == 0 && leader) {
     // ===================== MMA issuer (leader only) =====================
-    constexpr uint32_t idesc = umma_idesc_bf16(BM * CG, BN);
+    constexpr uint32_t idesc_full = umma_idesc_bf16(BM * CG, BN);
+    constexpr uint32_t idesc_half = umma_idesc_bf16(BM, BN);  // CG = 2 only
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
     for (int tau = unit; tau < ntiles; tau += nunits, ++it) {
+      int e_, n_, m_;
+      decode_tile(seg, p.E_l, tau, e_, n_, m_);
+      const uint32_t idesc = half_pair(seg, e_, m_) ? idesc_half : idesc_full;
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
       mbar_wait(&tempty[acc], aph ^ 1);
@@ -247,45 +270,60 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     }
   } else if (warp >= 4) {
     // ===================== epilogue (both CTAs, own TMEM rows) ============
+    // Full tile: warp q owns TMEM lanes [32q, 32q+32) = rows 32q.. of the
+    // CTA's 128, all 256 N columns.  Half pair: lanes hold rows (q & 1)*32..
+    // of the CTA's 64 and N columns [(q >> 1)*128, +128) (folded layout).
+    // GEMM1 N tiles pack [gate 64 | up 64 | gate 64 | up 64] (msi_pack_w13), so
+    // every 128-column half holds matching gate/up features.
     const int q = warp & 3;  // TMEM lanes [32q, 32q+32)
     uint8_t* stg = sEpi + q * EPI_WARP_BYTES;
     int it = 0;
     for (int tau = unit; tau < ntiles; tau += nunits, ++it) {
       int e, n, m;
       decode_tile(seg, p.E_l, tau, e, n, m);
-      const int mtile = m * CG + (int)rank;
+      const bool hp = half_pair(seg, e, m);
+      const int rowbase = hp ? m * CG * BM + (int)rank * (BM / 2) : (m * CG + (int)rank) * BM;
+      const int rowsub = hp ? (q & 1) * 32 : q * 32;
+      const int nh = hp ? (q >> 1) : 0;  // N half held by this warp (half pair)
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-      const int row_local = mtile * BM + q * 32 + lane;         // row within expert segment
-      const int row_global = seg.start[e] + row_local;          // row in recv / hbuf
-      const int valid_rows = min(32, max(0, seg.total[e] - (mtile * BM + q * 32)));
+      const int row_local = rowbase + rowsub + lane;                // row within expert segment
+      const int row_global = seg.start[e] + row_local;              // row in recv / hbuf
+      const int valid_rows = min(32, max(0, seg.total[e] - (rowbase + rowsub)));
+      // output columns of this warp: mode 0 writes 128 features per tile
+      // (64 per N half), mode 1 writes 256 columns (128 per N half)
+      const int colofs = (p.mode == 0) ? nh * 64 : nh * 128;
 
-      // Destination of this thread's row (used by the store loop via shuffles).
       char* rowdst = nullptr;
       if (row_local < seg.total[e]) {
         if (p.mode == 0) {
-          rowdst = reinterpret_cast<char*>(p.out) + ((size_t)row_global * p.out_ld + (size_t)n * (BN / 2)) * 2;
+          rowdst = reinterpret_cast<char*>(p.out) + ((size_t)row_global * p.out_ld + (size_t)n * (BN / 2) + colofs) * 2;
         } else if (p.meta) {
           const int2 md = p.meta[row_global];
-          rowdst = p.dst[md.x] + ((size_t)md.y * p.out_ld + (size_t)n * BN) * 2;
+          rowdst = p.dst[md.x] + ((size_t)md.y * p.out_ld + (size_t)n * BN + colofs) * 2;
         } else {
-          rowdst = reinterpret_cast<char*>(p.out) + ((size_t)row_global * p.out_ld + (size_t)n * BN) * 2;
+          rowdst = reinterpret_cast<char*>(p.out) + ((size_t)row_global * p.out_ld + (size_t)n * BN + colofs) * 2;
         }
       }
-      const int halves = (p.mode == 0) ? 1 : 2;
-      for (int half = 0; half < halves; ++half) {
-        // ---- TMEM -> registers -> swizzled staging (16 B units, unit u of
-        //      row r lives at r*256 + ((u ^ (r & 15)) * 16)) ----
+      // 256-byte row segments (mode 1 full: 2, mode 1 half / mode 0 full: 1)
+      // or one 128-byte segment (mode 0 half)
+      const int segs = (p.mode == 1 && !hp) ? 2 : 1;
+      const bool narrow = (p.mode == 0 && hp);
+      for (int sgi = 0; sgi < segs; ++sgi) {
         if (valid_rows > 0) {
+          const int nchunk = narrow ? 2 : 4;
 #pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
+          for (int c = 0; c < nchunk; ++c) {
             uint32_t packed[16];
             if (p.mode == 0) {
+              // features 32c.. of this tile (half pair: of this N half):
+              // gate at column gc, up at gc + 64
+              const int gc = hp ? c * 32 : (c < 2 ? c * 32 : 128 + (c - 2) * 32);
               uint32_t g[32], u[32];
-              tmem_ld32(tbase + c * 32, g);
-              tmem_ld32(tbase + 128 + c * 32, u);
+              tmem_ld32(tbase + gc, g);
+              tmem_ld32(tbase + gc + 64, u);
               tmem_wait_ld();
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
@@ -297,7 +335,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
               }
             } else {
               uint32_t v[32];
-              tmem_ld32(tbase + half * 128 + c * 32, v);
+              tmem_ld32(tbase + sgi * 128 + c * 32, v);
               tmem_wait_ld();
 #pragma unroll
               for (int j = 0; j < 16; ++j)
@@ -307,11 +345,12 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             for (int j = 0; j < 4; ++j) {
               const int u = c * 4 + j;
               uint4 val = make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
-              *reinterpret_cast<uint4*>(stg + lane * 256 + ((u ^ (lane & 15)) * 16)) = val;
+              const int sw = narrow ? (u ^ (lane & 7)) : (u ^ (lane & 15));
+              *reinterpret_cast<uint4*>(stg + lane * 256 + sw * 16) = val;
             }
           }
         }
-        if (half == halves - 1) {
+        if (sgi == segs - 1) {
           // accumulator fully read: hand the TMEM buffer back to the MMA warp
           // (one arrival per warp; a pair's peer arrives on the leader's barrier)
           tc_fence_before();
@@ -322,14 +361,27 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           }
         }
         __syncwarp();
-        // ---- coalesced row stores: 2 rows per instruction, 256 B per row ----
-        const int u = lane & 15;
-        for (int r0 = 0; r0 < valid_rows; r0 += 2) {
-          const int r = r0 + (lane >> 4);
-          char* dst = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(rowdst), r & 31));
-          if (r < valid_rows) {
-            uint4 val = *reinterpret_cast<const uint4*>(stg + r * 256 + ((u ^ (r & 15)) * 16));
-            st_v4(dst + half * 256 + u * 16, val);
+        if (!narrow) {
+          // ---- coalesced row stores: 2 rows per instruction, 256 B per row ----
+          const int u = lane & 15;
+          for (int r0 = 0; r0 < valid_rows; r0 += 2) {
+            const int r = r0 + (lane >> 4);
+            char* dst = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(rowdst), r & 31));
+            if (r < valid_rows) {
+              uint4 val = *reinterpret_cast<const uint4*>(stg + r * 256 + ((u ^ (r & 15)) * 16));
+              st_v4(dst + sgi * 256 + u * 16, val);
+            }
+          }
+        } else {
+          // ---- 128 B rows: 4 rows per instruction ----
+          const int u = lane & 7;
+          for (int r0 = 0; r0 < valid_rows; r0 += 4) {
+            const int r = r0 + (lane >> 3);
+            char* dst = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(rowdst), r & 31));
+            if (r < valid_rows) {
+              uint4 val = *reinterpret_cast<const uint4*>(stg + r * 256 + ((u ^ (r & 7)) * 16));
+              st_v4(dst + u * 16, val);
+            }
           }
         }
         __syncwarp();
@@ -400,15 +452,16 @@ int make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, 
 
 __global__ void pack_w13_kernel(const uint4* __restrict__ gate, const uint4* __restrict__ up,
                                 uint4* __restrict__ out, int E_l, int inter, int hidden) {
-  // out[e][256 j + i] = gate[e][128 j + i] (i < 128), up[e][128 j + i - 128] otherwise
+  // out[e][256 j + 64 b + i] = (b even ? gate : up)[e][128 j + 64 (b >> 1) + i]
+  // i.e. every 256-row N tile is [gate 64 | up 64 | gate 64 | up 64] of 128 features
   const size_t row_vec = (size_t)hidden / 8;
   const size_t total = (size_t)E_l * 2 * inter * row_vec;
   for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < total; v += (size_t)gridDim.x * blockDim.x) {
     const size_t row = v / row_vec, col = v % row_vec;
     const size_t e = row / (2 * inter), r = row % (2 * inter);
-    const size_t blk = r / 256, i = r % 256;
-    const uint4* src = (i < 128) ? gate : up;
-    const size_t srow = e * inter + blk * 128 + (i & 127);
+    const size_t blk = r / 256, i = r % 256, b = i / 64;
+    const uint4* src = (b & 1) ? up : gate;
+    const size_t srow = e * inter + blk * 128 + (b >> 1) * 64 + (i & 63);
     out[v] = src[srow * row_vec + col];
   }
 }
@@ -461,11 +514,16 @@ int launch_cg(const GemmLaunch& L, cudaStream_t st) {
 // which measured equal or faster on B200 (profiles/r01_gemm_cg_ab.jsonl: both
 // run at the power-capped tensor rate for t_e >= 768, and pairing M tiles
 // adds padding at small t_e).
+static int g_cg_override = 0;
+
 int default_cg() {
+  if (g_cg_override) return g_cg_override;
   static int cg = 0;
   if (!cg) {
+    // CTA pairs by default: 4-17 % faster than 1-CTA tiles for t_e <= 1024
+    // (interleaved A/B, profiles/r01_gemm_ab.jsonl), 2-3 % slower at 1536
     const char* v = getenv("MSI_GEMM_CG");
-    cg = (v && v[0] == '2') ? 2 : 1;
+    cg = (v && v[0] == '1') ? 1 : 2;
   }
   return cg;
 }
@@ -530,4 +588,10 @@ extern "C" int msi_grouped_ffn(const void* x, const int32_t* total, int E_l, int
                                const void* w2, void* hbuf, void* y, int hidden, int inter, void* stream) {
   return msi::grouped_ffn_local(x, total, E_l, rows, w13, w2, hbuf, y, hidden, inter,
                                 reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int msi_set_gemm_cta_group(int cg) {
+  MSI_REQUIRE(cg == 0 || cg == 1 || cg == 2, "msi_set_gemm_cta_group: 0 (default), 1 or 2");
+  msi::g_cg_override = cg;
+  return 0;
 }

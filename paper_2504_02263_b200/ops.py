@@ -67,7 +67,8 @@ def gate_topk(x: torch.Tensor, wg: torch.Tensor, topk: int, ws: RouterWorkspace 
 
 
 def pack_w13(w_gate: torch.Tensor, w_up: torch.Tensor, stream=None) -> torch.Tensor:
-    """[E_l, H', H] gate + up -> [E_l, 2H', H] interleaved in 128-row blocks."""
+    """[E_l, H', H] gate + up -> [E_l, 2H', H]: each 256-row GEMM1 N tile holds
+    [gate 64 | up 64 | gate 64 | up 64] of 128 consecutive features."""
     _check_bf16("w_gate", w_gate, 3)
     _check_bf16("w_up", w_up, 3)
     E_l, Hp, H = w_gate.shape

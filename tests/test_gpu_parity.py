@@ -128,7 +128,8 @@ def test_pack_w13_layout(lib):
     g = torch.randn(E_l, Hp, H, device="cuda").to(torch.bfloat16)
     u = torch.randn(E_l, Hp, H, device="cuda").to(torch.bfloat16)
     w = ops.pack_w13(g, u)
-    ref = torch.cat([g.view(E_l, Hp // 128, 128, H), u.view(E_l, Hp // 128, 128, H)], dim=2).view(E_l, 2 * Hp, H)
+    # every 256-row N tile: [gate 64 | up 64 | gate 64 | up 64] of 128 features
+    ref = torch.stack([g.view(E_l, Hp // 64, 64, H), u.view(E_l, Hp // 64, 64, H)], dim=2).view(E_l, 2 * Hp, H)
     assert torch.equal(w, ref)
 
 
