@@ -12,7 +12,7 @@ ARGS="--steps ${STEPS:-10} --warmup ${WARMUP:-3}"
 timeout 600 python bench.py $ARGS > gpurun_out/bench_n1.log 2>&1 || { echo "bench failed"; tail -20 gpurun_out/bench_n1.log; exit 1; }
 grep '^{' gpurun_out/bench_n1.log | tail -1 > gpurun_out/bench_n1.json
 NCU=/usr/local/cuda/bin/ncu
-SMALL="--steps 1 --warmup 3 --no-e2e --no-cpu --no-graph"
+SMALL="--steps 1 --warmup 3 --no-e2e --no-cpu --no-graph --no-m2n"
 timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_n1.csv \
     python bench.py $SMALL > gpurun_out/ncu_launches.log 2>&1 || echo "launch list failed"
 timeout 1200 $NCU --set full --clock-control none --import-source on -k regex:grouped_gemm -s 24 -c 2 \
