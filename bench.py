@@ -142,20 +142,47 @@ def measured_peaks() -> dict:
 _CPU_CACHE = {}
 
 
-def cpu_sample(model, b_a: int, threads: int) -> dict:
+def cpu_sample(model, b_a: int, threads: int, attn: bool = True) -> dict:
     """The oracle (CPU restatement, oracle/) on a bounded sample of one
-    micro-batch of the workload: router over all b_a tokens, one expert's
-    SwiGLU FFN over its share of rows (b_a*K/E), combine over b_a tokens; the
-    layer time is projected as router + E x expert + combine."""
+    micro-batch of the workload: the attention stage on a 32-sequence sample
+    (QKV projection, RoPE + KV append, paged attention at s = 730, output
+    projection), router over all b_a tokens, one expert's SwiGLU FFN over its
+    share of rows (b_a*K/E), combine over b_a tokens; the layer time is
+    projected as (b_a/32) x attention + router + E x expert + combine."""
     import numpy as np
     from oracle import oracle as O
+    from paper_2504_02263_b200.config import WorkloadSpec
 
     os.environ.setdefault("OMP_NUM_THREADS", str(threads))
     H, Hp, E, K = model.hidden, model.intermediate, model.experts, model.topk
     key = (model.name, b_a)
+    S = 32
     if key not in _CPU_CACHE:  # inputs are not part of the timed sample
-        _CPU_CACHE[key] = (O.synth_tokens(b_a, H, seed=1), O.synth_weights(H, Hp, E, seed=0, experts=[0]))
-    x, wts = _CPU_CACHE[key]
+        rng = np.random.default_rng(3)
+        n_heads = H // 128
+        g = max(1, min(model.gqa_group, n_heads))
+        while n_heads % g:
+            g -= 1
+        n_kv = n_heads // g
+        ctx = rng.integers(1, 2 * WorkloadSpec().avg_seq_len, size=S).astype(np.int32)
+        need = (ctx + 1 + 63) // 64
+        bt = np.zeros((S, int(need.max())), np.int32)
+        off = 0
+        for t in range(S):
+            bt[t, : need[t]] = np.arange(off, off + need[t])
+            off += need[t]
+        kc = O.bf16_round(rng.standard_normal((off, n_kv, 64, 128), dtype=np.float32))
+        vc = O.bf16_round(rng.standard_normal((off, n_kv, 64, 128), dtype=np.float32))
+        wqkv = O.bf16_round(rng.standard_normal(((n_heads + 2 * n_kv) * 128, H), dtype=np.float32) / np.sqrt(H))
+        wo = O.bf16_round(rng.standard_normal((H, n_heads * 128), dtype=np.float32) / np.sqrt(H))
+        _CPU_CACHE[key] = (O.synth_tokens(b_a, H, seed=1), O.synth_weights(H, Hp, E, seed=0, experts=[0]),
+                           (wqkv, wo, ctx, n_heads, n_kv, bt, kc, vc))
+    x, wts, (wqkv, wo, ctx, n_heads, n_kv, bt, kc, vc) = _CPU_CACHE[key]
+    t_attn = 0.0
+    if attn:
+        t0 = time.perf_counter()
+        O.attention_stage(x[:S], wqkv, wo, ctx, n_heads, n_kv, 1e6, bt, kc, vc)
+        t_attn = (time.perf_counter() - t0) * b_a / S
     t0 = time.perf_counter()
     idx, w = O.router(x, wts.wg, K)
     cnt, slot = O.place(idx, E)
@@ -168,11 +195,14 @@ def cpu_sample(model, b_a: int, threads: int) -> dict:
     t0 = time.perf_counter()
     O.combine(y, w, x)
     t_comb = time.perf_counter() - t0
-    t_layer = t_router + E * t_expert + t_comb
-    return {"tokens_per_s": b_a / t_layer, "t_router_s": t_router, "t_expert_s": t_expert,
+    t_layer = t_attn + t_router + E * t_expert + t_comb
+    return {"tokens_per_s": b_a / t_layer, "t_attention_s": t_attn, "t_router_s": t_router, "t_expert_s": t_expert,
             "t_combine_s": t_comb, "t_layer_s": t_layer,
-            "sample": f"1 micro-batch of {b_a} tokens: router+placement (all tokens), SwiGLU FFN of 1 of {E} experts "
-                      f"({rows} rows) x{E}, combine; numpy/OpenBLAS fp32 + C oracle"}
+            "sample": (f"1 micro-batch of {b_a} tokens: attention stage on {S} sequences (s=730 mean) scaled to "
+                       f"{b_a}, router+placement (all tokens), SwiGLU FFN of 1 of {E} experts ({rows} rows) x{E}, "
+                       "combine; numpy/OpenBLAS fp32 + C oracle") if attn else
+                      (f"1 micro-batch of {b_a} tokens: router+placement (all tokens), SwiGLU FFN of 1 of {E} "
+                       f"experts ({rows} rows) x{E}, combine; numpy/OpenBLAS fp32 + C oracle")}
 
 
 def eq5_report(all_stages: list, plan, L: int, ms_per_step: float, colocated: bool) -> dict:
@@ -279,20 +309,25 @@ def run_reference(args):
     model = as_model_spec(args.shape)
     threads = len(os.sched_getaffinity(0))
     n_a, n_e, colo = SPLITS.get(args.gpus, (1, 1, True))
+    if args.colocated:
+        colo = True
+    # the GPU arm's micro-batch (co-located: m micro-batches merged)
+    b_a = args.m * args.b_a if (colo and args.merge) else args.b_a
     vals = []
     info = None
     for i in range(args.warmup + args.steps):
-        info = cpu_sample(model, min(args.b_a, 256), threads)
+        info = cpu_sample(model, b_a, threads, attn=args.attn == "real")
         if i >= args.warmup:
             vals.append(info["tokens_per_s"])
     v = statistics.median(vals)
     line = {"impl": "reference", "metric": "decode tokens/s/GPU (MoE layer, ping-pong); M2N dispatch+combine p50 µs",
             "value": v, "unit": "layer-tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * min(args.b_a, 256) / v, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1e3 * b_a / v, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"{model.name} MoE layer, CPU oracle (reference has no implementation)",
                        "hidden": model.hidden, "intermediate": model.intermediate, "experts": model.experts,
-                       "topk": model.topk, "b_a": args.b_a, "m": args.m},
+                       "topk": model.topk, "b_a": b_a, "m": 1 if (colo and args.merge) else args.m,
+                       "attention_stage": args.attn},
             "cpu_baseline": {"value": v, "unit": "layer-tokens/s", "cores": threads, "kind": "port",
                              "sample": info["sample"], "cpu": cpu_model_name()},
             "e2e": {"value": v, "unit": "layer-tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -652,10 +687,11 @@ def main():
     line["gpu_launches"] = per_step * args.steps
     if not args.no_cpu:
         threads = len(os.sched_getaffinity(0))
-        cs = cpu_sample(model, args.b_a, threads)
+        cs = cpu_sample(model, args.b_a, threads, attn=args.attn == "real")
         line["cpu_baseline"] = {"value": cs["tokens_per_s"], "unit": "layer-tokens/s", "cores": threads,
                                 "kind": "port", "sample": cs["sample"], "cpu": cpu_model_name(),
-                                "t_router_s": cs["t_router_s"], "t_expert_s": cs["t_expert_s"]}
+                                "t_attention_s": cs["t_attention_s"], "t_router_s": cs["t_router_s"],
+                                "t_expert_s": cs["t_expert_s"]}
     print(json.dumps(line), flush=True)
     g.close()
     if world > 1:
