@@ -305,6 +305,23 @@ __device__ __forceinline__ uint32_t ld_shared_cluster_u32(uint32_t cluster_addr)
   asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(cluster_addr) : "memory");
   return v;
 }
+// Wait with cluster-scope acquire: for barriers a peer CTA arrives on
+// (mbarrier.arrive.release.cluster) after writing this CTA's shared memory.
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAITC:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1, 10000000;\n"
+      "@P1 bra DONEC;\n"
+      "bra LAB_WAITC;\n"
+      "DONEC:\n"
+      "}\n" ::"r"(addr), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void st_shared_cluster_u32(uint32_t cluster_addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
+}
 // Bit 24 of a shared::cluster address selects the CTA of a pair: clearing it
 // addresses the leader (rank 0) -- used to signal the leader's barriers.
 constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;

@@ -39,6 +39,7 @@ constexpr int BM = 128, BN = 256, BK = 64;
 constexpr int EPI_WARP_BYTES = 32 * 256;  // 32 rows x 128 bf16
 constexpr int kThreads = 256;
 constexpr int TMEM_COLS = 512;
+constexpr int TRING = 4;  // tile ids in flight between the scheduler and the roles
 
 // Per-CTA-group configuration.  CG=1: one CTA computes a 128x256 tile from
 // A 128x64 + B 256x64 per stage (48 KB).  CG=2: a CTA pair computes a 256x256
@@ -107,6 +108,9 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   uint64_t* empty = bars + STAGES;           // [STAGES]
   uint64_t* tfull = bars + 2 * STAGES;       // [2]
   uint64_t* tempty = bars + 2 * STAGES + 2;  // [2]   (CG=2: the leader's is used)
+  uint64_t* qfull = bars + 2 * STAGES + 4;   // [TRING] tile-id ring (per CTA)
+  uint64_t* qempty = qfull + TRING;          // [TRING] (CG=2: the leader's is used)
+  __shared__ int s_tau[TRING];
   __shared__ uint32_t s_tmem;
   __shared__ SegInfo<MAXE> seg;
   __shared__ int s_last, s_abort;
@@ -135,6 +139,9 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     tma_prefetch(&tmB);
     for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4 * CG); }
+    // ring consumers: MMA thread + 4 epilogue warps (+ the peer's producer
+    // and 4 epilogue warps, which arrive on the leader's barrier)
+    for (int i = 0; i < TRING; ++i) { mbar_init(&qfull[i], 1); mbar_init(&qempty[i], CG == 2 ? 10 : 5); }
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -206,12 +213,48 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     if constexpr (CG == 2) return half_pair_rows(sg, e, m);
     else return false;
   };
+  // ---- dynamic tile scheduler ------------------------------------------
+  // The leader's producer thread takes tile ids in order from p.tile_ctr and
+  // publishes them through a TRING-deep ring to every role of the CTA (and of
+  // the peer CTA).  Taking tiles in order keeps the CTAs that run together on
+  // neighbouring tiles (the M tiles of one N tile share its weights in L2)
+  // even though half-pair tiles cost half: a static round-robin drifts
+  // apart and re-reads weights from DRAM (measured 2.2x).
+  auto publish_tile = [&](int it) -> int {  // leader producer thread only
+    const int slot = it % TRING;
+    if (it >= TRING) mbar_wait_cluster(&qempty[slot], ((it / TRING) - 1) & 1);
+    const uint32_t t = atomicAdd(p.tile_ctr, 1u);
+    if (t == (uint32_t)(ntiles + nunits - 1)) *p.tile_ctr = 0;  // the launch's last fetch
+    s_tau[slot] = (int)t;
+    if constexpr (CG == 2) {
+      st_shared_cluster_u32(mapa_shared(smem_u32(&s_tau[slot]), 1), t);
+      mbar_arrive_cluster(mapa_shared(smem_u32(&qfull[slot]), 1));
+    }
+    mbar_arrive(&qfull[slot]);
+    return (int)t;
+  };
+  auto take_tile = [&](int it, bool arrive) -> int {  // consumers (one call per warp-role and tile)
+    const int slot = it % TRING;
+    mbar_wait_cluster(&qfull[slot], (it / TRING) & 1);
+    const int t = s_tau[slot];
+    if (arrive) {
+      if constexpr (CG == 2) {
+        if (leader) mbar_arrive(&qempty[slot]);
+        else mbar_arrive_cluster(mapa_shared(smem_u32(&qempty[slot]), 0));
+      } else {
+        mbar_arrive(&qempty[slot]);
+      }
+    }
+    return t;
+  };
 
   if (warp == 0 && lane == 0) {
     // ===================== TMA producer (both CTAs of a pair) ==============
     int stage = 0;
     uint32_t phase = 0;
-    for (int tau = unit; tau < ntiles; tau += nunits) {
+    for (int it = 0;; ++it) {
+      const int tau = leader ? publish_tile(it) : take_tile(it, true);
+      if (tau >= ntiles) break;
       int e, n, m;
       decode_tile(seg, p.E_l, tau, e, n, m);
       // this CTA's A rows: 128 (full tile / pair) or 64 (half pair: the odd
@@ -240,8 +283,9 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     constexpr uint32_t idesc_half = umma_idesc_bf16(BM, BN);  // CG = 2 only
     int stage = 0;
     uint32_t phase = 0;
-    int it = 0;
-    for (int tau = unit; tau < ntiles; tau += nunits, ++it) {
+    for (int it = 0;; ++it) {
+      const int tau = take_tile(it, true);
+      if (tau >= ntiles) break;
       int e_, n_, m_;
       decode_tile(seg, p.E_l, tau, e_, n_, m_);
       const uint32_t idesc = half_pair(seg, e_, m_) ? idesc_half : idesc_full;
@@ -277,8 +321,21 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     // every 128-column half holds matching gate/up features.
     const int q = warp & 3;  // TMEM lanes [32q, 32q+32)
     uint8_t* stg = sEpi + q * EPI_WARP_BYTES;
-    int it = 0;
-    for (int tau = unit; tau < ntiles; tau += nunits, ++it) {
+    for (int it = 0;; ++it) {
+      int tau = 0;
+      if (lane == 0) tau = take_tile(it, false);
+      tau = __shfl_sync(0xffffffffu, tau, 0);
+      __syncwarp();
+      if (lane == 0) {  // one ring arrival per epilogue warp
+        const int slot = it % TRING;
+        if constexpr (CG == 2) {
+          if (leader) mbar_arrive(&qempty[slot]);
+          else mbar_arrive_cluster(mapa_shared(smem_u32(&qempty[slot]), 0));
+        } else {
+          mbar_arrive(&qempty[slot]);
+        }
+      }
+      if (tau >= ntiles) break;
       int e, n, m;
       decode_tile(seg, p.E_l, tau, e, n, m);
       const bool hp = half_pair(seg, e, m);
@@ -529,6 +586,7 @@ int default_cg() {
 }
 
 int grouped_gemm_launch(const GemmLaunch& L, cudaStream_t st) {
+  MSI_REQUIRE(L.p.tile_ctr != nullptr, "grouped_gemm: tile counter required");
   MSI_REQUIRE(L.p.E_l >= 1 && L.p.E_l <= MSI_MAX_LOCAL_EXPERTS, "grouped_gemm: E_l out of range");
   MSI_REQUIRE(L.p.kdim % BK == 0 && L.p.n_total % BN == 0, "grouped_gemm: K %% 64 and N %% 256 required");
   const int cg = L.cta_group ? L.cta_group : default_cg();
@@ -545,9 +603,31 @@ int pack_w13(const void* gate, const void* up, void* out, int E_l, int inter, in
   return check_launch("pack_w13_kernel");
 }
 
+// Tile counters of the context-free msi_grouped_ffn, one pair per device
+// (allocated zeroed on first use; each launch leaves its counter at 0).
+// Calls on one device are therefore serialised on a stream by the caller.
+static uint32_t* local_tile_counters(int* rc) {
+  static uint32_t* ctr[64] = {};
+  int dev = 0;
+  *rc = (int)cudaGetDevice(&dev);
+  if (*rc) return nullptr;
+  if (dev < 0 || dev >= 64) { set_error("grouped_ffn: device id %d", dev); *rc = MSI_EINVAL; return nullptr; }
+  if (!ctr[dev]) {
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, 256);
+    if (e == cudaSuccess) e = cudaMemset(p, 0, 256);
+    if (e != cudaSuccess) { set_error("grouped_ffn: tile counters: %s", cudaGetErrorString(e)); *rc = (int)e; return nullptr; }
+    ctr[dev] = reinterpret_cast<uint32_t*>(p);
+  }
+  return ctr[dev];
+}
+
 int grouped_ffn_local(const void* x, const int32_t* total, int E_l, int rows, const void* w13,
                       const void* w2, void* hbuf, void* y, int hidden, int inter, cudaStream_t st) {
   MSI_REQUIRE(hidden % 256 == 0 && inter % 128 == 0, "grouped_ffn: hidden %% 256 and inter %% 128 required");
+  int crc = 0;
+  uint32_t* ctrs = local_tile_counters(&crc);
+  if (!ctrs) return crc;
   GemmLaunch g1{};
   g1.a = x;
   g1.a_rows = rows;
@@ -560,10 +640,12 @@ int grouped_ffn_local(const void* x, const int32_t* total, int E_l, int rows, co
   g1.p.mode = 0;
   g1.p.out = reinterpret_cast<__nv_bfloat16*>(hbuf);
   g1.p.out_ld = inter;
+  g1.p.tile_ctr = ctrs;
   int rc = grouped_gemm_launch(g1, st);
   if (rc) return rc;
   GemmLaunch g2{};
   g2.a = hbuf;
+  g2.p.tile_ctr = ctrs + 32;
   g2.a_rows = rows;
   g2.b = w2;
   g2.p.E_l = E_l;

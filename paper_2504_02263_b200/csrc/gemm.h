@@ -38,6 +38,9 @@ struct GemmParams {
   int out_ld;               // elements per output row (H' or H)
   const int2* meta;         // mode 1: (sender, t*K+k) per row
   char* dst[MSI_MAX_RANKS]; // mode 1: combine buffer base per sender index
+  // dynamic tile scheduler: CTAs (pairs) take tiles in order from this
+  // counter (0 at launch; the launch's last fetch resets it)
+  uint32_t* tile_ctr;
   // completion signal (last CTA): red.release.sys +1 on each sig[i]
   uint32_t* ticket;
   uint32_t* sig[MSI_MAX_RANKS];

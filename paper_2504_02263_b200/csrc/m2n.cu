@@ -770,6 +770,7 @@ extern "C" int msi_expert_ffn(msi_ctx* c, const void* w13, const void* w2, int m
   g1.p.mode = 0;
   g1.p.out = reinterpret_cast<__nv_bfloat16*>(c->hbuf);
   g1.p.out_ld = p.inter;
+  g1.p.tile_ctr = d.my_fticket + mb_slot * CTR_STRIDE + 1;  // spare words of the slot's ticket line
   int rc = grouped_gemm_launch(g1, st);
   if (rc) return rc;
 
@@ -791,6 +792,7 @@ extern "C" int msi_expert_ffn(msi_ctx* c, const void* w13, const void* w2, int m
   g2.p.meta = reinterpret_cast<const int2*>(c->heap + L.meta + mb_slot * L.meta_slot);
   for (int s = 0; s < p.n_a; ++s) g2.p.dst[s] = d.ybuf_of[s] + mb_slot * L.ybuf_slot;
   g2.p.ticket = d.my_fticket + mb_slot * CTR_STRIDE;
+  g2.p.tile_ctr = d.my_fticket + mb_slot * CTR_STRIDE + 2;
   for (int s = 0; s < p.n_a; ++s) g2.p.sig[s] = d.comb_of[s] + mb_slot * CTR_STRIDE;
   g2.p.n_sig = p.n_a;
   g2.p.epoch = epoch;
