@@ -6,7 +6,7 @@ DBRX-shaped layer (h = 6144, E = 16, K = 4); splits 1 = co-located loopback,
 micro-batch size b_a the round trip dispatch -> identity expert -> combine
 (msi_dispatch, msi_expert_echo, msi_combine) is timed per iteration with CUDA
 events on every attention GPU (max over them), after a host barrier, for
---iters iterations; NCCL all_to_all_single moves the identical bytes
+--iters iterations; NCCL all_to_all_single and batch_isend_irecv move the identical bytes
 (attention -> expert rows, then the same rows back) under the same protocol.
 This is the paper's M2N comparison on one NVSwitch box.
 
@@ -205,7 +205,31 @@ def main():
                 dist.all_to_all_single(rbuf[:sum(recv_split)], sbuf[:sum(send_split)], recv_split, send_split)
                 dist.all_to_all_single(back[:sum(send_split)], rbuf[:sum(recv_split)], send_split, recv_split)
 
+            soff = [sum(send_split[:d]) for d in range(world)]
+            roff = [sum(recv_split[:d]) for d in range(world)]
+
+            def nccl_p2p():
+                """Same exchange as NCCL point-to-point (batch_isend_irecv), both legs."""
+                for fwd in (True, False):
+                    ops_ = []
+                    for peer in range(world):
+                        if peer == rank:
+                            continue
+                        ns, nr = (send_split[peer], recv_split[peer]) if fwd else (recv_split[peer], send_split[peer])
+                        src, so = (sbuf, soff[peer]) if fwd else (rbuf, roff[peer])
+                        dst, ro = (rbuf, roff[peer]) if fwd else (back, soff[peer])
+                        if ns:
+                            ops_.append(dist.P2POp(dist.isend, src[so:so + ns], peer))
+                        if nr:
+                            ops_.append(dist.P2POp(dist.irecv, dst[ro:ro + nr], peer))
+                    if ops_:
+                        for req in dist.batch_isend_irecv(ops_):
+                            req.wait()
+
             nl = bench(nccl, min(args.iters, 500), 20)
+            pl = bench(nccl_p2p, min(args.iters, 500), 20)
+            rec["nccl_p2p_p50_us"] = pct(pl, 0.5)
+            rec["nccl_p2p_p99_us"] = pct(pl, 0.99)
             rec["nccl_p50_us"] = pct(nl, 0.5)
             rec["nccl_p99_us"] = pct(nl, 0.99)
             rec["speedup_p50"] = rec["nccl_p50_us"] / rec["ours_p50_us"]
