@@ -676,6 +676,11 @@ def main():
         "gpu_launches": None,
         "clocks": clocks,
         "stage_times": eq5_report(all_stages, plan, args.layers, elapsed_ms / args.steps, colo),
+        # whole-model equivalents: the layer step repeated for
+        # MoeModelSpec.layers layers; TBT vs WorkloadSpec.slo_tbt (catalog.py:132)
+        "whole_model": {"layers": model.layers, "tokens_per_s": value / model.layers,
+                        "tbt_ms": elapsed_ms / args.steps / args.layers * model.layers,
+                        "slo_tbt_ms": WorkloadSpec().slo_tbt * 1e3},
         "load_balance": lb_report,
         "attention": attn_report,
         "m2n": m2n,
