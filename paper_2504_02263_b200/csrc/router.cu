@@ -16,6 +16,7 @@
 // HBM-bound for small E (reads x once); FMA-bound for E = 256 (logits on
 // CUDA cores because the fixed reduction order is the bit-exactness contract).
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -299,6 +300,16 @@ int gate_topk(const void* x, const void* wg, int T, int H, int E, int K, int32_t
   }
   // Tile shapes: TE experts x TT tokens per warp; BT tokens per CTA.  Small E
   // is HBM-bound (want many CTAs); large E is FMA-bound (want token reuse).
+  // MSI_ROUTER_TILE=TTxTExBT overrides the choice (tuning experiments).
+  if (const char* ov = getenv("MSI_ROUTER_TILE")) {
+    int tt = 0, te = 0, bt = 0;
+    if (sscanf(ov, "%dx%dx%d", &tt, &te, &bt) == 3 && bt >= 4 && bt >= tt && bt <= 32 && bt % tt == 0 && E % te == 0) {
+#define MSI_RT(A, B) if (tt == A && te == B) return launch<A, B>(x, wg, T, H, E, K, bt, idx, w, cnt, slot, ws, pl, st);
+      MSI_RT(1, 8) MSI_RT(2, 8) MSI_RT(4, 8) MSI_RT(8, 8) MSI_RT(1, 16) MSI_RT(2, 16) MSI_RT(4, 16) MSI_RT(8, 4)
+      MSI_RT(4, 4) MSI_RT(2, 4)
+#undef MSI_RT
+    }
+  }
   if (E % 16 == 0 && E > 16)  // fine-grained MoE: FMA-bound, BT=4 keeps >=148 CTAs busy at small T
     return launch<4, 16>(x, wg, T, H, E, K, T >= 148 * 16 ? 16 : 4, idx, w, cnt, slot, ws, pl, st);
   // E = 8 / 16: W_g staged once per CTA (TMA bulk copy) and amortised over 32
