@@ -49,7 +49,8 @@ __global__ void __launch_bounds__(kWarps * 32)
 gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
                  int T, int H, int E, int K, int BT, int32_t* __restrict__ idx_out,
                  float* __restrict__ w_out, int32_t* __restrict__ cnt_out,
-                 int32_t* __restrict__ slot_out, int32_t* __restrict__ ws, const Placement pl) {
+                 int32_t* __restrict__ slot_out, int32_t* __restrict__ ws, const Placement pl,
+                 size_t smem_cap) {
   extern __shared__ __align__(16) float s_logit[];         // [BT][E]
   __shared__ int s_last;
 
@@ -92,7 +93,7 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
     // x chunks are prefetched PF iterations ahead (HBM latency), W_g rows are
     // small and L1/L2-resident; the accumulation order per (token, expert)
     // stays j-major, c-minor as pinned.
-    constexpr int PF = (TT * TE >= 32) ? 2 : 4;
+    constexpr int PF = (TT * TE > 32) ? 2 : 4;
     uint4 xq[PF][TT];
 #pragma unroll
     for (int u = 0; u < PF; ++u)
@@ -220,45 +221,69 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  // (loads are issued in batches of 8 ahead of the dependent stores: the last
-  //  CTA runs alone, so its L2 round trips must overlap)
+  // The last CTA runs alone, so its L2 round trips must overlap: every
+  // histogram entry is loaded at once into shared memory (the logits area is
+  // free), each warp scans whole experts across CTAs there, and the slot
+  // fix-up issues all of a thread's loads before its stores.
   const int nblk = gridDim.x;
-  constexpr int U = 8;
-  for (int e = threadIdx.x; e < P; e += blockDim.x) {
-    int run = 0;
-    for (int b0 = 0; b0 < nblk; b0 += U) {
-      int c[U];
+  const size_t nh = (size_t)nblk * P;
+  int32_t* s_hist = reinterpret_cast<int32_t*>(s_logit);  // [nblk][P] -> exclusive bases in place
+  const bool in_smem = nh * sizeof(int32_t) <= smem_cap;
+  if (in_smem) {
+    for (size_t i = threadIdx.x; i < nh; i += blockDim.x) s_hist[i] = __ldcg(&hist[i]);
+    __syncthreads();
+    for (int e = warp; e < P; e += kWarps) {  // warp-wide exclusive scan over CTAs
+      int carry = 0;
+      for (int b0 = 0; b0 < nblk; b0 += 32) {
+        const int b = b0 + lane;
+        const int v = b < nblk ? s_hist[(size_t)b * P + e] : 0;
+        int incl = v;
 #pragma unroll
-      for (int u = 0; u < U; ++u) c[u] = (b0 + u < nblk) ? __ldcg(&hist[(size_t)(b0 + u) * P + e]) : 0;
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (b0 + u < nblk) {
-          base[(size_t)(b0 + u) * P + e] = run;
-          run += c[u];
+        for (int off = 1; off < 32; off <<= 1) {
+          const int o = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= off) incl += o;
         }
+        if (b < nblk) s_hist[(size_t)b * P + e] = carry + incl - v;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (lane == 0) cnt_out[e] = carry;
     }
-    cnt_out[e] = run;
-  }
-  __threadfence_block();
-  __syncthreads();
-  const int TK = T * K, stride = blockDim.x;
-  for (int i0 = threadIdx.x; i0 < TK; i0 += stride * U) {
-    int ex[U], sl[U], bs[U];
+    __syncthreads();
+  } else {  // very large grids: scan in global memory, 8 loads in flight per thread
+    constexpr int U = 8;
+    for (int e = threadIdx.x; e < P; e += blockDim.x) {
+      int run = 0;
+      for (int b0 = 0; b0 < nblk; b0 += U) {
+        int c[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+        for (int u = 0; u < U; ++u) c[u] = (b0 + u < nblk) ? __ldcg(&hist[(size_t)(b0 + u) * P + e]) : 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (b0 + u < nblk) {
+            base[(size_t)(b0 + u) * P + e] = run;
+            run += c[u];
+          }
+      }
+      cnt_out[e] = run;
+    }
+    __threadfence_block();
+    __syncthreads();
+  }
+  const int32_t* bsrc = in_smem ? s_hist : base;
+  const int TK = T * K, stride = blockDim.x;
+  constexpr int V = 16;
+  for (int i0 = threadIdx.x; i0 < TK; i0 += stride * V) {
+    int ex[V], sl[V];
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
       const int i = i0 + u * stride;
       ex[u] = i < TK ? __ldcg(&pidx[i]) : 0;
       sl[u] = i < TK ? __ldcg(&slot_out[i]) : 0;
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int u = 0; u < V; ++u) {
       const int i = i0 + u * stride;
-      bs[u] = i < TK ? base[(size_t)((i / K) / BT) * P + ex[u]] : 0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = i0 + u * stride;
-      if (i < TK) slot_out[i] = sl[u] + bs[u];
+      if (i < TK) slot_out[i] = sl[u] + bsrc[(size_t)((i / K) / BT) * P + ex[u]];
     }
   }
   if (threadIdx.x == 0) ws[0] = 0;  // ticket ready for the next launch
@@ -279,7 +304,7 @@ int launch(const void* x, const void* wg, int T, int H, int E, int K, int BT, in
   if (smem > 48 * 1024) MSI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<nblk, kWarps * 32, smem, st>>>(reinterpret_cast<const __nv_bfloat16*>(x),
                                         reinterpret_cast<const __nv_bfloat16*>(wg), T, H, E, K, BT,
-                                        idx, w, cnt, slot, reinterpret_cast<int32_t*>(ws), pl);
+                                        idx, w, cnt, slot, reinterpret_cast<int32_t*>(ws), pl, smem);
   return check_launch("gate_topk_kernel");
 }
 
@@ -314,8 +339,19 @@ int gate_topk(const void* x, const void* wg, int T, int H, int E, int K, int32_t
     return launch<4, 16>(x, wg, T, H, E, K, T >= 148 * 16 ? 16 : 4, idx, w, cnt, slot, ws, pl, st);
   // E = 8 / 16: W_g staged once per CTA (TMA bulk copy) and amortised over 32
   // tokens (4 per warp); x is the only HBM stream
-  if (E % 16 == 0) return launch<4, 16>(x, wg, T, H, E, K, 32, idx, w, cnt, slot, ws, pl, st);
-  if (E % 8 == 0) return launch<4, 8>(x, wg, T, H, E, K, 32, idx, w, cnt, slot, ws, pl, st);
+  // (BT shrinks for small T so that ~100+ CTAs stream x: measured with
+  //  scripts/sweep_router_tiles.py -- DBRX T=1024: 50 -> 32 us at BT = 8)
+  const int bt = T >= 96 * 32 ? 32 : (T >= 96 * 16 ? 16 : 8);
+  if (E % 16 == 0) {
+    if (bt == 32) return launch<4, 16>(x, wg, T, H, E, K, 32, idx, w, cnt, slot, ws, pl, st);
+    if (bt == 16) return launch<2, 16>(x, wg, T, H, E, K, 16, idx, w, cnt, slot, ws, pl, st);
+    return launch<1, 16>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, pl, st);
+  }
+  if (E % 8 == 0) {
+    if (bt == 32) return launch<4, 8>(x, wg, T, H, E, K, 32, idx, w, cnt, slot, ws, pl, st);
+    if (bt == 16) return launch<2, 8>(x, wg, T, H, E, K, 16, idx, w, cnt, slot, ws, pl, st);
+    return launch<1, 8>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, pl, st);
+  }
   if (E % 4 == 0) return launch<1, 4>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, pl, st);
   if (E % 2 == 0) return launch<1, 2>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, pl, st);
   return launch<1, 1>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, pl, st);
