@@ -458,6 +458,10 @@ def main():
     if args.graph:
         runner.capture(xs)
         barrier()
+        for _ in range(args.warmup):  # warm-up replays of the captured step
+            runner.replay()
+        torch.cuda.synchronize()
+        barrier()
     if g.is_expert:
         rows0, calls0 = g.stats()
     clk = ClockSampler(local)
