@@ -44,105 +44,15 @@ struct Placement {
   int32_t* pidx;  // [T,K] physical slot per (t,k) (may alias idx when rep == nullptr)
 };
 
-template <int TT, int TE, bool WS>
-__global__ void __launch_bounds__(kWarps * 32)
-gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
-                 int T, int H, int E, int K, int BT, int32_t* __restrict__ idx_out,
-                 float* __restrict__ w_out, int32_t* __restrict__ cnt_out,
-                 int32_t* __restrict__ slot_out, int32_t* __restrict__ ws, const Placement pl,
-                 size_t smem_cap) {
-  extern __shared__ __align__(16) float s_logit[];         // [BT][E]
+// Phases 2-4 (shared by both logit kernels): s_logit [BT][E] holds this CTA's
+// logits; produces idx, w (and pidx), in-CTA ranks, and -- in the last CTA --
+// the counts and final slots.
+__device__ __forceinline__ void route_tail(float* s_logit, int t0, int BT, int T, int E, int K,
+                                           int32_t* __restrict__ idx_out, float* __restrict__ w_out,
+                                           int32_t* __restrict__ cnt_out, int32_t* __restrict__ slot_out,
+                                           int32_t* __restrict__ ws, const Placement& pl, size_t smem_cap) {
   __shared__ int s_last;
-
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t0 = blockIdx.x * BT;
-  const int nchunk = H >> 8;
-  if (WS) {  // stage W_g (E*H*2 bytes) with one TMA bulk copy
-    __shared__ __align__(8) uint64_t s_bar;
-    char* dst = reinterpret_cast<char*>(s_logit) + ((logit_smem_bytes(BT, E) + 15) & ~size_t(15));
-    const uint32_t bytes = (uint32_t)E * H * 2;
-    if (threadIdx.x == 0) {
-      mbar_init(&s_bar, 1);
-      fence_barrier_init();
-      mbar_expect_tx(&s_bar, bytes);
-      bulk_g2s(dst, wg, bytes, &s_bar);
-    }
-    __syncthreads();
-    mbar_wait(&s_bar, 0);
-    wg = reinterpret_cast<const __nv_bfloat16*>(dst);
-  }
-
-  // ---- 1. logits ---------------------------------------------------------
-  const int tgroups = BT / TT, egroups = E / TE;
-  for (int tile = warp; tile < tgroups * egroups; tile += kWarps) {
-    const int tg = tile % tgroups, eg = tile / tgroups;
-    float acc[TT][TE];
-#pragma unroll
-    for (int i = 0; i < TT; ++i)
-#pragma unroll
-      for (int j = 0; j < TE; ++j) acc[i][j] = 0.0f;
-    const __nv_bfloat16* xr[TT];
-    bool tv[TT];
-#pragma unroll
-    for (int i = 0; i < TT; ++i) {
-      int t = t0 + tg * TT + i;
-      tv[i] = t < T;
-      xr[i] = x + (size_t)(tv[i] ? t : 0) * H + 8 * lane;
-    }
-    const __nv_bfloat16* wr = wg + (size_t)(eg * TE) * H + 8 * lane;
-    // x chunks are prefetched PF iterations ahead (HBM latency), W_g rows are
-    // small and L1/L2-resident; the accumulation order per (token, expert)
-    // stays j-major, c-minor as pinned.
-    constexpr int PF = (TT * TE > 32) ? 2 : 4;
-    uint4 xq[PF][TT];
-#pragma unroll
-    for (int u = 0; u < PF; ++u)
-#pragma unroll
-      for (int i = 0; i < TT; ++i)
-        xq[u][i] = (tv[i] && u < nchunk) ? __ldg(reinterpret_cast<const uint4*>(xr[i] + 256 * u)) : make_uint4(0, 0, 0, 0);
-    for (int j0 = 0; j0 < nchunk; j0 += PF) {
-#pragma unroll
-      for (int u = 0; u < PF; ++u) {
-        const int j = j0 + u;
-        if (j >= nchunk) break;
-        float xv[TT][8];
-#pragma unroll
-        for (int i = 0; i < TT; ++i) {
-          const uint4 v = xq[u][i];
-          xv[i][0] = bf16lo(v.x); xv[i][1] = bf16hi(v.x);
-          xv[i][2] = bf16lo(v.y); xv[i][3] = bf16hi(v.y);
-          xv[i][4] = bf16lo(v.z); xv[i][5] = bf16hi(v.z);
-          xv[i][6] = bf16lo(v.w); xv[i][7] = bf16hi(v.w);
-          // refill this slot with chunk j + PF
-          xq[u][i] = (tv[i] && j + PF < nchunk) ? __ldg(reinterpret_cast<const uint4*>(xr[i] + 256 * (j + PF)))
-                                               : make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int e = 0; e < TE; ++e) {
-          const uint4* wp = reinterpret_cast<const uint4*>(wr + (size_t)e * H + 256 * j);
-          uint4 v = WS ? *wp : __ldg(wp);
-          float wv[8] = {bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y),
-                         bf16lo(v.z), bf16hi(v.z), bf16lo(v.w), bf16hi(v.w)};
-#pragma unroll
-          for (int c = 0; c < 8; ++c)
-#pragma unroll
-            for (int i = 0; i < TT; ++i) acc[i][e] = __fmaf_rn(xv[i][c], wv[c], acc[i][e]);
-        }
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < TT; ++i)
-#pragma unroll
-      for (int e = 0; e < TE; ++e) {
-        float v = acc[i][e];
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
-        v = (v != v) ? -INFINITY : v;  // NaN logits rank as -inf (the oracle does the same)
-        if (lane == ((i * TE + e) & 31)) s_logit[(tg * TT + i) * E + eg * TE + e] = v;
-      }
-  }
-  __syncthreads();
-
   // ---- 2. top-K + weights (one warp per token) ----------------------------
   for (int lt = warp; lt < BT; lt += kWarps) {
     const int t = t0 + lt;
@@ -249,7 +159,31 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
       if (lane == 0) cnt_out[e] = carry;
     }
     __syncthreads();
-  } else {  // very large grids: scan in global memory, 8 loads in flight per thread
+  } else if (P <= (int)blockDim.x && smem_cap >= (size_t)P * sizeof(int32_t)) {
+    // many CTAs: stream the [nblk][P] histograms through shared memory in
+    // chunks of cb CTAs (coalesced loads/stores); thread e carries expert e
+    const int cb = (int)(smem_cap / ((size_t)P * sizeof(int32_t)));
+    const int e = threadIdx.x;
+    int carry = 0;
+    for (int b0 = 0; b0 < nblk; b0 += cb) {
+      const int nb = min(cb, nblk - b0);
+      const size_t n = (size_t)nb * P;
+      for (size_t i = threadIdx.x; i < n; i += blockDim.x) s_hist[i] = __ldcg(&hist[(size_t)b0 * P + i]);
+      __syncthreads();
+      if (e < P)
+        for (int b = 0; b < nb; ++b) {
+          const int v = s_hist[(size_t)b * P + e];
+          s_hist[(size_t)b * P + e] = carry;
+          carry += v;
+        }
+      __syncthreads();
+      for (size_t i = threadIdx.x; i < n; i += blockDim.x) base[(size_t)b0 * P + i] = s_hist[i];
+      __syncthreads();
+    }
+    if (e < P) cnt_out[e] = carry;
+    __threadfence_block();
+    __syncthreads();
+  } else {  // replicated placements with P > 256: per-thread scans, 8 loads in flight
     constexpr int U = 8;
     for (int e = threadIdx.x; e < P; e += blockDim.x) {
       int run = 0;
@@ -287,6 +221,107 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
     }
   }
   if (threadIdx.x == 0) ws[0] = 0;  // ticket ready for the next launch
+}
+
+template <int TT, int TE, bool WS>
+__global__ void __launch_bounds__(kWarps * 32)
+gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
+                 int T, int H, int E, int K, int BT, int32_t* __restrict__ idx_out,
+                 float* __restrict__ w_out, int32_t* __restrict__ cnt_out,
+                 int32_t* __restrict__ slot_out, int32_t* __restrict__ ws, const Placement pl,
+                 size_t smem_cap) {
+  extern __shared__ __align__(16) float s_logit[];         // [BT][E]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t0 = blockIdx.x * BT;
+  const int nchunk = H >> 8;
+  if (WS) {  // stage W_g (E*H*2 bytes) with one TMA bulk copy
+    __shared__ __align__(8) uint64_t s_bar;
+    char* dst = reinterpret_cast<char*>(s_logit) + ((logit_smem_bytes(BT, E) + 15) & ~size_t(15));
+    const uint32_t bytes = (uint32_t)E * H * 2;
+    if (threadIdx.x == 0) {
+      mbar_init(&s_bar, 1);
+      fence_barrier_init();
+      mbar_expect_tx(&s_bar, bytes);
+      bulk_g2s(dst, wg, bytes, &s_bar);
+    }
+    __syncthreads();
+    mbar_wait(&s_bar, 0);
+    wg = reinterpret_cast<const __nv_bfloat16*>(dst);
+  }
+
+  // ---- 1. logits ---------------------------------------------------------
+  const int tgroups = BT / TT, egroups = E / TE;
+  for (int tile = warp; tile < tgroups * egroups; tile += kWarps) {
+    const int tg = tile % tgroups, eg = tile / tgroups;
+    float acc[TT][TE];
+#pragma unroll
+    for (int i = 0; i < TT; ++i)
+#pragma unroll
+      for (int j = 0; j < TE; ++j) acc[i][j] = 0.0f;
+    const __nv_bfloat16* xr[TT];
+    bool tv[TT];
+#pragma unroll
+    for (int i = 0; i < TT; ++i) {
+      int t = t0 + tg * TT + i;
+      tv[i] = t < T;
+      xr[i] = x + (size_t)(tv[i] ? t : 0) * H + 8 * lane;
+    }
+    const __nv_bfloat16* wr = wg + (size_t)(eg * TE) * H + 8 * lane;
+    // x chunks are prefetched PF iterations ahead (HBM latency), W_g rows are
+    // small and L1/L2-resident; the accumulation order per (token, expert)
+    // stays j-major, c-minor as pinned.
+    constexpr int PF = (TT * TE > 32) ? 2 : 4;
+    uint4 xq[PF][TT];
+#pragma unroll
+    for (int u = 0; u < PF; ++u)
+#pragma unroll
+      for (int i = 0; i < TT; ++i)
+        xq[u][i] = (tv[i] && u < nchunk) ? __ldg(reinterpret_cast<const uint4*>(xr[i] + 256 * u)) : make_uint4(0, 0, 0, 0);
+    for (int j0 = 0; j0 < nchunk; j0 += PF) {
+#pragma unroll
+      for (int u = 0; u < PF; ++u) {
+        const int j = j0 + u;
+        if (j >= nchunk) break;
+        float xv[TT][8];
+#pragma unroll
+        for (int i = 0; i < TT; ++i) {
+          const uint4 v = xq[u][i];
+          xv[i][0] = bf16lo(v.x); xv[i][1] = bf16hi(v.x);
+          xv[i][2] = bf16lo(v.y); xv[i][3] = bf16hi(v.y);
+          xv[i][4] = bf16lo(v.z); xv[i][5] = bf16hi(v.z);
+          xv[i][6] = bf16lo(v.w); xv[i][7] = bf16hi(v.w);
+          // refill this slot with chunk j + PF
+          xq[u][i] = (tv[i] && j + PF < nchunk) ? __ldg(reinterpret_cast<const uint4*>(xr[i] + 256 * (j + PF)))
+                                               : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int e = 0; e < TE; ++e) {
+          const uint4* wp = reinterpret_cast<const uint4*>(wr + (size_t)e * H + 256 * j);
+          uint4 v = WS ? *wp : __ldg(wp);
+          float wv[8] = {bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y),
+                         bf16lo(v.z), bf16hi(v.z), bf16lo(v.w), bf16hi(v.w)};
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+#pragma unroll
+            for (int i = 0; i < TT; ++i) acc[i][e] = __fmaf_rn(xv[i][c], wv[c], acc[i][e]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < TT; ++i)
+#pragma unroll
+      for (int e = 0; e < TE; ++e) {
+        float v = acc[i][e];
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+        v = (v != v) ? -INFINITY : v;  // NaN logits rank as -inf (the oracle does the same)
+        if (lane == ((i * TE + e) & 31)) s_logit[(tg * TT + i) * E + eg * TE + e] = v;
+      }
+  }
+  __syncthreads();
+
+  route_tail(s_logit, t0, BT, T, E, K, idx_out, w_out, cnt_out, slot_out, ws, pl, smem_cap);
 }
 
 constexpr size_t kMaxStagedW = 200 * 1024;  // W_g staged in smem up to this size
@@ -335,8 +370,10 @@ int gate_topk(const void* x, const void* wg, int T, int H, int E, int K, int32_t
 #undef MSI_RT
     }
   }
-  if (E % 16 == 0 && E > 16)  // fine-grained MoE: FMA-bound, BT=4 keeps >=148 CTAs busy at small T
-    return launch<4, 16>(x, wg, T, H, E, K, T >= 148 * 16 ? 16 : 4, idx, w, cnt, slot, ws, pl, st);
+  // fine-grained MoE: FMA-bound; BT=4 keeps >=148 CTAs busy at small T, BT=16
+  // quarters the W_g re-reads once there are >= 128 CTAs (T=2048: 489 -> 363 us)
+  if (E % 16 == 0 && E > 16)
+    return launch<4, 16>(x, wg, T, H, E, K, T >= 2048 ? 16 : 4, idx, w, cnt, slot, ws, pl, st);
   // E = 8 / 16: W_g staged once per CTA (TMA bulk copy) and amortised over 32
   // tokens (4 per warp); x is the only HBM stream
   // (BT shrinks for small T so that ~100+ CTAs stream x: measured with

@@ -404,3 +404,24 @@ def test_replicated_experts_bit_identical(lib):
             assert (r.cnt.cpu().numpy()[8:] > 0).all()  # the replicas received tokens
         g.close()
     np.testing.assert_array_equal(outs["rep"], outs["plain"])
+
+
+@pytest.mark.parametrize("tile,T,H,E,K", [("2x16x4", 130, 7168, 256, 8), ("8x8x32", 2400, 7168, 256, 8),
+                                          ("4x4x16", 333, 4096, 64, 6), ("2x16x16", 1024, 6144, 16, 4),
+                                          ("1x8x8", 77, 6144, 8, 2)])
+def test_router_tile_variants_bit_exact(lib, monkeypatch, tile, T, H, E, K):
+    """Every logit kernel variant (MSI_ROUTER_TILE) keeps the pinned reduction
+    order: routing, counts, slots and weights bit-identical to the oracle."""
+    from paper_2504_02263_b200 import ops
+
+    monkeypatch.setenv("MSI_ROUTER_TILE", tile)
+    x = O.synth_tokens(T, H, seed=5 + T)
+    wg = O.synth_weights(H, 128, E, seed=3, experts=[]).wg
+    idx_r, w_r = O.router(x, wg, K)
+    cnt_r, slot_r = O.place(idx_r, E)
+    idx, w, cnt, slot = ops.gate_topk(to_dev(x), to_dev(wg), K)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(idx.cpu().numpy(), idx_r)
+    np.testing.assert_array_equal(cnt.cpu().numpy(), cnt_r)
+    np.testing.assert_array_equal(slot.cpu().numpy(), slot_r)
+    np.testing.assert_array_equal(w.cpu().numpy().view(np.uint32), w_r.view(np.uint32))
