@@ -80,6 +80,7 @@ struct AttnArgs {
 
 __global__ void __launch_bounds__(kThreads, 2)
     decode_attn_kernel(const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tv,
+                       const __grid_constant__ CUtensorMap tk16, const __grid_constant__ CUtensorMap tv16,
                        const AttnArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -109,14 +110,27 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (lane == 0) {
       tma_prefetch(&tk);
       tma_prefetch(&tv);
+      tma_prefetch(&tk16);
+      tma_prefetch(&tv16);
       const int* btr = a.bt + (size_t)seq * a.max_pages + p0;
       for (int i = 0; i < np; ++i) {
         const int s = i % kStages;
         if (i >= kStages) mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
         const int row = (btr[i] * a.n_kv + kvh) * kPage;
-        mbar_expect_tx(&full[s], 2 * kTileBytes);
-        tma_load_3d(smem + s * 2 * kTileBytes, &tk, 0, 0, row, &full[s]);
-        tma_load_3d(smem + s * 2 * kTileBytes + kTileBytes, &tv, 0, 0, row, &full[s]);
+        const int valid = len - (p0 + i) * kPage;  // rows of this page in use (>= 1)
+        if (valid >= kPage) {
+          mbar_expect_tx(&full[s], 2 * kTileBytes);
+          tma_load_3d(smem + s * 2 * kTileBytes, &tk, 0, 0, row, &full[s]);
+          tma_load_3d(smem + s * 2 * kTileBytes + kTileBytes, &tv, 0, 0, row, &full[s]);
+        } else {  // a sequence's last, partial page: only the 16-row groups in use
+          const int nq = (valid + 15) / 16;
+          mbar_expect_tx(&full[s], 2 * nq * (kTileBytes / 4));
+          for (int q = 0; q < nq; ++q) {
+            tma_load_3d(smem + s * 2 * kTileBytes + q * (kTileBytes / 4), &tk16, 0, 0, row + 16 * q, &full[s]);
+            tma_load_3d(smem + s * 2 * kTileBytes + kTileBytes + q * (kTileBytes / 4), &tv16, 0, 0, row + 16 * q,
+                        &full[s]);
+          }
+        }
       }
     }
     return;
@@ -350,7 +364,7 @@ typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint3
 
 // Cache tile map: the cache viewed as [rows][2 halves][64 dims] (rows =
 // num_pages * n_kv * 64), box = one (page, KV head) tile, SWIZZLE_128B.
-int kv_tmap(CUtensorMap* m, const void* base, uint64_t rows) {
+int kv_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint32_t box_rows) {
   static PFN_encodeTiled_t enc = nullptr;
   if (!enc) {
     void* p = nullptr;
@@ -364,7 +378,7 @@ int kv_tmap(CUtensorMap* m, const void* base, uint64_t rows) {
   }
   cuuint64_t dims[3] = {64, 2, rows};
   cuuint64_t strides[2] = {128, 256};
-  cuuint32_t box[3] = {64, 2, (cuuint32_t)kPage};
+  cuuint32_t box[3] = {64, 2, box_rows};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -435,24 +449,25 @@ extern "C" int msi_decode_attention(const void* q, const void* k_cache, const vo
               ws_bytes, need);
   const uint64_t rows = (uint64_t)num_pages * n_kv * MSI_KV_PAGE;
   // tiny cache of encoded maps (eager calls re-use the same cache tensors)
-  static thread_local struct { const void* p; uint64_t rows; CUtensorMap m; } cache[4];
+  static thread_local struct { const void* p; uint64_t rows; uint32_t box; CUtensorMap m; } cache[8];
   static thread_local int next = 0;
-  auto lookup = [&](const void* p, CUtensorMap* m) -> int {
+  auto lookup = [&](const void* p, uint32_t box, CUtensorMap* m) -> int {
     for (auto& c : cache)
-      if (c.p == p && c.rows == rows) {
+      if (c.p == p && c.rows == rows && c.box == box) {
         *m = c.m;
         return 0;
       }
-    int rc = kv_tmap(m, p, rows);
+    int rc = kv_tmap(m, p, rows, box);
     if (rc) return rc;
-    cache[next] = {p, rows, *m};
-    next = (next + 1) % 4;
+    cache[next] = {p, rows, box, *m};
+    next = (next + 1) % 8;
     return 0;
   };
-  CUtensorMap tk, tv;
-  int rc = lookup(k_cache, &tk);
-  if (rc) return rc;
-  rc = lookup(v_cache, &tv);
+  CUtensorMap tk, tv, tk16, tv16;  // full-page boxes and 16-row boxes (partial last pages)
+  int rc = lookup(k_cache, MSI_KV_PAGE, &tk);
+  if (!rc) rc = lookup(v_cache, MSI_KV_PAGE, &tv);
+  if (!rc) rc = lookup(k_cache, 16, &tk16);
+  if (!rc) rc = lookup(v_cache, 16, &tv16);
   if (rc) return rc;
   static bool attr = false;
   if (!attr) {
@@ -477,7 +492,7 @@ extern "C" int msi_decode_attention(const void* q, const void* k_cache, const vo
   const long grid = (long)T * n_kv * splits;
   MSI_REQUIRE(grid < (1L << 31), "decode_attention: grid too large");
   cudaStream_t st = (cudaStream_t)stream;
-  decode_attn_kernel<<<(unsigned)grid, kThreads, kSmem, st>>>(tk, tv, a);
+  decode_attn_kernel<<<(unsigned)grid, kThreads, kSmem, st>>>(tk, tv, tk16, tv16, a);
   rc = check_launch("decode_attn_kernel");
   if (rc || splits == 1) return rc;
   attn_split_combine_kernel<<<(unsigned)((size_t)T * n_heads), MSI_HEAD_DIM, 0, st>>>(a.part_o, a.part_ml, splits,
