@@ -13,10 +13,7 @@ from paper_2504_02263_b200 import ops  # noqa: E402
 CASES = {(3072, 6144, 8, 2): ["4x8x32", "2x8x16", "1x8x8", "4x8x16", "2x8x8", "8x4x32", "4x4x16"],
          (1024, 6144, 16, 4): ["4x16x32", "2x16x16", "1x16x8", "4x8x16", "2x8x8", "1x8x8"],
          (4096, 7168, 256, 8): ["4x16x16", "4x16x4", "8x8x32"],
-         (2048, 7168, 256, 8): ["4x16x16", "4x16x4"],
-         (1024, 7168, 256, 8): ["4x16x4", "4x16x16"],
-         (512, 7168, 256, 8): ["4x16x4", "2x16x4"],
-         (128, 7168, 256, 8): ["4x16x4", "2x16x4"]}
+         (512, 7168, 256, 8): ["4x16x4", "2x16x4"]}
 for (T, H, E, K), tiles in CASES.items():
     x = torch.randn(T, H, device="cuda").to(torch.bfloat16)
     wg = (torch.randn(E, H, device="cuda") / H ** 0.5).to(torch.bfloat16)
@@ -29,6 +26,7 @@ for (T, H, E, K), tiles in CASES.items():
         else:
             os.environ["MSI_ROUTER_TILE"] = tile
         out = ops.gate_topk(x, wg, K, ws=ws)
+        torch.cuda.synchronize()
         same = all(torch.equal(a, b) for a, b in zip(out, ref))
         for _ in range(3):
             ops.gate_topk(x, wg, K, ws=ws)
