@@ -119,3 +119,24 @@ def test_profile_csv_roundtrip(tmp_path):
     assert cm.k3 == pytest.approx(8e-5 / 256) and cm.util_curve(1 << 20) == 0.7
     assert math.isclose(PM.attention_time(64, cm), 2e-5, rel_tol=1e-12)
 
+
+
+def test_calibrate_tool_helpers(tmp_path):
+    """calibrate.py's CPU-side pieces: the M2N JSONL -> UtilCurve rows and the
+    held-out check (the GPU timing parts run on a B200 only)."""
+    import json
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import calibrate as C
+
+    p = tmp_path / "m2n.jsonl"
+    recs = [{"T": t, "pair_bytes_avg": t * 49152.0, "ingress_bytes_busiest": t * 49152,
+             "dispatch_only_p50_us": 20.0 + t * 0.1} for t in (1, 4, 64, 1024)]
+    p.write_text("noise line\n" + "\n".join(json.dumps(r) for r in recs) + "\n")
+    rows = C.util_from_m2n(str(p))
+    assert [r[1] for r in rows] == [49152, 196608, 3145728, 50331648]
+    assert all(0 < r[2] <= 1 for r in rows) and rows[-1][2] > rows[0][2]
+    pts = [("expert", b, 1e-4 + 3e-7 * b) for b in (256, 512, 768, 1024, 1536, 2048)]
+    h = C.held_out(pts, "expert")
+    assert h["max_rel_err"] < 1e-9 and h["fit_on"] == [256, 768, 1536]
