@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--exact", action="store_true", help="every expert gets exactly t_e rows (no raggedness)")
     ap.add_argument("--ab", type=int, default=0,
                     help="interleaved A/B of the 1-CTA and CTA-pair kernels: N alternating rounds, medians")
+    ap.add_argument("--ab-env", default="",
+                    help="A/B an env setting instead, e.g. MSI_GEMM_PREFETCH=0:8 (variant 1 : variant 2)")
     args = ap.parse_args()
 
     import torch
@@ -56,9 +58,13 @@ def main():
             from paper_2504_02263_b200 import _lib
             lib = _lib.load()
             per = {1: [], 2: []}
+            env_key, env_vals = (args.ab_env.split("=")[0], args.ab_env.split("=")[1].split(":")) if args.ab_env else (None, None)
             for rnd in range(args.ab):
                 for cg in ((1, 2) if rnd % 2 == 0 else (2, 1)):
-                    lib.msi_set_gemm_cta_group(cg)
+                    if env_key:
+                        os.environ[env_key] = env_vals[cg - 1]
+                    else:
+                        lib.msi_set_gemm_cta_group(cg)
                     for _ in range(2):
                         ops.grouped_ffn(x, tot, w13, w2, hbuf, y)
                     torch.cuda.synchronize()
@@ -71,7 +77,7 @@ def main():
                     per[cg].append(s0.elapsed_time(e0) / args.iters)
             lib.msi_set_gemm_cta_group(0)
             flops = 6.0 * sum(totals) * H * Hp
-            rec = {"ab": args.ab, "te": te, "exact": args.exact, "rows": sum(totals),
+            rec = {"ab": args.ab, "ab_env": args.ab_env or "cta_group 1:2", "te": te, "exact": args.exact, "rows": sum(totals),
                    "odd_tiles": sum(((t + 127) // 128) % 2 for t in totals)}
             for cg in (1, 2):
                 ms = sorted(per[cg])[len(per[cg]) // 2]
