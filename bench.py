@@ -434,12 +434,14 @@ def main():
 
     # expert-FFN timing inside the timed region (events on the launching stream)
     ffn_events = []
-    orig_step = layer.expert_step
+    orig_ffn = layer.expert_ffn
 
-    def timed_expert_step(mb=0, stream=None):
+    def timed_expert_ffn(mb=0, stream=None):
+        # the runner calls expert_wait first, so these events time the FFN
+        # kernels (GEMM1 + GEMM2) only, not the wait for the senders' rows
         s, e = torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True)
         s.record()
-        r = orig_step(mb, stream)
+        r = orig_ffn(mb, stream)
         e.record()
         ffn_events.append((s, e))
         return r
@@ -451,7 +453,7 @@ def main():
     # The step is captured once into a CUDA graph (device-tracked epochs) and
     # replayed; the FFN timing events are captured with it, so the values read
     # after the loop are those of the last timed replay.
-    layer.expert_step = timed_expert_step
+    layer.expert_ffn = timed_expert_ffn
     attn_events = []
     for stg in att_stages or []:
         stg.timing = attn_events
@@ -477,7 +479,7 @@ def main():
     torch.cuda.synchronize()
     barrier()
     clocks = clk.stop()
-    layer.expert_step = orig_step
+    layer.expert_ffn = orig_ffn
     elapsed_ms = t_start.elapsed_time(t_end)
     st = g.status()
     if st != 0:
@@ -645,11 +647,11 @@ def main():
     peak = peaks.get("bf16_tflops_sustained") or 1404.8
     # our kernels per (micro-batch, layer): attention (stand-in 1; real: rope_append +
     # decode_attn [+ split combine]; its two projections are cuBLAS), router,
-    # dispatch, 2 GEMMs, combine
+    # dispatch, expert wait + 2 GEMMs, combine
     attn_launches = (1 if kv_bytes else 0)
     if att_stages:
         attn_launches = 2 + (1 if att_stages[0].ws is not None else 0)
-    launches_per_mbl = attn_launches + 1 + 1 + 2 + 1
+    launches_per_mbl = attn_launches + 1 + 1 + 3 + 1  # expert: wait + 2 GEMMs
     line = {
         "metric": "decode tokens/s/GPU (MoE layer, ping-pong); M2N dispatch+combine p50 µs",
         "value": value, "unit": "layer-tokens/s", "value_per_gpu": value / world,
@@ -692,7 +694,7 @@ def main():
     # our kernels inside the timed region (per rank, summed over roles)
     per_step = plan.m * args.layers * (launches_per_mbl if colo else 0)
     if not colo:
-        per_step = plan.m * args.layers * (n_a * (attn_launches + 3) + n_e * 2)
+        per_step = plan.m * args.layers * (n_a * (attn_launches + 3) + n_e * 3)
     line["gpu_launches"] = per_step * args.steps
     if not args.no_cpu:
         threads = len(os.sched_getaffinity(0))

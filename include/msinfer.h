@@ -147,6 +147,12 @@ int msi_dispatch(msi_ctx* ctx, const void* x, const int32_t* cnt,
                  const int32_t* idx, const int32_t* slot, int T, int mb_slot,
                  uint32_t epoch, void* stream);
 
+/* Block `stream` (one spinning thread, no other SM use) until every sender
+ * released `mb_slot`'s epoch -- the wait msi_expert_ffn performs itself --
+ * so that the FFN launched after it starts on resident rows and can be timed
+ * without the pipeline wait (PAPER.md:408-411 receiver side).  Epoch rules as
+ * msi_expert_ffn (pass the same value; 0 = device-tracked). */
+int msi_expert_wait(msi_ctx* ctx, int mb_slot, uint32_t epoch, void* stream);
 /* ---- (2) expert FFN (SwiGLU): waits for all senders'
  * rows, then two tcgen05/TMEM/TMA grouped GEMMs over the local experts:
  *   H = bf16(silu(X W_gate^T) * (X W_up^T)),  Y = bf16(H W_down^T)

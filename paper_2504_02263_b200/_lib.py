@@ -66,6 +66,7 @@ SIGNATURES = {
     "msi_dispatch": (_I, [_P, _P, _P, _P, _P, _I, _I, _U32, _P]),
     "msi_expert_ffn": (_I, [_P, _P, _P, _I, _U32, _P]),
     "msi_expert_echo": (_I, [_P, _I, _U32, _P]),
+    "msi_expert_wait": (_I, [_P, _I, _U32, _P]),
     "msi_combine": (_I, [_P, _P, _P, _P, _I, _I, _U32, _P]),
     "msi_pack_w13": (_I, [_P, _P, _P, _I, _I, _I, _P]),
     "msi_set_gemm_cta_group": (_I, [_I]),

@@ -358,6 +358,17 @@ dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32
 // real expert step.
 constexpr int kEchoThreads = 512;
 
+// Expert-side wait for a slot's rows (one thread): spins until every sender
+// released the slot's epoch (device-resolved like msi_expert_ffn's), so the
+// FFN kernels that follow start on data already in place and their timing is
+// compute only.  On timeout it sets the abort flag the FFN kernels honour.
+__global__ void expert_wait_kernel(const DevCtx c, int mb, uint32_t epoch) {
+  epoch = resolve_epoch(epoch, c.my_euse + mb * CTR_STRIDE, 1u, c.my_status);
+  if (epoch == 0) return;  // the FFN kernels see the same mismatch and abort
+  if (!wait_geq(c.my_arrive + mb * CTR_STRIDE, epoch * (uint32_t)c.n_a, c.timeout_ns, c.my_status))
+    c.my_status[1] = 1;
+}
+
 __global__ void __launch_bounds__(kEchoThreads)
 echo_kernel(const DevCtx c, int mb, uint32_t epoch) {
   __shared__ int s_ok, s_last;
@@ -801,6 +812,14 @@ extern "C" int msi_expert_ffn(msi_ctx* c, const void* w13, const void* w2, int m
   g2.p.trace = d.trace;  // stamps 13 (GEMM2 start), 14 (release to combine)
   g2.p.trace_slot = 12;
   return grouped_gemm_launch(g2, st);
+}
+
+extern "C" int msi_expert_wait(msi_ctx* c, int mb_slot, uint32_t epoch, void* stream) {
+  if (!c || !c->finalized) { set_error("msi_expert_wait: context not finalized"); return MSI_ESTATE; }
+  if (!c->expert) { set_error("msi_expert_wait: rank %d has no expert role", c->rank); return MSI_EINVAL; }
+  MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots, "msi_expert_wait: bad slot");
+  expert_wait_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(c->dev, mb_slot, epoch);
+  return check_launch("expert_wait_kernel");
 }
 
 extern "C" int msi_expert_echo(msi_ctx* c, int mb_slot, uint32_t epoch, void* stream) {

@@ -278,6 +278,18 @@ class MoEDecodeLayer:
 
     # -- (2) expert FFN -------------------------------------------------------
     def expert_step(self, mb: int = 0, stream=None) -> int:
+        """Wait for the slot's rows (msi_expert_wait), then the SwiGLU FFN
+        (msi_expert_ffn: GEMM1 + GEMM2 whose epilogue is the N2M send)."""
+        self.expert_wait(mb, stream)
+        return self.expert_ffn(mb, stream)
+
+    def expert_wait(self, mb: int = 0, stream=None):
+        if os.environ.get("MSI_EXPERT_WAIT", "1") == "0":  # A/B switch: rely on GEMM1's own wait
+            return
+        epoch = 0 if self.device_epochs else self.epoch_e[mb] + 1
+        _lib.call("msi_expert_wait", self.g.ctx, mb, epoch, ops._stream(stream))
+
+    def expert_ffn(self, mb: int = 0, stream=None) -> int:
         if self.w13 is None or self.w2 is None:
             raise ValueError("expert_step needs w13/w2 on this expert rank")
         self.epoch_e[mb] += 1
@@ -381,7 +393,7 @@ class PingPongRunner:
                     r = lay.router(h, j)
                     lay.dispatch(h, r, j)
                     self._ev(("disp", j, l, 1))
-                    self._ev(("ffn", j, l, 0)); lay.expert_step(j); self._ev(("ffn", j, l, 1))
+                    lay.expert_wait(j); self._ev(("ffn", j, l, 0)); lay.expert_ffn(j); self._ev(("ffn", j, l, 1))
                     self._ev(("comb", j, l, 0)); lay.combine(r, resid=h, out=self._out(xs, j)); self._ev(("comb", j, l, 1))
         elif g.role == "attention":
             routes, hs = [None] * m, [None] * m
@@ -403,7 +415,7 @@ class PingPongRunner:
         else:
             for l in range(L):
                 for j in range(m):
-                    self._ev(("ffn", j, l, 0)); lay.expert_step(j); self._ev(("ffn", j, l, 1))
+                    lay.expert_wait(j); self._ev(("ffn", j, l, 0)); lay.expert_ffn(j); self._ev(("ffn", j, l, 1))
         return xs
 
     # -- CUDA graph: one whole step (m x L) captured per rank -----------------
