@@ -35,6 +35,47 @@ SPLITS = {1: (1, 1, True), 2: (1, 1, False), 4: (3, 1, False), 8: (6, 2, False),
           3: (2, 1, False), 5: (4, 1, False), 6: (4, 2, False), 7: (5, 2, False)}
 
 
+def choose_split(world: int, shape: str, plan_arg: str, split: str = "", colocated: bool = False):
+    """(n_a, n_e, colocated, source) for this run.
+
+    --split a+e / --colocated force a layout.  --plan config uses the
+    BASELINE.json configuration splits (SPLITS: 1+1, 3+1, 6+2 ...).  The
+    default, --plan planner, asks Algorithm 1 (planner.search_box)
+    for the best layout of this box with the B200-calibrated coefficients of
+    profiles/r01_calibration_<shape>.json; shapes without a calibration fall
+    back to the config splits.  For Mixtral-8x22B the search picks co-location
+    at every N > 1 (the disaggregated splits fail its balance constraint:
+    T_a is ~half of T_e per token on identical GPUs)."""
+    if split:
+        n_a, n_e = (int(v) for v in split.split("+"))
+        if n_a + n_e != world:
+            raise SystemExit(f"--split {split} needs {n_a + n_e} GPUs")
+        return n_a, n_e, False, "--split"
+    if colocated or world == 1:
+        return world, world, True, "--colocated" if colocated else "1 GPU: co-located"
+    if plan_arg == "planner":
+        import glob
+        cal = None
+        for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_calibration_*.json"))):
+            with open(path) as fh:
+                c = json.load(fh)
+            if str(c.get("shape", "")).lower() == shape.lower():
+                cal = c
+        if cal is not None:
+            from paper_2504_02263_b200 import perf_model as PM
+            from paper_2504_02263_b200 import planner as PL
+            from paper_2504_02263_b200.config import WorkloadSpec, as_model_spec, b200_gpu
+            c = cal
+            cm = PM.CostModel(k1=c["k1_s_per_tok"], k2=c["k2_s"], k3=c["k3_s_per_tok"], k4=c["k4_s"],
+                              util_curve=PM.UtilCurve.from_points(c["util_table"]))
+            p = PL.search_box(as_model_spec(shape), b200_gpu(), PL.cm_scaled_for_experts(cm, c["experts_local"]),
+                              WorkloadSpec(), world)
+            if p:
+                return p.n_a, p.n_e, bool(p.colocated), "planner.search_box (calibrated B200 costs, profiles/r01_calibration_8x22b.json)"
+    n_a, n_e, colo = SPLITS[world]
+    return n_a, n_e, colo, "BASELINE.json config split"
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -49,7 +90,9 @@ def parse():
     ap.add_argument("--attn", default="real", choices=["real", "standin", "none"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--split", default="", help="attention+expert GPUs, e.g. 2+2 (default: config-3 ratio)")
+    ap.add_argument("--split", default="", help="attention+expert GPUs, e.g. 6+2 (disaggregated)")
+    ap.add_argument("--plan", default="planner", choices=["planner", "config"],
+                    help="N > 1 layout: Algorithm 1 on the calibrated B200 costs (default) or the BASELINE config splits")
     ap.add_argument("--skew", type=float, default=0.0,
                     help="make experts 0/1 hot (gate-logit bias); 0 = random-init routing")
     ap.add_argument("--balance", action="store_true",
@@ -281,9 +324,59 @@ def m2n_latency(layer, g, x, world: int, iters: int = 1000, warm: int = 50) -> d
     if g.status() != 0:
         raise RuntimeError("device status after the M2N round trips")
     T, H, K = (x.shape[0], x.shape[1], g.model.topk) if x is not None else (0, 0, 0)
-    return {"p50_us": v[len(v) // 2], "p99_us": v[min(len(v) - 1, int(0.99 * len(v)))], "iters": iters,
+    p50 = v[len(v) // 2]
+    return {"p50_us": p50, "p99_us": v[min(len(v) - 1, int(0.99 * len(v)))], "iters": iters,
             "tokens_per_attention_gpu": T, "dispatch_bytes_per_attention_gpu": T * K * H * 2,
-            "how": "graph replay of dispatch -> expert echo -> combine, barrier each, max over ranks"}
+            "how": "graph replay of dispatch -> expert echo -> combine, barrier each, max over ranks",
+            "roofline": m2n_roofline(g, route, world, g.model.hidden, p50)}
+
+
+def m2n_roofline(g, route, world: int, H: int, p50_us: float) -> dict:
+    """Bytes the round trip must move and the rate it reached.
+
+    N > 1: the two legs run one after the other (rows out, rows back), so the
+    link-time lower bound is, per leg, the busiest GPU's max(egress, ingress)
+    NVLink bytes (dispatch: 2H + 8 B metadata per remote (t, k) row; return:
+    2H), summed over the legs.  achieved = those bytes / p50, against the
+    measured 770 GB/s peer copy per direction (B200_PROFILING.md) and the
+    900 GB/s nominal.  N = 1: everything is local, so the bound is HBM:
+    dispatch reads x and writes T*K rows, the echo reads and writes T*K rows,
+    the combine reads T*K rows and writes T; against MEASURED_PEAKS hbm_gbs."""
+    import torch
+    import torch.distributed as dist
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    plan = g.plan
+    rows_to = torch.zeros(world, dtype=torch.int64, device=dev)
+    if g.is_attention and route is not None:
+        q = (route.dest.to(torch.int64) // g.E_l).flatten()
+        ranks = torch.tensor(plan.expert_ranks(), dtype=torch.int64, device=dev)
+        rows_to += torch.bincount(ranks[q], minlength=world)[:world]
+    if world > 1:
+        mats = [torch.zeros_like(rows_to) for _ in range(world)]
+        dist.all_gather(mats, rows_to)
+        mat = torch.stack(mats).cpu()
+    else:
+        mat = rows_to.cpu()[None, :]
+    if world == 1:
+        rows = int(mat.sum())
+        T = route.T if route is not None else 0
+        by = T * H * 2 + rows * H * 2 + 2 * rows * H * 2 + rows * H * 2 + T * H * 2
+        peak = measured_peaks().get("hbm_gbs") or 6546.6
+        gbs = by / (p50_us * 1e-6) / 1e9
+        return {"bound": "hbm", "bytes": by, "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                "peak_kind": "measured hbm_gbs (MEASURED_PEAKS.json); co-located 1 GPU: all rows local"}
+    off = mat.clone()
+    off.fill_diagonal_(0)
+    out_rows, in_rows = off.sum(1), off.sum(0)  # per rank: remote rows sent / received in the dispatch leg
+    leg1 = int(torch.maximum(out_rows, in_rows).max()) * (2 * H + 8)
+    leg2 = int(torch.maximum(in_rows, out_rows).max()) * 2 * H  # the return leg mirrors it
+    by = leg1 + leg2
+    gbs = by / (p50_us * 1e-6) / 1e9
+    return {"bound": "nvlink", "bytes_busiest_gpu": by, "dispatch_leg_bytes": leg1, "return_leg_bytes": leg2,
+            "remote_rows_matrix": off.tolist(), "achieved": gbs, "unit": "GB/s",
+            "peak": 770.0, "frac": gbs / 770.0, "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
+            "nominal": 900.0, "frac_nominal": gbs / 900.0}
 
 
 def cpu_model_name() -> str:
@@ -308,9 +401,7 @@ def run_reference(args):
 
     model = as_model_spec(args.shape)
     threads = len(os.sched_getaffinity(0))
-    n_a, n_e, colo = SPLITS.get(args.gpus, (1, 1, True))
-    if args.colocated:
-        colo = True
+    n_a, n_e, colo, _ = choose_split(args.gpus, args.shape, args.plan, args.split, args.colocated)
     # the GPU arm's micro-batch (co-located: m micro-batches merged)
     b_a = args.m * args.b_a if (colo and args.merge) else args.b_a
     vals = []
@@ -351,14 +442,7 @@ def main():
         if rank == 0:
             print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}))
         sys.exit(2)
-    n_a, n_e, colo = SPLITS[world]
-    if args.split:  # e.g. "2+2"
-        n_a, n_e = (int(v) for v in args.split.split("+"))
-        colo = False
-        if n_a + n_e != world:
-            raise SystemExit(f"--split {args.split} needs {n_a + n_e} GPUs")
-    if args.colocated:  # every GPU holds both roles (config 5: 8 -> 8, 32 experts per GPU)
-        n_a, n_e, colo = world, world, True
+    n_a, n_e, colo, plan_source = choose_split(world, args.shape, args.plan, args.split, args.colocated)
     model = as_model_spec(args.shape)
     m_eff, b_a = args.m, args.b_a
     if colo and args.merge:
@@ -659,7 +743,9 @@ def main():
         "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights seed 0, N(0,1) tokens)",
         "config": {"workload": f"{model.name}-shaped MoE layer, " +
-                   ("co-located 1 GPU" if colo else f"{n_a} attention + {n_e} expert GPUs"),
+                   (f"co-located {world} GPU" + ("s (every GPU both roles, M2N all-to-all)" if world > 1 else "")
+                    if colo else f"{n_a} attention + {n_e} expert GPUs"),
+                   "plan_source": plan_source,
                    "hidden": model.hidden, "intermediate": model.intermediate, "experts": model.experts,
                    "topk": model.topk, "n_a": n_a, "n_e": n_e, "m": plan.m, "b_a": args.b_a,
                    "tokens_per_step_per_attention_gpu": plan.m * args.b_a * args.layers,
@@ -692,11 +778,11 @@ def main():
         "m2n": m2n,
     }
     # our kernels inside the timed region (per rank, summed over roles)
-    per_step = plan.m * args.layers * (launches_per_mbl if colo else 0)
+    per_step = plan.m * args.layers * (launches_per_mbl * world if colo else 0)
     if not colo:
         per_step = plan.m * args.layers * (n_a * (attn_launches + 3) + n_e * 3)
     line["gpu_launches"] = per_step * args.steps
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1:  # the CPU baseline is timed at N = 1 only
         threads = len(os.sched_getaffinity(0))
         cs = cpu_sample(model, args.b_a, threads, attn=args.attn == "real")
         line["cpu_baseline"] = {"value": cs["tokens_per_s"], "unit": "layer-tokens/s", "cores": threads,

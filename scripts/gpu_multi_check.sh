@@ -1,0 +1,8 @@
+set -u
+mkdir -p gpurun_out
+nvidia-smi -L
+MSI_TEST_OVERSUBSCRIBE=1 timeout 900 python -m pytest tests/test_gpu_multi.py -x -q > gpurun_out/multi_oversub.log 2>&1; tail -3 gpurun_out/multi_oversub.log
+for N in 2 4; do
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus $N --steps 10 --warmup 3 > gpurun_out/bench_n$N.log 2>&1; grep '^{' gpurun_out/bench_n$N.log | tail -1 > gpurun_out/bench_n$N.json; tail -c 300 gpurun_out/bench_n$N.log
+done
+timeout 300 python bench.py --no-cpu --no-e2e > gpurun_out/bench_n1_m2n.log 2>&1; grep '^{' gpurun_out/bench_n1_m2n.log > gpurun_out/bench_n1_m2n.json

@@ -99,6 +99,7 @@ PLANS = [
     (6, 2, False, "tiny", [64, 64, 33, 64, 1, 50], 3, 2),
     (2, 2, True, FINE, [64, 37], 2, 2),            # co-located 2 -> 2 (config 5 pattern)
     (4, 4, True, FINE, [16, 64, 1, 40], 2, 1),      # co-located 4 -> 4, 16 experts per GPU
+    (8, 8, True, "tiny", [64, 5, 64, 33, 1, 64, 50, 64], 1, 2),  # co-located 8 -> 8 (bench N=8 layout), 1 expert per GPU
     (2, 2, False, "tiny", [64, 48], 2, 1, "skew"),  # replicated hot experts (load balancing)
 ]
 

@@ -425,3 +425,94 @@ def test_router_tile_variants_bit_exact(lib, monkeypatch, tile, T, H, E, K):
     np.testing.assert_array_equal(cnt.cpu().numpy(), cnt_r)
     np.testing.assert_array_equal(slot.cpu().numpy(), slot_r)
     np.testing.assert_array_equal(w.cpu().numpy().view(np.uint32), w_r.view(np.uint32))
+
+
+# ------------------------------------------------------------- edge cases --
+def test_router_nonfinite_tokens_bit_exact(lib):
+    """Rows with NaN / +-Inf entries: NaN logits rank as -inf, ties go to the
+    lower expert; idx / counts / slots / weights still bit-exact vs the oracle."""
+    from paper_2504_02263_b200 import ops
+
+    T, H, E, K = 40, 512, 8, 2
+    x = O.synth_tokens(T, H, seed=31)
+    x[3, 7] = 0x7FC0          # NaN -> every logit of token 3 is NaN
+    x[5, :] = 0x7F80          # +Inf row -> +-Inf / NaN logits
+    x[9, 100] = 0xFF80        # one -Inf entry
+    wg = O.synth_weights(H, 128, E, seed=0, experts=[]).wg
+    idx_r, w_r = O.router(x, wg, K)
+    cnt_r, slot_r = O.place(idx_r, E)
+    idx, w, cnt, slot = ops.gate_topk(to_dev(x), to_dev(wg), K)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(idx.cpu().numpy(), idx_r)
+    np.testing.assert_array_equal(cnt.cpu().numpy(), cnt_r)
+    np.testing.assert_array_equal(slot.cpu().numpy(), slot_r)
+    # weights: bit-exact where finite; NaN exactly where the oracle's softmax is
+    # NaN (NaN payload bits differ between x86 and CUDA, so compare the class)
+    wg_ = w.cpu().numpy()
+    fin = np.isfinite(w_r)
+    np.testing.assert_array_equal(np.isnan(wg_), np.isnan(w_r))
+    np.testing.assert_array_equal(wg_[fin].view(np.uint32), w_r[fin].view(np.uint32))
+    assert fin[[0, 1, 2, 4]].all()
+
+
+def test_colocated_layer_concentrated_routing(lib):
+    """Every token routed to the same two experts (a collision-heavy load):
+    six experts get empty segments, two get all T rows; placement bit-exact,
+    outputs within tolerance."""
+    from paper_2504_02263_b200 import ops, runtime
+    from paper_2504_02263_b200.config import DeploymentPlan, as_model_spec
+
+    model = as_model_spec("tiny")
+    T = 96
+    plan = DeploymentPlan(n_a=1, n_e=1, m=1, b_a=T, colocated=True)
+    g = runtime.M2NGroup(model, plan, rank=0)
+    wts = O.synth_weights(model.hidden, model.intermediate, model.experts, seed=0)
+    x = O.synth_tokens(T, model.hidden, seed=41)
+    # a shared constant feature that only experts 3 and 6 respond to (logit
+    # shifts +32 / +24 against N(0, 1) logits): top-2 = {3, 6} for every token
+    x[:, 0] = O.bf16_round(np.full(T, 8.0, np.float32))
+    wgf = O.bf16_to_f32(wts.wg).copy()
+    wgf[:, 0] = 0.0
+    wgf[3, 0], wgf[6, 0] = 4.0, 3.0
+    wts.wg[:] = O.bf16_round(wgf)
+    w13 = ops.pack_w13(to_dev(wts.w_gate), to_dev(wts.w_up))
+    layer = runtime.MoEDecodeLayer(g, wg=to_dev(wts.wg), w13=w13, w2=to_dev(wts.w_down))
+    xd = to_dev(x)
+    r = layer.router(xd, 0)
+    layer.dispatch(xd, r, 0)
+    layer.expert_step(0)
+    out = layer.combine(r)
+    torch.cuda.synchronize()
+    assert g.status() == 0
+    ref = O.moe_layer([x], wts, model.topk, n_e=1)
+    assert set(np.unique(ref.idx[0])) == {3, 6}, "construction should route every token to experts 3 and 6"
+    np.testing.assert_array_equal(r.idx[:T].cpu().numpy(), ref.idx[0])
+    np.testing.assert_array_equal(r.cnt.cpu().numpy(), ref.cnt[0])
+    np.testing.assert_array_equal(r.slot[:T].cpu().numpy(), ref.slot[0])
+    ybuf = to_host(g.ybuf_view(0)[:T])
+    assert_close_bf16(ybuf, ref.y[0], "expert outputs")
+    np.testing.assert_array_equal(to_host(out), O.combine(ybuf, r.w[:T].cpu().numpy()))
+    g.close()
+
+
+def test_colocated_layer_empty_microbatch(lib):
+    """A micro-batch with T = 0 tokens still runs the whole protocol (counts,
+    arrival and combine signals advance) and the next micro-batch is exact."""
+    g, layer, wts, model = _colocated_layer("tiny", b_a=32)
+    for T in (0, 32, 0, 5):
+        x = O.synth_tokens(max(T, 1), model.hidden, seed=50 + T)[:T]
+        xd = to_dev(x) if T else torch.empty((0, model.hidden), dtype=torch.bfloat16, device="cuda")
+        r = layer.router(xd, 0)
+        layer.dispatch(xd, r, 0)
+        layer.expert_step(0)
+        out = layer.combine(r)
+        torch.cuda.synchronize()
+        assert g.status() == 0, f"device status after T={T}"
+        assert out.shape == (T, model.hidden)
+        if T:
+            ref = O.moe_layer([x], wts, model.topk, n_e=1)
+            np.testing.assert_array_equal(r.idx[:T].cpu().numpy(), ref.idx[0])
+            assert_close_bf16(to_host(out), ref.out[0], f"layer output T={T}")
+        else:
+            assert int(r.cnt.sum()) == 0
+    g.close()
