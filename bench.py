@@ -111,56 +111,81 @@ def parse():
 
 # ------------------------------------------------------------------ clocks --
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled DURING the timed
+    region: NVML polled every 5 ms on a thread; only samples between
+    window_open() and window_close() (wall clock around the timed loop and
+    its final synchronize) count.  Falls back to nvidia-smi -lms 100 when
+    NVML is unavailable."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+             ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80))
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.samples = []  # (t, sm_mhz, reasons_mask, power_w)
+        self.smax = None
+        self.win = [None, None]
+        self._stop = threading.Event()
+        self.t = None
+        self.nv = None
+
+    def _handle(self):
+        import pynvml as nv
+        nv.nvmlInit()
+        try:
+            import torch
+            pr = torch.cuda.get_device_properties(self.index)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            h = nv.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+        return nv, h
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except OSError:
-            self.proc = None
+            self.nv, self.h = self._handle()
+            self.smax = float(self.nv.nvmlDeviceGetMaxClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+        except Exception:
+            self.nv = None
+            return
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        nv, h = self.nv, self.h
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                pw = nv.nvmlDeviceGetPowerUsage(h) / 1e3
+                self.samples.append((time.perf_counter(), float(sm), int(rs), pw))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def window_open(self):
+        self.win[0] = time.perf_counter()
+
+    def window_close(self):
+        self.win[1] = time.perf_counter()
 
     def stop(self) -> dict:
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sm.append(float(f[1]))
-                smax = float(f[2])
-            except ValueError:
-                continue
-            for n, v in zip(names, f[5:9]):
-                if v.lower().startswith("active"):
+        if self.nv is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        self._stop.set()
+        self.t.join(timeout=1)
+        t0, t1 = self.win
+        inside = [x for x in self.samples if t0 is not None and t1 is not None and t0 <= x[0] <= t1]
+        sm = [x[1] for x in inside]
+        reasons = set()
+        for x in inside:
+            for n, bit in self.NAMES:
+                if x[2] & bit:
                     reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.smax,
+                "sm_mhz_min": min(sm) if sm else None, "power_w_median": statistics.median(x[3] for x in inside)
+                if inside else None, "reasons": sorted(reasons), "samples": len(sm),
+                "how": "NVML every 5 ms, samples inside the timed region only"}
 
 
 def ncu_traffic(name: str, b_a: int, n_a: int, n_e: int, colo: bool) -> dict | None:
@@ -556,11 +581,13 @@ def main():
     barrier()
     step = runner.replay if args.graph else (lambda: runner.run(xs))
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk.window_open()
     t_start.record()
     for _ in range(args.steps):
         step()
     t_end.record()
     torch.cuda.synchronize()
+    clk.window_close()
     barrier()
     clocks = clk.stop()
     layer.expert_ffn = orig_ffn

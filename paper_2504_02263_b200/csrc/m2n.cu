@@ -715,7 +715,7 @@ extern "C" int msi_dispatch(msi_ctx* c, const void* x, const int32_t* cnt, const
   if (!c->attn) { set_error("msi_dispatch: rank %d has no attention role", c->rank); return MSI_EINVAL; }
   MSI_REQUIRE(T >= 0 && T <= c->plan.max_tokens, "msi_dispatch: T=%d exceeds max_tokens=%d", T, c->plan.max_tokens);
   MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots && epoch != 0xffffffffu, "msi_dispatch: bad slot/epoch");
-  MSI_REQUIRE(x && cnt && idx && slot, "msi_dispatch: null pointer");
+  MSI_REQUIRE(cnt && (T == 0 || (x && idx && slot)), "msi_dispatch: null pointer");
   // row bases [E] (long long) + the all-gathered count table [n_a][E] + padded sizes (u32)
   const size_t table = disp_table_bytes(c->plan.experts, c->plan.n_a);
   const size_t bytes = (size_t)T * c->plan.topk * c->plan.hidden * 2;
@@ -836,7 +836,7 @@ extern "C" int msi_combine(msi_ctx* c, void* out, const float* w, const void* re
   if (!c->attn) { set_error("msi_combine: rank %d has no attention role", c->rank); return MSI_EINVAL; }
   MSI_REQUIRE(T >= 0 && T <= c->plan.max_tokens, "msi_combine: T out of range");
   MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots , "msi_combine: bad slot");
-  MSI_REQUIRE(out && w, "msi_combine: null pointer");
+  MSI_REQUIRE(T == 0 || (out && w), "msi_combine: null pointer");
   const msi_plan& p = c->plan;
   const Layout& L = c->my_layout;
   const size_t n = (size_t)T * p.hidden / 8;

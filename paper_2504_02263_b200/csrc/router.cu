@@ -350,7 +350,8 @@ int gate_topk(const void* x, const void* wg, int T, int H, int E, int K, int32_t
               int R = 0, int P = 0, int sender = 0, int32_t* pidx = nullptr) {
   MSI_REQUIRE(T >= 0 && H > 0 && H % 256 == 0, "gate_topk: H must be a positive multiple of 256 (got %d)", H);
   MSI_REQUIRE(E >= 1 && E <= 1024 && K >= 1 && K <= E && K <= 32, "gate_topk: need 1 <= K <= min(E, 32), E <= 1024");
-  MSI_REQUIRE(x && wg && idx && w && cnt && slot && ws, "gate_topk: null pointer");
+  // an empty micro-batch (T = 0) may pass null token / output buffers
+  MSI_REQUIRE((x || T == 0) && wg && (T == 0 || (idx && w && slot)) && cnt && ws, "gate_topk: null pointer");
   MSI_REQUIRE(!rep || (R >= 1 && P >= E && P <= 4096 && pidx && sender >= 0),
               "gate_topk: replica table needs R >= 1, E <= P <= 4096, pidx and sender >= 0");
   const Placement pl{rep, R, rep ? P : E, sender, rep ? pidx : idx};
