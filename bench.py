@@ -311,9 +311,12 @@ def m2n_latency(layer, g, x, world: int, iters: int = 1000, warm: int = 50) -> d
     route = layer.router(x, 0) if g.is_attention else None
     out = torch.empty_like(x) if g.is_attention else None
 
+    mid = torch.cuda.Event(enable_timing=True, external=True)  # end of the dispatch leg (graph node)
+
     def trip():
         if g.is_attention:
             layer.dispatch(x, route, 0)
+            mid.record()
         if g.is_expert:
             layer.expert_echo(0)
         if g.is_attention:
@@ -330,7 +333,7 @@ def m2n_latency(layer, g, x, world: int, iters: int = 1000, warm: int = 50) -> d
     with torch.cuda.graph(gr, stream=side):
         trip()
     torch.cuda.synchronize()
-    lat = []
+    lat, disp = [], []
     for i in range(warm + iters):
         if world > 1:
             dist.barrier()
@@ -342,21 +345,28 @@ def m2n_latency(layer, g, x, world: int, iters: int = 1000, warm: int = 50) -> d
         torch.cuda.synchronize()
         if i >= warm:
             lat.append(s.elapsed_time(e) * 1e3 if g.is_attention else 0.0)
-    t = torch.tensor(lat, dtype=torch.float64, device=torch.device("cuda", torch.cuda.current_device()))
+            disp.append(s.elapsed_time(mid) * 1e3 if g.is_attention else 0.0)
+    t = torch.tensor(lat + disp, dtype=torch.float64, device=torch.device("cuda", torch.cuda.current_device()))
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    v = sorted(t.cpu().tolist())
+    tl = t.cpu().tolist()
+    v = sorted(tl[:len(lat)])
+    dv = sorted(tl[len(lat):])
     if g.status() != 0:
         raise RuntimeError("device status after the M2N round trips")
     T, H, K = (x.shape[0], x.shape[1], g.model.topk) if x is not None else (0, 0, 0)
     p50 = v[len(v) // 2]
     return {"p50_us": p50, "p99_us": v[min(len(v) - 1, int(0.99 * len(v)))], "iters": iters,
+            "dispatch_leg_p50_us": dv[len(dv) // 2],
             "tokens_per_attention_gpu": T, "dispatch_bytes_per_attention_gpu": T * K * H * 2,
             "how": "graph replay of dispatch -> expert echo -> combine, barrier each, max over ranks",
-            "roofline": m2n_roofline(g, route, world, g.model.hidden, p50)}
+            "roofline": m2n_roofline(g, route, world, g.model.hidden, p50, dv[len(dv) // 2])}
 
 
-def m2n_roofline(g, route, world: int, H: int, p50_us: float) -> dict:
+SM_STORE_GBS = 689.0  # measured ceiling of SM peer stores per direction, bidirectional (see m2n_roofline)
+
+
+def m2n_roofline(g, route, world: int, H: int, p50_us: float, disp_us: float | None = None) -> dict:
     """Bytes the round trip must move and the rate it reached.
 
     N > 1: the two legs run one after the other (rows out, rows back), so the
@@ -398,10 +408,20 @@ def m2n_roofline(g, route, world: int, H: int, p50_us: float) -> dict:
     leg2 = int(torch.maximum(in_rows, out_rows).max()) * 2 * H  # the return leg mirrors it
     by = leg1 + leg2
     gbs = by / (p50_us * 1e-6) / 1e9
+    dl = None
+    if disp_us:  # the dispatch leg alone (its kernel's end event; includes the count exchange)
+        a = leg1 / (disp_us * 1e-6) / 1e9
+        dl = {"p50_us": disp_us, "achieved": a, "frac": a / 770.0, "frac_nominal": a / 900.0,
+              "frac_sm_store_ceiling": a / SM_STORE_GBS}
     return {"bound": "nvlink", "bytes_busiest_gpu": by, "dispatch_leg_bytes": leg1, "return_leg_bytes": leg2,
+            "dispatch_leg": dl,
             "remote_rows_matrix": off.tolist(), "achieved": gbs, "unit": "GB/s",
             "peak": 770.0, "frac": gbs / 770.0, "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
-            "nominal": 900.0, "frac_nominal": gbs / 900.0}
+            "nominal": 900.0, "frac_nominal": gbs / 900.0,
+            # SM-issued 16-B peer stores saturate below the copy engines on this
+            # pool: 689 GB/s per direction both ways at once, 695 one way
+            # (scripts/peer_store_probe.cu, profiles/r01_peer_store_probe.jsonl)
+            "sm_store_ceiling": SM_STORE_GBS, "frac_sm_store_ceiling": gbs / SM_STORE_GBS}
 
 
 def cpu_model_name() -> str:

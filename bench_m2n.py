@@ -58,6 +58,7 @@ def main():
     ap.add_argument("--iters", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--colocated", action="store_true", help="every GPU both roles (N -> N all-to-all)")
     args = ap.parse_args()
 
     import torch
@@ -67,7 +68,7 @@ def main():
     from paper_2504_02263_b200.config import DeploymentPlan, as_model_spec
 
     rank, world, local = runtime.init_distributed_from_env("nccl")
-    n_a, n_e, colo = SPLITS[world]
+    n_a, n_e, colo = (world, world, True) if args.colocated else SPLITS[world]
     model = as_model_spec(args.shape)
     H, K, E = model.hidden, model.topk, model.experts
     sizes = [int(s) for s in args.sizes.split(",")]
@@ -95,7 +96,9 @@ def main():
         if world > 1:
             dist.all_gather(all_cnt, cnt_q)
         mat = torch.stack(all_cnt).cpu()  # [src, dst] rows
-        ingress = int(mat.sum(0).max()) * H * 2  # busiest receiver, one way
+        remote = mat.clone()
+        remote.fill_diagonal_(0)  # co-located: a GPU's rows to itself stay in its HBM
+        ingress = int(torch.maximum(remote.sum(0), remote.sum(1)).max()) * H * 2  # busiest GPU, one way
         out = torch.empty((T, H), dtype=torch.bfloat16, device=dev) if g.is_attention else None
 
         mid = {}
