@@ -59,6 +59,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--colocated", action="store_true", help="every GPU both roles (N -> N all-to-all)")
+    ap.add_argument("--chain", type=int, default=16,
+                    help="steady-state: this many back-to-back round trips per graph replay (0 = off)")
     args = ap.parse_args()
 
     import torch
@@ -157,13 +159,14 @@ def main():
                 dist.all_reduce(ok, op=dist.ReduceOp.MIN)
             return bool(ok.item())
 
-        def graphed(fn):
-            """Capture fn once (device-tracked epochs) and return its replay."""
+        def graphed(fn, reps: int = 1):
+            """Capture fn (reps times back to back; device-tracked epochs) and return its replay."""
             gr = torch.cuda.CUDAGraph()
             side = torch.cuda.Stream(device=dev)
             side.wait_stream(torch.cuda.current_stream())
             with torch.cuda.graph(gr, stream=side):
-                fn()
+                for _ in range(reps):
+                    fn()
             torch.cuda.synchronize()
             if world > 1:
                 dist.barrier()
@@ -176,6 +179,14 @@ def main():
                "dispatch_only_p50_us": pct(disp, 0.5), "verified": verify()}
         glat = bench(graphed(ours), args.iters, args.warmup)
         rec["verified_graph"] = verify()
+        if args.chain:
+            # steady state (a decode loop's layers back to back): `chain` round
+            # trips per replay, no host barrier between them; per-trip time =
+            # replay time / chain (the first trip still carries the barrier skew)
+            cl = bench(graphed(ours, args.chain), max(args.iters // args.chain, 20), 5)
+            rec["ours_chain_per_trip_p50_us"] = pct(cl, 0.5) / args.chain
+            rec["chain"] = args.chain
+            rec["verified_chain"] = verify()
         # one traced eager round trip: %globaltimer phase stamps of every rank,
         # relative to attention rank 0's dispatch start (µs)
         g.set_trace(True)
@@ -241,6 +252,10 @@ def main():
                 rec["nccl_graph_p50_us"] = pct(ngl, 0.5)
                 rec["nccl_graph_p99_us"] = pct(ngl, 0.99)
                 rec["speedup_graph_p50"] = rec["nccl_graph_p50_us"] / rec["ours_graph_p50_us"]
+                if args.chain:
+                    ncl = bench(graphed(nccl, args.chain), max(args.iters // args.chain, 20), 5)
+                    rec["nccl_chain_per_trip_p50_us"] = pct(ncl, 0.5) / args.chain
+                    rec["speedup_chain_p50"] = rec["nccl_chain_per_trip_p50_us"] / rec["ours_chain_per_trip_p50_us"]
             except Exception as exc:  # NCCL graph capture unavailable: report eager only
                 rec["nccl_graph_error"] = str(exc)[:200]
         results.append(rec)
