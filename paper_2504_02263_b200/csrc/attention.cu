@@ -83,6 +83,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                        const __grid_constant__ CUtensorMap tk16, const __grid_constant__ CUtensorMap tv16,
                        const AttnArgs a) {
   extern __shared__ uint8_t smem_raw[];
+  pdl_trigger();
+  pdl_wait();
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * 2 * kTileBytes);
   uint64_t* empty = full + kStages;
@@ -296,6 +298,8 @@ __global__ void attn_split_combine_kernel(const float* __restrict__ part_o, cons
                                           int splits, __nv_bfloat16* __restrict__ out) {
   const size_t hrow = blockIdx.x;
   const int d = threadIdx.x;
+  pdl_trigger();
+  pdl_wait();
   const float* ml = part_ml + hrow * splits * 2;
   float M = -INFINITY;
   for (int s = 0; s < splits; ++s) M = fmaxf(M, ml[2 * s]);
@@ -319,6 +323,8 @@ __global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv, int64_
                                    __nv_bfloat16* __restrict__ q_out) {
   __shared__ float s_cos[kD / 2], s_sin[kD / 2];
   const int t = blockIdx.x;
+  pdl_trigger();
+  pdl_wait();
   const int p = pos[t];
   if (threadIdx.x < kD / 2) {
     const int i = threadIdx.x;
@@ -418,9 +424,9 @@ extern "C" int msi_rope_append(const void* qkv, int64_t qkv_ld, const int32_t* p
   MSI_REQUIRE(theta > 0.f && max_pages > 0 && num_pages > 0, "rope_append: bad theta / page counts");
   MSI_REQUIRE(qkv && pos && block_table && k_cache && v_cache && q_out, "rope_append: null pointer");
   if (T == 0) return 0;
-  rope_append_kernel<<<T, 128, 0, (cudaStream_t)stream>>>(
-      (const __nv_bfloat16*)qkv, qkv_ld, pos, n_heads, n_kv, theta, block_table, max_pages,
-      (__nv_bfloat16*)k_cache, (__nv_bfloat16*)v_cache, (__nv_bfloat16*)q_out);
+  MSI_CUDA(launch_k(rope_append_kernel, dim3(T), dim3(128), 0, (cudaStream_t)stream, (const __nv_bfloat16*)qkv,
+                    (int64_t)qkv_ld, pos, n_heads, n_kv, theta, block_table, max_pages, (__nv_bfloat16*)k_cache,
+                    (__nv_bfloat16*)v_cache, (__nv_bfloat16*)q_out));
   return check_launch("rope_append_kernel");
 }
 
@@ -493,10 +499,10 @@ extern "C" int msi_decode_attention(const void* q, const void* k_cache, const vo
   const long grid = (long)T * n_kv * splits;
   MSI_REQUIRE(grid < (1L << 31), "decode_attention: grid too large");
   cudaStream_t st = (cudaStream_t)stream;
-  decode_attn_kernel<<<(unsigned)grid, kThreads, kSmem, st>>>(tk, tv, tk16, tv16, a);
+  MSI_CUDA(launch_k(decode_attn_kernel, dim3((unsigned)grid), dim3(kThreads), kSmem, st, tk, tv, tk16, tv16, a));
   rc = check_launch("decode_attn_kernel");
   if (rc || splits == 1) return rc;
-  attn_split_combine_kernel<<<(unsigned)((size_t)T * n_heads), MSI_HEAD_DIM, 0, st>>>(a.part_o, a.part_ml, splits,
-                                                                                       a.out);
+  MSI_CUDA(launch_k(attn_split_combine_kernel, dim3((unsigned)((size_t)T * n_heads)), dim3(MSI_HEAD_DIM), 0, st,
+                    (const float*)a.part_o, (const float*)a.part_ml, splits, a.out));
   return check_launch("attn_split_combine_kernel");
 }

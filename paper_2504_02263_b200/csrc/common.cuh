@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/msinfer.h"
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
@@ -39,6 +41,34 @@ int check_launch(const char* what);
       return (int)e_;                                                      \
     }                                                                      \
   } while (0)
+
+// -------------------------------------- programmatic dependent launch --
+// Kernels of the MoE path are launched with programmatic stream
+// serialization (launch_k below): each one triggers its dependents at entry
+// (so the next kernel's CTAs are scheduled and run their prologue while this
+// one drains) and calls griddepcontrol.wait before touching anything an
+// earlier kernel on the stream produced -- the full stream-order guarantee,
+// minus the launch gap.  Both instructions are no-ops without the attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+bool pdl_enabled();  // MSI_PDL=1 enables (A/B switch)
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ------------------------------------------------------------------- bf16 --
 __device__ __forceinline__ float bf16lo(uint32_t v) { return __uint_as_float(v << 16); }

@@ -120,6 +120,8 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   const bool leader = rank == 0;
   const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;  // pair / CTA index
   const int nunits = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  pdl_trigger();  // the next kernel (GEMM2 / combine) may launch and queue now
+  pdl_wait();     // everything earlier on the stream is complete and visible
   uint32_t epoch = p.epoch;
   if (p.epoch_src) epoch = resolve_epoch(p.epoch, p.epoch_src, 1u, p.status);
 
@@ -556,13 +558,22 @@ int launch_cg(const GemmLaunch& L, cudaStream_t st) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attrs[1];
-  attrs[0].id = cudaLaunchAttributeClusterDimension;
-  attrs[0].val.clusterDim.x = CG;
-  attrs[0].val.clusterDim.y = 1;
-  attrs[0].val.clusterDim.z = 1;
+  cudaLaunchAttribute attrs[2];
+  int na = 0;
+  if (CG == 2) {
+    attrs[na].id = cudaLaunchAttributeClusterDimension;
+    attrs[na].val.clusterDim.x = CG;
+    attrs[na].val.clusterDim.y = 1;
+    attrs[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled()) {  // programmatic dependent launch (common.cuh)
+    attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.attrs = attrs;
-  cfg.numAttrs = CG == 2 ? 1 : 0;
+  cfg.numAttrs = na;
   MSI_CUDA(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<CG, MAXE>, ta, tb, L.p));
   return check_launch("grouped_gemm_kernel");
 }

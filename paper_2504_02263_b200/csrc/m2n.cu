@@ -58,6 +58,15 @@ int check_launch(const char* what) {
   return 0;
 }
 
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MSI_PDL");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 namespace {
 
 constexpr int CTR_STRIDE = 32;  // u32 per counter line (128 B)
@@ -199,6 +208,8 @@ dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32
   extern __shared__ __align__(128) long long s_rowbase[];  // [E] first row of this sender in expert e's segment
   __shared__ int s_abort;
   const int tid = threadIdx.x;
+  pdl_trigger();
+  pdl_wait();
   epoch = resolve_epoch(epoch, c.my_ause + mb * CTR_STRIDE, 1u, c.my_status);
   if (epoch == 0) return;  // host/device epoch mismatch: status set, nothing sent
   const int s = c.my_a;
@@ -363,6 +374,8 @@ constexpr int kEchoThreads = 512;
 // FFN kernels that follow start on data already in place and their timing is
 // compute only.  On timeout it sets the abort flag the FFN kernels honour.
 __global__ void expert_wait_kernel(const DevCtx c, int mb, uint32_t epoch) {
+  pdl_trigger();
+  pdl_wait();
   epoch = resolve_epoch(epoch, c.my_euse + mb * CTR_STRIDE, 1u, c.my_status);
   if (epoch == 0) return;  // the FFN kernels see the same mismatch and abort
   if (!wait_geq(c.my_arrive + mb * CTR_STRIDE, epoch * (uint32_t)c.n_a, c.timeout_ns, c.my_status))
@@ -376,6 +389,8 @@ echo_kernel(const DevCtx c, int mb, uint32_t epoch) {
   __shared__ int s_first[MSI_MAX_LOCAL_EXPERTS + 1];  // exclusive prefix of totals
   const int tid = threadIdx.x, lane = tid & 31;
   const uint32_t* arrive = c.my_arrive + mb * CTR_STRIDE;
+  pdl_trigger();
+  pdl_wait();
   epoch = resolve_epoch(epoch, c.my_euse + mb * CTR_STRIDE, 1u, c.my_status);
   if (epoch == 0) return;
   if (blockIdx.x == 0 && tid == 0) trace_stamp(c.trace, 3);
@@ -471,6 +486,8 @@ combine_kernel(const char* __restrict__ ybase, const float* __restrict__ w, cons
                int32_t* status, unsigned long long* trace) {
   __shared__ int s_ok;
   const bool t0 = blockIdx.x == 0 && threadIdx.x == 0;
+  pdl_trigger();
+  pdl_wait();
   if (wait_ctr) {
     epoch = resolve_epoch(epoch, epoch_src, 0u, status);  // set by this slot's dispatch
     if (epoch == 0) return;
@@ -731,8 +748,8 @@ extern "C" int msi_dispatch(msi_ctx* c, const void* x, const int32_t* cnt, const
     }
     int grid = (T + kThr / 32 - 1) / (kThr / 32);
     grid = grid < 1 ? 1 : (grid > 2 * num_sms() ? 2 * num_sms() : grid);
-    dispatch_kernel<true><<<grid, kThr, smem, st>>>(c->dev, reinterpret_cast<const __nv_bfloat16*>(x), cnt, idx,
-                                                    slot, T, mb_slot, epoch);
+    MSI_CUDA(launch_k(dispatch_kernel<true>, dim3(grid), dim3(kThr), smem, st, c->dev,
+                      reinterpret_cast<const __nv_bfloat16*>(x), cnt, idx, slot, T, mb_slot, epoch));
     return check_launch("dispatch_kernel<tma>");
   }
   // SM-store variant: ~64 KB of row stores per CTA, at most one CTA per SM
@@ -740,8 +757,8 @@ extern "C" int msi_dispatch(msi_ctx* c, const void* x, const int32_t* cnt, const
   // use few CTAs, which keeps the last-CTA release cheap
   int grid = (int)((bytes + 65535) / 65536);
   grid = grid < 1 ? 1 : (grid > num_sms() ? num_sms() : grid);
-  dispatch_kernel<false><<<grid, kDispThreads, table, st>>>(
-      c->dev, reinterpret_cast<const __nv_bfloat16*>(x), cnt, idx, slot, T, mb_slot, epoch);
+  MSI_CUDA(launch_k(dispatch_kernel<false>, dim3(grid), dim3(kDispThreads), table, st, c->dev,
+                    reinterpret_cast<const __nv_bfloat16*>(x), cnt, idx, slot, T, mb_slot, epoch));
   return check_launch("dispatch_kernel");
 }
 
@@ -818,7 +835,8 @@ extern "C" int msi_expert_wait(msi_ctx* c, int mb_slot, uint32_t epoch, void* st
   if (!c || !c->finalized) { set_error("msi_expert_wait: context not finalized"); return MSI_ESTATE; }
   if (!c->expert) { set_error("msi_expert_wait: rank %d has no expert role", c->rank); return MSI_EINVAL; }
   MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots, "msi_expert_wait: bad slot");
-  expert_wait_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(c->dev, mb_slot, epoch);
+  MSI_CUDA(launch_k(expert_wait_kernel, dim3(1), dim3(1), 0, reinterpret_cast<cudaStream_t>(stream), c->dev,
+                    mb_slot, epoch));
   return check_launch("expert_wait_kernel");
 }
 
@@ -826,7 +844,8 @@ extern "C" int msi_expert_echo(msi_ctx* c, int mb_slot, uint32_t epoch, void* st
   if (!c || !c->finalized) { set_error("msi_expert_echo: context not finalized"); return MSI_ESTATE; }
   if (!c->expert) { set_error("msi_expert_echo: rank %d has no expert role", c->rank); return MSI_EINVAL; }
   MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots , "msi_expert_echo: bad slot");
-  echo_kernel<<<num_sms(), kEchoThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(c->dev, mb_slot, epoch);
+  MSI_CUDA(launch_k(echo_kernel, dim3(num_sms()), dim3(kEchoThreads), 0, reinterpret_cast<cudaStream_t>(stream),
+                    c->dev, mb_slot, epoch));
   return check_launch("echo_kernel");
 }
 
@@ -842,11 +861,12 @@ extern "C" int msi_combine(msi_ctx* c, void* out, const float* w, const void* re
   const size_t n = (size_t)T * p.hidden / 8;
   int grid = (int)((n + 255) / 256);
   grid = grid < 1 ? 1 : (grid > 4 * num_sms() ? 4 * num_sms() : grid);
-  combine_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      c->heap + L.ybuf + mb_slot * L.ybuf_slot, w, reinterpret_cast<const uint16_t*>(resid),
-      reinterpret_cast<uint16_t*>(out), T, p.topk, p.hidden, c->dev.my_comb + mb_slot * CTR_STRIDE,
-      epoch, (uint32_t)p.n_e, c->dev.my_ause + mb_slot * CTR_STRIDE, c->timeout_ns, c->dev.my_status,
-      c->dev.trace);
+  MSI_CUDA(launch_k(combine_kernel, dim3(grid), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream),
+                    (const char*)(c->heap + L.ybuf + mb_slot * L.ybuf_slot), w,
+                    reinterpret_cast<const uint16_t*>(resid), reinterpret_cast<uint16_t*>(out), T, p.topk, p.hidden,
+                    (const uint32_t*)(c->dev.my_comb + mb_slot * CTR_STRIDE), epoch, (uint32_t)p.n_e,
+                    (const uint32_t*)(c->dev.my_ause + mb_slot * CTR_STRIDE), c->timeout_ns, c->dev.my_status,
+                    c->dev.trace));
   return check_launch("combine_kernel");
 }
 

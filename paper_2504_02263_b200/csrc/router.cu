@@ -235,6 +235,8 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t0 = blockIdx.x * BT;
   const int nchunk = H >> 8;
+  pdl_trigger();
+  pdl_wait();
   if (WS) {  // stage W_g (E*H*2 bytes) with one TMA bulk copy
     __shared__ __align__(8) uint64_t s_bar;
     char* dst = reinterpret_cast<char*>(s_logit) + ((logit_smem_bytes(BT, E) + 15) & ~size_t(15));
@@ -337,9 +339,9 @@ int launch(const void* x, const void* wg, int T, int H, int E, int K, int BT, in
   const size_t smem = ((head + 15) & ~size_t(15)) + (stage ? wbytes : 0);
   auto kern = stage ? gate_topk_kernel<TT, TE, true> : gate_topk_kernel<TT, TE, false>;
   if (smem > 48 * 1024) MSI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<nblk, kWarps * 32, smem, st>>>(reinterpret_cast<const __nv_bfloat16*>(x),
-                                        reinterpret_cast<const __nv_bfloat16*>(wg), T, H, E, K, BT,
-                                        idx, w, cnt, slot, reinterpret_cast<int32_t*>(ws), pl, smem);
+  MSI_CUDA(launch_k(kern, dim3(nblk), dim3(kWarps * 32), smem, st, reinterpret_cast<const __nv_bfloat16*>(x),
+                    reinterpret_cast<const __nv_bfloat16*>(wg), T, H, E, K, BT, idx, w, cnt, slot,
+                    reinterpret_cast<int32_t*>(ws), pl, smem));
   return check_launch("gate_topk_kernel");
 }
 
