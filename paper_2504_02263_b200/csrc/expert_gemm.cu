@@ -96,7 +96,7 @@ __device__ __forceinline__ bool half_pair_rows(const SegInfo<MAXE>& s, int e, in
 template <int CG, int MAXE>
 __global__ void __launch_bounds__(kThreads, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const GemmParams p) {
+                    const __grid_constant__ CUtensorMap tmA64, const GemmParams p) {
   using C = Cfg<CG, MAXE>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -139,6 +139,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     s_abort = ok ? 0 : 1;
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    if (CG == 2) tma_prefetch(&tmA64);
     for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4 * CG); }
     // ring consumers: MMA thread + 4 epilogue warps (+ the peer's producer
@@ -260,16 +261,19 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       int e, n, m;
       decode_tile(seg, p.E_l, tau, e, n, m);
       // this CTA's A rows: 128 (full tile / pair) or 64 (half pair: the odd
-      // last 128-row tile of a segment split 64/64 over the pair; the box
-      // still moves 128 rows, the MMA reads the first 64)
-      const int rowA = seg.start[e] + m * CG * BM + (int)rank * (half_pair(seg, e, m) ? BM / 2 : BM);
+      // last 128-row tile of a segment split 64/64 over the pair, moved with
+      // a 64-row box so the half-cost MMA is not fed a full tile's bytes)
+      const bool hp = half_pair(seg, e, m);
+      const int rowA = seg.start[e] + m * CG * BM + (int)rank * (hp ? BM / 2 : BM);
       const int rowB = e * p.n_total + n * BN + (int)rank * C::B_ROWS;
+      const CUtensorMap* mA = (CG == 2 && hp && p.a64) ? &tmA64 : &tmA;
+      const uint32_t a_bytes = (CG == 2 && hp && p.a64) ? C::A_BYTES / 2 : C::A_BYTES;
       for (int kb = 0; kb < kblocks; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* st = sA + stage * C::STAGE_BYTES;
         if constexpr (CG == 2) {
-          if (leader) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
-          tma_load_2d_pair(st, &tmA, kb * BK, rowA, &full[stage]);
+          if (leader) mbar_expect_tx(&full[stage], 2 * (a_bytes + C::B_BYTES));
+          tma_load_2d_pair(st, mA, kb * BK, rowA, &full[stage]);
           tma_load_2d_pair(st + C::A_BYTES, &tmB, kb * BK, rowB, &full[stage]);
         } else {
           mbar_expect_tx(&full[stage], C::STAGE_BYTES);
@@ -527,6 +531,13 @@ __global__ void pack_w13_kernel(const uint4* __restrict__ gate, const uint4* __r
 
 }  // namespace
 
+// Half-pair tiles load their 64 A rows per CTA with a 64-row TMA box
+// (MSI_GEMM_A64=0 restores the 128-row box, for A/B runs).
+bool half_pair_box64() {
+  const char* e = getenv("MSI_GEMM_A64");  // read per launch: bench_gemm.py --ab-env flips it
+  return !(e && e[0] == '0');
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -540,8 +551,10 @@ int num_sms() {
 template <int CG, int MAXE>
 int launch_cg(const GemmLaunch& L, cudaStream_t st) {
   using C = Cfg<CG, MAXE>;
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, ta64;
   int rc = make_tmap(&ta, L.a, (uint64_t)L.p.kdim, (uint64_t)L.a_rows, BK, BM);
+  if (rc) return rc;
+  rc = make_tmap(&ta64, L.a, (uint64_t)L.p.kdim, (uint64_t)L.a_rows, BK, BM / 2);  // half-pair A boxes
   if (rc) return rc;
   rc = make_tmap(&tb, L.b, (uint64_t)L.p.kdim, (uint64_t)L.p.E_l * L.p.n_total, BK, C::B_ROWS);
   if (rc) return rc;
@@ -574,7 +587,9 @@ int launch_cg(const GemmLaunch& L, cudaStream_t st) {
   }
   cfg.attrs = attrs;
   cfg.numAttrs = na;
-  MSI_CUDA(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<CG, MAXE>, ta, tb, L.p));
+  GemmParams prm = L.p;
+  prm.a64 = half_pair_box64();
+  MSI_CUDA(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<CG, MAXE>, ta, tb, ta64, prm));
   return check_launch("grouped_gemm_kernel");
 }
 

@@ -41,6 +41,8 @@ struct GemmParams {
   // dynamic tile scheduler: CTAs (pairs) take tiles in order from this
   // counter (0 at launch; the launch's last fetch resets it)
   uint32_t* tile_ctr;
+  // half-pair tiles load A with the 64-row box (set by the launcher)
+  int a64;
   // completion signal (last CTA): red.release.sys +1 on each sig[i]
   uint32_t* ticket;
   uint32_t* sig[MSI_MAX_RANKS];
