@@ -532,10 +532,10 @@ __global__ void pack_w13_kernel(const uint4* __restrict__ gate, const uint4* __r
 }  // namespace
 
 // Half-pair tiles load their 64 A rows per CTA with a 64-row TMA box
-// (MSI_GEMM_A64=0 restores the 128-row box, for A/B runs).
+// (MSI_GEMM_A64=1; 0 = the 128-row box, for A/B runs).
 bool half_pair_box64() {
   const char* e = getenv("MSI_GEMM_A64");  // read per launch: bench_gemm.py --ab-env flips it
-  return !(e && e[0] == '0');
+  return e && e[0] == '1';
 }
 
 int num_sms() {
