@@ -366,6 +366,20 @@ def m2n_latency(layer, g, x, world: int, iters: int = 1000, warm: int = 50) -> d
 SM_STORE_GBS = 689.0  # measured ceiling of SM peer stores per direction, bidirectional (see m2n_roofline)
 
 
+def m2n_leg_bytes(mat, H: int):
+    """mat[src][dst] = (t, k) rows attention rank src routes to GPU dst.
+    Returns (dispatch-leg bytes, return-leg bytes, remote-rows matrix) of the
+    busiest GPU: rows a GPU keeps for itself never cross NVLink; per leg the
+    bound is max over GPUs of max(egress, ingress); dispatch rows carry 8 B of
+    metadata on top of the 2H-byte row, returned rows do not."""
+    n = len(mat)
+    off = [[0 if i == j else int(mat[i][j]) for j in range(n)] for i in range(n)]
+    out_rows = [sum(r) for r in off]
+    in_rows = [sum(off[i][j] for i in range(n)) for j in range(n)]
+    busiest = max(max(o, i) for o, i in zip(out_rows, in_rows)) if n else 0
+    return busiest * (2 * H + 8), busiest * 2 * H, off
+
+
 def m2n_roofline(g, route, world: int, H: int, p50_us: float, disp_us: float | None = None) -> dict:
     """Bytes the round trip must move and the rate it reached.
 
@@ -401,11 +415,7 @@ def m2n_roofline(g, route, world: int, H: int, p50_us: float, disp_us: float | N
         gbs = by / (p50_us * 1e-6) / 1e9
         return {"bound": "hbm", "bytes": by, "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                 "peak_kind": "measured hbm_gbs (MEASURED_PEAKS.json); co-located 1 GPU: all rows local"}
-    off = mat.clone()
-    off.fill_diagonal_(0)
-    out_rows, in_rows = off.sum(1), off.sum(0)  # per rank: remote rows sent / received in the dispatch leg
-    leg1 = int(torch.maximum(out_rows, in_rows).max()) * (2 * H + 8)
-    leg2 = int(torch.maximum(in_rows, out_rows).max()) * 2 * H  # the return leg mirrors it
+    leg1, leg2, off = m2n_leg_bytes(mat.tolist(), H)
     by = leg1 + leg2
     gbs = by / (p50_us * 1e-6) / 1e9
     dl = None
@@ -415,7 +425,7 @@ def m2n_roofline(g, route, world: int, H: int, p50_us: float, disp_us: float | N
               "frac_sm_store_ceiling": a / SM_STORE_GBS}
     return {"bound": "nvlink", "bytes_busiest_gpu": by, "dispatch_leg_bytes": leg1, "return_leg_bytes": leg2,
             "dispatch_leg": dl,
-            "remote_rows_matrix": off.tolist(), "achieved": gbs, "unit": "GB/s",
+            "remote_rows_matrix": off, "achieved": gbs, "unit": "GB/s",
             "peak": 770.0, "frac": gbs / 770.0, "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
             "nominal": 900.0, "frac_nominal": gbs / 900.0,
             # SM-issued 16-B peer stores saturate below the copy engines on this
