@@ -348,7 +348,7 @@ def m2n_latency(layer, g, x, world: int, iters: int = 1000, warm: int = 50) -> d
             disp.append(s.elapsed_time(mid) * 1e3 if g.is_attention else 0.0)
     t = torch.tensor(lat + disp, dtype=torch.float64, device=torch.device("cuda", torch.cuda.current_device()))
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        allreduce_(t, dist.ReduceOp.MAX)
     tl = t.cpu().tolist()
     v = sorted(tl[:len(lat)])
     dv = sorted(tl[len(lat):])
@@ -364,6 +364,34 @@ def m2n_latency(layer, g, x, world: int, iters: int = 1000, warm: int = 50) -> d
 
 
 SM_STORE_GBS = 689.0  # measured ceiling of SM peer stores per direction, bidirectional (see m2n_roofline)
+
+
+def _over() -> bool:
+    """MSI_OVERSUBSCRIBE=1: validation runs with more ranks than GPUs (ranks
+    share GPUs round-robin, host collectives over gloo).  Numbers from such a
+    run are not measurements."""
+    return os.environ.get("MSI_OVERSUBSCRIBE") == "1"
+
+
+def allreduce_(t, op=None):
+    """In-place all-reduce of a (device) tensor; staged through the host on gloo."""
+    import torch.distributed as dist
+    op = op if op is not None else dist.ReduceOp.SUM
+    if dist.get_backend() == "gloo" and t.is_cuda:
+        c = t.cpu()
+        dist.all_reduce(c, op=op)
+        t.copy_(c)
+    else:
+        dist.all_reduce(t, op=op)
+
+
+def allgather(t) -> list:
+    import torch
+    import torch.distributed as dist
+    src = t.cpu() if dist.get_backend() == "gloo" else t
+    out = [torch.zeros_like(src) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, src)
+    return out
 
 
 def m2n_leg_bytes(mat, H: int):
@@ -402,9 +430,7 @@ def m2n_roofline(g, route, world: int, H: int, p50_us: float, disp_us: float | N
         ranks = torch.tensor(plan.expert_ranks(), dtype=torch.int64, device=dev)
         rows_to += torch.bincount(ranks[q], minlength=world)[:world]
     if world > 1:
-        mats = [torch.zeros_like(rows_to) for _ in range(world)]
-        dist.all_gather(mats, rows_to)
-        mat = torch.stack(mats).cpu()
+        mat = torch.stack([m.cpu() for m in allgather(rows_to)])
     else:
         mat = rows_to.cpu()[None, :]
     if world == 1:
@@ -492,7 +518,7 @@ def main():
     from paper_2504_02263_b200 import runtime
     from paper_2504_02263_b200.config import DeploymentPlan, WorkloadSpec, as_model_spec
 
-    rank, world, local = runtime.init_distributed_from_env("nccl")
+    rank, world, local = runtime.init_distributed_from_env("gloo" if _over() else "nccl")
     if world != args.gpus:
         if rank == 0:
             print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}))
@@ -550,7 +576,7 @@ def main():
                 h = att_stages[j].forward(x, 0) if att_stages else x
                 cnt += _ops.gate_topk(h, wg, model.topk)[2].double()
         if world > 1:
-            dist.all_reduce(cnt)
+            allreduce_(cnt)
         loads = cnt.cpu().numpy()
         if args.balance:
             from paper_2504_02263_b200.balance import balanced_slots
@@ -652,8 +678,10 @@ def main():
     t = torch.tensor([elapsed_ms, sum(ffn_ms), len(ffn_ms), rows, calls], dtype=torch.float64, device=dev)
     if world > 1:
         tmax = t.clone()
-        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(tmax[1:], op=dist.ReduceOp.SUM)
+        m_, s_ = tmax[:1].clone(), tmax[1:].clone()
+        allreduce_(m_, dist.ReduceOp.MAX)
+        allreduce_(s_, dist.ReduceOp.SUM)
+        tmax = torch.cat([m_, s_])
         t = tmax
     elapsed_ms, ffn_total_ms, ffn_n, rows_total, calls_total = t.tolist()
     # rows each expert GPU processed per FFN call (load balance evidence)
@@ -753,7 +781,7 @@ def main():
         barrier()
         e2e_ms = torch.tensor([s.elapsed_time(e)], dtype=torch.float64, device=dev)
         if world > 1:
-            dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+            allreduce_(e2e_ms, dist.ReduceOp.MAX)
         bytes_io = plan.m * args.b_a * model.hidden * 2 if xs else 0
         tok = n_a * plan.m * args.b_a * args.layers * args.steps
         ok = all(torch.equal(h.to(dev), o) for h, o in zip(host_out[(args.steps - 1) % 2], outs)) if xs else True

@@ -518,6 +518,8 @@ def init_distributed_from_env(backend: str = "nccl"):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    if os.environ.get("MSI_OVERSUBSCRIBE") == "1" and torch.cuda.is_available():
+        local %= torch.cuda.device_count()  # validation runs: several ranks per GPU (use gloo)
     if world > 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         torch.cuda.set_device(local)
