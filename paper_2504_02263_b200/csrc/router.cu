@@ -21,6 +21,7 @@
 #include "common.cuh"
 
 namespace msi {
+
 namespace {
 
 constexpr int kWarps = 8;
@@ -223,6 +224,122 @@ __device__ __forceinline__ void route_tail(float* s_logit, int t0, int BT, int T
   if (threadIdx.x == 0) ws[0] = 0;  // ticket ready for the next launch
 }
 
+// Logits of one warp tile: TT tokens from t_first x TE experts from e_first.
+// Lane l accumulates elements 256j + 8l + c (j ascending, c = 0..7) with
+// fmaf from +0, then an xor butterfly 16,8,4,2,1 -- the pinned order
+// (oracle/msi_oracle.c); every lane returns the final values, NaN as -inf.
+template <int TT, int TE, bool WS, int PF = (TT * TE > 32) ? 2 : 4>
+__device__ __forceinline__ void tile_logits(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
+                                            int t_first, int e_first, int T, int H, float (&acc)[TT][TE]) {
+  const int lane = threadIdx.x & 31;
+  const int nchunk = H >> 8;
+#pragma unroll
+  for (int i = 0; i < TT; ++i)
+#pragma unroll
+    for (int j = 0; j < TE; ++j) acc[i][j] = 0.0f;
+  const __nv_bfloat16* xr[TT];
+  bool tv[TT];
+#pragma unroll
+  for (int i = 0; i < TT; ++i) {
+    int t = t_first + i;
+    tv[i] = t < T;
+    xr[i] = x + (size_t)(tv[i] ? t : 0) * H + 8 * lane;
+  }
+  const __nv_bfloat16* wr = wg + (size_t)e_first * H + 8 * lane;
+  // x chunks are prefetched PF iterations ahead (HBM latency), W_g rows are
+  // small and L1/L2-resident; the accumulation order per (token, expert)
+  // stays j-major, c-minor as pinned.
+  uint4 xq[PF][TT];
+#pragma unroll
+  for (int u = 0; u < PF; ++u)
+#pragma unroll
+    for (int i = 0; i < TT; ++i)
+      xq[u][i] = (tv[i] && u < nchunk) ? __ldg(reinterpret_cast<const uint4*>(xr[i] + 256 * u)) : make_uint4(0, 0, 0, 0);
+  for (int j0 = 0; j0 < nchunk; j0 += PF) {
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      const int j = j0 + u;
+      if (j >= nchunk) break;
+      float xv[TT][8];
+#pragma unroll
+      for (int i = 0; i < TT; ++i) {
+        const uint4 v = xq[u][i];
+        xv[i][0] = bf16lo(v.x); xv[i][1] = bf16hi(v.x);
+        xv[i][2] = bf16lo(v.y); xv[i][3] = bf16hi(v.y);
+        xv[i][4] = bf16lo(v.z); xv[i][5] = bf16hi(v.z);
+        xv[i][6] = bf16lo(v.w); xv[i][7] = bf16hi(v.w);
+        // refill this slot with chunk j + PF
+        xq[u][i] = (tv[i] && j + PF < nchunk) ? __ldg(reinterpret_cast<const uint4*>(xr[i] + 256 * (j + PF)))
+                                             : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int e = 0; e < TE; ++e) {
+        const uint4* wp = reinterpret_cast<const uint4*>(wr + (size_t)e * H + 256 * j);
+        uint4 v = WS ? *wp : __ldg(wp);
+        float wv[8] = {bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y),
+                       bf16lo(v.z), bf16hi(v.z), bf16lo(v.w), bf16hi(v.w)};
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+#pragma unroll
+          for (int i = 0; i < TT; ++i) acc[i][e] = __fmaf_rn(xv[i][c], wv[c], acc[i][e]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < TT; ++i)
+#pragma unroll
+    for (int e = 0; e < TE; ++e) {
+      float v = acc[i][e];
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+      acc[i][e] = (v != v) ? -INFINITY : v;  // NaN logits rank as -inf (the oracle does the same)
+    }
+}
+
+// Fine-grained MoE (E >= 64, FMA-bound): the logits get their own 2-D grid --
+// CTA (blockIdx.x, blockIdx.y) = BT tokens x EB experts, one TT x TE warp
+// tile per warp at a time, <= 128 registers so 2 CTAs share an SM -- into a
+// [T][E] fp32 scratch; route_kernel then runs phases 2-4 on 32-token blocks.
+// Same per-(token, expert) reduction order as the fused kernel: bit-identical.
+template <int TT, int TE>
+__global__ void __launch_bounds__(kWarps * 32, 2)
+gate_logits_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg, int T, int H, int E,
+                   int BT, int EB, float* __restrict__ logits) {
+  pdl_trigger();
+  pdl_wait();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t0 = blockIdx.x * BT, e0 = blockIdx.y * EB;
+  const int tgroups = BT / TT, egroups = EB / TE;
+  for (int tile = warp; tile < tgroups * egroups; tile += kWarps) {
+    const int tg = tile % tgroups, eg = tile / tgroups;
+    float acc[TT][TE];
+    tile_logits<TT, TE, false, (TT * TE >= 32 ? 2 : 4)>(x, wg, t0 + tg * TT, e0 + eg * TE, T, H, acc);
+#pragma unroll
+    for (int i = 0; i < TT; ++i) {
+      const int t = t0 + tg * TT + i;
+#pragma unroll
+      for (int e = 0; e < TE; ++e)
+        if (lane == ((i * TE + e) & 31) && t < T) logits[(size_t)t * E + e0 + eg * TE + e] = acc[i][e];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kWarps * 32)
+route_kernel(const float* __restrict__ logits, int T, int E, int K, int BT, int32_t* __restrict__ idx_out,
+             float* __restrict__ w_out, int32_t* __restrict__ cnt_out, int32_t* __restrict__ slot_out,
+             int32_t* __restrict__ ws, const Placement pl, size_t smem_cap) {
+  extern __shared__ __align__(16) float s_logit[];  // [BT][E]
+  pdl_trigger();
+  pdl_wait();
+  const int t0 = blockIdx.x * BT;
+  const int rows = min(BT, T - t0);
+  const float4* src = reinterpret_cast<const float4*>(logits + (size_t)t0 * E);
+  float4* dst = reinterpret_cast<float4*>(s_logit);
+  for (int i = threadIdx.x; i < rows * E / 4; i += blockDim.x) dst[i] = __ldcg(src + i);
+  __syncthreads();
+  route_tail(s_logit, t0, BT, T, E, K, idx_out, w_out, cnt_out, slot_out, ws, pl, smem_cap);
+}
+
 template <int TT, int TE, bool WS>
 __global__ void __launch_bounds__(kWarps * 32)
 gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
@@ -234,7 +351,6 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t0 = blockIdx.x * BT;
-  const int nchunk = H >> 8;
   pdl_trigger();
   pdl_wait();
   if (WS) {  // stage W_g (E*H*2 bytes) with one TMA bulk copy
@@ -257,69 +373,12 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
   for (int tile = warp; tile < tgroups * egroups; tile += kWarps) {
     const int tg = tile % tgroups, eg = tile / tgroups;
     float acc[TT][TE];
+    tile_logits<TT, TE, WS>(x, wg, t0 + tg * TT, eg * TE, T, H, acc);
 #pragma unroll
     for (int i = 0; i < TT; ++i)
 #pragma unroll
-      for (int j = 0; j < TE; ++j) acc[i][j] = 0.0f;
-    const __nv_bfloat16* xr[TT];
-    bool tv[TT];
-#pragma unroll
-    for (int i = 0; i < TT; ++i) {
-      int t = t0 + tg * TT + i;
-      tv[i] = t < T;
-      xr[i] = x + (size_t)(tv[i] ? t : 0) * H + 8 * lane;
-    }
-    const __nv_bfloat16* wr = wg + (size_t)(eg * TE) * H + 8 * lane;
-    // x chunks are prefetched PF iterations ahead (HBM latency), W_g rows are
-    // small and L1/L2-resident; the accumulation order per (token, expert)
-    // stays j-major, c-minor as pinned.
-    constexpr int PF = (TT * TE > 32) ? 2 : 4;
-    uint4 xq[PF][TT];
-#pragma unroll
-    for (int u = 0; u < PF; ++u)
-#pragma unroll
-      for (int i = 0; i < TT; ++i)
-        xq[u][i] = (tv[i] && u < nchunk) ? __ldg(reinterpret_cast<const uint4*>(xr[i] + 256 * u)) : make_uint4(0, 0, 0, 0);
-    for (int j0 = 0; j0 < nchunk; j0 += PF) {
-#pragma unroll
-      for (int u = 0; u < PF; ++u) {
-        const int j = j0 + u;
-        if (j >= nchunk) break;
-        float xv[TT][8];
-#pragma unroll
-        for (int i = 0; i < TT; ++i) {
-          const uint4 v = xq[u][i];
-          xv[i][0] = bf16lo(v.x); xv[i][1] = bf16hi(v.x);
-          xv[i][2] = bf16lo(v.y); xv[i][3] = bf16hi(v.y);
-          xv[i][4] = bf16lo(v.z); xv[i][5] = bf16hi(v.z);
-          xv[i][6] = bf16lo(v.w); xv[i][7] = bf16hi(v.w);
-          // refill this slot with chunk j + PF
-          xq[u][i] = (tv[i] && j + PF < nchunk) ? __ldg(reinterpret_cast<const uint4*>(xr[i] + 256 * (j + PF)))
-                                               : make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int e = 0; e < TE; ++e) {
-          const uint4* wp = reinterpret_cast<const uint4*>(wr + (size_t)e * H + 256 * j);
-          uint4 v = WS ? *wp : __ldg(wp);
-          float wv[8] = {bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y),
-                         bf16lo(v.z), bf16hi(v.z), bf16lo(v.w), bf16hi(v.w)};
-#pragma unroll
-          for (int c = 0; c < 8; ++c)
-#pragma unroll
-            for (int i = 0; i < TT; ++i) acc[i][e] = __fmaf_rn(xv[i][c], wv[c], acc[i][e]);
-        }
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < TT; ++i)
-#pragma unroll
-      for (int e = 0; e < TE; ++e) {
-        float v = acc[i][e];
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
-        v = (v != v) ? -INFINITY : v;  // NaN logits rank as -inf (the oracle does the same)
-        if (lane == ((i * TE + e) & 31)) s_logit[(tg * TT + i) * E + eg * TE + e] = v;
-      }
+      for (int e = 0; e < TE; ++e)
+        if (lane == ((i * TE + e) & 31)) s_logit[(tg * TT + i) * E + eg * TE + e] = acc[i][e];
   }
   __syncthreads();
 
@@ -343,6 +402,62 @@ int launch(const void* x, const void* wg, int T, int H, int E, int K, int BT, in
                     reinterpret_cast<const __nv_bfloat16*>(wg), T, H, E, K, BT, idx, w, cnt, slot,
                     reinterpret_cast<int32_t*>(ws), pl, smem));
   return check_launch("gate_topk_kernel");
+}
+
+// [T][E] fp32 logits scratch of the split path: after the ticket word and the
+// CTA histograms / bases (sized for the smallest BT = 4), 256-B aligned.
+size_t split_logits_offset(int T, int P) {
+  const size_t nblk = ((size_t)T + 3) / 4;
+  return (64 + 2 * nblk * (size_t)P * sizeof(int32_t) + 255) & ~size_t(255);
+}
+
+template <int TT>
+int launch_split(const void* x, const void* wg, int T, int H, int E, int K, int BTL, int EB, int32_t* idx,
+                 float* w, int32_t* cnt, int32_t* slot, void* ws, const Placement& pl, cudaStream_t st) {
+  constexpr int TE = 8;
+  MSI_REQUIRE(BTL % TT == 0 && EB % TE == 0 && E % EB == 0, "gate_topk: bad split tile %dx%d", BTL, EB);
+  float* logits = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + split_logits_offset(T, pl.P));
+  MSI_CUDA(launch_k(gate_logits_kernel<TT, TE>, dim3((T + BTL - 1) / BTL, E / EB), dim3(kWarps * 32), 0, st,
+                    reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<const __nv_bfloat16*>(wg), T, H, E,
+                    BTL, EB, logits));
+  constexpr int BT = 32;
+  size_t head = logit_smem_bytes(BT, E);
+  if (head < (size_t)pl.P * 4) head = (size_t)pl.P * 4;
+  const size_t smem = (head + 15) & ~size_t(15);
+  static size_t attr = 48 * 1024;
+  if (smem > attr) {
+    MSI_CUDA(cudaFuncSetAttribute(route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  MSI_CUDA(launch_k(route_kernel, dim3((T + BT - 1) / BT), dim3(kWarps * 32), smem, st, (const float*)logits, T, E, K,
+                    BT, idx, w, cnt, slot, reinterpret_cast<int32_t*>(ws), pl, smem));
+  return check_launch("gate_logits_kernel + route_kernel");
+}
+
+// Split-path tiles: TT tokens per warp tile (TE = 8 experts), BTL tokens x EB
+// experts per CTA.  MSI_ROUTER_SPLIT=TTxBTLxEB forces the split path with that
+// tile (any T), =0 forces the fused kernel.
+int route_split(const void* x, const void* wg, int T, int H, int E, int K, int32_t* idx, float* w, int32_t* cnt,
+                int32_t* slot, void* ws, const Placement& pl, cudaStream_t st) {
+  // measured best at small T (scripts/sweep_router_split.py, T = 128: 2x4x32)
+  int tt = 2, btl = 4, eb = 32;
+  if (const char* ov = getenv("MSI_ROUTER_SPLIT")) {
+    int a = 0, b = 0, c = 0;
+    if (sscanf(ov, "%dx%dx%d", &a, &b, &c) == 3) { tt = a; btl = b; eb = c; }
+  }
+  if (E % eb) eb = 8;
+  if (tt == 4) return launch_split<4>(x, wg, T, H, E, K, btl, eb, idx, w, cnt, slot, ws, pl, st);
+  if (tt == 2) return launch_split<2>(x, wg, T, H, E, K, btl, eb, idx, w, cnt, slot, ws, pl, st);
+  return launch_split<1>(x, wg, T, H, E, K, btl, eb, idx, w, cnt, slot, ws, pl, st);
+}
+
+// The split path wins only at small T (T = 128: 92 -> 71 us); from T ~ 512 on
+// the fused kernel's W_g reuse across its 16-32 tokens is worth more than the
+// split grid's occupancy (profiles/r01_router_split_sweep.jsonl).
+bool split_enabled(int E, int T) {
+  const char* ov = getenv("MSI_ROUTER_SPLIT");
+  if (ov) return ov[0] != '0';
+  return E >= 64 && E % 8 == 0 && T <= 256;
 }
 
 }  // namespace
@@ -373,8 +488,11 @@ int gate_topk(const void* x, const void* wg, int T, int H, int E, int K, int32_t
 #undef MSI_RT
     }
   }
-  // fine-grained MoE: FMA-bound; BT=4 keeps >=148 CTAs busy at small T, BT=16
-  // quarters the W_g re-reads once there are >= 128 CTAs (T=2048: 489 -> 363 us)
+  // fine-grained MoE at small T: logits on their own 2-D grid, then top-K /
+  // placement (route_split)
+  if (split_enabled(E, T) && E >= 64 && E % 8 == 0) return route_split(x, wg, T, H, E, K, idx, w, cnt, slot, ws, pl, st);
+  // BT=4 keeps >=148 CTAs busy at small T, BT=16 quarters the W_g re-reads
+  // once there are >= 128 CTAs (T=2048: 489 -> 363 us)
   if (E % 16 == 0 && E > 16)
     return launch<4, 16>(x, wg, T, H, E, K, T >= 2048 ? 16 : 4, idx, w, cnt, slot, ws, pl, st);
   // E = 8 / 16: W_g staged once per CTA (TMA bulk copy) and amortised over 32
@@ -399,7 +517,9 @@ int gate_topk(const void* x, const void* wg, int T, int H, int E, int K, int32_t
 
 size_t gate_topk_workspace(int T, int E) {
   const size_t nblk = ((size_t)T + 3) / 4;  // smallest BT used above
-  return 64 /* ticket + pad */ + 2 * nblk * (size_t)E * sizeof(int32_t);  // CTA histograms + bases
+  const size_t base = 64 /* ticket + pad */ + 2 * nblk * (size_t)E * sizeof(int32_t);  // CTA histograms + bases
+  // split path (E >= 64): + [T][E] fp32 logits (E here is the physical slot count P >= logical E)
+  return E >= 64 ? split_logits_offset(T, E) + (size_t)T * E * sizeof(float) : base;
 }
 
 }  // namespace msi

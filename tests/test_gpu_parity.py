@@ -427,6 +427,30 @@ def test_router_tile_variants_bit_exact(lib, monkeypatch, tile, T, H, E, K):
     np.testing.assert_array_equal(w.cpu().numpy().view(np.uint32), w_r.view(np.uint32))
 
 
+@pytest.mark.parametrize("split,T,H,E,K", [("default", 130, 7168, 256, 8), ("default", 2400, 7168, 256, 8),
+                                           ("4x32x64", 777, 7168, 256, 8), ("2x4x32", 301, 7168, 256, 8),
+                                           ("1x1x128", 40, 7168, 256, 8), ("4x8x64", 515, 4096, 64, 6),
+                                           ("0", 515, 4096, 64, 6)])
+def test_router_split_path_bit_exact(lib, monkeypatch, split, T, H, E, K):
+    """Fine-grained MoE (E >= 64): the logits kernel on its (token x expert) grid
+    plus the route kernel give routing, counts, slots and weights bit-identical
+    to the oracle for every tile choice (MSI_ROUTER_SPLIT; 0 = fused kernel)."""
+    from paper_2504_02263_b200 import ops
+
+    if split != "default":
+        monkeypatch.setenv("MSI_ROUTER_SPLIT", split)
+    x = O.synth_tokens(T, H, seed=9 + T)
+    wg = O.synth_weights(H, 128, E, seed=4, experts=[]).wg
+    idx_r, w_r = O.router(x, wg, K)
+    cnt_r, slot_r = O.place(idx_r, E)
+    idx, w, cnt, slot = ops.gate_topk(to_dev(x), to_dev(wg), K)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(idx.cpu().numpy(), idx_r)
+    np.testing.assert_array_equal(cnt.cpu().numpy(), cnt_r)
+    np.testing.assert_array_equal(slot.cpu().numpy(), slot_r)
+    np.testing.assert_array_equal(w.cpu().numpy().view(np.uint32), w_r.view(np.uint32))
+
+
 # ------------------------------------------------------------- edge cases --
 def test_router_nonfinite_tokens_bit_exact(lib):
     """Rows with NaN / +-Inf entries: NaN logits rank as -inf, ties go to the
