@@ -22,6 +22,8 @@
 
 namespace msi {
 
+int num_sms();  // expert_gemm.cu
+
 namespace {
 
 constexpr int kWarps = 8;
@@ -404,6 +406,7 @@ int launch(const void* x, const void* wg, int T, int H, int E, int K, int BT, in
   return check_launch("gate_topk_kernel");
 }
 
+
 // [T][E] fp32 logits scratch of the split path: after the ticket word and the
 // CTA histograms / bases (sized for the smallest BT = 4), 256-B aligned.
 size_t split_logits_offset(int T, int P) {
@@ -417,7 +420,8 @@ int launch_split(const void* x, const void* wg, int T, int H, int E, int K, int 
   constexpr int TE = 8;
   MSI_REQUIRE(BTL % TT == 0 && EB % TE == 0 && E % EB == 0, "gate_topk: bad split tile %dx%d", BTL, EB);
   float* logits = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + split_logits_offset(T, pl.P));
-  MSI_CUDA(launch_k(gate_logits_kernel<TT, TE>, dim3((T + BTL - 1) / BTL, E / EB), dim3(kWarps * 32), 0, st,
+  const dim3 grid((T + BTL - 1) / BTL, E / EB);
+  MSI_CUDA(launch_k(gate_logits_kernel<TT, TE>, grid, dim3(kWarps * 32), 0, st,
                     reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<const __nv_bfloat16*>(wg), T, H, E,
                     BTL, EB, logits));
   constexpr int BT = 32;

@@ -45,17 +45,19 @@ for T in [int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "128,512,2048,4
     res["default_us"] = dflt_us
     res["default_exact"] = all(torch.equal(a.view(torch.int32), b.view(torch.int32)) for a, b in zip(d, ref))
     best = None
-    for tt in (1, 2, 4):
-        for a in (1, 2, 4, 8):
-            for eb in (32, 64, 128):
-                env = f"{tt}x{tt * a}x{eb}"
-                us, o = run(x, wg, ws, env)
-                ok = all(torch.equal(p.view(torch.int32), q.view(torch.int32)) for p, q in zip(o, ref))
-                if not ok:
-                    res.setdefault("MISMATCH", []).append(env)
-                if best is None or us < best[1]:
-                    best = (env, us)
-                res[env] = round(us, 1)
+    for wf in ("0",):
+        for tt in (1, 2, 4):
+            for a in (1, 2, 4, 8):
+                for eb in (32, 64, 128):
+                    env = f"{tt}x{tt * a}x{eb}"
+                    us, o = run(x, wg, ws, env)
+                    ok = all(torch.equal(p.view(torch.int32), q.view(torch.int32)) for p, q in zip(o, ref))
+                    key = f"wf{wf}:{env}"
+                    if not ok:
+                        res.setdefault("MISMATCH", []).append(key)
+                    if best is None or us < best[1]:
+                        best = (key, us)
+                    res[key] = round(us, 1)
     res["best"] = best
     res["tfma_fused"] = T * E * H / (ref_us * 1e-6) / 1e12
     res["tfma_best"] = T * E * H / (best[1] * 1e-6) / 1e12
