@@ -116,7 +116,9 @@ int msi_ctx_workspace(msi_ctx* ctx, void** ptr, size_t* bytes);
  * sender's tokens routed to idx[t,k] (ascending token order).  Bit-exact with
  * oracle/msi_oracle.c (pinned fp32 reduction order, deterministic exp).
  * workspace: msi_gate_topk_workspace(T, E) bytes, zero-filled once before the
- * first call (the kernel leaves it zeroed).  H % 256 == 0, 1 <= K <= min(E,32). */
+ * first call (the kernels reset the ticket word they need at zero); for E >= 64
+ * it includes a [T][E] fp32 logits scratch (small-T split path).
+ * H % 256 == 0, 1 <= K <= min(E,32). */
 size_t msi_gate_topk_workspace(int T, int E);
 int msi_gate_topk(const void* x, const void* wg, int T, int H, int E, int K,
                   int32_t* idx, float* w, int32_t* cnt, int32_t* slot,
