@@ -495,10 +495,15 @@ int gate_topk(const void* x, const void* wg, int T, int H, int E, int K, int32_t
   // fine-grained MoE at small T: logits on their own 2-D grid, then top-K /
   // placement (route_split)
   if (split_enabled(E, T) && E >= 64 && E % 8 == 0) return route_split(x, wg, T, H, E, K, idx, w, cnt, slot, ws, pl, st);
-  // BT=4 keeps >=148 CTAs busy at small T, BT=16 quarters the W_g re-reads
-  // once there are >= 128 CTAs (T=2048: 489 -> 363 us)
-  if (E % 16 == 0 && E > 16)
-    return launch<4, 16>(x, wg, T, H, E, K, T >= 2048 ? 16 : 4, idx, w, cnt, slot, ws, pl, st);
+  // One CTA per SM fits (255 registers): BT = the smallest multiple of 4 that
+  // covers T in one wave of num_sms() CTAs (<= 32), so no second partial wave
+  // (T = 4096: BT 16 -> 28, 256 -> 147 CTAs) and W_g is re-read by as few
+  // CTAs as possible
+  if (E % 16 == 0 && E > 16) {
+    int bt = 4 * ((T + 4 * num_sms() - 1) / (4 * num_sms()));
+    bt = bt < 4 ? 4 : (bt > 32 ? 32 : bt);
+    return launch<4, 16>(x, wg, T, H, E, K, bt, idx, w, cnt, slot, ws, pl, st);
+  }
   // E = 8 / 16: W_g staged once per CTA (TMA bulk copy) and amortised over 32
   // tokens (4 per warp); x is the only HBM stream
   // (BT shrinks for small T so that ~100+ CTAs stream x: measured with
