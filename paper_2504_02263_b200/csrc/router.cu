@@ -342,8 +342,10 @@ route_kernel(const float* __restrict__ logits, int T, int E, int K, int BT, int3
   route_tail(s_logit, t0, BT, T, E, K, idx_out, w_out, cnt_out, slot_out, ws, pl, smem_cap);
 }
 
+// Small warp tiles (TT * TE <= 16) are capped at 128 registers so two CTAs
+// share an SM (16 warps; the staged W_g of E <= 16 fits twice in smem).
 template <int TT, int TE, bool WS>
-__global__ void __launch_bounds__(kWarps * 32)
+__global__ void __launch_bounds__(kWarps * 32, (TT * TE <= 16) ? 2 : 1)
 gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
                  int T, int H, int E, int K, int BT, int32_t* __restrict__ idx_out,
                  float* __restrict__ w_out, int32_t* __restrict__ cnt_out,
