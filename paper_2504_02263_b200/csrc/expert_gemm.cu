@@ -565,6 +565,10 @@ int launch_cg(const GemmLaunch& L, cudaStream_t st) {
     attr = true;
   }
   int grid = L.grid > 0 ? L.grid : num_sms();
+  if (const char* g = getenv("MSI_GEMM_GRID")) {  // A/B: persistent grid on fewer SMs
+    const int v = atoi(g);
+    if (v >= CG && v < grid) grid = v;
+  }
   grid -= grid % CG;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
