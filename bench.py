@@ -91,6 +91,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--split", default="", help="attention+expert GPUs, e.g. 6+2 (disaggregated)")
+    ap.add_argument("--tp-e", dest="tp_e", type=int, default=1,
+                    help="expert GPUs per expert node (tensor parallel over h'; disaggregated layouts)")
     ap.add_argument("--plan", default="planner", choices=["planner", "config"],
                     help="N > 1 layout: Algorithm 1 on the calibrated B200 costs (default) or the BASELINE config splits")
     ap.add_argument("--skew", type=float, default=0.0,
@@ -426,9 +428,10 @@ def m2n_roofline(g, route, world: int, H: int, p50_us: float, disp_us: float | N
     plan = g.plan
     rows_to = torch.zeros(world, dtype=torch.int64, device=dev)
     if g.is_attention and route is not None:
-        q = (route.dest.to(torch.int64) // g.E_l).flatten()
+        node = (route.dest.to(torch.int64) // g.E_l).flatten()
         ranks = torch.tensor(plan.expert_ranks(), dtype=torch.int64, device=dev)
-        rows_to += torch.bincount(ranks[q], minlength=world)[:world]
+        for r in range(plan.tp_e):  # expert TP: every GPU of the node receives the row
+            rows_to += torch.bincount(ranks[node * plan.tp_e + r], minlength=world)[:world]
     if world > 1:
         mat = torch.stack([m.cpu() for m in allgather(rows_to)])
     else:
@@ -532,7 +535,7 @@ def main():
         # once per layer instead of m times).
         m_eff, b_a = 1, args.m * args.b_a
     args.b_a = b_a
-    plan = DeploymentPlan(n_a=n_a, n_e=n_e, m=m_eff, b_a=b_a, colocated=colo)
+    plan = DeploymentPlan(n_a=n_a, n_e=n_e, m=m_eff, b_a=b_a, colocated=colo, tp_e=1 if colo else args.tp_e)
     dev = torch.device(f"cuda:{local}")
     gen = torch.Generator(device=dev)
     gen.manual_seed(1 + rank)
@@ -582,7 +585,8 @@ def main():
             from paper_2504_02263_b200.balance import balanced_slots
             slots = balanced_slots(loads, n_e, max_replicas=min(n_e, 2))
     g = runtime.M2NGroup(model, plan, rank=rank, device=dev, slots=slots)
-    _, w13, w2 = runtime.synth_device_weights(model, runtime.local_experts(g), seed=0, device=dev)
+    _, w13, w2 = runtime.synth_device_weights(model, runtime.local_experts(g), seed=0, device=dev, tp=g.tp,
+                                              tp_rank=g.tp_rank)
     layer = runtime.MoEDecodeLayer(g, wg=wg if g.is_attention else None,
                                    w13=w13 if g.is_expert else None, w2=w2 if g.is_expert else None)
     kv_bytes = 0
@@ -811,7 +815,8 @@ def main():
     tokens = n_a * plan.m * args.b_a * args.layers * args.steps
     value = tokens / (elapsed_ms / 1e3)
     ffn_avg_s = (ffn_total_ms / max(ffn_n, 1)) / 1e3
-    flops_per_call = 6.0 * (rows_total / max(calls_total, 1)) * model.hidden * model.intermediate
+    # per expert GPU: its rows x its h'/tp_e slice of every expert
+    flops_per_call = 6.0 * (rows_total / max(calls_total, 1)) * model.hidden * model.intermediate / plan.tp_e
     achieved = flops_per_call / ffn_avg_s / 1e12 if ffn_n else None
     peak = peaks.get("bf16_tflops_sustained") or 1404.8
     # our kernels per (micro-batch, layer): attention (stand-in 1; real: rope_append +
@@ -839,7 +844,7 @@ def main():
                    "L_sim": args.layers, "attention_stage": args.attn,
                    "l2": (f"working set (expert weights {model.experts * 3 * model.hidden * model.intermediate * 2 / 1e9:.1f} GB"
                           " + KV cache) >> 126 MB L2; no flush needed"),
-                   "parallelism": f"dp{n_a}-ep{n_e}",
+                   "parallelism": f"dp{n_a}-ep{n_e}" + (f"-etp{plan.tp_e}" if plan.tp_e > 1 else ""),
                    "launch": "CUDA graph per rank (device-tracked epochs)" if args.graph else "eager"},
         "roofline": {"bound": "tensor", "kernel": "expert FFN (grouped_gemm_kernel x2: gate/up+SiLU, down+N2M)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

@@ -65,6 +65,13 @@ typedef struct {
   int32_t topk;                          /* K   (MoeModelSpec.topk)               */
   int32_t max_tokens;                    /* b_a: tokens per attention GPU per mb  */
   int32_t slots;                         /* m:   micro-batch slots (ping-pong)    */
+  int32_t tp_e;                          /* expert GPUs per expert node (tensor   */
+                                         /* parallel over h'; 0 or 1 = none).     */
+                                         /* Node j = expert indices [j tp_e,      */
+                                         /* (j+1) tp_e); every GPU of a node gets */
+                                         /* all of the node's rows and holds h'/  */
+                                         /* tp_e features of each local expert;   */
+                                         /* the combine sums the tp_e partials.   */
 } msi_plan;
 
 typedef struct msi_ctx msi_ctx;

@@ -213,6 +213,18 @@ def expert_ffn(xe: np.ndarray, w_gate: np.ndarray, w_up: np.ndarray,
     return bf16_round(y)
 
 
+def expert_ffn_tp(xe: np.ndarray, w_gate: np.ndarray, w_up: np.ndarray, w_down: np.ndarray,
+                  tp: int) -> np.ndarray:
+    """Expert tensor parallelism over h' (config.DeploymentPlan.tp_e): TP rank
+    r owns features [r h'/tp, (r+1) h'/tp) and returns the bf16 partial
+    y_r = bf16(H_r . W_down[:, F_r]^T).  xe [t,H] -> [t, tp, H]."""
+    Hp = w_gate.shape[0]
+    f = Hp // tp
+    parts = [expert_ffn(xe, w_gate[r * f:(r + 1) * f], w_up[r * f:(r + 1) * f], w_down[:, r * f:(r + 1) * f])
+             for r in range(tp)]
+    return np.stack(parts, axis=1)
+
+
 # --------------------------------------------------------------- combine --- #
 def combine(y: np.ndarray, w: np.ndarray, resid: np.ndarray | None = None) -> np.ndarray:
     """y [T,K,H] bf16, w [T,K] fp32 -> out [T,H] bf16 (optional residual)."""
@@ -238,15 +250,18 @@ class LayerResult:
 
 
 def moe_layer(xs: list, wts: LayerWeights, K: int, n_e: int, resid: bool = False,
-              rep: np.ndarray | None = None, phys2log: np.ndarray | None = None) -> LayerResult:
+              rep: np.ndarray | None = None, phys2log: np.ndarray | None = None, tp: int = 1) -> LayerResult:
     """Full MoE layer step for n_a senders (one micro-batch): route, place,
     dispatch, SwiGLU experts, combine.  With a replica table ``rep`` [E, R+1]
     and ``phys2log`` [P] the placement, counts and receive layout are per
     physical slot (``idx`` stays logical; ``LayerResult.pidx`` holds the
-    slots); every slot runs its logical expert's weights."""
+    slots); every slot runs its logical expert's weights.  ``tp`` > 1: expert
+    tensor parallelism -- n_e expert GPUs form n_e / tp nodes (the layout is
+    per node), ``y`` holds the tp partials [T, K, tp, H] and the combine sums
+    them in ascending (k, r) order."""
     E = wts.wg.shape[0]
     P = E if rep is None else len(phys2log)
-    E_l = P // n_e
+    E_l = P // (n_e // tp)
     H = wts.wg.shape[1]
     idxs, ws, slots, cnts, pidxs = [], [], [], [], []
     for s_, x in enumerate(xs):
@@ -257,7 +272,7 @@ def moe_layer(xs: list, wts: LayerWeights, K: int, n_e: int, resid: bool = False
     cnt = np.stack(cnts)
     layout = dispatch_layout(cnt, E_l)
     # gather each slot's rows in receive order, run its expert, scatter back
-    ys = [np.empty((x.shape[0], K, H), np.uint16) for x in xs]
+    ys = [np.empty((x.shape[0], K, tp, H), np.uint16) for x in xs]
     for p in range(P):
         e = p if rep is None else int(phys2log[p])
         srcs = []
@@ -268,12 +283,15 @@ def moe_layer(xs: list, wts: LayerWeights, K: int, n_e: int, resid: bool = False
         if e < 0 or not any(len(t) for _, t, _ in srcs):
             continue
         rows = np.concatenate([xs[s_][t] for s_, t, _ in srcs])
-        y = expert_ffn(rows, wts.w_gate[e], wts.w_up[e], wts.w_down[e])
+        y = expert_ffn_tp(rows, wts.w_gate[e], wts.w_up[e], wts.w_down[e], tp)
         off = 0
         for s_, t, k in srcs:
             ys[s_][t, k] = y[off:off + len(t)]
             off += len(t)
-    outs = [combine(y, w, x if resid else None) for y, w, x in zip(ys, ws, xs)]
+    outs = [combine(y.reshape(y.shape[0], K * tp, H), np.repeat(w, tp, axis=1), x if resid else None)
+            for y, w, x in zip(ys, ws, xs)]
+    if tp == 1:
+        ys = [y[:, :, 0] for y in ys]
     res = LayerResult(idxs, ws, cnt, slots, layout, ys, outs)
     res.pidx = pidxs
     return res

@@ -35,6 +35,7 @@ class Plan(ctypes.Structure):
         ("attn_ranks", ctypes.c_int32 * MAX_RANKS), ("expert_ranks", ctypes.c_int32 * MAX_RANKS),
         ("hidden", ctypes.c_int32), ("inter", ctypes.c_int32), ("experts", ctypes.c_int32),
         ("topk", ctypes.c_int32), ("max_tokens", ctypes.c_int32), ("slots", ctypes.c_int32),
+        ("tp_e", ctypes.c_int32),
     ]
 
 

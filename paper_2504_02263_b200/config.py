@@ -363,13 +363,17 @@ def save_config(bundle: ConfigBundle, path) -> None:
 class DeploymentPlan:
     """Roles of one decode deployment on a single NVSwitch box.
 
-    SPEC.md:311 vocabulary: ``tp_a``/``tp_e`` (fixed to 1 here), ``n_a``
+    SPEC.md:311 vocabulary: ``tp_a`` (fixed to 1 here), ``tp_e``, ``n_a``
     attention GPUs (data-parallel replicas), ``m`` micro-batches
     (ping-pong), ``B`` = global batch per micro-batch
-    (= n_a * b_a).  Added: ``n_e`` expert GPUs (expert e lives on expert GPU
-    e // (E / n_e), contiguous blocks) and ``b_a``.  ``colocated`` puts both
-    roles on every GPU (the 1-GPU report point, and the DeepSeek-shaped 8->8
-    case); then n_a == n_e == world size.
+    (= n_a * b_a).  Added: ``n_e`` expert GPUs and ``b_a``.  Expert GPUs form
+    n_e / tp_e expert nodes of tp_e GPUs (the paper's expert node = one expert
+    over tp_e GPUs); expert e lives on node
+    e // (E / nodes), contiguous blocks, and every GPU of the node holds h'/tp_e
+    features of each of the node's experts (tensor parallel over h'; the
+    combine sums the tp_e partial outputs).  ``colocated`` puts both roles on
+    every GPU (the 1-GPU report point, and the DeepSeek-shaped 8->8 case); then
+    n_a == n_e == world size and tp_e == 1.
     """
 
     n_a: int = 1
@@ -382,10 +386,14 @@ class DeploymentPlan:
 
     def __post_init__(self):
         _positive("plan", self, ("n_a", "n_e", "m", "b_a"))
-        if self.tp_a != 1 or self.tp_e != 1:
-            raise ConfigError("plan: only tp_a = tp_e = 1 is supported")
+        if self.tp_a != 1:
+            raise ConfigError("plan: only tp_a = 1 is supported")
+        if self.tp_e < 1 or self.n_e % self.tp_e:
+            raise ConfigError(f"plan: tp_e ({self.tp_e}) must divide n_e ({self.n_e})")
         if self.colocated and self.n_a != self.n_e:
             raise ConfigError("plan: colocated plans need n_a == n_e")
+        if self.colocated and self.tp_e != 1:
+            raise ConfigError("plan: expert TP (tp_e > 1) needs separate expert GPUs")
 
     @property
     def B(self) -> int:  # noqa: N802 - SPEC name
@@ -410,14 +418,21 @@ class DeploymentPlan:
             return "both"
         return "attention" if rank < self.n_a else "expert"
 
+    @property
+    def expert_nodes(self) -> int:
+        return self.n_e // self.tp_e
+
     def check_model(self, model: MoeModelSpec) -> None:
-        if model.experts % self.n_e:
+        if model.experts % self.expert_nodes:
             raise ConfigError(
-                f"plan: experts ({model.experts}) must divide evenly over n_e ({self.n_e})")
+                f"plan: experts ({model.experts}) must divide evenly over the {self.expert_nodes} expert nodes")
+        if model.intermediate % (128 * self.tp_e):
+            raise ConfigError(f"plan: intermediate ({model.intermediate}) must split into tp_e multiples of 128")
 
     def experts_per_gpu(self, model: MoeModelSpec) -> int:
+        """Experts whose (TP slice of the) weights every expert GPU holds."""
         self.check_model(model)
-        return model.experts // self.n_e
+        return model.experts // self.expert_nodes
 
 
 def plan_from_dict(raw: dict) -> DeploymentPlan:

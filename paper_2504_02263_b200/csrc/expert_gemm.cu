@@ -365,7 +365,8 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           rowdst = reinterpret_cast<char*>(p.out) + ((size_t)row_global * p.out_ld + (size_t)n * (BN / 2) + colofs) * 2;
         } else if (p.meta) {
           const int2 md = p.meta[row_global];
-          rowdst = p.dst[md.x] + ((size_t)md.y * p.out_ld + (size_t)n * BN + colofs) * 2;
+          const size_t drow = (size_t)md.y * (p.row_mul ? p.row_mul : 1) + p.row_add;
+          rowdst = p.dst[md.x] + (drow * p.out_ld + (size_t)n * BN + colofs) * 2;
         } else {
           rowdst = reinterpret_cast<char*>(p.out) + ((size_t)row_global * p.out_ld + (size_t)n * BN + colofs) * 2;
         }

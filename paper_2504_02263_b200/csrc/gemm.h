@@ -43,6 +43,9 @@ struct GemmParams {
   uint32_t* tile_ctr;
   // half-pair tiles load A with the 64-row box (set by the launcher)
   int a64;
+  // mode 1 destination row = meta.y * row_mul + row_add (expert TP: the
+  // partial of TP rank r of (t, k) goes to row (t*K + k)*tp + r); 0 = 1, 0
+  int row_mul, row_add;
   // completion signal (last CTA): red.release.sys +1 on each sig[i]
   uint32_t* ticket;
   uint32_t* sig[MSI_MAX_RANKS];

@@ -74,6 +74,11 @@ constexpr size_t ALIGN = 4096;
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// Expert tensor parallelism: tp GPUs form an expert node sharing its experts.
+inline int plan_tp(const msi_plan& p) { return p.tp_e > 1 ? p.tp_e : 1; }
+inline int plan_nodes(const msi_plan& p) { return p.n_e / plan_tp(p); }
+inline int plan_el(const msi_plan& p) { return p.experts / plan_nodes(p); }
+
 struct Layout {
   size_t arrive, comb, dticket, fticket, ause, euse, status, stats, trace, cntab, ctrl_bytes;
   size_t ybuf, ybuf_slot;
@@ -98,11 +103,11 @@ Layout make_layout(const msi_plan& p, bool attn, bool expert) {
   L.cntab = off; off += (size_t)p.slots * p.n_a * p.experts * 8;
   L.ctrl_bytes = align_up(off, ALIGN);
   off = L.ctrl_bytes;
-  const int E_l = p.experts / p.n_e;
+  const int E_l = plan_el(p);  // experts per expert node (tp_e GPUs share them)
   const int per_tok = p.topk < E_l ? p.topk : E_l;
   int64_t cap = (int64_t)p.n_a * p.max_tokens * per_tok + (int64_t)E_l * (MSI_ROW_ALIGN - 1);
   L.cap = (cap + 127) / 128 * 128;
-  L.ybuf_slot = (size_t)p.max_tokens * p.topk * p.hidden * 2;
+  L.ybuf_slot = (size_t)p.max_tokens * p.topk * plan_tp(p) * p.hidden * 2;  // tp_e partials per (t, k)
   L.ybuf = off;
   if (attn) off += align_up(L.ybuf_slot * p.slots, ALIGN);
   L.recv_slot = (size_t)L.cap * p.hidden * 2;
@@ -119,6 +124,7 @@ Layout make_layout(const msi_plan& p, bool attn, bool expert) {
 struct DevCtx {
   int n_a, n_e, n_world, E, K, H, Hp, E_l, slots, max_tokens;
   int my_a, my_e;
+  int tp, nodes, my_node, my_tp;  // expert TP: node = tp GPUs; this GPU's node and rank in it
   long long cap;
   uint64_t timeout_ns;
   uint64_t* cntab_of[MSI_MAX_RANKS];   // count table on every rank of the world
@@ -169,8 +175,11 @@ bool role_expert(const msi_plan& p, int r) {
 int validate(const msi_plan& p) {
   MSI_REQUIRE(p.world >= 1 && p.world <= MSI_MAX_RANKS, "plan: world must be in [1, %d]", MSI_MAX_RANKS);
   MSI_REQUIRE(p.n_a >= 1 && p.n_a <= p.world && p.n_e >= 1 && p.n_e <= p.world, "plan: bad n_a/n_e");
-  MSI_REQUIRE(p.experts >= 1 && p.experts % p.n_e == 0, "plan: experts must divide over n_e");
-  MSI_REQUIRE(p.experts / p.n_e <= MSI_MAX_LOCAL_EXPERTS, "plan: at most %d experts per GPU", MSI_MAX_LOCAL_EXPERTS);
+  MSI_REQUIRE(p.tp_e >= 0 && p.tp_e <= p.n_e && p.n_e % plan_tp(p) == 0, "plan: tp_e must divide n_e");
+  MSI_REQUIRE(p.experts >= 1 && p.experts % plan_nodes(p) == 0, "plan: experts must divide over the expert nodes");
+  MSI_REQUIRE(plan_el(p) <= MSI_MAX_LOCAL_EXPERTS, "plan: at most %d experts per GPU", MSI_MAX_LOCAL_EXPERTS);
+  MSI_REQUIRE(p.inter % (128 * plan_tp(p)) == 0, "plan: inter must split into tp_e multiples of 128");
+  MSI_REQUIRE(p.topk * plan_tp(p) <= 32, "plan: topk * tp_e <= 32");
   MSI_REQUIRE(p.topk >= 1 && p.topk <= p.experts && p.topk <= 32, "plan: bad topk");
   MSI_REQUIRE(p.hidden % 256 == 0 && p.inter % 128 == 0, "plan: hidden %% 256 and inter %% 128 required");
   MSI_REQUIRE(p.max_tokens >= 1 && p.slots >= 1 && p.slots <= 16, "plan: bad max_tokens/slots");
@@ -259,7 +268,7 @@ dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32
     s_pad[e] = (uint32_t)((total + MSI_ROW_ALIGN - 1) / MSI_ROW_ALIGN * MSI_ROW_ALIGN);
   }
   __syncthreads();
-  for (int q = tid; q < c.n_e; q += blockDim.x) {
+  for (int q = tid; q < c.nodes; q += blockDim.x) {  // per expert node (all its GPUs share the layout)
     long long run = 0;
     for (int el = 0; el < c.E_l; ++el) {
       const int e = q * c.E_l + el;
@@ -320,14 +329,17 @@ dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32
   const int per_part = (nchunk + parts - 1) / parts;
   for (int item = gwarp; item < T * parts; item += nwarps) {
     const int t = item / parts, part = item - t * parts;
-    // lane k (< K) resolves destination k
+    // lane j (< K * tp) resolves destination j: (t, k = j / tp) on GPU r = j % tp
+    // of expert node e / E_l (every GPU of a node receives the row)
     char* my_dst = nullptr;
-    if (lane < c.K) {
-      const int e = idx[(size_t)t * c.K + lane];
-      const int q = e / c.E_l;
-      const long long row = s_rowbase[e] + slot[(size_t)t * c.K + lane];
+    const int ndst = c.K * c.tp;
+    if (lane < ndst) {
+      const int k = lane / c.tp, r = lane - (lane / c.tp) * c.tp;
+      const int e = idx[(size_t)t * c.K + k];
+      const int q = (e / c.E_l) * c.tp + r;
+      const long long row = s_rowbase[e] + slot[(size_t)t * c.K + k];
       my_dst = c.recv_of[q] + ((size_t)mb * c.cap + row) * row_bytes;
-      if (part == 0) c.meta_of[q][(size_t)mb * c.cap + row] = make_int2(s, t * c.K + lane);
+      if (part == 0) c.meta_of[q][(size_t)mb * c.cap + row] = make_int2(s, t * c.K + k);
     }
     const char* src = reinterpret_cast<const char*>(x + (size_t)t * c.H) + lane * 16;
     const int j_end = min(nchunk, (part + 1) * per_part);
@@ -337,7 +349,7 @@ dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32
 #pragma unroll
       for (int u = 0; u < U; ++u)
         if (j0 + u < j_end) v[u] = ld_nc_v4(src + (size_t)(j0 + u) * 512);
-      for (int k = 0; k < c.K; ++k) {
+      for (int k = 0; k < ndst; ++k) {
         char* d = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(my_dst), k)) + lane * 16;
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -402,7 +414,7 @@ echo_kernel(const DevCtx c, int mb, uint32_t epoch) {
   const size_t tab = (size_t)mb * c.n_a * c.E;
   for (int i = tid; i < c.n_a * c.E_l; i += blockDim.x) {  // all entries in parallel
     const int s = i / c.E_l, el = i - s * c.E_l;
-    atomicAdd(&s_total[el], (int)(uint32_t)ld_relaxed_sys64(c.my_cntab + tab + (size_t)s * c.E + c.my_e * c.E_l + el));
+    atomicAdd(&s_total[el], (int)(uint32_t)ld_relaxed_sys64(c.my_cntab + tab + (size_t)s * c.E + c.my_node * c.E_l + el));
   }
   __syncthreads();
   if (tid == 0) {  // 128-aligned segment starts and the flat row prefix
@@ -428,7 +440,8 @@ echo_kernel(const DevCtx c, int mb, uint32_t epoch) {
       const long long row = s_start[el] + (i - s_first[el]);
       const int2 md = c.meta_of[c.my_e][(size_t)mb * c.cap + row];
       const char* src = c.recv_of[c.my_e] + ((size_t)mb * c.cap + row) * row_bytes + lane * 16;
-      char* dst = c.ybuf_of[md.x] + (size_t)mb * c.max_tokens * c.K * row_bytes + (size_t)md.y * row_bytes + lane * 16;
+      char* dst = c.ybuf_of[md.x] + (size_t)mb * c.max_tokens * c.K * c.tp * row_bytes +
+                  ((size_t)md.y * c.tp + c.my_tp) * row_bytes + lane * 16;
       for (int j = 0; j < nchunk; j += 8) {
         uint4 v[8];
 #pragma unroll
@@ -455,8 +468,10 @@ echo_kernel(const DevCtx c, int mb, uint32_t epoch) {
 }
 
 // ------------------------------------------------------------- combine ----
+// y rows: (t*K + k)*tp + r, r < tp the expert-TP partials of (t, k); fp32
+// fmaf over ascending (k, r) -- tp = 1 is the plain top-K combine
 __device__ __forceinline__ void combine_row8(const char* ybase, const float* w, const uint16_t* resid,
-                                             uint16_t* out, int t, int col8, int K, int H) {
+                                             uint16_t* out, int t, int col8, int K, int H, int tp) {
   float acc[8];
   if (resid) {
     uint4 r = *reinterpret_cast<const uint4*>(resid + (size_t)t * H + col8 * 8);
@@ -466,9 +481,9 @@ __device__ __forceinline__ void combine_row8(const char* ybase, const float* w, 
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
   }
-  for (int k = 0; k < K; ++k) {
-    const float wk = w[(size_t)t * K + k];
-    uint4 y = __ldcg(reinterpret_cast<const uint4*>(ybase + (((size_t)t * K + k) * H + col8 * 8) * 2));
+  for (int kr = 0; kr < K * tp; ++kr) {
+    const float wk = w[(size_t)t * K + kr / tp];
+    uint4 y = __ldcg(reinterpret_cast<const uint4*>(ybase + (((size_t)t * K * tp + kr) * H + col8 * 8) * 2));
     acc[0] = __fmaf_rn(wk, bf16lo(y.x), acc[0]); acc[1] = __fmaf_rn(wk, bf16hi(y.x), acc[1]);
     acc[2] = __fmaf_rn(wk, bf16lo(y.y), acc[2]); acc[3] = __fmaf_rn(wk, bf16hi(y.y), acc[3]);
     acc[4] = __fmaf_rn(wk, bf16lo(y.z), acc[4]); acc[5] = __fmaf_rn(wk, bf16hi(y.z), acc[5]);
@@ -481,7 +496,7 @@ __device__ __forceinline__ void combine_row8(const char* ybase, const float* w, 
 
 __global__ void __launch_bounds__(256)
 combine_kernel(const char* __restrict__ ybase, const float* __restrict__ w, const uint16_t* __restrict__ resid,
-               uint16_t* __restrict__ out, int T, int K, int H, const uint32_t* wait_ctr,
+               uint16_t* __restrict__ out, int T, int K, int H, int tp, const uint32_t* wait_ctr,
                uint32_t epoch, uint32_t mul, const uint32_t* epoch_src, uint64_t timeout_ns,
                int32_t* status, unsigned long long* trace) {
   __shared__ int s_ok;
@@ -501,7 +516,7 @@ combine_kernel(const char* __restrict__ ybase, const float* __restrict__ w, cons
   const size_t n = (size_t)T * per_row;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const int t = (int)(i / per_row), c8 = (int)(i % per_row);
-    combine_row8(ybase, w, resid, out, t, c8, K, H);
+    combine_row8(ybase, w, resid, out, t, c8, K, H, tp);
   }
   if (t0) trace_stamp(trace, 8);
 }
@@ -622,8 +637,11 @@ extern "C" int msi_ctx_finalize(msi_ctx* c) {
   DevCtx& d = c->dev;
   memset(&d, 0, sizeof(d));
   d.n_a = p.n_a; d.n_e = p.n_e; d.n_world = p.world; d.E = p.experts; d.K = p.topk;
-  d.H = p.hidden; d.Hp = p.inter; d.E_l = p.experts / p.n_e; d.slots = p.slots;
+  d.H = p.hidden; d.Hp = p.inter; d.E_l = plan_el(p); d.slots = p.slots;
   d.max_tokens = p.max_tokens; d.my_a = c->my_a; d.my_e = c->my_e;
+  d.tp = plan_tp(p); d.nodes = plan_nodes(p);
+  d.my_node = c->my_e >= 0 ? c->my_e / d.tp : -1;
+  d.my_tp = c->my_e >= 0 ? c->my_e % d.tp : 0;
   d.cap = c->my_layout.cap;
   d.timeout_ns = c->timeout_ns;
   for (int r = 0; r < p.world; ++r) {
@@ -737,7 +755,7 @@ extern "C" int msi_dispatch(msi_ctx* c, const void* x, const int32_t* cnt, const
   const size_t table = disp_table_bytes(c->plan.experts, c->plan.n_a);
   const size_t bytes = (size_t)T * c->plan.topk * c->plan.hidden * 2;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (dispatch_uses_tma()) {
+  if (dispatch_uses_tma() && plan_tp(c->plan) == 1) {
     // TMA variant: 8 warps per CTA, one token row buffer each, a warp per token
     constexpr int kThr = 256;
     const size_t smem = table + (kThr / 32) * ((size_t)c->plan.hidden * 2 + 8);
@@ -774,18 +792,19 @@ extern "C" int msi_expert_ffn(msi_ctx* c, const void* w13, const void* w2, int m
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const size_t tab = (size_t)mb_slot * p.n_a * p.experts;
 
+  const int hp_l = p.inter / d.tp;  // this GPU's slice of h' (expert TP)
   GemmLaunch g1{};
   g1.a = c->heap + L.recv + mb_slot * L.recv_slot;
   g1.a_rows = L.cap;
   g1.b = w13;
   g1.p.E_l = d.E_l;
-  g1.p.n_total = 2 * p.inter;
-  g1.p.nt = 2 * p.inter / 256;
+  g1.p.n_total = 2 * hp_l;
+  g1.p.nt = 2 * hp_l / 256;
   g1.p.kdim = p.hidden;
   g1.p.cntab = d.my_cntab + tab;
   g1.p.n_a = p.n_a;
   g1.p.E = p.experts;
-  g1.p.e0 = c->my_e * d.E_l;
+  g1.p.e0 = d.my_node * d.E_l;
   g1.p.wait_ctr = d.my_arrive + mb_slot * CTR_STRIDE;
   g1.p.epoch = epoch;  // 0: device-tracked (euse + 1)
   g1.p.epoch_src = d.my_euse + mb_slot * CTR_STRIDE;
@@ -797,7 +816,7 @@ extern "C" int msi_expert_ffn(msi_ctx* c, const void* w13, const void* w2, int m
   g1.p.trace_slot = 9;
   g1.p.mode = 0;
   g1.p.out = reinterpret_cast<__nv_bfloat16*>(c->hbuf);
-  g1.p.out_ld = p.inter;
+  g1.p.out_ld = hp_l;
   g1.p.tile_ctr = d.my_fticket + mb_slot * CTR_STRIDE + 1;  // spare words of the slot's ticket line
   int rc = grouped_gemm_launch(g1, st);
   if (rc) return rc;
@@ -809,11 +828,13 @@ extern "C" int msi_expert_ffn(msi_ctx* c, const void* w13, const void* w2, int m
   g2.p.E_l = d.E_l;
   g2.p.n_total = p.hidden;
   g2.p.nt = p.hidden / 256;
-  g2.p.kdim = p.inter;
+  g2.p.kdim = hp_l;
   g2.p.cntab = d.my_cntab + tab;
   g2.p.n_a = p.n_a;
   g2.p.E = p.experts;
-  g2.p.e0 = c->my_e * d.E_l;
+  g2.p.e0 = d.my_node * d.E_l;
+  g2.p.row_mul = d.tp;   // partial of (t, k) from TP rank r lands in row (t*K + k)*tp + r
+  g2.p.row_add = d.my_tp;
   g2.p.status = d.my_status;
   g2.p.mode = 1;
   g2.p.out_ld = p.hidden;
@@ -864,7 +885,7 @@ extern "C" int msi_combine(msi_ctx* c, void* out, const float* w, const void* re
   MSI_CUDA(launch_k(combine_kernel, dim3(grid), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream),
                     (const char*)(c->heap + L.ybuf + mb_slot * L.ybuf_slot), w,
                     reinterpret_cast<const uint16_t*>(resid), reinterpret_cast<uint16_t*>(out), T, p.topk, p.hidden,
-                    (const uint32_t*)(c->dev.my_comb + mb_slot * CTR_STRIDE), epoch, (uint32_t)p.n_e,
+                    plan_tp(p), (const uint32_t*)(c->dev.my_comb + mb_slot * CTR_STRIDE), epoch, (uint32_t)p.n_e,
                     (const uint32_t*)(c->dev.my_ause + mb_slot * CTR_STRIDE), c->timeout_ns, c->dev.my_status,
                     c->dev.trace));
   return check_launch("combine_kernel");
@@ -879,7 +900,7 @@ extern "C" int msi_combine_local(const void* y, const float* w, const void* resi
   grid = grid > 4 * num_sms() ? 4 * num_sms() : grid;
   combine_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const char*>(y), w, reinterpret_cast<const uint16_t*>(resid),
-      reinterpret_cast<uint16_t*>(out), T, K, H, nullptr, 0, 0, nullptr, 0, nullptr, nullptr);
+      reinterpret_cast<uint16_t*>(out), T, K, H, 1, nullptr, 0, 0, nullptr, 0, nullptr, nullptr);
   return check_launch("combine_kernel");
 }
 

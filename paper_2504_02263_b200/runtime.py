@@ -62,6 +62,7 @@ def make_plan_struct(model: MoeModelSpec, plan: DeploymentPlan, slots=None) -> _
     p.hidden, p.inter = model.hidden, model.intermediate
     p.experts, p.topk = (model.experts if slots is None else slots.P), model.topk
     p.max_tokens, p.slots = plan.b_a, plan.m
+    p.tp_e = plan.tp_e
     return p
 
 
@@ -114,7 +115,12 @@ class M2NGroup:
         self.is_expert = self.role in ("expert", "both")
         self.attn_index = plan.attention_ranks().index(rank) if self.is_attention else -1
         self.expert_index = plan.expert_ranks().index(rank) if self.is_expert else -1
+        if slots is not None and plan.tp_e != 1:
+            raise ValueError("replicated placements with expert TP are not supported")
         self.E_l = plan.experts_per_gpu(self.model) if slots is None else slots.P_l  # local (physical) slots
+        self.tp = plan.tp_e  # expert TP: this GPU holds h'/tp of each local expert
+        self.tp_rank = self.expert_index % plan.tp_e if self.is_expert else 0
+        self.node = self.expert_index // plan.tp_e if self.is_expert else -1
         self.P = self.model.experts if slots is None else slots.P
         ws = ctypes.c_void_p()
         nb = ctypes.c_size_t()
@@ -137,9 +143,13 @@ class M2NGroup:
         return device_view(ptr, (n // 8, 2), torch.int32, self.device)
 
     def ybuf_view(self, slot: int) -> torch.Tensor:
+        """[max_tokens, K, H] expert outputs; with expert TP [max_tokens, K, tp, H]
+        (the tp partial outputs of every (t, k), summed by the combine)."""
         ptr, n = self.buffer(_lib.BUF_YBUF, slot)
-        m = self.model
-        return device_view(ptr, (n // (2 * m.hidden * m.topk), m.topk, m.hidden), torch.bfloat16, self.device)
+        m, tp = self.model, self.plan.tp_e
+        rows = n // (2 * m.hidden * m.topk * tp)
+        shape = (rows, m.topk, m.hidden) if tp == 1 else (rows, m.topk, tp, m.hidden)
+        return device_view(ptr, shape, torch.bfloat16, self.device)
 
     def cntab_view(self, slot: int) -> torch.Tensor:
         ptr, n = self.buffer(_lib.BUF_CNTAB, slot)
@@ -476,17 +486,21 @@ class PingPongRunner:
         return out
 
 
-def synth_device_weights(model: MoeModelSpec, experts, seed: int = 0, device="cuda"):
+def synth_device_weights(model: MoeModelSpec, experts, seed: int = 0, device="cuda", tp: int = 1,
+                         tp_rank: int = 0):
     """Random-init bf16 weights on the device (SURVEY.md §8(d) scales):
     wg ~ N(0, 1/H), W_gate/W_up ~ N(0, 1/H), W_down ~ N(0, 1/H').  Returns
-    (wg [E,H], w13 [E_l,2H',H] packed, w2 [E_l,H,H'])."""
+    (wg [E,H], w13 [E_l,2H'/tp,H] packed, w2 [E_l,H,H'/tp]); with expert TP
+    the slice of features [tp_rank H'/tp, (tp_rank+1) H'/tp) of every expert."""
     H, Hp, E = model.hidden, model.intermediate, model.experts
+    Hs = Hp // tp
+    f0 = tp_rank * Hs
     gen = torch.Generator(device=device)
     gen.manual_seed(seed)
     wg = (torch.randn((E, H), generator=gen, device=device) / H ** 0.5).to(torch.bfloat16)
     experts = list(experts)
-    w13 = torch.empty((len(experts), 2 * Hp, H), dtype=torch.bfloat16, device=device)
-    w2 = torch.empty((len(experts), H, Hp), dtype=torch.bfloat16, device=device)
+    w13 = torch.empty((len(experts), 2 * Hs, H), dtype=torch.bfloat16, device=device)
+    w2 = torch.empty((len(experts), H, Hs), dtype=torch.bfloat16, device=device)
     for i, e in enumerate(experts):
         if e < 0:  # empty slot of a replicated placement: never routed to
             w13[i].zero_()
@@ -495,9 +509,9 @@ def synth_device_weights(model: MoeModelSpec, experts, seed: int = 0, device="cu
         gen.manual_seed(seed * 100003 + 1 + e)
         wgt = (torch.randn((1, Hp, H), generator=gen, device=device) / H ** 0.5).to(torch.bfloat16)
         wup = (torch.randn((1, Hp, H), generator=gen, device=device) / H ** 0.5).to(torch.bfloat16)
-        w13[i:i + 1] = ops.pack_w13(wgt, wup)
+        w13[i:i + 1] = ops.pack_w13(wgt[:, f0:f0 + Hs].contiguous(), wup[:, f0:f0 + Hs].contiguous())
         del wgt, wup
-        w2[i] = (torch.randn((H, Hp), generator=gen, device=device) / Hp ** 0.5).to(torch.bfloat16)
+        w2[i] = (torch.randn((H, Hp), generator=gen, device=device) / Hp ** 0.5).to(torch.bfloat16)[:, f0:f0 + Hs]
     return wg, w13, w2
 
 
@@ -508,7 +522,7 @@ def local_experts(group: M2NGroup) -> list:
         return []
     if group.slots is not None:
         return group.slots.logical_of_local(group.expert_index)
-    return list(range(group.expert_index * group.E_l, (group.expert_index + 1) * group.E_l))
+    return list(range(group.node * group.E_l, (group.node + 1) * group.E_l))
 
 
 def init_distributed_from_env(backend: str = "nccl"):

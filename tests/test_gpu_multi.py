@@ -26,7 +26,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, n_a, n_e, colo, shape, tokens, m, layers, outdir, slots=None):
+def _worker(rank, world, port, n_a, n_e, colo, shape, tokens, m, layers, outdir, slots=None, tp=1):
     import sys
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
@@ -39,7 +39,7 @@ def _worker(rank, world, port, n_a, n_e, colo, shape, tokens, m, layers, outdir,
     torch.cuda.set_device(gpu)
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     model = as_model_spec(shape)
-    plan = DeploymentPlan(n_a=n_a, n_e=n_e, m=m, b_a=max(tokens), colocated=colo)
+    plan = DeploymentPlan(n_a=n_a, n_e=n_e, m=m, b_a=max(tokens), colocated=colo, tp_e=tp)
     g = runtime.M2NGroup(model, plan, rank=rank, device=f"cuda:{gpu}", timeout_s=60, slots=slots)
     wts = O.synth_weights(model.hidden, model.intermediate, model.experts, seed=0)
 
@@ -49,8 +49,10 @@ def _worker(rank, world, port, n_a, n_e, colo, shape, tokens, m, layers, outdir,
     w13 = w2 = wg = None
     if g.is_expert:
         ex = [max(e, 0) for e in runtime.local_experts(g)]  # empty slots (-1) are never routed to
-        w13 = ops.pack_w13(dev(wts.w_gate[ex]), dev(wts.w_up[ex]))
-        w2 = dev(wts.w_down[ex])
+        f = model.intermediate // tp  # expert TP: this GPU's feature slice
+        fs = slice(g.tp_rank * f, (g.tp_rank + 1) * f)
+        w13 = ops.pack_w13(dev(wts.w_gate[ex][:, fs]), dev(wts.w_up[ex][:, fs]))
+        w2 = dev(wts.w_down[ex][:, :, fs])
     if g.is_attention:
         wg = dev(wts.wg)
     layer = runtime.MoEDecodeLayer(g, wg=wg, w13=w13, w2=w2)
@@ -101,12 +103,14 @@ PLANS = [
     (4, 4, True, FINE, [16, 64, 1, 40], 2, 1),      # co-located 4 -> 4, 16 experts per GPU
     (8, 8, True, "tiny", [64, 5, 64, 33, 1, 64, 50, 64], 1, 2),  # co-located 8 -> 8 (bench N=8 layout), 1 expert per GPU
     (2, 2, False, "tiny", [64, 48], 2, 1, "skew"),  # replicated hot experts (load balancing)
+    (1, 2, False, "tiny", [64], 2, 2, None, 2),     # expert TP: one node of 2 GPUs (h' split)
+    (2, 4, False, "tiny", [48, 33], 2, 1, None, 2),  # 2 attention + 2 expert nodes x 2 GPUs
 ]
 
 
-@pytest.mark.parametrize("n_a,n_e,colo,shape,tokens,m,layers,balanced",
-                         [p if len(p) == 8 else p + (None,) for p in PLANS])
-def test_m2n_multi_gpu(lib, tmp_path, n_a, n_e, colo, shape, tokens, m, layers, balanced):
+@pytest.mark.parametrize("n_a,n_e,colo,shape,tokens,m,layers,balanced,tp",
+                         [p + (None, 1)[len(p) - 7:] for p in PLANS])
+def test_m2n_multi_gpu(lib, tmp_path, n_a, n_e, colo, shape, tokens, m, layers, balanced, tp):
     import torch.multiprocessing as mp
 
     from oracle import oracle as O
@@ -123,20 +127,20 @@ def test_m2n_multi_gpu(lib, tmp_path, n_a, n_e, colo, shape, tokens, m, layers, 
         loads[0], loads[4] = 20.0, 15.0
         slots = balanced_slots(loads, n_e, max_replicas=2)
     port = _free_port()
-    mp.spawn(_worker, args=(world, port, n_a, n_e, colo, shape, tokens, m, layers, str(tmp_path), slots),
+    mp.spawn(_worker, args=(world, port, n_a, n_e, colo, shape, tokens, m, layers, str(tmp_path), slots, tp),
              nprocs=world, join=True)
     wts = O.synth_weights(model.hidden, model.intermediate, model.experts, seed=0)
     got = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(world)]
     for r in range(world):
         assert got[r]["status"][0] == 0, f"rank {r} device status {got[r]['status']}"
-    E_l = model.experts // n_e if slots is None else slots.P_l
+    E_l = model.experts // (n_e // tp) if slots is None else slots.P_l
     from _util import assert_close_bf16
     for l in range(layers):
         for j in range(m):
             xs = [O.synth_tokens(tokens[s], model.hidden, seed=1000 * l + 10 * j + s) for s in range(n_a)]
             ref = O.moe_layer(xs, wts, model.topk, n_e=n_e, resid=True,
                               rep=None if slots is None else slots.rep,
-                              phys2log=None if slots is None else slots.phys2log)
+                              phys2log=None if slots is None else slots.phys2log, tp=tp)
             for s in range(n_a):
                 a = got[s]
                 np.testing.assert_array_equal(a[f"idx_{l}_{j}"], ref.idx[s])
@@ -144,7 +148,9 @@ def test_m2n_multi_gpu(lib, tmp_path, n_a, n_e, colo, shape, tokens, m, layers, 
                 np.testing.assert_array_equal(a[f"cnt_{l}_{j}"], ref.cnt[s])
                 np.testing.assert_array_equal(a[f"slot_{l}_{j}"], ref.slot[s])
                 assert_close_bf16(a[f"y_{l}_{j}"], ref.y[s], f"expert outputs s={s} l={l} j={j}")
-                np.testing.assert_array_equal(a[f"out_{l}_{j}"], O.combine(a[f"y_{l}_{j}"], a[f"w_{l}_{j}"], xs[s]))
+                yk = a[f"y_{l}_{j}"].reshape(tokens[s], model.topk * tp, model.hidden)
+                np.testing.assert_array_equal(a[f"out_{l}_{j}"],
+                                              O.combine(yk, np.repeat(a[f"w_{l}_{j}"], tp, axis=1), xs[s]))
                 assert_close_bf16(a[f"out_{l}_{j}"], ref.out[s], f"layer output s={s}")
                 # placement: every (t, k) row landed at the oracle's row on the right GPU
                 np.testing.assert_array_equal(a[f"dest_{l}_{j}"], ref.pidx[s])
@@ -152,6 +158,7 @@ def test_m2n_multi_gpu(lib, tmp_path, n_a, n_e, colo, shape, tokens, m, layers, 
                 T = tokens[s]
                 for t in range(T):
                     for k in range(model.topk):
-                        er = got[(0 if colo else n_a) + q[t, k]]
-                        np.testing.assert_array_equal(er[f"recv_{l}_{j}"][rows[t, k]], xs[s][t])
-                        np.testing.assert_array_equal(er[f"meta_{l}_{j}"][rows[t, k]], [s, t * model.topk + k])
+                        for r in range(tp):  # every GPU of the expert node got the row
+                            er = got[(0 if colo else n_a) + q[t, k] * tp + r]
+                            np.testing.assert_array_equal(er[f"recv_{l}_{j}"][rows[t, k]], xs[s][t])
+                            np.testing.assert_array_equal(er[f"meta_{l}_{j}"][rows[t, k]], [s, t * model.topk + k])

@@ -27,3 +27,18 @@ def test_integration_stub_matches_signatures():
                [t.__name__ if hasattr(t, "__name__") else t for t in want], name
         checked += 1
     assert checked >= 7
+
+
+def test_integration_stub_plan_struct_matches_library():
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    block = text.split("## 2. ctypes binding")[1].split("```python")[1].split("```")[0]
+    start = block.index("class msi_plan(ctypes.Structure):")
+    lines = []
+    for ln in block[start:].splitlines()[1:]:
+        code = ln.split("#")[0].rstrip()
+        lines.append(code.replace("_fields_ = ", "").strip())
+        if code.endswith(")]"):
+            break
+    fields = eval(" ".join(lines), {"ctypes": ctypes})
+    assert [f[0] for f in fields] == [f[0] for f in _lib.Plan._fields_]
+    assert ctypes.sizeof(type("S", (ctypes.Structure,), {"_fields_": fields})) == ctypes.sizeof(_lib.Plan)

@@ -176,3 +176,25 @@ def test_golden_fixtures(name):
         res = O.moe_layer([x], wts, K, n_e=1, resid=True)
         np.testing.assert_array_equal(res.y[0], g["y"])
         np.testing.assert_array_equal(res.out[0], g["out"])
+
+
+def test_expert_tp_partials_sum_to_the_full_layer():
+    """Expert TP (tp = 2 nodes of 2 GPUs): the per-rank partials y_r cover
+    disjoint feature slices, their fp32 sum is the full expert output up to
+    bf16 rounding, and the layer output matches tp = 1 within the bf16
+    tolerance; routing / counts / placement are identical."""
+    from _util import assert_close_bf16
+
+    wts = O.synth_weights(512, 256, 8, seed=0)
+    xs = [O.synth_tokens(24, 512, seed=11), O.synth_tokens(17, 512, seed=12)]
+    r1 = O.moe_layer(xs, wts, 2, n_e=2)
+    r2 = O.moe_layer(xs, wts, 2, n_e=4, tp=2)
+    for s in range(2):
+        np.testing.assert_array_equal(r1.idx[s], r2.idx[s])
+        np.testing.assert_array_equal(r1.slot[s], r2.slot[s])
+        assert r2.y[s].shape == (xs[s].shape[0], 2, 2, 512)
+        ysum = O.bf16_to_f32(r2.y[s][:, :, 0]) + O.bf16_to_f32(r2.y[s][:, :, 1])
+        assert_close_bf16(O.bf16_round(ysum), r1.y[s], "tp partial sum")
+        assert_close_bf16(r2.out[s], r1.out[s], "tp layer output")
+    np.testing.assert_array_equal(r1.cnt, r2.cnt)
+    assert [len(l[0]) for l in r2.layout] == [4, 4]  # 2 nodes x E_l = 4
