@@ -35,8 +35,9 @@ SPLITS = {1: (1, 1, True), 2: (1, 1, False), 4: (3, 1, False), 8: (6, 2, False),
           3: (2, 1, False), 5: (4, 1, False), 6: (4, 2, False), 7: (5, 2, False)}
 
 
-def choose_split(world: int, shape: str, plan_arg: str, split: str = "", colocated: bool = False):
-    """(n_a, n_e, colocated, source) for this run.
+def choose_split(world: int, shape: str, plan_arg: str, split: str = "", colocated: bool = False,
+                 tp_e: int = 1):
+    """(n_a, n_e expert GPUs, colocated, source, tp_e) for this run.
 
     --split a+e / --colocated force a layout.  --plan config uses the
     BASELINE.json configuration splits (SPLITS: 1+1, 3+1, 6+2 ...).  The
@@ -50,9 +51,9 @@ def choose_split(world: int, shape: str, plan_arg: str, split: str = "", colocat
         n_a, n_e = (int(v) for v in split.split("+"))
         if n_a + n_e != world:
             raise SystemExit(f"--split {split} needs {n_a + n_e} GPUs")
-        return n_a, n_e, False, "--split"
+        return n_a, n_e, False, "--split", tp_e
     if colocated or world == 1:
-        return world, world, True, "--colocated" if colocated else "1 GPU: co-located"
+        return world, world, True, "--colocated" if colocated else "1 GPU: co-located", 1
     if plan_arg == "planner":
         import glob
         cal = None
@@ -71,9 +72,12 @@ def choose_split(world: int, shape: str, plan_arg: str, split: str = "", colocat
             p = PL.search_box(as_model_spec(shape), b200_gpu(), PL.cm_scaled_for_experts(cm, c["experts_local"]),
                               WorkloadSpec(), world)
             if p:
-                return p.n_a, p.n_e, bool(p.colocated), "planner.search_box (calibrated B200 costs, profiles/r01_calibration_8x22b.json)"
+                src = "planner.search_box (calibrated B200 costs, profiles/r01_calibration_8x22b.json)"
+                if p.tp_e > 1:  # expert nodes of tp_e GPUs
+                    src += f"; expert TP {p.tp_e}"
+                return p.n_a, p.n_e * p.tp_e, bool(p.colocated), src, p.tp_e
     n_a, n_e, colo = SPLITS[world]
-    return n_a, n_e, colo, "BASELINE.json config split"
+    return n_a, n_e, colo, "BASELINE.json config split", tp_e
 
 
 def parse():
@@ -485,7 +489,7 @@ def run_reference(args):
 
     model = as_model_spec(args.shape)
     threads = len(os.sched_getaffinity(0))
-    n_a, n_e, colo, _ = choose_split(args.gpus, args.shape, args.plan, args.split, args.colocated)
+    n_a, n_e, colo, _, _ = choose_split(args.gpus, args.shape, args.plan, args.split, args.colocated)
     # the GPU arm's micro-batch (co-located: m micro-batches merged)
     b_a = args.m * args.b_a if (colo and args.merge) else args.b_a
     vals = []
@@ -526,7 +530,8 @@ def main():
         if rank == 0:
             print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}))
         sys.exit(2)
-    n_a, n_e, colo, plan_source = choose_split(world, args.shape, args.plan, args.split, args.colocated)
+    n_a, n_e, colo, plan_source, tp_e = choose_split(world, args.shape, args.plan, args.split, args.colocated,
+                                                     args.tp_e)
     model = as_model_spec(args.shape)
     m_eff, b_a = args.m, args.b_a
     if colo and args.merge:
@@ -535,7 +540,7 @@ def main():
         # once per layer instead of m times).
         m_eff, b_a = 1, args.m * args.b_a
     args.b_a = b_a
-    plan = DeploymentPlan(n_a=n_a, n_e=n_e, m=m_eff, b_a=b_a, colocated=colo, tp_e=1 if colo else args.tp_e)
+    plan = DeploymentPlan(n_a=n_a, n_e=n_e, m=m_eff, b_a=b_a, colocated=colo, tp_e=1 if colo else tp_e)
     dev = torch.device(f"cuda:{local}")
     gen = torch.Generator(device=dev)
     gen.manual_seed(1 + rank)

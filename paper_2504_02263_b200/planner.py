@@ -10,9 +10,10 @@ Two searches share the same evaluation:
   argmax of throughput per unit cost (tpuc) with the SPEC's tie-break (fewer
   GPUs, then smaller m, then smaller tp_a).  One expert per expert node.
 * ``search_box``  -- the same objective on one 8xB200 NVSwitch box as this
-  runtime deploys it: n_a attention GPUs + n_e expert GPUs (E_l = E / n_e
-  experts each, tp = 1), or all GPUs co-located, m micro-batches, per-GPU
-  b_a.  This is what chooses ``bench.py``'s split from measured coefficients.
+  runtime deploys it: n_a attention GPUs + n_e expert nodes of tp_e GPUs
+  (E_l = E / n_e experts each, h' split tp_e ways), or all GPUs co-located,
+  m micro-batches, per-GPU b_a.  This is what chooses ``bench.py``'s layout
+  from measured coefficients.
 
 Per candidate: b_e = B K / (m E_nodes) rows per expert
 node per micro-batch, T_a = k1 b_a + k2, T_e = k3 b_e + k4, T_c = Eq. 6,
@@ -222,28 +223,34 @@ def search(model: MoeModelSpec, gpu_a: GpuSpec, gpu_e: GpuSpec, cm: PM.CostModel
 
 def search_box(model: MoeModelSpec, gpu: GpuSpec, cm_for, workload: WorkloadSpec, n_gpus: int = 8,
                max_microbatches: int = 4, balance_slack: float = 0.25, swiglu: bool = True,
-               explain: list | None = None) -> Plan | NoPlan:
-    """One B200 box: splits n_a + n_e = n_gpus (n_e | E) with m in {2..N_m},
-    or all GPUs co-located (m = 1, merged batch).  ``cm_for(E_l)`` returns
-    the cost model calibrated for E_l local experts per expert GPU (the
-    expert intercept is the weight stream of those E_l experts)."""
+               explain: list | None = None, tp_choices=(1, 2, 4)) -> Plan | NoPlan:
+    """One B200 box: n_a attention GPUs + n_e expert nodes of tp_e GPUs
+    (n_a + n_e tp_e = n_gpus, E divisible by n_e) with m in {2..N_m}, or all
+    GPUs co-located (m = 1, merged batch).  ``cm_for(E_l)`` returns the cost
+    model calibrated for E_l local experts per expert GPU (the expert
+    intercept is the weight stream of those E_l experts); with expert TP each
+    GPU streams E_l / tp_e experts' weights and does 1 / tp_e of the per-row
+    work.  The returned Plan's n_e counts expert nodes (GPUs = n_e tp_e)."""
     best, reasons = None, []
     E = model.experts
-    cands = [(n_gpus - n_e, n_e, False) for n_e in range(1, n_gpus) if E % n_e == 0]
+    cands = [(n_gpus - nodes * tp, nodes, tp, False) for tp in tp_choices for nodes in range(1, n_gpus)
+             if 0 < nodes * tp < n_gpus and E % nodes == 0 and model.intermediate % (128 * tp) == 0]
     if E % n_gpus == 0:
-        cands.append((n_gpus, n_gpus, True))
-    for n_a, n_e, colo in cands:
+        cands.append((n_gpus, n_gpus, 1, True))
+    for n_a, n_e, tp, colo in cands:
         E_l = E // n_e
-        cm = cm_for(E_l)
+        cm = cm_for(E_l / tp)
+        cm = PM.CostModel(k1=cm.k1, k2=cm.k2, k3=cm.k3 / tp, k4=cm.k4, util_curve=cm.util_curve,
+                          comm_backend=cm.comm_backend)
         for m in ([1] if colo else range(2, max_microbatches + 1)):
-            p, r = max_batch_under_slo(model, gpu, gpu, cm, workload, 1, 1, n_a, n_e, m,
+            p, r = max_batch_under_slo(model, gpu, gpu, cm, workload, 1, tp, n_a, n_e, m,
                                        balance_slack=balance_slack, colocated=colo, swiglu=swiglu,
                                        expert_nodes_hold=E_l)
             if explain is not None:
-                explain.append({"n_a": n_a, "n_e": n_e, "colocated": colo, "m": m,
+                explain.append({"n_a": n_a, "n_e": n_e, "tp_e": tp, "colocated": colo, "m": m,
                                 "tpuc": p.tpuc if p else None, "B": p.B if p else None, "reason": r})
             if p is None:
-                reasons.append(((n_a, n_e, m), r))
+                reasons.append(((n_a, n_e, tp, m), r))
             elif _better(p, best):
                 best = p
     return best if best is not None else NoPlan(reasons)

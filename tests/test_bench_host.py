@@ -7,7 +7,8 @@ import bench
 def test_choose_split_planner_picks_colocation_for_8x22b():
     assert bench.choose_split(1, "mixtral-8x22b", "planner")[:3] == (1, 1, True)
     for n in (2, 4, 8):
-        n_a, n_e, colo, src = bench.choose_split(n, "mixtral-8x22b", "planner")
+        n_a, n_e, colo, src, tp = bench.choose_split(n, "mixtral-8x22b", "planner")
+        assert tp == 1
         assert (n_a, n_e, colo) == (n, n, True)
         assert src.startswith("planner.search_box")
 
@@ -16,6 +17,7 @@ def test_choose_split_config_and_overrides():
     assert bench.choose_split(8, "mixtral-8x22b", "config")[:3] == (6, 2, False)
     assert bench.choose_split(4, "mixtral-8x22b", "config")[:3] == (3, 1, False)
     assert bench.choose_split(4, "mixtral-8x22b", "planner", split="2+2")[:3] == (2, 2, False)
+    assert bench.choose_split(4, "mixtral-8x22b", "planner", split="2+2", tp_e=2)[4] == 2
     assert bench.choose_split(4, "dbrx", "planner", colocated=True)[:3] == (4, 4, True)
     # no calibration for this shape: the BASELINE config split
     assert bench.choose_split(4, "dbrx", "planner")[3] == "BASELINE.json config split"

@@ -115,3 +115,4 @@ def test_search_box_b200():
     assert p and p.gpus == 8 and p.T_iter_upper <= 0.150
     assert len(table) >= 4
     assert any(r["colocated"] for r in table)
+    assert any(r["tp_e"] == 2 and not r["colocated"] for r in table)  # expert-TP layouts are candidates
