@@ -227,11 +227,11 @@ class MoEDecodeLayer:
                 raise ValueError("attention ranks need wg [E, H]")
         if group.is_expert and (w13 is not None or w2 is not None):
             # (weights may be omitted on an expert rank that only runs expert_echo)
-            E_l = group.E_l
-            if w13 is None or tuple(w13.shape) != (E_l, 2 * m.intermediate, m.hidden):
-                raise ValueError(f"expert ranks need w13 [{E_l}, {2 * m.intermediate}, {m.hidden}]")
-            if w2 is None or tuple(w2.shape) != (E_l, m.hidden, m.intermediate):
-                raise ValueError(f"expert ranks need w2 [{E_l}, {m.hidden}, {m.intermediate}]")
+            E_l, hs = group.E_l, m.intermediate // group.tp  # expert TP: this GPU's h' slice
+            if w13 is None or tuple(w13.shape) != (E_l, 2 * hs, m.hidden):
+                raise ValueError(f"expert ranks need w13 [{E_l}, {2 * hs}, {m.hidden}]")
+            if w2 is None or tuple(w2.shape) != (E_l, m.hidden, hs):
+                raise ValueError(f"expert ranks need w2 [{E_l}, {m.hidden}, {hs}]")
         self.wg, self.w13, self.w2 = wg, w13, w2
         # epochs: 0 = "next use of the slot" counted on the device (default;
         # required inside CUDA graphs, whose replays the host cannot count).
