@@ -35,6 +35,16 @@ SPLITS = {1: (1, 1, True), 2: (1, 1, False), 4: (3, 1, False), 8: (6, 2, False),
           3: (2, 1, False), 5: (4, 1, False), 6: (4, 2, False), 7: (5, 2, False)}
 
 
+def apply_plan_json(args):
+    """--plan-json: the planner's DeploymentPlan (and model) replace the layout,
+    m and b_a arguments; returns the fixed (n_a, n_e, colocated, source, tp_e)."""
+    from paper_2504_02263_b200.config import load_plan
+    bundle, plan = load_plan(args.plan_json)
+    args.shape = bundle.model
+    args.m, args.b_a = plan.m, plan.b_a
+    return plan.n_a, plan.n_e, plan.colocated, f"--plan-json {os.path.basename(args.plan_json)}", plan.tp_e
+
+
 def choose_split(world: int, shape: str, plan_arg: str, split: str = "", colocated: bool = False,
                  tp_e: int = 1):
     """(n_a, n_e expert GPUs, colocated, source, tp_e) for this run.
@@ -97,6 +107,8 @@ def parse():
     ap.add_argument("--split", default="", help="attention+expert GPUs, e.g. 6+2 (disaggregated)")
     ap.add_argument("--tp-e", dest="tp_e", type=int, default=1,
                     help="expert GPUs per expert node (tensor parallel over h'; disaggregated layouts)")
+    ap.add_argument("--plan-json", default="", help="a planner output (python -m paper_2504_02263_b200.planner "
+                    "--out ...): model, layout, m and b_a from its plan section")
     ap.add_argument("--plan", default="planner", choices=["planner", "config"],
                     help="N > 1 layout: Algorithm 1 on the calibrated B200 costs (default) or the BASELINE config splits")
     ap.add_argument("--skew", type=float, default=0.0,
@@ -487,9 +499,10 @@ def run_reference(args):
     from paper_2504_02263_b200.config import as_model_spec
     import numpy as np  # noqa: F401
 
+    n_a, n_e, colo, _, _ = (apply_plan_json(args) if args.plan_json else
+                            choose_split(args.gpus, args.shape, args.plan, args.split, args.colocated))
     model = as_model_spec(args.shape)
     threads = len(os.sched_getaffinity(0))
-    n_a, n_e, colo, _, _ = choose_split(args.gpus, args.shape, args.plan, args.split, args.colocated)
     # the GPU arm's micro-batch (co-located: m micro-batches merged)
     b_a = args.m * args.b_a if (colo and args.merge) else args.b_a
     vals = []
@@ -530,8 +543,13 @@ def main():
         if rank == 0:
             print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}))
         sys.exit(2)
-    n_a, n_e, colo, plan_source, tp_e = choose_split(world, args.shape, args.plan, args.split, args.colocated,
-                                                     args.tp_e)
+    if args.plan_json:
+        n_a, n_e, colo, plan_source, tp_e = apply_plan_json(args)
+        if (n_a if colo else n_a + n_e) != world:
+            raise SystemExit(f"--plan-json needs {n_a if colo else n_a + n_e} ranks, WORLD_SIZE={world}")
+    else:
+        n_a, n_e, colo, plan_source, tp_e = choose_split(world, args.shape, args.plan, args.split,
+                                                         args.colocated, args.tp_e)
     model = as_model_spec(args.shape)
     m_eff, b_a = args.m, args.b_a
     if colo and args.merge:

@@ -444,8 +444,23 @@ def load_plan(path) -> tuple[ConfigBundle, DeploymentPlan]:
     doc = _read_json(Path(path))
     if not isinstance(doc, dict):
         raise ConfigError("config: top level must be a JSON object")
-    _check_keys(doc, _TOP_KEYS + ("plan",), "config")
+    _check_keys(doc, _TOP_KEYS + ("plan", "plan_info"), "config")
     plan = plan_from_dict(doc.get("plan", {}))
-    bundle = _bundle({k: v for k, v in doc.items() if k != "plan"})
+    bundle = _bundle({k: v for k, v in doc.items() if k not in ("plan", "plan_info")})
     plan.check_model(bundle.model)
     return bundle, plan
+
+
+def save_plan(bundle: ConfigBundle, plan: DeploymentPlan, path, extra: dict | None = None) -> None:
+    """Write a config file with the additive ``plan`` section (the planner's
+    output, read back by ``load_plan``).  ``extra`` keys (e.g. the planner's
+    predicted times) go under ``plan_info``, which ``load_plan`` ignores."""
+    plan.check_model(bundle.model)
+    doc = config_to_dict(bundle)
+    doc["plan"] = asdict(plan)
+    text = json.dumps(doc, indent=2) + "\n"
+    if extra:
+        doc2 = dict(doc)
+        doc2["plan_info"] = extra
+        text = json.dumps(doc2, indent=2, default=float) + "\n"
+    Path(path).write_text(text)

@@ -267,3 +267,61 @@ def cm_scaled_for_experts(cm: PM.CostModel, e_l_calibrated: int):
                             util_curve=cm.util_curve, comm_backend=cm.comm_backend)
 
     return f
+
+
+def to_deployment(p: Plan, b_a: int | None = None):
+    """A ``search_box`` result as the runtime's ``config.DeploymentPlan``
+    (expert GPUs = nodes x tp_e; b_a defaults to the plan's per-GPU batch)."""
+    from .config import DeploymentPlan
+
+    if not p:
+        raise ConfigError("to_deployment: empty search result")
+    ba = int(b_a if b_a is not None else max(1, round(p.b_a)))
+    if p.colocated:
+        return DeploymentPlan(n_a=p.n_a, n_e=p.n_a, m=p.m, b_a=ba, colocated=True)
+    return DeploymentPlan(n_a=p.n_a, n_e=p.n_e * p.tp_e, m=p.m, b_a=ba, tp_e=p.tp_e)
+
+
+def main(argv=None) -> int:
+    """Plan JSON output: run Algorithm 1 on one B200 box with calibrated
+    coefficients and write the config + ``plan`` section that ``load_plan`` /
+    ``bench.py --plan-json`` read.
+
+      python -m paper_2504_02263_b200.planner --model mixtral-8x22b \
+          --calibration profiles/r01_calibration_8x22b.json --gpus 8 --out plan.json
+    """
+    import argparse
+    import json
+
+    from .config import Catalog, ConfigBundle, SearchLimits, as_model_spec, b200_gpu, load_config, save_plan
+
+    ap = argparse.ArgumentParser(description=main.__doc__)
+    ap.add_argument("--config", help="config JSON (model/workload/limits); default: builtin model")
+    ap.add_argument("--model", default="mixtral-8x22b")
+    ap.add_argument("--calibration", required=True, help="calibrate.py JSON (k1..k4, util table)")
+    ap.add_argument("--gpus", type=int, default=8)
+    ap.add_argument("--b-a", dest="b_a", type=int, default=None, help="per-GPU micro-batch (default: the plan's)")
+    ap.add_argument("--out", required=True)
+    a = ap.parse_args(argv)
+    if a.config:
+        bundle = load_config(a.config)
+    else:
+        gpu = b200_gpu()
+        bundle = ConfigBundle(Catalog([gpu]), as_model_spec(a.model), WorkloadSpec(), SearchLimits())
+    with open(a.calibration) as fh:
+        c = json.load(fh)
+    cm = PM.CostModel(k1=c["k1_s_per_tok"], k2=c["k2_s"], k3=c["k3_s_per_tok"], k4=c["k4_s"],
+                      util_curve=PM.UtilCurve.from_points(c["util_table"]))
+    p = search_box(bundle.model, b200_gpu(), cm_scaled_for_experts(cm, c["experts_local"]), bundle.workload,
+                   a.gpus)
+    if not p:
+        print(json.dumps({"error": "no feasible plan", "reasons": [list(map(str, r)) for r in p.reasons][:20]}))
+        return 1
+    dp = to_deployment(p, a.b_a)
+    save_plan(bundle, dp, a.out, extra=p.to_dict())
+    print(json.dumps({"plan": dp.__dict__, "tpuc": p.tpuc, "T_iter_upper": p.T_iter_upper, "out": a.out}))
+    return 0
+
+
+if __name__ == "__main__":
+    raise SystemExit(main())

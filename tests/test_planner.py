@@ -116,3 +116,29 @@ def test_search_box_b200():
     assert len(table) >= 4
     assert any(r["colocated"] for r in table)
     assert any(r["tp_e"] == 2 and not r["colocated"] for r in table)  # expert-TP layouts are candidates
+
+
+def test_plan_json_round_trip(tmp_path):
+    """Plan JSON output: the planner CLI writes the
+    config + plan section, load_plan reads back the same DeploymentPlan, and
+    bench.py's --plan-json takes its layout from it."""
+    import argparse
+    import json
+    import os
+
+    import bench
+    from paper_2504_02263_b200.config import load_plan
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / "plan.json"
+    rc = PL.main(["--calibration", os.path.join(root, "profiles", "r01_calibration_8x22b.json"),
+                  "--gpus", "4", "--b-a", "1024", "--out", str(out)])
+    assert rc == 0
+    bundle, plan = load_plan(out)
+    assert (plan.n_a, plan.n_e, plan.colocated, plan.b_a) == (4, 4, True, 1024)
+    assert bundle.model.name == MIXTRAL.name
+    assert "tpuc" in json.loads(out.read_text())["plan_info"]
+    args = argparse.Namespace(plan_json=str(out), shape="tiny", m=3, b_a=64)
+    n_a, n_e, colo, src, tp = bench.apply_plan_json(args)
+    assert (n_a, n_e, colo, tp, args.m, args.b_a) == (4, 4, True, 1, 1, 1024)
+    assert args.shape.name == MIXTRAL.name and src.startswith("--plan-json")
