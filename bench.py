@@ -875,6 +875,8 @@ def main():
                      "traffic": traffic.get("ffn_pair") if traffic else None,
                      "traffic_source": "profiles/r01_ncu_traffic.json (ncu --set full, dram read+write per launch pair)"
                      if traffic else None,
+                     "frac_burst": (achieved / (peaks.get("bf16_tflops") or 1677.4)) if achieved else None,
+                     "frac_nominal_dense": (achieved / 2250.0) if achieved else None,
                      "flops_per_launch_pair": flops_per_call, "avg_launch_pair_ms": ffn_avg_s * 1e3,
                      "peak_kind": "measured bf16_tflops_sustained (MEASURED_PEAKS.json)"},
         "e2e": e2e,
