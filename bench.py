@@ -370,15 +370,44 @@ def m2n_latency(layer, g, x, world: int, iters: int = 1000, warm: int = 50) -> d
     tl = t.cpu().tolist()
     v = sorted(tl[:len(lat)])
     dv = sorted(tl[len(lat):])
+    # steady state: CHAIN round trips back to back in one graph (a decode
+    # loop's layers), so the per-iteration host-barrier skew is paid once per
+    # CHAIN; per-trip time = replay time / CHAIN, max over ranks, p50
+    CHAIN, reps = 16, 64
+    grc = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(grc, stream=side):
+        for _ in range(CHAIN):
+            trip()
+    torch.cuda.synchronize()
+    chain = []
+    for i in range(reps + 4):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        grc.replay()
+        e.record()
+        torch.cuda.synchronize()
+        if i >= 4:
+            chain.append(s.elapsed_time(e) * 1e3 / CHAIN if g.is_attention else 0.0)
+    tc = torch.tensor(chain, dtype=torch.float64, device=torch.device("cuda", torch.cuda.current_device()))
+    if world > 1:
+        allreduce_(tc, dist.ReduceOp.MAX)
+    cv = sorted(tc.cpu().tolist())
     if g.status() != 0:
         raise RuntimeError("device status after the M2N round trips")
     T, H, K = (x.shape[0], x.shape[1], g.model.topk) if x is not None else (0, 0, 0)
     p50 = v[len(v) // 2]
+    c50 = cv[len(cv) // 2]
     return {"p50_us": p50, "p99_us": v[min(len(v) - 1, int(0.99 * len(v)))], "iters": iters,
             "dispatch_leg_p50_us": dv[len(dv) // 2],
             "tokens_per_attention_gpu": T, "dispatch_bytes_per_attention_gpu": T * K * H * 2,
             "how": "graph replay of dispatch -> expert echo -> combine, barrier each, max over ranks",
-            "roofline": m2n_roofline(g, route, world, g.model.hidden, p50, dv[len(dv) // 2])}
+            "roofline": m2n_roofline(g, route, world, g.model.hidden, p50, dv[len(dv) // 2]),
+            "steady_state": {"per_trip_p50_us": c50, "chain": CHAIN, "replays": reps,
+                             "roofline": m2n_roofline(g, route, world, g.model.hidden, c50),
+                             "how": f"{CHAIN} round trips back to back per graph replay, per-trip p50, max over ranks"}}
 
 
 SM_STORE_GBS = 689.0  # measured ceiling of SM peer stores per direction, bidirectional (see m2n_roofline)
