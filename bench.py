@@ -667,6 +667,7 @@ def main():
         ffn_events.append((s, e))
         return r
 
+    barrier()  # every rank set up (weights, KV cache) before the first cross-GPU wait
     for _ in range(args.warmup):
         runner.run(xs)
     torch.cuda.synchronize()
