@@ -28,6 +28,7 @@ run() {  # tag ngpus args...
   echo "$tag $* rc=$rc"
 }
 for ba in 64 128 256 512 1024; do run cfg3_n1 1 --b-a $ba; done
-for ba in 64 128 256 512 1024; do run cfg3_3+1 4 --b-a $ba; done
+for ba in 64 128 256 512 1024; do run cfg3_3+1 4 --split 3+1 --b-a $ba; done
+for ba in 64 256 1024; do run cfg3_colo4 4 --b-a $ba; done
 for ba in 64 128 256 512 1024; do run cfg2_2+2 4 --shape mixtral-8x7b --split 2+2 --micro-batches 2 --b-a $ba; done
 for ba in 128 256 512 1024 2048 4096; do run cfg5_colo4 4 --shape deepseek-v3 --colocated --micro-batches 1 --b-a $ba; done
