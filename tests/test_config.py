@@ -109,3 +109,25 @@ def test_matches_reference_moeplan():
         with pytest.raises(ValueError) as e2:
             C.config_from_dict(bad)
         assert str(e1.value) == str(e2.value)
+
+
+def test_plan_expert_tp_validation():
+    """Expert TP (tp_e): nodes of tp_e expert GPUs share their experts; tp_e
+    must divide n_e, experts divide over the nodes, h' split in 128s, and
+    co-located plans keep tp_e = 1."""
+    m = C.as_model_spec("mixtral-8x22b")
+    p = C.DeploymentPlan(n_a=2, n_e=4, tp_e=2)
+    assert p.expert_nodes == 2 and p.experts_per_gpu(m) == 4 and p.world == 6
+    assert p.expert_ranks() == [2, 3, 4, 5]
+    with pytest.raises(C.ConfigError, match="tp_e"):
+        C.DeploymentPlan(n_a=2, n_e=3, tp_e=2)
+    with pytest.raises(C.ConfigError, match="expert TP"):
+        C.DeploymentPlan(n_a=2, n_e=2, tp_e=2, colocated=True)
+    with pytest.raises(C.ConfigError, match="tp_a"):
+        C.DeploymentPlan(n_a=2, n_e=2, tp_a=2)
+    with pytest.raises(C.ConfigError, match="divide evenly"):
+        C.DeploymentPlan(n_a=1, n_e=6, tp_e=2).check_model(m)  # 3 nodes for 8 experts
+    tiny = C.as_model_spec("tiny")  # h' = 1536 = 12 x 128: tp 4 -> 384 = 3 x 128
+    C.DeploymentPlan(n_a=1, n_e=4, tp_e=4).check_model(tiny)
+    with pytest.raises(C.ConfigError, match="intermediate"):
+        C.DeploymentPlan(n_a=1, n_e=8, tp_e=8).check_model(tiny)  # 192 not a multiple of 128
