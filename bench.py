@@ -877,7 +877,9 @@ def main():
     attn_launches = (1 if kv_bytes else 0)
     if att_stages:
         attn_launches = 2 + (1 if att_stages[0].ws is not None else 0)
-    launches_per_mbl = attn_launches + 1 + 1 + 3 + 1  # expert: wait + 2 GEMMs
+    # router: one fused kernel, or logits + route kernels (E >= 64 at T <= 256)
+    router_launches = 2 if (model.experts >= 64 and model.experts % 8 == 0 and args.b_a <= 256) else 1
+    launches_per_mbl = attn_launches + router_launches + 1 + 3 + 1  # expert: wait + 2 GEMMs
     line = {
         "metric": "decode tokens/s/GPU (MoE layer, ping-pong); M2N dispatch+combine p50 µs",
         "value": value, "unit": "layer-tokens/s", "value_per_gpu": value / world,
@@ -924,7 +926,7 @@ def main():
     # our kernels inside the timed region (per rank, summed over roles)
     per_step = plan.m * args.layers * (launches_per_mbl * world if colo else 0)
     if not colo:
-        per_step = plan.m * args.layers * (n_a * (attn_launches + 3) + n_e * 3)
+        per_step = plan.m * args.layers * (n_a * (attn_launches + router_launches + 2) + n_e * 3)
     line["gpu_launches"] = per_step * args.steps
     if not args.no_cpu and world == 1:  # the CPU baseline is timed at N = 1 only
         threads = len(os.sched_getaffinity(0))
