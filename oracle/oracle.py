@@ -17,6 +17,9 @@ oracle restates the paper's semantics with the build's precision contract:
 * expert   PAPER.md:285-286 (FFN in/out GEMMs) + SwiGLU per BASELINE
            north_star -> ``expert_ffn`` (fp32 accumulate; bf16 rounding at
            X, H, Y; tolerance-checked)
+* expert TP (tp_e GPUs per expert node) ->
+           ``expert_ffn_tp`` (per-rank h' slices, bf16 partials) and
+           ``moe_layer(tp=)`` (the combine sums the partials, ascending (k, r))
 * combine  PAPER.md:83, 97 -> ``combine`` (fp32 fmaf, ascending k; bit-exact
            given identical expert outputs)
 * pipeline SPEC.md:237-272 -> paper_2504_02263_b200.pipeline (closed forms)
