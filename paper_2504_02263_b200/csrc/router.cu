@@ -45,7 +45,16 @@ struct Placement {
   const int32_t* rep;
   int R, P, sender;
   int32_t* pidx;  // [T,K] physical slot per (t,k) (may alias idx when rep == nullptr)
+  int prof;       // MSI_ROUTER_PROF=1: %globaltimer phase stamps into ws[2..8] (diagnostics)
 };
+
+__device__ __forceinline__ void rprof(const Placement& pl, int32_t* ws, int i) {
+  if (pl.prof) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    ws[i] = (int32_t)(uint32_t)t;
+  }
+}
 
 // Phases 2-4 (shared by both logit kernels): s_logit [BT][E] holds this CTA's
 // logits; produces idx, w (and pidx), in-CTA ranks, and -- in the last CTA --
@@ -56,6 +65,7 @@ __device__ __forceinline__ void route_tail(float* s_logit, int t0, int BT, int T
                                            int32_t* __restrict__ ws, const Placement& pl, size_t smem_cap) {
   __shared__ int s_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (blockIdx.x == 0 && threadIdx.x == 0) rprof(pl, ws, 3);
   // ---- 2. top-K + weights (one warp per token) ----------------------------
   for (int lt = warp; lt < BT; lt += kWarps) {
     const int t = t0 + lt;
@@ -101,6 +111,7 @@ __device__ __forceinline__ void route_tail(float* s_logit, int t0, int BT, int T
   }
   __syncthreads();
 
+  if (blockIdx.x == 0 && threadIdx.x == 0) rprof(pl, ws, 4);
   // ---- 3. in-CTA ranks (BT <= 32 tokens = one warp chunk): lane = token,
   //      bit `lane` of mask[p] says "this token chose physical slot p", so the
   //      rank of (t,k) among the CTA's earlier tokens is popc(mask[p] & lanes_below)
@@ -130,10 +141,12 @@ __device__ __forceinline__ void route_tail(float* s_logit, int t0, int BT, int T
   //      adds them to every slot; its totals are this sender's counts --------
   __threadfence();
   __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) rprof(pl, ws, 5);
   if (threadIdx.x == 0) s_last = (atomicAdd(&ws[0], 1) == (int)gridDim.x - 1);
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  if (threadIdx.x == 0) rprof(pl, ws, 6);
   // The last CTA runs alone, so its L2 round trips must overlap: every
   // histogram entry is loaded at once into shared memory (the logits area is
   // free), each warp scans whole experts across CTAs there, and the slot
@@ -206,6 +219,7 @@ __device__ __forceinline__ void route_tail(float* s_logit, int t0, int BT, int T
     __threadfence_block();
     __syncthreads();
   }
+  if (threadIdx.x == 0) rprof(pl, ws, 7);
   const int32_t* bsrc = in_smem ? s_hist : base;
   const int TK = T * K, stride = blockDim.x;
   constexpr int V = 16;
@@ -223,6 +237,8 @@ __device__ __forceinline__ void route_tail(float* s_logit, int t0, int BT, int T
       if (i < TK) slot_out[i] = sl[u] + bsrc[(size_t)((i / K) / BT) * P + ex[u]];
     }
   }
+  __syncthreads();
+  if (threadIdx.x == 0) rprof(pl, ws, 8);
   if (threadIdx.x == 0) ws[0] = 0;  // ticket ready for the next launch
 }
 
@@ -357,6 +373,7 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
   const int t0 = blockIdx.x * BT;
   pdl_trigger();
   pdl_wait();
+  if (blockIdx.x == 0 && threadIdx.x == 0) rprof(pl, ws, 1);
   if (WS) {  // stage W_g (E*H*2 bytes) with one TMA bulk copy
     __shared__ __align__(8) uint64_t s_bar;
     char* dst = reinterpret_cast<char*>(s_logit) + ((logit_smem_bytes(BT, E) + 15) & ~size_t(15));
@@ -371,6 +388,7 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
     mbar_wait(&s_bar, 0);
     wg = reinterpret_cast<const __nv_bfloat16*>(dst);
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) rprof(pl, ws, 2);
 
   // ---- 1. logits ---------------------------------------------------------
   const int tgroups = BT / TT, egroups = E / TE;
@@ -477,7 +495,8 @@ int gate_topk(const void* x, const void* wg, int T, int H, int E, int K, int32_t
   MSI_REQUIRE((x || T == 0) && wg && (T == 0 || (idx && w && slot)) && cnt && ws, "gate_topk: null pointer");
   MSI_REQUIRE(!rep || (R >= 1 && P >= E && P <= 4096 && pidx && sender >= 0),
               "gate_topk: replica table needs R >= 1, E <= P <= 4096, pidx and sender >= 0");
-  const Placement pl{rep, R, rep ? P : E, sender, rep ? pidx : idx};
+  const char* pe = getenv("MSI_ROUTER_PROF");
+  const Placement pl{rep, R, rep ? P : E, sender, rep ? pidx : idx, (pe && pe[0] == '1') ? 1 : 0};
   if (T == 0) {
     MSI_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * pl.P, st));
     return 0;
