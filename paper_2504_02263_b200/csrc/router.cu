@@ -56,6 +56,26 @@ __device__ __forceinline__ void rprof(const Placement& pl, int32_t* ws, int i) {
   }
 }
 
+// All CTA histograms into shared memory with 16 independent L2 loads in
+// flight per thread (one at a time was a serial chain of L2 round trips:
+// ~30 us for 147 x 256 entries).
+__device__ __forceinline__ void load_hist(int32_t* s_hist, const int32_t* hist, size_t nh) {
+  constexpr int U = 16;
+  for (size_t i0 = threadIdx.x; i0 < nh; i0 += (size_t)blockDim.x * U) {
+    int32_t v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const size_t i = i0 + (size_t)u * blockDim.x;
+      v[u] = i < nh ? __ldcg(&hist[i]) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const size_t i = i0 + (size_t)u * blockDim.x;
+      if (i < nh) s_hist[i] = v[u];
+    }
+  }
+}
+
 // Phases 2-4 (shared by both logit kernels): s_logit [BT][E] holds this CTA's
 // logits; produces idx, w (and pidx), in-CTA ranks, and -- in the last CTA --
 // the counts and final slots.
@@ -155,8 +175,24 @@ __device__ __forceinline__ void route_tail(float* s_logit, int t0, int BT, int T
   const size_t nh = (size_t)nblk * P;
   int32_t* s_hist = reinterpret_cast<int32_t*>(s_logit);  // [nblk][P] -> exclusive bases in place
   const bool in_smem = nh * sizeof(int32_t) <= smem_cap;
-  if (in_smem) {
-    for (size_t i = threadIdx.x; i < nh; i += blockDim.x) s_hist[i] = __ldcg(&hist[i]);
+  if (in_smem && P >= 64 && P <= (int)blockDim.x) {
+    // many experts: one thread per expert walks the CTAs in shared memory
+    // (the warp-per-expert shuffle scan below costs ~80 us at P = 256)
+    load_hist(s_hist, hist, nh);
+    __syncthreads();
+    const int e = threadIdx.x;
+    if (e < P) {
+      int carry = 0;
+      for (int b = 0; b < nblk; ++b) {
+        const int v = s_hist[(size_t)b * P + e];
+        s_hist[(size_t)b * P + e] = carry;
+        carry += v;
+      }
+      cnt_out[e] = carry;
+    }
+    __syncthreads();
+  } else if (in_smem) {
+    load_hist(s_hist, hist, nh);
     __syncthreads();
     for (int e = warp; e < P; e += kWarps) {  // warp-wide exclusive scan over CTAs
       int carry = 0;
@@ -222,8 +258,41 @@ __device__ __forceinline__ void route_tail(float* s_logit, int t0, int BT, int T
   if (threadIdx.x == 0) rprof(pl, ws, 7);
   const int32_t* bsrc = in_smem ? s_hist : base;
   const int TK = T * K, stride = blockDim.x;
+  int done = 0;
+  if ((((uintptr_t)pidx | (uintptr_t)slot_out) & 15) == 0) {
+    // 16-B vectors: 4 (t, k) entries per load, 8 vectors in flight per thread
+    // (the single last CTA is latency-bound here: E = 256, T = 4096 took 38 us
+    // with scalar loads)
+    constexpr int V4 = 8;
+    const int n4 = TK / 4;
+    const int4* p4 = reinterpret_cast<const int4*>(pidx);
+    int4* s4 = reinterpret_cast<int4*>(slot_out);
+    for (int j0 = threadIdx.x; j0 < n4; j0 += stride * V4) {
+      int4 ex[V4], sl[V4];
+#pragma unroll
+      for (int u = 0; u < V4; ++u) {
+        const int j = j0 + u * stride;
+        ex[u] = j < n4 ? __ldcg(p4 + j) : make_int4(0, 0, 0, 0);
+        sl[u] = j < n4 ? __ldcg(s4 + j) : make_int4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < V4; ++u) {
+        const int j = j0 + u * stride;
+        if (j < n4) {
+          const int i = 4 * j;
+          int4 o;
+          o.x = sl[u].x + bsrc[(size_t)(((i + 0) / K) / BT) * P + ex[u].x];
+          o.y = sl[u].y + bsrc[(size_t)(((i + 1) / K) / BT) * P + ex[u].y];
+          o.z = sl[u].z + bsrc[(size_t)(((i + 2) / K) / BT) * P + ex[u].z];
+          o.w = sl[u].w + bsrc[(size_t)(((i + 3) / K) / BT) * P + ex[u].w];
+          s4[j] = o;
+        }
+      }
+    }
+    done = n4 * 4;
+  }
   constexpr int V = 16;
-  for (int i0 = threadIdx.x; i0 < TK; i0 += stride * V) {
+  for (int i0 = done + threadIdx.x; i0 < TK; i0 += stride * V) {
     int ex[V], sl[V];
 #pragma unroll
     for (int u = 0; u < V; ++u) {
@@ -417,6 +486,11 @@ int launch(const void* x, const void* wg, int T, int H, int E, int K, int BT, in
   const bool stage = E <= 16 && wbytes <= kMaxStagedW;  // (unstaged measured 10-50 % slower)
   size_t head = logit_smem_bytes(BT, E);
   if (head < (size_t)pl.P * 4) head = (size_t)pl.P * 4;  // the [P] slot masks reuse this space
+  // Wide tiles run one CTA per SM anyway (registers): give the last CTA room
+  // to scan all [nblk][P] histograms in shared memory at once (E = 256,
+  // T = 4096: the chunked scan took 40 us of the 568 us kernel)
+  const size_t nh_bytes = (size_t)nblk * pl.P * 4;
+  if (!stage && TT * TE > 16 && nh_bytes > head && nh_bytes <= 200 * 1024) head = nh_bytes;
   const size_t smem = ((head + 15) & ~size_t(15)) + (stage ? wbytes : 0);
   auto kern = stage ? gate_topk_kernel<TT, TE, true> : gate_topk_kernel<TT, TE, false>;
   if (smem > 48 * 1024) MSI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
