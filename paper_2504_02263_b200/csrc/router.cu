@@ -1,7 +1,9 @@
 // router.cu -- fused gate GEMM + top-K + normalized weights + per-expert
 // counts + slot placement.
 //
-// One kernel launch.  Each CTA owns BT consecutive tokens:
+// One kernel launch (fine-grained MoE at small T: a logits kernel on a
+// token x expert grid, then route_kernel for phases 2-4).  Each CTA owns BT
+// consecutive tokens:
 //   1. logits[t,e] in the pinned fp32 order (lane l accumulates elements
 //      256j + 8l + c with fmaf, then an xor butterfly 16,8,4,2,1) -- the
 //      order oracle/msi_oracle.c restates, so routing is bit-exact;
@@ -11,8 +13,10 @@
 //      "token lane chose e", so rank = popc(mask[e] & lanes_below); the
 //      CTA's per-expert histogram goes to the workspace;
 //   4. the last CTA to finish (ticket) scans the histograms over CTAs
-//      (independent loads) into per-CTA bases, writes cnt[E] and adds the
-//      bases to every slot.
+//      (batched independent loads into shared memory) into per-CTA bases,
+//      writes cnt[E] and adds the bases to every slot (16-B vectors).
+// MSI_ROUTER_PROF=1 writes %globaltimer phase stamps into workspace words
+// 1..8 (scripts/router_phase_probe.py).
 // HBM-bound for small E (reads x once); FMA-bound for E = 256 (logits on
 // CUDA cores because the fixed reduction order is the bit-exactness contract).
 #include <cstdio>
