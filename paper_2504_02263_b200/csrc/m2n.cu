@@ -494,6 +494,42 @@ __device__ __forceinline__ void combine_row8(const char* ybase, const float* w, 
   *reinterpret_cast<uint4*>(out + (size_t)t * H + col8 * 8) = o;
 }
 
+// Same arithmetic as combine_row8 with KR = K * tp known at compile time:
+// every y row of the token is loaded before the first FMA (KR independent
+// loads in flight instead of a serial load -> FMA chain per k); the fmaf
+// order (residual, then ascending (k, r)) is unchanged, so results are
+// bit-identical.
+template <int KR>
+__device__ __forceinline__ void combine_row8_fixed(const char* ybase, const float* w, const uint16_t* resid,
+                                                   uint16_t* out, int t, int col8, int K, int H, int tp) {
+  uint4 y[KR];
+  float wk[KR];
+#pragma unroll
+  for (int kr = 0; kr < KR; ++kr) {
+    y[kr] = __ldcg(reinterpret_cast<const uint4*>(ybase + (((size_t)t * KR + kr) * H + col8 * 8) * 2));
+    wk[kr] = w[(size_t)t * K + kr / tp];
+  }
+  float acc[8];
+  if (resid) {
+    uint4 r = *reinterpret_cast<const uint4*>(resid + (size_t)t * H + col8 * 8);
+    acc[0] = bf16lo(r.x); acc[1] = bf16hi(r.x); acc[2] = bf16lo(r.y); acc[3] = bf16hi(r.y);
+    acc[4] = bf16lo(r.z); acc[5] = bf16hi(r.z); acc[6] = bf16lo(r.w); acc[7] = bf16hi(r.w);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+  }
+#pragma unroll
+  for (int kr = 0; kr < KR; ++kr) {
+    acc[0] = __fmaf_rn(wk[kr], bf16lo(y[kr].x), acc[0]); acc[1] = __fmaf_rn(wk[kr], bf16hi(y[kr].x), acc[1]);
+    acc[2] = __fmaf_rn(wk[kr], bf16lo(y[kr].y), acc[2]); acc[3] = __fmaf_rn(wk[kr], bf16hi(y[kr].y), acc[3]);
+    acc[4] = __fmaf_rn(wk[kr], bf16lo(y[kr].z), acc[4]); acc[5] = __fmaf_rn(wk[kr], bf16hi(y[kr].z), acc[5]);
+    acc[6] = __fmaf_rn(wk[kr], bf16lo(y[kr].w), acc[6]); acc[7] = __fmaf_rn(wk[kr], bf16hi(y[kr].w), acc[7]);
+  }
+  uint4 o = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
+                       pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
+  *reinterpret_cast<uint4*>(out + (size_t)t * H + col8 * 8) = o;
+}
+
 __global__ void __launch_bounds__(256)
 combine_kernel(const char* __restrict__ ybase, const float* __restrict__ w, const uint16_t* __restrict__ resid,
                uint16_t* __restrict__ out, int T, int K, int H, int tp, const uint32_t* wait_ctr,
@@ -514,9 +550,16 @@ combine_kernel(const char* __restrict__ ybase, const float* __restrict__ w, cons
   }
   const int per_row = H / 8;
   const size_t n = (size_t)T * per_row;
+  const int KR = K * tp;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const int t = (int)(i / per_row), c8 = (int)(i % per_row);
-    combine_row8(ybase, w, resid, out, t, c8, K, H, tp);
+    switch (KR) {
+      case 1: combine_row8_fixed<1>(ybase, w, resid, out, t, c8, K, H, tp); break;
+      case 2: combine_row8_fixed<2>(ybase, w, resid, out, t, c8, K, H, tp); break;
+      case 4: combine_row8_fixed<4>(ybase, w, resid, out, t, c8, K, H, tp); break;
+      case 8: combine_row8_fixed<8>(ybase, w, resid, out, t, c8, K, H, tp); break;
+      default: combine_row8(ybase, w, resid, out, t, c8, K, H, tp);
+    }
   }
   if (t0) trace_stamp(trace, 8);
 }
