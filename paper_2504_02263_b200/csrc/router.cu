@@ -50,6 +50,7 @@ struct Placement {
   int R, P, sender;
   int32_t* pidx;  // [T,K] physical slot per (t,k) (may alias idx when rep == nullptr)
   int prof;       // MSI_ROUTER_PROF=1: %globaltimer phase stamps into ws[2..8] (diagnostics)
+  int pfw;        // 1 = prefetch the next W_g chunk into L1 (MSI_ROUTER_PFW, unstaged W_g only)
 };
 
 __device__ __forceinline__ void rprof(const Placement& pl, int32_t* ws, int i) {
@@ -321,7 +322,8 @@ __device__ __forceinline__ void route_tail(float* s_logit, int t0, int BT, int T
 // (oracle/msi_oracle.c); every lane returns the final values, NaN as -inf.
 template <int TT, int TE, bool WS, int PF = (TT * TE > 32) ? 2 : 4>
 __device__ __forceinline__ void tile_logits(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
-                                            int t_first, int e_first, int T, int H, float (&acc)[TT][TE]) {
+                                            int t_first, int e_first, int T, int H, float (&acc)[TT][TE],
+                                            int pfw = 0) {
   const int lane = threadIdx.x & 31;
   const int nchunk = H >> 8;
 #pragma unroll
@@ -351,6 +353,14 @@ __device__ __forceinline__ void tile_logits(const __nv_bfloat16* __restrict__ x,
     for (int u = 0; u < PF; ++u) {
       const int j = j0 + u;
       if (j >= nchunk) break;
+      // unstaged W_g: pull chunk j + 1 of the TE rows into L1 now, so the
+      // loads below hit L1 instead of paying an L2 round trip per chunk (no
+      // registers held; the arithmetic and its order are unchanged)
+      if (!WS && pfw && j + 1 < nchunk && (lane & 7) == 0) {
+#pragma unroll
+        for (int e = 0; e < TE; ++e)
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(wr + (size_t)e * H + 256 * (j + 1)));
+      }
       float xv[TT][8];
 #pragma unroll
       for (int i = 0; i < TT; ++i) {
@@ -395,7 +405,7 @@ __device__ __forceinline__ void tile_logits(const __nv_bfloat16* __restrict__ x,
 template <int TT, int TE>
 __global__ void __launch_bounds__(kWarps * 32, 2)
 gate_logits_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg, int T, int H, int E,
-                   int BT, int EB, float* __restrict__ logits) {
+                   int BT, int EB, float* __restrict__ logits, int pfw) {
   pdl_trigger();
   pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -404,7 +414,7 @@ gate_logits_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __r
   for (int tile = warp; tile < tgroups * egroups; tile += kWarps) {
     const int tg = tile % tgroups, eg = tile / tgroups;
     float acc[TT][TE];
-    tile_logits<TT, TE, false, (TT * TE >= 32 ? 2 : 4)>(x, wg, t0 + tg * TT, e0 + eg * TE, T, H, acc);
+    tile_logits<TT, TE, false, (TT * TE >= 32 ? 2 : 4)>(x, wg, t0 + tg * TT, e0 + eg * TE, T, H, acc, pfw);
 #pragma unroll
     for (int i = 0; i < TT; ++i) {
       const int t = t0 + tg * TT + i;
@@ -468,7 +478,7 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
   for (int tile = warp; tile < tgroups * egroups; tile += kWarps) {
     const int tg = tile % tgroups, eg = tile / tgroups;
     float acc[TT][TE];
-    tile_logits<TT, TE, WS>(x, wg, t0 + tg * TT, eg * TE, T, H, acc);
+    tile_logits<TT, TE, WS>(x, wg, t0 + tg * TT, eg * TE, T, H, acc, pl.pfw);
 #pragma unroll
     for (int i = 0; i < TT; ++i)
 #pragma unroll
@@ -521,7 +531,7 @@ int launch_split(const void* x, const void* wg, int T, int H, int E, int K, int 
   const dim3 grid((T + BTL - 1) / BTL, E / EB);
   MSI_CUDA(launch_k(gate_logits_kernel<TT, TE>, grid, dim3(kWarps * 32), 0, st,
                     reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<const __nv_bfloat16*>(wg), T, H, E,
-                    BTL, EB, logits));
+                    BTL, EB, logits, pl.pfw));
   constexpr int BT = 32;
   size_t head = logit_smem_bytes(BT, E);
   if (head < (size_t)pl.P * 4) head = (size_t)pl.P * 4;
@@ -574,7 +584,9 @@ int gate_topk(const void* x, const void* wg, int T, int H, int E, int K, int32_t
   MSI_REQUIRE(!rep || (R >= 1 && P >= E && P <= 4096 && pidx && sender >= 0),
               "gate_topk: replica table needs R >= 1, E <= P <= 4096, pidx and sender >= 0");
   const char* pe = getenv("MSI_ROUTER_PROF");
-  const Placement pl{rep, R, rep ? P : E, sender, rep ? pidx : idx, (pe && pe[0] == '1') ? 1 : 0};
+  const char* pf = getenv("MSI_ROUTER_PFW");
+  const Placement pl{rep, R, rep ? P : E, sender, rep ? pidx : idx, (pe && pe[0] == '1') ? 1 : 0,
+                     (pf && pf[0] == '1') ? 1 : 0};
   if (T == 0) {
     MSI_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * pl.P, st));
     return 0;
