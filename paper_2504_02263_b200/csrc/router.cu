@@ -31,6 +31,12 @@ int num_sms();  // expert_gemm.cu
 namespace {
 
 constexpr int kWarps = 8;
+
+// Packed fp32x2 FMAs in the logits loop (compile with -DMSI_ROUTER_FFMA2=0 for
+// the scalar-FFMA build; both are bit-identical)
+#ifndef MSI_ROUTER_FFMA2
+#define MSI_ROUTER_FFMA2 1
+#endif
 constexpr uint32_t kTaken = 0x7fc0dead;  // NaN payload marking an already-selected expert
 
 // Shared memory: logits [max(BT,16)][E] fp32 (reused by the last CTA for
@@ -330,6 +336,13 @@ __device__ __forceinline__ void tile_logits(const __nv_bfloat16* __restrict__ x,
   for (int i = 0; i < TT; ++i)
 #pragma unroll
     for (int j = 0; j < TE; ++j) acc[i][j] = 0.0f;
+#if MSI_ROUTER_FFMA2
+  float2 acc2[TT][(TE + 1) / 2];
+#pragma unroll
+  for (int i = 0; i < TT; ++i)
+#pragma unroll
+    for (int j = 0; j < (TE + 1) / 2; ++j) acc2[i][j] = make_float2(0.0f, 0.0f);
+#endif
   const __nv_bfloat16* xr[TT];
   bool tv[TT];
 #pragma unroll
@@ -373,6 +386,28 @@ __device__ __forceinline__ void tile_logits(const __nv_bfloat16* __restrict__ x,
         xq[u][i] = (tv[i] && j + PF < nchunk) ? __ldg(reinterpret_cast<const uint4*>(xr[i] + 256 * (j + PF)))
                                              : make_uint4(0, 0, 0, 0);
       }
+#if MSI_ROUTER_FFMA2
+      if constexpr (TE % 2 == 0) {
+        // two experts per packed FFMA2 (sm_100 fma.rn.f32x2): each half is
+        // the same IEEE fmaf in the same c order, so the logits are
+        // bit-identical to the scalar loop at half the FMA issue count
+#pragma unroll
+        for (int e = 0; e < TE; e += 2) {
+          const uint4* wp0 = reinterpret_cast<const uint4*>(wr + (size_t)e * H + 256 * j);
+          const uint4* wp1 = reinterpret_cast<const uint4*>(wr + (size_t)(e + 1) * H + 256 * j);
+          const uint4 v0 = WS ? *wp0 : __ldg(wp0), v1 = WS ? *wp1 : __ldg(wp1);
+          const float2 w2[8] = {{bf16lo(v0.x), bf16lo(v1.x)}, {bf16hi(v0.x), bf16hi(v1.x)},
+                                {bf16lo(v0.y), bf16lo(v1.y)}, {bf16hi(v0.y), bf16hi(v1.y)},
+                                {bf16lo(v0.z), bf16lo(v1.z)}, {bf16hi(v0.z), bf16hi(v1.z)},
+                                {bf16lo(v0.w), bf16lo(v1.w)}, {bf16hi(v0.w), bf16hi(v1.w)}};
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+#pragma unroll
+            for (int i = 0; i < TT; ++i) acc2[i][e >> 1] = __ffma2_rn(make_float2(xv[i][c], xv[i][c]), w2[c], acc2[i][e >> 1]);
+        }
+        continue;
+      }
+#endif
 #pragma unroll
       for (int e = 0; e < TE; ++e) {
         const uint4* wp = reinterpret_cast<const uint4*>(wr + (size_t)e * H + 256 * j);
@@ -386,6 +421,17 @@ __device__ __forceinline__ void tile_logits(const __nv_bfloat16* __restrict__ x,
       }
     }
   }
+#if MSI_ROUTER_FFMA2
+  if constexpr (TE % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < TT; ++i)
+#pragma unroll
+      for (int e = 0; e < TE; e += 2) {
+        acc[i][e] = acc2[i][e >> 1].x;
+        acc[i][e + 1] = acc2[i][e >> 1].y;
+      }
+  }
+#endif
 #pragma unroll
   for (int i = 0; i < TT; ++i)
 #pragma unroll
