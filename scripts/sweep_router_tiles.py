@@ -14,6 +14,10 @@ CASES = {(3072, 6144, 8, 2): ["4x8x32", "2x8x16", "1x8x8", "4x8x16", "2x8x8", "8
          (1024, 6144, 16, 4): ["4x16x32", "2x16x16", "1x16x8", "4x8x16", "2x8x8", "1x8x8"],
          (4096, 7168, 256, 8): ["4x16x16", "4x16x4", "8x8x32"],
          (512, 7168, 256, 8): ["4x16x4", "2x16x4"]}
+if sys.argv[1:] == ["e256"]:  # E = 256 only (re-sweep after the FFMA2 logits loop)
+    CASES = {(4096, 7168, 256, 8): ["4x16x28", "8x8x32", "8x8x24", "8x4x32", "4x8x28", "2x16x28"],
+             (2048, 7168, 256, 8): ["4x16x16", "8x8x16", "4x8x16", "2x16x16"],
+             (512, 7168, 256, 8): ["4x16x4", "2x16x4", "4x8x4", "8x8x8"]}
 for (T, H, E, K), tiles in CASES.items():
     x = torch.randn(T, H, device="cuda").to(torch.bfloat16)
     wg = (torch.randn(E, H, device="cuda") / H ** 0.5).to(torch.bfloat16)
