@@ -387,10 +387,12 @@ __device__ __forceinline__ void tile_logits(const __nv_bfloat16* __restrict__ x,
                                              : make_uint4(0, 0, 0, 0);
       }
 #if MSI_ROUTER_FFMA2
-      if constexpr (TE % 2 == 0) {
+      if constexpr (TE % 2 == 0 && !WS) {
         // two experts per packed FFMA2 (sm_100 fma.rn.f32x2): each half is
         // the same IEEE fmaf in the same c order, so the logits are
-        // bit-identical to the scalar loop at half the FMA issue count
+        // bit-identical to the scalar loop at half the FMA issue count.
+        // FMA-bound unstaged path only: the HBM-bound staged-W_g kernels
+        // (E <= 16) measured ~3 % slower with it (E = 16: 29 -> 30 us)
 #pragma unroll
         for (int e = 0; e < TE; e += 2) {
           const uint4* wp0 = reinterpret_cast<const uint4*>(wr + (size_t)e * H + 256 * j);
@@ -422,7 +424,7 @@ __device__ __forceinline__ void tile_logits(const __nv_bfloat16* __restrict__ x,
     }
   }
 #if MSI_ROUTER_FFMA2
-  if constexpr (TE % 2 == 0) {
+  if constexpr (TE % 2 == 0 && !WS) {
 #pragma unroll
     for (int i = 0; i < TT; ++i)
 #pragma unroll
