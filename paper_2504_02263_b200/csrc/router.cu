@@ -37,6 +37,9 @@ constexpr int kWarps = 8;
 #ifndef MSI_ROUTER_FFMA2
 #define MSI_ROUTER_FFMA2 1
 #endif
+#ifndef MSI_ROUTER_EP
+#define MSI_ROUTER_EP 1
+#endif
 constexpr uint32_t kTaken = 0x7fc0dead;  // NaN payload marking an already-selected expert
 
 // Shared memory: logits [max(BT,16)][E] fp32 (reused by the last CTA for
@@ -393,19 +396,30 @@ __device__ __forceinline__ void tile_logits(const __nv_bfloat16* __restrict__ x,
         // bit-identical to the scalar loop at half the FMA issue count.
         // FMA-bound unstaged path only: the HBM-bound staged-W_g kernels
         // (E <= 16) measured ~3 % slower with it (E = 16: 29 -> 30 us)
+        // EP expert pairs interleaved per c step: independent FFMA2s between
+        // two updates of one accumulator (MSI_ROUTER_EP, default 1)
+        constexpr int EP = (TE % (2 * MSI_ROUTER_EP) == 0) ? MSI_ROUTER_EP : 1;
 #pragma unroll
-        for (int e = 0; e < TE; e += 2) {
-          const uint4* wp0 = reinterpret_cast<const uint4*>(wr + (size_t)e * H + 256 * j);
-          const uint4* wp1 = reinterpret_cast<const uint4*>(wr + (size_t)(e + 1) * H + 256 * j);
-          const uint4 v0 = WS ? *wp0 : __ldg(wp0), v1 = WS ? *wp1 : __ldg(wp1);
-          const float2 w2[8] = {{bf16lo(v0.x), bf16lo(v1.x)}, {bf16hi(v0.x), bf16hi(v1.x)},
-                                {bf16lo(v0.y), bf16lo(v1.y)}, {bf16hi(v0.y), bf16hi(v1.y)},
-                                {bf16lo(v0.z), bf16lo(v1.z)}, {bf16hi(v0.z), bf16hi(v1.z)},
-                                {bf16lo(v0.w), bf16lo(v1.w)}, {bf16hi(v0.w), bf16hi(v1.w)}};
+        for (int e0 = 0; e0 < TE; e0 += 2 * EP) {
+          float2 w2[EP][8];
+#pragma unroll
+          for (int p = 0; p < EP; ++p) {
+            const int e = e0 + 2 * p;
+            const uint4* wp0 = reinterpret_cast<const uint4*>(wr + (size_t)e * H + 256 * j);
+            const uint4* wp1 = reinterpret_cast<const uint4*>(wr + (size_t)(e + 1) * H + 256 * j);
+            const uint4 v0 = WS ? *wp0 : __ldg(wp0), v1 = WS ? *wp1 : __ldg(wp1);
+            w2[p][0] = make_float2(bf16lo(v0.x), bf16lo(v1.x)); w2[p][1] = make_float2(bf16hi(v0.x), bf16hi(v1.x));
+            w2[p][2] = make_float2(bf16lo(v0.y), bf16lo(v1.y)); w2[p][3] = make_float2(bf16hi(v0.y), bf16hi(v1.y));
+            w2[p][4] = make_float2(bf16lo(v0.z), bf16lo(v1.z)); w2[p][5] = make_float2(bf16hi(v0.z), bf16hi(v1.z));
+            w2[p][6] = make_float2(bf16lo(v0.w), bf16lo(v1.w)); w2[p][7] = make_float2(bf16hi(v0.w), bf16hi(v1.w));
+          }
 #pragma unroll
           for (int c = 0; c < 8; ++c)
 #pragma unroll
-            for (int i = 0; i < TT; ++i) acc2[i][e >> 1] = __ffma2_rn(make_float2(xv[i][c], xv[i][c]), w2[c], acc2[i][e >> 1]);
+            for (int p = 0; p < EP; ++p)
+#pragma unroll
+              for (int i = 0; i < TT; ++i)
+                acc2[i][(e0 >> 1) + p] = __ffma2_rn(make_float2(xv[i][c], xv[i][c]), w2[p][c], acc2[i][(e0 >> 1) + p]);
         }
         continue;
       }
