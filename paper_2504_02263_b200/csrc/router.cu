@@ -339,13 +339,13 @@ __device__ __forceinline__ void tile_logits(const __nv_bfloat16* __restrict__ x,
   for (int i = 0; i < TT; ++i)
 #pragma unroll
     for (int j = 0; j < TE; ++j) acc[i][j] = 0.0f;
-#if MSI_ROUTER_FFMA2
+  // packed FFMA2 accumulators (two experts per float2) on the unstaged path
+  constexpr bool kPair = MSI_ROUTER_FFMA2 && TE % 2 == 0 && !WS;
   float2 acc2[TT][(TE + 1) / 2];
 #pragma unroll
   for (int i = 0; i < TT; ++i)
 #pragma unroll
     for (int j = 0; j < (TE + 1) / 2; ++j) acc2[i][j] = make_float2(0.0f, 0.0f);
-#endif
   const __nv_bfloat16* xr[TT];
   bool tv[TT];
 #pragma unroll
@@ -389,8 +389,7 @@ __device__ __forceinline__ void tile_logits(const __nv_bfloat16* __restrict__ x,
         xq[u][i] = (tv[i] && j + PF < nchunk) ? __ldg(reinterpret_cast<const uint4*>(xr[i] + 256 * (j + PF)))
                                              : make_uint4(0, 0, 0, 0);
       }
-#if MSI_ROUTER_FFMA2
-      if constexpr (TE % 2 == 0 && !WS) {
+      if constexpr (kPair) {
         // two experts per packed FFMA2 (sm_100 fma.rn.f32x2): each half is
         // the same IEEE fmaf in the same c order, so the logits are
         // bit-identical to the scalar loop at half the FMA issue count.
@@ -421,24 +420,22 @@ __device__ __forceinline__ void tile_logits(const __nv_bfloat16* __restrict__ x,
               for (int i = 0; i < TT; ++i)
                 acc2[i][(e0 >> 1) + p] = __ffma2_rn(make_float2(xv[i][c], xv[i][c]), w2[p][c], acc2[i][(e0 >> 1) + p]);
         }
-        continue;
-      }
-#endif
+      } else {
 #pragma unroll
-      for (int e = 0; e < TE; ++e) {
-        const uint4* wp = reinterpret_cast<const uint4*>(wr + (size_t)e * H + 256 * j);
-        uint4 v = WS ? *wp : __ldg(wp);
-        float wv[8] = {bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y),
-                       bf16lo(v.z), bf16hi(v.z), bf16lo(v.w), bf16hi(v.w)};
+        for (int e = 0; e < TE; ++e) {
+          const uint4* wp = reinterpret_cast<const uint4*>(wr + (size_t)e * H + 256 * j);
+          uint4 v = WS ? *wp : __ldg(wp);
+          float wv[8] = {bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y),
+                         bf16lo(v.z), bf16hi(v.z), bf16lo(v.w), bf16hi(v.w)};
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
+          for (int c = 0; c < 8; ++c)
 #pragma unroll
-          for (int i = 0; i < TT; ++i) acc[i][e] = __fmaf_rn(xv[i][c], wv[c], acc[i][e]);
+            for (int i = 0; i < TT; ++i) acc[i][e] = __fmaf_rn(xv[i][c], wv[c], acc[i][e]);
+        }
       }
     }
   }
-#if MSI_ROUTER_FFMA2
-  if constexpr (TE % 2 == 0 && !WS) {
+  if constexpr (kPair) {
 #pragma unroll
     for (int i = 0; i < TT; ++i)
 #pragma unroll
@@ -447,7 +444,6 @@ __device__ __forceinline__ void tile_logits(const __nv_bfloat16* __restrict__ x,
         acc[i][e + 1] = acc2[i][e >> 1].y;
       }
   }
-#endif
 #pragma unroll
   for (int i = 0; i < TT; ++i)
 #pragma unroll
