@@ -100,7 +100,7 @@ def parse():
     # (not "--m": torchrun would take it as an abbreviation of its own options)
     ap.add_argument("--micro-batches", dest="m", type=int, default=3, help="m, micro-batches per step")
     ap.add_argument("--layers", type=int, default=4, help="L_sim layers per step")
-    ap.add_argument("--attn", default="real", choices=["real", "standin", "none"])
+    ap.add_argument("--attn", default="real", choices=["real", "none"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--split", default="", help="attention+expert GPUs, e.g. 6+2 (disaggregated)")
@@ -640,11 +640,7 @@ def main():
                                               tp_rank=g.tp_rank)
     layer = runtime.MoEDecodeLayer(g, wg=wg if g.is_attention else None,
                                    w13=w13 if g.is_expert else None, w2=w2 if g.is_expert else None)
-    kv_bytes = 0
-    if args.attn == "standin" and g.is_attention:
-        # decode-attention HBM load of one micro-batch: b_a tokens x s x (K,V) x h/g x bf16
-        kv_bytes = args.b_a * wl.avg_seq_len * 2 * (model.hidden // model.gqa_group) * 2
-    runner = runtime.PingPongRunner(layer, layers=args.layers, kv_bytes=kv_bytes, chain=False,
+    runner = runtime.PingPongRunner(layer, layers=args.layers, chain=False,
                                     record_timeline=True, attn=att_stages)
     x0 = [x.clone() for x in xs] if xs else None
 
@@ -874,7 +870,7 @@ def main():
     # our kernels per (micro-batch, layer): attention (stand-in 1; real: rope_append +
     # decode_attn [+ split combine]; its two projections are cuBLAS), router,
     # dispatch, expert wait + 2 GEMMs, combine
-    attn_launches = (1 if kv_bytes else 0)
+    attn_launches = 0
     if att_stages:
         attn_launches = 2 + (1 if att_stages[0].ws is not None else 0)
     # router: one fused kernel, or logits + route kernels (E >= 64 at T <= 256)

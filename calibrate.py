@@ -71,19 +71,24 @@ def profile_expert(model, e_l: int, tes: list, iters: int) -> list:
 
 
 def profile_attention(model, seq_len: int, bas: list, iters: int) -> list:
-    import torch
-    from paper_2504_02263_b200 import ops
-    dev = torch.device("cuda:0")
-    per_tok = seq_len * 2 * (model.hidden // model.gqa_group) * 2
-    kv = torch.empty(max(bas) * per_tok, dtype=torch.uint8, device=dev)
-    kv.random_(0, 255)
-    cs = torch.zeros(4, dtype=torch.int64, device=dev)
+    """T_a(b_a): the real attention stage (QKV projection, RoPE + KV append,
+    paged decode attention at mean context seq_len, output projection)."""
+    from paper_2504_02263_b200 import attention as A
+    dev = torch_device()
+    w = A.AttentionWeights(model, dev, seed=0)
     out = []
     for b in bas:
-        view = kv[: b * per_tok]
-        ms = time_ms(lambda: ops.attn_standin(view, cs), iters)
+        st = A.AttentionStage(model, b, 1, dev, weights=w, avg_seq_len=seq_len, seed=b)
+        x = st.y.clone().normal_()
+        ms = time_ms(lambda: st.forward(x, 0), iters)
         out.append(("attention", b, ms / 1e3))
+        del st, x
     return out
+
+
+def torch_device():
+    import torch
+    return torch.device("cuda:0")
 
 
 def util_from_m2n(path: str) -> list:

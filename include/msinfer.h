@@ -98,6 +98,12 @@ int msi_ctx_import(msi_ctx* ctx, int peer_rank, const msi_ipc_handle* handle);
  * across ranks, before the first dispatch). */
 int msi_ctx_finalize(msi_ctx* ctx);
 int msi_ctx_buffer(msi_ctx* ctx, int which, int slot, void** ptr, size_t* bytes);
+/* Recovery after a device-side wait timed out (MSI_ETIMEOUT, sticky abort
+ * flag): synchronizes the device and zeroes this rank's control words (arrival
+ * counters, tickets, tile counters, slot use counts, status, count table) and
+ * the router workspace.  Every rank of the deployment calls it, then a barrier
+ * across ranks, as after msi_ctx_finalize; epochs restart at 1. */
+int msi_ctx_reset(msi_ctx* ctx);
 /* Device status word: 0 = ok, else a MSI_E* code set by a device-side wait. */
 int msi_poll_status(msi_ctx* ctx, int32_t* status);
 /* Expert-role counters: rows through msi_expert_ffn and number of calls since
@@ -201,12 +207,6 @@ int msi_grouped_ffn(const void* x, const int32_t* total, int E_l, int rows,
 /* Stand-alone combine on a local [T,K,H] buffer (no waits). */
 int msi_combine_local(const void* y, const float* w, const void* resid,
                       void* out, int T, int K, int H, void* stream);
-/* Attention-stage stand-in: streams `kv_bytes` of a KV buffer per call and
- * folds them into a checksum (the decode-attention HBM load of one
- * micro-batch; out of scope as a kernel). */
-int msi_attn_standin(const void* kv, size_t kv_bytes, float* checksum,
-                     void* stream);
-
 /* ---- Attention stage: GQA decode over paged KV.
  * The reference models it as T_a = k1*b_a + k2 with the KV traffic
  * 2*b*s*h*bytes/g (Table 3).

@@ -55,6 +55,7 @@ SIGNATURES = {
     "msi_ctx_import": (_I, [_P, _I, ctypes.POINTER(IpcHandle)]),
     "msi_ctx_finalize": (_I, [_P]),
     "msi_ctx_buffer": (_I, [_P, _I, _I, ctypes.POINTER(_P), ctypes.POINTER(_SZ)]),
+    "msi_ctx_reset": (_I, [_P]),
     "msi_poll_status": (_I, [_P, ctypes.POINTER(ctypes.c_int32)]),
     "msi_set_wait_timeout": (_I, [_P, _U64]),
     "msi_ctx_stats": (_I, [_P, ctypes.POINTER(_U64), ctypes.POINTER(_U64)]),
@@ -73,7 +74,6 @@ SIGNATURES = {
     "msi_set_gemm_cta_group": (_I, [_I]),
     "msi_grouped_ffn": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _I, _I, _P]),
     "msi_combine_local": (_I, [_P, _P, _P, _P, _I, _I, _I, _P]),
-    "msi_attn_standin": (_I, [_P, _SZ, _P, _P]),
     "msi_rope_append": (_I, [_P, ctypes.c_int64, _P, _I, _I, _I, ctypes.c_float, _P, _I, _P, _P,
                              ctypes.c_int64, _P, _P]),
     "msi_decode_attention_workspace": (_SZ, [_I, _I, _I, _I]),

@@ -476,11 +476,7 @@ extern "C" int msi_decode_attention(const void* q, const void* k_cache, const vo
   if (!rc) rc = lookup(k_cache, 16, &tk16);
   if (!rc) rc = lookup(v_cache, 16, &tv16);
   if (rc) return rc;
-  static bool attr = false;
-  if (!attr) {
-    MSI_CUDA(cudaFuncSetAttribute(decode_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
-    attr = true;
-  }
+  if (int arc = smem_attr(reinterpret_cast<const void*>(decode_attn_kernel), kSmem)) return arc;
   AttnArgs a;
   a.q = (const __nv_bfloat16*)q;
   a.bt = block_table;

@@ -54,6 +54,11 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 
 bool pdl_enabled();  // MSI_PDL=1 enables (A/B switch)
 
+// Raise kernel `fn`'s dynamic shared-memory limit to >= bytes on the current
+// device.  The attribute is per (function, device context), so the cache is
+// keyed by both and guarded by a mutex (m2n.cu).
+int smem_attr(const void* fn, size_t bytes);
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                             Args&&... args) {

@@ -540,13 +540,12 @@ bool half_pair_box64() {
 }
 
 int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return n;
+  static int n[64] = {};  // per device (all B200s have 148; no race: idempotent)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!n[dev]) cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev);
+  return n[dev];
 }
 
 template <int CG, int MAXE>
@@ -559,12 +558,7 @@ int launch_cg(const GemmLaunch& L, cudaStream_t st) {
   if (rc) return rc;
   rc = make_tmap(&tb, L.b, (uint64_t)L.p.kdim, (uint64_t)L.p.E_l * L.p.n_total, BK, C::B_ROWS);
   if (rc) return rc;
-  static bool attr = false;
-  if (!attr) {
-    MSI_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<CG, MAXE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)C::SMEM));
-    attr = true;
-  }
+  if (int arc = smem_attr(reinterpret_cast<const void*>(grouped_gemm_kernel<CG, MAXE>), C::SMEM)) return arc;
   int grid = L.grid > 0 ? L.grid : num_sms();
   if (const char* g = getenv("MSI_GEMM_GRID")) {  // A/B: persistent grid on fewer SMs
     const int v = atoi(g);
@@ -598,10 +592,8 @@ int launch_cg(const GemmLaunch& L, cudaStream_t st) {
   return check_launch("grouped_gemm_kernel");
 }
 
-// CTA-group selection: MSI_GEMM_CG=1|2 overrides; default = the 1-CTA kernel,
-// which measured equal or faster on B200 (profiles/r01_gemm_cg_ab.jsonl: both
-// run at the power-capped tensor rate for t_e >= 768, and pairing M tiles
-// adds padding at small t_e).
+// CTA-group selection: MSI_GEMM_CG=1|2 (or msi_set_gemm_cta_group) overrides;
+// default = CTA pairs (see default_cg).
 static int g_cg_override = 0;
 
 int default_cg() {

@@ -32,6 +32,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -55,6 +56,26 @@ int check_launch(const char* what) {
     set_error("%s launch: %s", what, cudaGetErrorString(e));
     return (int)e;
   }
+  return 0;
+}
+
+int smem_attr(const void* fn, size_t bytes) {
+  if (bytes <= 48 * 1024) return 0;
+  struct Entry { const void* fn; int dev; size_t bytes; };
+  static std::mutex mu;
+  static std::vector<Entry> done;
+  int dev = 0;
+  MSI_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  for (Entry& e : done)
+    if (e.fn == fn && e.dev == dev) {
+      if (e.bytes >= bytes) return 0;
+      MSI_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+      e.bytes = bytes;
+      return 0;
+    }
+  MSI_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  done.push_back({fn, dev, bytes});
   return 0;
 }
 
@@ -564,25 +585,6 @@ combine_kernel(const char* __restrict__ ybase, const float* __restrict__ w, cons
   if (t0) trace_stamp(trace, 8);
 }
 
-// -------------------------------------------------- attention stand-in ----
-__global__ void __launch_bounds__(512) attn_standin_kernel(const uint4* __restrict__ kv, size_t n16, float* checksum) {
-  // 4 independent 16 B loads in flight per thread per iteration (HBM streaming)
-  float s = 0.0f;
-  const size_t stride = (size_t)gridDim.x * blockDim.x;
-  size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  for (; i + 3 * stride < n16; i += 4 * stride) {
-    uint4 v0 = ld_nc_v4(kv + i), v1 = ld_nc_v4(kv + i + stride);
-    uint4 v2 = ld_nc_v4(kv + i + 2 * stride), v3 = ld_nc_v4(kv + i + 3 * stride);
-    s += bf16lo(v0.x) + bf16hi(v1.w) + bf16lo(v2.y) + bf16hi(v3.z);
-  }
-  for (; i < n16; i += stride) {
-    uint4 v = ld_nc_v4(kv + i);
-    s += bf16lo(v.x) + bf16hi(v.w);
-  }
-  for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-  if ((threadIdx.x & 31) == 0 && s == 1234.5f) atomicAdd(checksum, s);  // keeps the loads live
-}
-
 }  // namespace
 }  // namespace msi
 
@@ -621,17 +623,24 @@ extern "C" int msi_ctx_create(const msi_plan* plan, int rank, msi_ctx** out) {
   for (int i = 0; i < plan->n_e; ++i) if (plan->expert_ranks[i] == rank) c->my_e = i;
   c->my_layout = make_layout(*plan, c->attn, c->expert);
   c->heap_bytes = c->my_layout.total;
+  auto fail = [&](const char* what, cudaError_t e) {
+    set_error("msi_ctx_create: %s: %s", what, cudaGetErrorString(e));
+    if (c->heap) cudaFree(c->heap);
+    if (c->hbuf) cudaFree(c->hbuf);
+    if (c->workspace) cudaFree(c->workspace);
+    delete c;
+    return (int)e;
+  };
   cudaError_t e = cudaMalloc(&c->heap, c->heap_bytes);
-  if (e != cudaSuccess) { set_error("heap cudaMalloc(%zu): %s", c->heap_bytes, cudaGetErrorString(e)); delete c; return (int)e; }
-  cudaMemset(c->heap, 0, c->my_layout.ctrl_bytes);
+  if (e != cudaSuccess) return fail("heap cudaMalloc", e);
+  if ((e = cudaMemset(c->heap, 0, c->my_layout.ctrl_bytes)) != cudaSuccess) return fail("heap memset", e);
   if (c->expert) {
     e = cudaMalloc(&c->hbuf, (size_t)c->my_layout.cap * plan->inter * 2);
-    if (e != cudaSuccess) { set_error("hbuf cudaMalloc: %s", cudaGetErrorString(e)); cudaFree(c->heap); delete c; return (int)e; }
+    if (e != cudaSuccess) return fail("hbuf cudaMalloc", e);
   }
   c->ws_bytes = msi_gate_topk_workspace(plan->max_tokens, plan->experts);
-  e = cudaMalloc(&c->workspace, c->ws_bytes);
-  if (e != cudaSuccess) { set_error("workspace cudaMalloc: %s", cudaGetErrorString(e)); return (int)e; }
-  cudaMemset(c->workspace, 0, c->ws_bytes);
+  if ((e = cudaMalloc(&c->workspace, c->ws_bytes)) != cudaSuccess) return fail("workspace cudaMalloc", e);
+  if ((e = cudaMemset(c->workspace, 0, c->ws_bytes)) != cudaSuccess) return fail("workspace memset", e);
   c->peer[rank] = c->heap;
   c->opened[rank] = true;
   *out = c;
@@ -720,6 +729,15 @@ extern "C" int msi_ctx_finalize(msi_ctx* c) {
   return 0;
 }
 
+extern "C" int msi_ctx_reset(msi_ctx* c) {
+  if (!c || !c->finalized) { set_error("msi_ctx_reset: context not finalized"); return MSI_ESTATE; }
+  MSI_CUDA(cudaDeviceSynchronize());
+  MSI_CUDA(cudaMemset(c->heap, 0, c->my_layout.ctrl_bytes));  // counters, tickets, uses, status, count table
+  MSI_CUDA(cudaMemset(c->workspace, 0, c->ws_bytes));
+  MSI_CUDA(cudaDeviceSynchronize());
+  return 0;
+}
+
 extern "C" int msi_ctx_buffer(msi_ctx* c, int which, int slot, void** ptr, size_t* bytes) {
   if (!c || !ptr || !bytes || slot < 0 || slot >= c->plan.slots) { set_error("msi_ctx_buffer: bad argument"); return MSI_EINVAL; }
   const Layout& L = c->my_layout;
@@ -802,11 +820,7 @@ extern "C" int msi_dispatch(msi_ctx* c, const void* x, const int32_t* cnt, const
     // TMA variant: 8 warps per CTA, one token row buffer each, a warp per token
     constexpr int kThr = 256;
     const size_t smem = table + (kThr / 32) * ((size_t)c->plan.hidden * 2 + 8);
-    static size_t attr = 0;
-    if (smem > attr) {
-      MSI_CUDA(cudaFuncSetAttribute(dispatch_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = smem;
-    }
+    if (int rc = smem_attr(reinterpret_cast<const void*>(dispatch_kernel<true>), smem)) return rc;
     int grid = (T + kThr / 32 - 1) / (kThr / 32);
     grid = grid < 1 ? 1 : (grid > 2 * num_sms() ? 2 * num_sms() : grid);
     MSI_CUDA(launch_k(dispatch_kernel<true>, dim3(grid), dim3(kThr), smem, st, c->dev,
@@ -945,12 +959,4 @@ extern "C" int msi_combine_local(const void* y, const float* w, const void* resi
       reinterpret_cast<const char*>(y), w, reinterpret_cast<const uint16_t*>(resid),
       reinterpret_cast<uint16_t*>(out), T, K, H, 1, nullptr, 0, 0, nullptr, 0, nullptr, nullptr);
   return check_launch("combine_kernel");
-}
-
-extern "C" int msi_attn_standin(const void* kv, size_t kv_bytes, float* checksum, void* stream) {
-  MSI_REQUIRE(kv && checksum && kv_bytes % 16 == 0, "msi_attn_standin: bad argument");
-  if (kv_bytes == 0) return 0;
-  attn_standin_kernel<<<4 * num_sms(), 512, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<const uint4*>(kv), kv_bytes / 16, checksum);
-  return check_launch("attn_standin_kernel");
 }

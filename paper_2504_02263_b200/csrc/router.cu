@@ -565,7 +565,7 @@ int launch(const void* x, const void* wg, int T, int H, int E, int K, int BT, in
   if (!stage && TT * TE > 16 && nh_bytes > head && nh_bytes <= 200 * 1024) head = nh_bytes;
   const size_t smem = ((head + 15) & ~size_t(15)) + (stage ? wbytes : 0);
   auto kern = stage ? gate_topk_kernel<TT, TE, true> : gate_topk_kernel<TT, TE, false>;
-  if (smem > 48 * 1024) MSI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (int arc = smem_attr(reinterpret_cast<const void*>(kern), smem)) return arc;
   MSI_CUDA(launch_k(kern, dim3(nblk), dim3(kWarps * 32), smem, st, reinterpret_cast<const __nv_bfloat16*>(x),
                     reinterpret_cast<const __nv_bfloat16*>(wg), T, H, E, K, BT, idx, w, cnt, slot,
                     reinterpret_cast<int32_t*>(ws), pl, smem));
@@ -594,11 +594,7 @@ int launch_split(const void* x, const void* wg, int T, int H, int E, int K, int 
   size_t head = logit_smem_bytes(BT, E);
   if (head < (size_t)pl.P * 4) head = (size_t)pl.P * 4;
   const size_t smem = (head + 15) & ~size_t(15);
-  static size_t attr = 48 * 1024;
-  if (smem > attr) {
-    MSI_CUDA(cudaFuncSetAttribute(route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  if (int arc = smem_attr(reinterpret_cast<const void*>(route_kernel), smem)) return arc;
   MSI_CUDA(launch_k(route_kernel, dim3((T + BT - 1) / BT), dim3(kWarps * 32), smem, st, (const float*)logits, T, E, K,
                     BT, idx, w, cnt, slot, reinterpret_cast<int32_t*>(ws), pl, smem));
   return check_launch("gate_logits_kernel + route_kernel");

@@ -116,11 +116,6 @@ def combine_local(y: torch.Tensor, w: torch.Tensor, resid: torch.Tensor | None =
     return out
 
 
-def attn_standin(kv: torch.Tensor, checksum: torch.Tensor, stream=None):
-    _lib.call("msi_attn_standin", _ptr(kv), kv.numel() * kv.element_size(), _ptr(checksum),
-              _stream(stream))
-
-
 # ---------------------------------------------------------- attention ---- #
 def _check_i32(name, t):
     if t.dtype != torch.int32 or not t.is_cuda or not t.is_contiguous():

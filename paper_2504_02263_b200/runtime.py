@@ -342,15 +342,14 @@ class PingPongRunner:
     Residual: x_{l+1} = x_l + MoE(x_l), written in place by the combine.
     """
 
-    def __init__(self, layer: MoEDecodeLayer, layers: int, kv_bytes: int = 0, record_timeline: bool = False,
+    def __init__(self, layer: MoEDecodeLayer, layers: int, record_timeline: bool = False,
                  chain: bool = True, attn: list | None = None):
         self.layer = layer
         self.L = layers
         g = layer.g
         # attn: one attention.AttentionStage per micro-batch (attention ranks):
         # the real decode attention layer whose output feeds the MoE layer.
-        # Without it, kv_bytes > 0 runs the HBM stand-in and the MoE layer
-        # reads x directly.
+        # Without it the MoE layer reads x directly.
         self.attn = attn if g.is_attention else None
         if self.attn is not None and len(self.attn) != g.plan.m:
             raise ValueError("need one AttentionStage per micro-batch")
@@ -363,11 +362,6 @@ class PingPongRunner:
         if not chain and g.is_attention:
             self.outs = [torch.empty((g.plan.b_a, g.model.hidden), dtype=torch.bfloat16, device=g.device)
                          for _ in range(g.plan.m)]
-        self.kv = None
-        if kv_bytes and g.is_attention:
-            self.kv = torch.empty(kv_bytes // 2, dtype=torch.bfloat16, device=g.device)
-            self.kv.normal_()
-            self.checksum = torch.zeros(1, dtype=torch.float32, device=g.device)
         self.record = record_timeline
         self.events = []
 
@@ -375,8 +369,6 @@ class PingPongRunner:
         """Attention stage of micro-batch j, layer l -> the MoE layer's input."""
         if self.attn is not None:
             return self.attn[j].forward(x, l)
-        if self.kv is not None:
-            ops.attn_standin(self.kv, self.checksum)
         return x
 
     def _out(self, xs, j):

@@ -2,7 +2,8 @@
 memory (one process per GPU), checked against the oracle's multi-sender
 layer: routing / counts / placement bit-exact on every rank, expert outputs
 and layer outputs within tolerance, combine bit-exact given the GPU's own
-expert outputs.  Skipped when the box has fewer GPUs than the plan needs.
+expert outputs.  On a box with fewer GPUs than the plan has ranks, ranks share
+GPUs round-robin (MSI_TEST_NO_OVERSUBSCRIBE=1 skips those plans instead).
 """
 
 import os
@@ -35,7 +36,7 @@ def _worker(rank, world, port, n_a, n_e, colo, shape, tokens, m, layers, outdir,
     from paper_2504_02263_b200 import ops, runtime
     from paper_2504_02263_b200.config import DeploymentPlan, as_model_spec
 
-    gpu = rank % torch.cuda.device_count()  # > 1 rank per GPU only with MSI_TEST_OVERSUBSCRIBE=1
+    gpu = rank % torch.cuda.device_count()  # fewer GPUs than ranks: ranks share GPUs round-robin
     torch.cuda.set_device(gpu)
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     model = as_model_spec(shape)
@@ -117,8 +118,12 @@ def test_m2n_multi_gpu(lib, tmp_path, n_a, n_e, colo, shape, tokens, m, layers, 
     from paper_2504_02263_b200.config import as_model_spec
 
     world = n_a if colo else n_a + n_e
-    if torch.cuda.device_count() < world and os.environ.get("MSI_TEST_OVERSUBSCRIBE") != "1":
+    if torch.cuda.device_count() < world and os.environ.get("MSI_TEST_NO_OVERSUBSCRIBE") == "1":
         pytest.skip(f"needs {world} GPUs, box has {torch.cuda.device_count()}")
+    # On a box with fewer GPUs than ranks the ranks share GPUs round-robin (one
+    # process per rank, CUDA IPC between processes on one device works the same
+    # way; the device-side waits just time-slice).  Numerics and placement are
+    # identical; only timing is meaningless there.
     model = as_model_spec(shape)
     slots = None
     if balanced == "skew":  # experts 0 and 4 hot: replicated over both expert GPUs

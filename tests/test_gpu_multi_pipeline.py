@@ -43,11 +43,12 @@ def _worker(rank, world, port, n_a, n_e, shape, T, m, L, outdir):
     from paper_2504_02263_b200 import ops, runtime
     from paper_2504_02263_b200.config import DeploymentPlan, as_model_spec
 
-    torch.cuda.set_device(rank)
+    gpu = rank % torch.cuda.device_count()  # fewer GPUs than ranks: share round-robin
+    torch.cuda.set_device(gpu)
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     model = as_model_spec(shape)
     plan = DeploymentPlan(n_a=n_a, n_e=n_e, m=m, b_a=T)
-    g = runtime.M2NGroup(model, plan, rank=rank, device=f"cuda:{rank}", timeout_s=30)
+    g = runtime.M2NGroup(model, plan, rank=rank, device=f"cuda:{gpu}", timeout_s=60)
     wts = O.synth_weights(model.hidden, model.intermediate, model.experts, seed=0)
 
     def dev(a):
@@ -61,8 +62,8 @@ def _worker(rank, world, port, n_a, n_e, shape, T, m, L, outdir):
     stages, xs = None, None
     if g.is_attention:
         wg = dev(wts.wg)
-        w = A.AttentionWeights(model, f"cuda:{rank}", seed=5)
-        stages = [A.AttentionStage(model, T, L, f"cuda:{rank}", weights=w, avg_seq_len=80,
+        w = A.AttentionWeights(model, f"cuda:{gpu}", seed=5)
+        stages = [A.AttentionStage(model, T, L, f"cuda:{gpu}", weights=w, avg_seq_len=80,
                                    seed=100 * g.attn_index + j, headroom=64) for j in range(m)]
         xs = [dev(O.synth_tokens(T, model.hidden, seed=7 * g.attn_index + j)) for j in range(m)]
     layer = runtime.MoEDecodeLayer(g, wg=wg, w13=w13, w2=w2)
@@ -119,7 +120,7 @@ def test_pingpong_attention_multi_gpu(lib, tmp_path, n_a, n_e, T, m, L):
     from paper_2504_02263_b200.config import as_model_spec
 
     world = n_a + n_e
-    if torch.cuda.device_count() < world:
+    if torch.cuda.device_count() < world and os.environ.get("MSI_TEST_NO_OVERSUBSCRIBE") == "1":
         pytest.skip(f"needs {world} GPUs")
     model = as_model_spec("tiny")
     mp.spawn(_worker, args=(world, _free_port(), n_a, n_e, "tiny", T, m, L, str(tmp_path)), nprocs=world,
