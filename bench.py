@@ -119,7 +119,7 @@ def parse():
     ap.add_argument("--colocated", action="store_true",
                     help="every GPU is both an attention and an expert GPU (DeepSeek-V3-shaped config 5)")
     ap.add_argument("--no-merge", dest="merge", action="store_false",
-                    help="N=1 co-located: keep m separate micro-batches instead of one merged batch")
+                    help="co-located layouts (any N): keep m separate micro-batches instead of one merged batch")
     ap.add_argument("--no-m2n", action="store_true", help="skip the M2N round-trip p50 measurement")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch eagerly from Python instead of replaying a captured CUDA graph")
@@ -227,67 +227,45 @@ def measured_peaks() -> dict:
 _CPU_CACHE = {}
 
 
-def cpu_sample(model, b_a: int, threads: int, attn: bool = True) -> dict:
-    """The oracle (CPU restatement, oracle/) on a bounded sample of one
-    micro-batch of the workload: the attention stage on a 32-sequence sample
-    (QKV projection, RoPE + KV append, paged attention at s = 730, output
-    projection), router over all b_a tokens, one expert's SwiGLU FFN over its
-    share of rows (b_a*K/E), combine over b_a tokens; the layer time is
-    projected as (b_a/32) x attention + router + E x expert + combine."""
-    import numpy as np
+def cpu_layer(model, T: int, attn: bool = True, steps: int = 1, warmup: int = 0, seed: int = 0) -> dict:
+    """The CPU baseline: oracle.CpuDecodeLayer (oracle/) executes the whole
+    layer step for the T tokens of one attention GPU's step on the host cores
+    -- attention stage over every sequence's paged KV cache (s = 730 mean),
+    router + placement, every expert's SwiGLU FFN over its routed rows, combine
+    -- nothing sampled or projected.  Returns the median over ``steps`` timed
+    steps after ``warmup`` untimed ones."""
     from oracle import oracle as O
+    from paper_2504_02263_b200.attention import ROPE_THETA, head_layout
     from paper_2504_02263_b200.config import WorkloadSpec
 
-    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
-    H, Hp, E, K = model.hidden, model.intermediate, model.experts, model.topk
-    key = (model.name, b_a)
-    S = 32
-    if key not in _CPU_CACHE:  # inputs are not part of the timed sample
-        rng = np.random.default_rng(3)
-        n_heads = H // 128
-        g = max(1, min(model.gqa_group, n_heads))
-        while n_heads % g:
-            g -= 1
-        n_kv = n_heads // g
-        ctx = rng.integers(1, 2 * WorkloadSpec().avg_seq_len, size=S).astype(np.int32)
-        need = (ctx + 1 + 63) // 64
-        bt = np.zeros((S, int(need.max())), np.int32)
-        off = 0
-        for t in range(S):
-            bt[t, : need[t]] = np.arange(off, off + need[t])
-            off += need[t]
-        kc = O.bf16_round(rng.standard_normal((off, n_kv, 64, 128), dtype=np.float32))
-        vc = O.bf16_round(rng.standard_normal((off, n_kv, 64, 128), dtype=np.float32))
-        wqkv = O.bf16_round(rng.standard_normal(((n_heads + 2 * n_kv) * 128, H), dtype=np.float32) / np.sqrt(H))
-        wo = O.bf16_round(rng.standard_normal((H, n_heads * 128), dtype=np.float32) / np.sqrt(H))
-        _CPU_CACHE[key] = (O.synth_tokens(b_a, H, seed=1), O.synth_weights(H, Hp, E, seed=0, experts=[0]),
-                           (wqkv, wo, ctx, n_heads, n_kv, bt, kc, vc))
-    x, wts, (wqkv, wo, ctx, n_heads, n_kv, bt, kc, vc) = _CPU_CACHE[key]
-    t_attn = 0.0
-    if attn:
-        t0 = time.perf_counter()
-        O.attention_stage(x[:S], wqkv, wo, ctx, n_heads, n_kv, 1e6, bt, kc, vc)
-        t_attn = (time.perf_counter() - t0) * b_a / S
-    t0 = time.perf_counter()
-    idx, w = O.router(x, wts.wg, K)
-    cnt, slot = O.place(idx, E)
-    t_router = time.perf_counter() - t0
-    rows = max(1, b_a * K // E)
-    t0 = time.perf_counter()
-    O.expert_ffn(x[:rows], wts.w_gate[0], wts.w_up[0], wts.w_down[0])
-    t_expert = time.perf_counter() - t0
-    y = np.zeros((b_a, K, H), np.uint16)
-    t0 = time.perf_counter()
-    O.combine(y, w, x)
-    t_comb = time.perf_counter() - t0
-    t_layer = t_attn + t_router + E * t_expert + t_comb
-    return {"tokens_per_s": b_a / t_layer, "t_attention_s": t_attn, "t_router_s": t_router, "t_expert_s": t_expert,
-            "t_combine_s": t_comb, "t_layer_s": t_layer,
-            "sample": (f"1 micro-batch of {b_a} tokens: attention stage on {S} sequences (s=730 mean) scaled to "
-                       f"{b_a}, router+placement (all tokens), SwiGLU FFN of 1 of {E} experts ({rows} rows) x{E}, "
-                       "combine; numpy/OpenBLAS fp32 + C oracle") if attn else
-                      (f"1 micro-batch of {b_a} tokens: router+placement (all tokens), SwiGLU FFN of 1 of {E} "
-                       f"experts ({rows} rows) x{E}, combine; numpy/OpenBLAS fp32 + C oracle")}
+    key = (model.name, T, attn)
+    if key not in _CPU_CACHE:  # inputs and weights are not part of the timed step
+        n_heads, n_kv = head_layout(model)
+        ctx = np.random.default_rng(seed + 3).integers(1, 2 * WorkloadSpec().avg_seq_len, size=T).astype(np.int32)
+        lay = O.CpuDecodeLayer(model.hidden, model.intermediate, model.experts, model.topk, T, n_heads, n_kv, ctx,
+                               theta=ROPE_THETA, seed=seed)
+        _CPU_CACHE[key] = (lay, O.fill_normal((T, model.hidden), seed + 5))
+    lay, x = _CPU_CACHE[key]
+    times, phases = [], []
+    for i in range(warmup + steps):
+        if attn:
+            _, ph = lay.step(x)
+        else:
+            t0 = time.perf_counter()
+            lay.moe(x)
+            ph = {"attention_s": 0.0, "moe_s": time.perf_counter() - t0}
+            ph["layer_s"] = ph["moe_s"]
+        if i >= warmup:
+            times.append(ph["layer_s"])
+            phases.append(ph)
+    t = statistics.median(times)
+    ph = phases[times.index(t)] if t in times else phases[-1]
+    return {"tokens_per_s": T / t, "t_layer_s": t, "t_attention_s": ph["attention_s"], "t_moe_s": ph["moe_s"],
+            "sample": (f"the whole layer step for {T} tokens per step (one attention GPU's m x b_a), no sampling: "
+                       + ("attention stage (QKV projection, RoPE + paged-KV append, GQA decode over every "
+                          "sequence's cache at s = 730 mean, output projection + residual), " if attn else "")
+                       + f"router + placement, SwiGLU FFN of all {model.experts} experts over their routed rows, "
+                       "combine; oracle/ (numpy/OpenBLAS fp32 GEMMs + OpenMP C)")}
 
 
 def eq5_report(all_stages: list, plan, L: int, ms_per_step: float, colocated: bool) -> dict:
@@ -518,75 +496,72 @@ def cpu_model_name() -> str:
     return "unknown"
 
 
-def run_reference(args):
-    """--impl reference: the reference ships no implementation of this path
-    (SURVEY.md §0); its CPU restatement (oracle/) is timed on the host cores."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
+def _u16(t) -> "np.ndarray":
+    return t.detach().contiguous().view(__import__("torch").int16).cpu().numpy().view(np.uint16)
+
+
+def parity_check(layer, g, runner, att_stages, xs, wg, w13, w2, model, n_experts_checked: int = 2) -> dict | None:
+    """Oracle parity of the bench's own data, outside the timed region: the
+    MoE input of micro-batch 0 at the last layer of the last timed step (the
+    attention stage's output) and what the GPU made of it.  Routing (idx, w,
+    cnt, slot) must be bit-exact; the combine is bit-exact
+    given the GPU's expert outputs; on a rank that holds every expert (N = 1)
+    the outputs of ``n_experts_checked`` experts are compared with the
+    oracle's SwiGLU within the bf16 tolerance (rel-L2 <= 5e-3, max-abs <=
+    2^-7 max|ref|).  Returns None on ranks without the attention role."""
+    from oracle import oracle as O
+
+    if not g.is_attention:
+        return None
+    r = layer._routes[0]
+    T, K = r.T, model.topk
+    h = att_stages[0].y[:T] if att_stages else xs[0][:T]
+    hx = _u16(h)
+    idx_r, w_r = O.router(hx, _u16(wg), K)
+    dest_r = idx_r if g.slots is None else O.physical_slots(idx_r, g.slots.rep, g.attn_index)
+    cnt_r, slot_r = O.place(dest_r, g.P)
+    rep = {"checked_on": "micro-batch 0, last layer of the last timed step (outside the timed region)",
+           "tokens": T,
+           "routing_bit_exact": bool(np.array_equal(r.idx[:T].cpu().numpy(), idx_r)
+                                     and np.array_equal(r.w[:T].cpu().numpy().view(np.uint32), w_r.view(np.uint32))
+                                     and np.array_equal(r.dest[:T].cpu().numpy(), dest_r)
+                                     and np.array_equal(r.cnt.cpu().numpy(), cnt_r)
+                                     and np.array_equal(r.slot[:T].cpu().numpy(), slot_r))}
+    tp = g.plan.tp_e
+    ybuf = _u16(g.ybuf_view(0)[:T])
+    yk = ybuf.reshape(T, K * tp, model.hidden)
+    out = _u16(runner._out([x for x in xs], 0)[:T]) if xs else None
+    if out is not None:
+        rep["combine_bit_exact"] = bool(np.array_equal(out, O.combine(yk, np.repeat(w_r, tp, axis=1), hx)))
+    if g.is_expert and g.plan.n_e == 1 and tp == 1 and g.slots is None and w13 is not None:
+        rels, ok = {}, True
+        loads = np.bincount(idx_r.ravel(), minlength=model.experts)
+        for e in sorted({int(np.argmax(loads)), int(np.argmin(loads))} | {0})[:n_experts_checked]:
+            t, k = np.nonzero(idx_r == e)
+            order = np.argsort(slot_r[t, k])
+            t, k = t[order], k[order]
+            two_hp = w13.shape[1]
+            v = w13[e].view(two_hp // 256, 2, 2, 64, model.hidden)  # msi_pack_w13 layout -> gate / up
+            gate, up = _u16(v[:, :, 0].reshape(two_hp // 2, -1)), _u16(v[:, :, 1].reshape(two_hp // 2, -1))
+            ref = O.bf16_to_f32(O.expert_ffn(hx[t], gate, up, _u16(w2[e]))).astype(np.float64)
+            got = O.bf16_to_f32(ybuf[t, k]).astype(np.float64)
+            rel = float(np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30))
+            mx = float(np.abs(got - ref).max()) / max(float(np.abs(ref).max()), 1e-30)
+            rels[int(e)] = {"rows": int(len(t)), "rel_l2": rel, "max_abs_over_max_ref": mx}
+            ok &= rel <= 5e-3 and mx <= 2.0 ** -7
+        rep["experts"] = rels
+        rep["experts_within_tolerance"] = bool(ok)
+    return rep
+
+
+def resolve_layout(args, world: int):
+    """(n_a, n_e, colocated, plan_source, tp_e, model, m, b_a) of this run --
+    shared by both arms so they describe the same workload."""
     from paper_2504_02263_b200.config import as_model_spec
-    import numpy as np  # noqa: F401
 
-    n_a, n_e, colo, _, _ = (apply_plan_json(args) if args.plan_json else
-                            choose_split(args.gpus, args.shape, args.plan, args.split, args.colocated))
-    model = as_model_spec(args.shape)
-    threads = len(os.sched_getaffinity(0))
-    # the GPU arm's micro-batch (co-located: m micro-batches merged)
-    b_a = args.m * args.b_a if (colo and args.merge) else args.b_a
-    vals = []
-    info = None
-    for i in range(args.warmup + args.steps):
-        info = cpu_sample(model, b_a, threads, attn=args.attn == "real")
-        if i >= args.warmup:
-            vals.append(info["tokens_per_s"])
-    v = statistics.median(vals)
-    line = {"impl": "reference", "metric": "decode tokens/s/GPU (MoE layer, ping-pong); M2N dispatch+combine p50 µs",
-            "value": v, "unit": "layer-tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * b_a / v, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"{model.name} MoE layer, CPU oracle (reference has no implementation)",
-                       "hidden": model.hidden, "intermediate": model.intermediate, "experts": model.experts,
-                       "topk": model.topk, "b_a": b_a, "m": 1 if (colo and args.merge) else args.m,
-                       "attention_stage": args.attn},
-            "cpu_baseline": {"value": v, "unit": "layer-tokens/s", "cores": threads, "kind": "port",
-                             "sample": info["sample"], "cpu": cpu_model_name()},
-            "e2e": {"value": v, "unit": "layer-tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
-
-
-# --------------------------------------------------------------- GPU leg ----
-def main():
-    args = parse()
-    if args.impl == "reference":
-        run_reference(args)
-        return
-    import torch
-    import torch.distributed as dist
-
-    from paper_2504_02263_b200 import runtime
-    from paper_2504_02263_b200.config import DeploymentPlan, WorkloadSpec, as_model_spec
-
-    rank, world, local = runtime.init_distributed_from_env("gloo" if _over() else "nccl")
-    if world != args.gpus:
-        if rank == 0:
-            print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}))
-        sys.exit(2)
-    if args.plan_json:
-        n_a, n_e, colo, plan_source, tp_e = apply_plan_json(args)
-        if (n_a if colo else n_a + n_e) != world:
-            raise SystemExit(f"--plan-json needs {n_a if colo else n_a + n_e} ranks, WORLD_SIZE={world}")
-    else:
-        n_a, n_e, colo, plan_source, tp_e = choose_split(world, args.shape, args.plan, args.split,
-                                                         args.colocated, args.tp_e)
-    model = as_model_spec(args.shape)
-    m_eff, b_a = args.m, args.b_a
-    if colo and args.merge:
-        # One co-located GPU has no ping-pong partner: its m micro-batches are
-        # merged into one batch (same tokens per step, expert weights streamed
-        # once per layer instead of m times).
-        m_eff, b_a = 1, args.m * args.b_a
+    n_a, n_e, colo, plan_source, tp_e, model, m_eff, b_a = resolve_layout(args, world)
     args.b_a = b_a
-    plan = DeploymentPlan(n_a=n_a, n_e=n_e, m=m_eff, b_a=b_a, colocated=colo, tp_e=1 if colo else tp_e)
+    plan = DeploymentPlan(n_a=n_a, n_e=n_e, m=m_eff, b_a=b_a, colocated=colo, tp_e=tp_e)
     dev = torch.device(f"cuda:{local}")
     gen = torch.Generator(device=dev)
     gen.manual_seed(1 + rank)
@@ -703,6 +678,14 @@ def main():
     st = g.status()
     if st != 0:
         raise RuntimeError(f"device status {st} (timeout in a device-side wait)")
+    parity = parity_check(layer, g, runner, att_stages, xs, wg, w13, w2, model)
+    if world > 1:
+        allp = [None] * world
+        dist.all_gather_object(allp, parity)
+        ranks = [p for p in allp if p is not None]
+        parity = {"per_attention_rank": ranks,
+                  "routing_bit_exact": all(p["routing_bit_exact"] for p in ranks),
+                  "combine_bit_exact": all(p.get("combine_bit_exact", True) for p in ranks)}
     ffn_ms = [s.elapsed_time(e) for s, e in ffn_events]
     attn_ms = [s.elapsed_time(e) for s, e in attn_events]
     for stg in att_stages or []:
@@ -882,20 +865,7 @@ def main():
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights seed 0, N(0,1) tokens)",
-        "config": {"workload": f"{model.name}-shaped MoE layer, " +
-                   (f"co-located {world} GPU" + ("s (every GPU both roles, M2N all-to-all)" if world > 1 else "")
-                    if colo else f"{n_a} attention + {n_e} expert GPUs"),
-                   "plan_source": plan_source,
-                   "hidden": model.hidden, "intermediate": model.intermediate, "experts": model.experts,
-                   "topk": model.topk, "n_a": n_a, "n_e": n_e, "m": plan.m, "b_a": args.b_a,
-                   "tokens_per_step_per_attention_gpu": plan.m * args.b_a * args.layers,
-                   "microbatching": ("co-located: m micro-batches merged into one batch (no ping-pong partner)"
-                                     if colo and args.merge else "ping-pong, m micro-batches"),
-                   "L_sim": args.layers, "attention_stage": args.attn,
-                   "l2": (f"working set (expert weights {model.experts * 3 * model.hidden * model.intermediate * 2 / 1e9:.1f} GB"
-                          " + KV cache) >> 126 MB L2; no flush needed"),
-                   "parallelism": f"dp{n_a}-ep{n_e}" + (f"-etp{plan.tp_e}" if plan.tp_e > 1 else ""),
-                   "launch": "CUDA graph per rank (device-tracked epochs)" if args.graph else "eager"},
+        "config": bench_config(args, model, n_a, n_e, colo, plan_source, plan.tp_e, plan.m, args.b_a, world),
         "roofline": {"bound": "tensor", "kernel": "expert FFN (grouped_gemm_kernel x2: gate/up+SiLU, down+N2M)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None,
@@ -906,6 +876,7 @@ def main():
                      "frac_nominal_dense": (achieved / 2250.0) if achieved else None,
                      "flops_per_launch_pair": flops_per_call, "avg_launch_pair_ms": ffn_avg_s * 1e3,
                      "peak_kind": "measured bf16_tflops_sustained (MEASURED_PEAKS.json)"},
+        "parity": parity,
         "e2e": e2e,
         "gpu_launches": None,
         "clocks": clocks,
@@ -926,11 +897,11 @@ def main():
     line["gpu_launches"] = per_step * args.steps
     if not args.no_cpu and world == 1:  # the CPU baseline is timed at N = 1 only
         threads = len(os.sched_getaffinity(0))
-        cs = cpu_sample(model, args.b_a, threads, attn=args.attn == "real")
+        cs = cpu_layer(model, plan.m * args.b_a, attn=args.attn == "real", steps=1, warmup=1)
         line["cpu_baseline"] = {"value": cs["tokens_per_s"], "unit": "layer-tokens/s", "cores": threads,
                                 "kind": "port", "sample": cs["sample"], "cpu": cpu_model_name(),
-                                "t_attention_s": cs["t_attention_s"], "t_router_s": cs["t_router_s"],
-                                "t_expert_s": cs["t_expert_s"]}
+                                "t_layer_s": cs["t_layer_s"], "t_attention_s": cs["t_attention_s"],
+                                "t_moe_s": cs["t_moe_s"]}
     print(json.dumps(line), flush=True)
     g.close()
     if world > 1:

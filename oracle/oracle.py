@@ -66,6 +66,10 @@ def lib():
         L.orc_bf16_round.restype = None
         L.orc_swiglu.argtypes = [P, P, P, ctypes.c_size_t]
         L.orc_swiglu.restype = None
+        L.orc_decode_attention.argtypes = [P, P, P, P, i, P, i, i, i, ctypes.c_float, P]
+        L.orc_decode_attention.restype = None
+        L.orc_fill_normal.argtypes = [P, P, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_float]
+        L.orc_fill_normal.restype = None
         L.msi_det_expf.argtypes = [ctypes.c_float]
         L.msi_det_expf.restype = ctypes.c_float
         _LIB = L
@@ -399,3 +403,117 @@ def attention_stage(x: np.ndarray, wqkv: np.ndarray, wo: np.ndarray, pos: np.nda
     q = rope_append(qkv, pos, n_heads, n_kv, theta, block_table, k_cache, v_cache)
     o = decode_attention(q, k_cache, v_cache, block_table, pos.astype(np.int64) + 1)
     return bf16_round(bf16_to_f32(x) + bf16_to_f32(o) @ bf16_to_f32(wo).T)
+
+
+def decode_attention_c(q: np.ndarray, k_cache: np.ndarray, v_cache: np.ndarray, block_table: np.ndarray,
+                       seq_lens: np.ndarray, scale: float | None = None) -> np.ndarray:
+    """``decode_attention`` in C (OpenMP over (sequence, KV head)): same fp32
+    math, different summation order (tests/test_oracle.py checks agreement).
+    Used by the CPU baseline, which runs the whole attention stage."""
+    q = np.ascontiguousarray(q, np.uint16)
+    T, nh, d = q.shape
+    if d != HEAD_DIM:
+        raise ValueError("head dim must be 128")
+    n_kv = k_cache.shape[1]
+    if nh % n_kv or nh // n_kv > 16:
+        raise ValueError("need n_heads = G * n_kv with G <= 16")
+    scale = 1.0 / np.sqrt(d) if scale is None else scale
+    bt = np.ascontiguousarray(block_table, np.int32)
+    lens = np.ascontiguousarray(seq_lens, np.int32)
+    out = np.empty((T, nh * d), np.uint16)
+    lib().orc_decode_attention(_p(q), _p(np.ascontiguousarray(k_cache)), _p(np.ascontiguousarray(v_cache)),
+                               _p(bt), bt.shape[1], _p(lens), T, nh, n_kv, float(scale), _p(out))
+    return out
+
+
+def fill_normal(shape, seed: int, scale: float = 1.0, as_f32: bool = False) -> np.ndarray:
+    """N(0, scale^2) rounded to bf16 (uint16 bits, or the same values as fp32),
+    generated in parallel in C (synthetic inputs for the CPU baseline)."""
+    n = int(np.prod(shape))
+    if as_f32:
+        out = np.empty(shape, np.float32)
+        lib().orc_fill_normal(_p(out), None, n, seed, float(scale))
+    else:
+        out = np.empty(shape, np.uint16)
+        lib().orc_fill_normal(None, _p(out), n, seed, float(scale))
+    return out
+
+
+# ------------------------------------------------- CPU baseline layer ------ #
+class CpuDecodeLayer:
+    """The bench's decode layer step on the host cores (the CPU baseline the
+    GPU path is timed against; the reference ships no implementation of the
+    path): for T tokens of one attention GPU's step, the whole
+    co-located layer with the oracle's arithmetic --
+
+      attention stage  x W_qkv^T, RoPE + paged-KV append, GQA decode over the
+                       paged cache (``decode_attention_c``), + x + o W_o^T
+      router           ``router`` + ``place`` (bit-exact contract)
+      experts          SwiGLU of every expert over its routed rows (fp32 BLAS,
+                       bf16 rounding at H and Y)
+      combine          ``combine`` with the attention output as residual
+
+    Weights are held as fp32 copies of bf16 values (a CPU keeps its GEMM
+    operands in the format its BLAS runs); the KV cache is bf16 pages.  No
+    part of a step is sampled or projected."""
+
+    def __init__(self, H: int, Hp: int, E: int, K: int, T: int, n_heads: int, n_kv: int,
+                 ctx: np.ndarray, theta: float = 1e6, seed: int = 0):
+        self.H, self.Hp, self.E, self.K, self.T = H, Hp, E, K, T
+        self.n_heads, self.n_kv, self.theta = n_heads, n_kv, theta
+        s = seed * 1000
+        self.wg = fill_normal((E, H), s + 1, 1.0 / np.sqrt(H))
+        self.w_gate = [fill_normal((Hp, H), s + 10 + e, 1.0 / np.sqrt(H), as_f32=True) for e in range(E)]
+        self.w_up = [fill_normal((Hp, H), s + 100 + e, 1.0 / np.sqrt(H), as_f32=True) for e in range(E)]
+        self.w_down = [fill_normal((H, Hp), s + 200 + e, 1.0 / np.sqrt(Hp), as_f32=True) for e in range(E)]
+        width = (n_heads + 2 * n_kv) * HEAD_DIM
+        self.wqkv = fill_normal((width, H), s + 300, 1.0 / np.sqrt(H), as_f32=True)
+        self.wo = fill_normal((H, n_heads * HEAD_DIM), s + 301, 1.0 / np.sqrt(n_heads * HEAD_DIM), as_f32=True)
+        self.ctx = np.asarray(ctx, np.int32)
+        need = (self.ctx.astype(np.int64) + 1 + KV_PAGE - 1) // KV_PAGE
+        self.pages = int(need.sum())
+        rng = np.random.default_rng(seed + 7919)
+        perm = rng.permutation(self.pages).astype(np.int32)
+        self.bt = np.zeros((T, int(need.max())), np.int32)
+        off = 0
+        for t in range(T):
+            self.bt[t, : need[t]] = perm[off: off + need[t]]
+            off += need[t]
+        self.k_cache = fill_normal((self.pages, n_kv, KV_PAGE, HEAD_DIM), s + 400)
+        self.v_cache = fill_normal((self.pages, n_kv, KV_PAGE, HEAD_DIM), s + 401)
+
+    def attention(self, x: np.ndarray) -> np.ndarray:
+        qkv = bf16_round(bf16_to_f32(x) @ self.wqkv.T)
+        q = rope_append(qkv, self.ctx, self.n_heads, self.n_kv, self.theta, self.bt, self.k_cache, self.v_cache)
+        o = decode_attention_c(q, self.k_cache, self.v_cache, self.bt, self.ctx.astype(np.int64) + 1)
+        return bf16_round(bf16_to_f32(x) + bf16_to_f32(o) @ self.wo.T)
+
+    def moe(self, h: np.ndarray) -> np.ndarray:
+        idx, w = router(h, self.wg, self.K)
+        cnt, slot = place(idx, self.E)
+        y = np.zeros((h.shape[0], self.K, self.H), np.uint16)
+        hf = bf16_to_f32(h)
+        for e in range(self.E):
+            t, k = np.nonzero(idx == e)
+            if len(t) == 0:
+                continue
+            order = np.argsort(slot[t, k], kind="stable")  # receive order
+            t, k = t[order], k[order]
+            xe = hf[t]
+            g = np.ascontiguousarray(xe @ self.w_gate[e].T)
+            u = np.ascontiguousarray(xe @ self.w_up[e].T)
+            act = np.empty(g.shape, np.uint16)
+            lib().orc_swiglu(_p(g), _p(u), _p(act), g.size)
+            y[t, k] = bf16_round(bf16_to_f32(act) @ self.w_down[e].T)
+        return combine(y, w, h)
+
+    def step(self, x: np.ndarray) -> tuple[np.ndarray, dict]:
+        """One layer step: x bf16 [T, H] -> layer output bf16 [T, H] and the
+        per-phase seconds."""
+        import time
+        t0 = time.perf_counter()
+        h = self.attention(x)
+        t1 = time.perf_counter()
+        out = self.moe(h)
+        t2 = time.perf_counter()
+        return out, {"attention_s": t1 - t0, "moe_s": t2 - t1, "layer_s": t2 - t0}

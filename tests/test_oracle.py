@@ -198,3 +198,52 @@ def test_expert_tp_partials_sum_to_the_full_layer():
         assert_close_bf16(r2.out[s], r1.out[s], "tp layer output")
     np.testing.assert_array_equal(r1.cnt, r2.cnt)
     assert [len(l[0]) for l in r2.layout] == [4, 4]  # 2 nodes x E_l = 4
+
+
+def test_decode_attention_c_matches_numpy():
+    """The C attention used by the CPU baseline agrees with the readable numpy
+    restatement (fp32 both; only the summation order differs)."""
+    rng = np.random.default_rng(0)
+    T, nh, nkv = 5, 12, 3
+    lens = np.array([1, 64, 65, 200, 17], np.int32)
+    need = (lens + 63) // 64
+    bt = np.zeros((T, need.max()), np.int32)
+    perm = rng.permutation(need.sum()).astype(np.int32)
+    off = 0
+    for t in range(T):
+        bt[t, :need[t]] = perm[off:off + need[t]]
+        off += need[t]
+    kc = O.fill_normal((need.sum(), nkv, 64, 128), 1)
+    vc = O.fill_normal((need.sum(), nkv, 64, 128), 2)
+    q = O.fill_normal((T, nh, 128), 3, 0.2)
+    a = O.bf16_to_f32(O.decode_attention(q, kc, vc, bt, lens)).astype(np.float64)
+    b = O.bf16_to_f32(O.decode_attention_c(q, kc, vc, bt, lens)).astype(np.float64)
+    assert np.abs(a - b).max() <= 2 ** -7 * np.abs(a).max()
+    assert np.linalg.norm(a - b) / np.linalg.norm(a) < 1e-3
+
+
+def test_fill_normal_thread_independent_and_normal():
+    a = O.fill_normal((1 << 16,), 7, as_f32=True)
+    b = O.bf16_to_f32(O.fill_normal((1 << 16,), 7))
+    np.testing.assert_array_equal(a, b)
+    assert abs(a.mean()) < 0.02 and abs(a.std() - 1.0) < 0.02
+
+
+def test_cpu_decode_layer_matches_oracle_pieces():
+    """The CPU baseline's layer step is the oracle's attention stage followed
+    by the oracle's MoE layer (routing bit-exact, output within tolerance)."""
+    H, Hp, E, K, T = 512, 256, 8, 2, 24
+    ctx = np.random.default_rng(1).integers(1, 150, size=T).astype(np.int32)
+    L = O.CpuDecodeLayer(H, Hp, E, K, T, n_heads=4, n_kv=2, ctx=ctx, seed=3)
+    x = O.fill_normal((T, H), 9)
+    kc, vc = L.k_cache.copy(), L.v_cache.copy()
+    out, ph = L.step(x)
+    assert ph["layer_s"] > 0
+    wq = O.bf16_round(L.wqkv)
+    wo = O.bf16_round(L.wo)
+    h = O.attention_stage(x, wq, wo, ctx.copy(), 4, 2, L.theta, L.bt, kc, vc)
+    wts = O.LayerWeights(L.wg, np.stack([O.bf16_round(w) for w in L.w_gate]),
+                         np.stack([O.bf16_round(w) for w in L.w_up]), np.stack([O.bf16_round(w) for w in L.w_down]))
+    ref = O.moe_layer([h], wts, K, n_e=1, resid=True)
+    from _util import assert_close_bf16
+    assert_close_bf16(out, ref.out[0], "cpu layer")
