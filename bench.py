@@ -559,6 +559,99 @@ def resolve_layout(args, world: int):
     shared by both arms so they describe the same workload."""
     from paper_2504_02263_b200.config import as_model_spec
 
+    if args.plan_json:
+        n_a, n_e, colo, plan_source, tp_e = apply_plan_json(args)
+        if (n_a if colo else n_a + n_e) != world:
+            raise SystemExit(f"--plan-json needs {n_a if colo else n_a + n_e} ranks, WORLD_SIZE={world}")
+    else:
+        n_a, n_e, colo, plan_source, tp_e = choose_split(world, args.shape, args.plan, args.split,
+                                                         args.colocated, args.tp_e)
+    model = as_model_spec(args.shape)
+    m_eff, b_a = args.m, args.b_a
+    if colo and args.merge:
+        # A co-located GPU runs attention and experts on the same SMs, so a
+        # ping-pong partner would only halve its GEMMs: its m micro-batches are
+        # merged into one batch (same tokens per step, expert weights streamed
+        # once per layer instead of m times; DESIGN.md §6 overlap probe).
+        m_eff, b_a = 1, args.m * args.b_a
+    return n_a, n_e, colo, plan_source, (1 if colo else tp_e), model, m_eff, b_a
+
+
+def bench_config(args, model, n_a: int, n_e: int, colo: bool, plan_source: str, tp_e: int, m: int, b_a: int,
+                 world: int) -> dict:
+    """The workload the line describes (identical in both arms' lines)."""
+    return {"workload": f"{model.name}-shaped MoE layer, " +
+            (f"co-located {world} GPU" + ("s (every GPU both roles, M2N all-to-all)" if world > 1 else "")
+             if colo else f"{n_a} attention + {n_e} expert GPUs"),
+            "plan_source": plan_source,
+            "hidden": model.hidden, "intermediate": model.intermediate, "experts": model.experts,
+            "topk": model.topk, "n_a": n_a, "n_e": n_e, "m": m, "b_a": b_a,
+            "tokens_per_step_per_attention_gpu": m * b_a * args.layers,
+            "microbatching": ("co-located: m micro-batches merged into one batch (no ping-pong partner)"
+                              if colo and args.merge else "ping-pong, m micro-batches"),
+            "L_sim": args.layers, "attention_stage": args.attn,
+            "l2": (f"working set (expert weights {model.experts * 3 * model.hidden * model.intermediate * 2 / 1e9:.1f} GB"
+                   " + KV cache) >> 126 MB L2; no flush needed"),
+            "parallelism": f"dp{n_a}-ep{n_e}" + (f"-etp{tp_e}" if tp_e > 1 else ""),
+            "launch": "CUDA graph per rank (device-tracked epochs)" if args.graph else "eager"}
+
+
+def run_reference(args):
+    """--impl reference: the reference ships no implementation of this path
+    (SURVEY.md §0), so its CPU restatement (oracle/, kind "port") runs the
+    same workload on the host cores: each step is the whole layer for one
+    attention GPU's m x b_a tokens (attention stage, router, all experts,
+    combine; nothing projected).  ``value`` is the host's layer-tokens/s --
+    a CPU throughput, not a per-GPU figure.  Under torchrun only rank 0 runs."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    world = args.gpus
+    n_a, n_e, colo, plan_source, tp_e, model, m_eff, b_a = resolve_layout(args, world)
+    threads = len(os.sched_getaffinity(0))
+    T = m_eff * b_a  # tokens of one attention GPU per layer step
+    attn = args.attn == "real"
+    cpu_layer(model, T, attn=attn, steps=1, warmup=0)  # build weights / KV cache (untimed setup) + first touch
+    secs = []
+    info = None
+    t_all = time.perf_counter()
+    for i in range(args.warmup + args.steps):
+        info = cpu_layer(model, T, attn=attn, steps=1, warmup=0)
+        if i >= args.warmup:
+            secs.append(info["t_layer_s"])
+    v = T * len(secs) / sum(secs)
+    line = {"impl": "reference", "metric": "decode tokens/s/GPU (MoE layer, ping-pong); M2N dispatch+combine p50 µs",
+            "value": v, "unit": "layer-tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sum(secs) / len(secs), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, N(0,1) tokens)",
+            "config": bench_config(args, model, n_a, n_e, colo, plan_source, tp_e, m_eff, b_a, world),
+            "cpu_baseline": {"value": v, "unit": "layer-tokens/s", "cores": threads, "kind": "port",
+                             "sample": info["sample"], "cpu": cpu_model_name(),
+                             "t_attention_s": info["t_attention_s"], "t_moe_s": info["t_moe_s"],
+                             "note": "host CPU throughput for one attention GPU's tokens per step; not a per-GPU "
+                                     "figure (the reference has no GPU implementation of this path)"},
+            "e2e": {"value": v, "unit": "layer-tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": time.perf_counter() - t_all}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- GPU leg ----
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_2504_02263_b200 import runtime
+    from paper_2504_02263_b200.config import DeploymentPlan, WorkloadSpec, as_model_spec
+
+    rank, world, local = runtime.init_distributed_from_env("gloo" if _over() else "nccl")
+    if world != args.gpus:
+        if rank == 0:
+            print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}))
+        sys.exit(2)
     n_a, n_e, colo, plan_source, tp_e, model, m_eff, b_a = resolve_layout(args, world)
     args.b_a = b_a
     plan = DeploymentPlan(n_a=n_a, n_e=n_e, m=m_eff, b_a=b_a, colocated=colo, tp_e=tp_e)

@@ -33,3 +33,28 @@ def test_m2n_leg_bytes():
     mat = [[0, 0, 0, 2048], [0, 0, 0, 2048], [0, 0, 0, 2048], [0, 0, 0, 0]]
     leg1, leg2, _ = bench.m2n_leg_bytes(mat, H)
     assert leg1 == 6144 * (2 * H + 8) and leg2 == 6144 * 2 * H
+
+
+def test_reference_arm_runs_whole_layer_and_reports_bench_config():
+    """--impl reference times the oracle's whole layer per step (no
+    projection): ms_per_step x steps fits the wall time, and its config is
+    bench_config() -- the dict the GPU arm prints."""
+    import json
+    import os
+    import subprocess
+    import sys
+    import types
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--shape", "tiny",
+                          "--b-a", "32", "--steps", "2", "--warmup", "1"], capture_output=True, text=True,
+                         timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["steps"] == 2
+    assert line["ms_per_step"] * line["steps"] / 1e3 <= line["wall_s"]
+    assert "no sampling" in line["cpu_baseline"]["sample"]
+    from paper_2504_02263_b200.config import as_model_spec
+    args = types.SimpleNamespace(layers=4, merge=True, attn="real", graph=True)
+    want = bench.bench_config(args, as_model_spec("tiny"), 1, 1, True, "1 GPU: co-located", 1, 1, 96, 1)
+    assert line["config"] == want
