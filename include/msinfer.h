@@ -44,8 +44,8 @@ enum {
 
 /* Buffer ids for msi_ctx_buffer (inspection by tests / benches). */
 enum {
-  MSI_BUF_RECV = 0,   /* expert GPU: received token rows  [cap][H] bf16 per slot */
-  MSI_BUF_META = 1,   /* expert GPU: (sender, t*K+k) per received row, int32x2 */
+  MSI_BUF_RECV = 0,   /* expert GPU: received rows [E_l][n_a][max_tokens][H] bf16 per slot */
+  MSI_BUF_META = 1,   /* expert GPU: (sender, t*K+k) per receive row, int32x2 */
   MSI_BUF_YBUF = 2,   /* attention GPU: expert outputs [max_tokens*K][H] bf16 per slot */
   MSI_BUF_HBUF = 3,   /* expert GPU: SwiGLU activations [cap][H'] bf16 (one, shared) */
   MSI_BUF_CNTAB = 4   /* count table [n_a][E] of (epoch<<32 | count) per slot */
@@ -149,10 +149,12 @@ int msi_gate_topk_placed(const void* x, const void* wg, int T, int H, int E, int
                          void* workspace, void* stream);
 
 /* ---- (1) M2N dispatch (sender; receiver PAPER.md:408-411)
- * Publishes cnt to every rank, waits for all senders' counts, then stores each
- * row x[t] into the expert GPUs' receive buffers over NVLink peer memory at
- * row seg_start[e] + sum_{s'<s} cnt[s'][e] + slot[t,k], with its (s, t*K+k)
- * metadata, and releases the receivers' arrival counters.  `epoch` counts the
+ * Stores each row x[t] over NVLink peer memory into its expert GPU's receive
+ * region for (local expert e_l, sender s) -- receive row
+ * (e_l * n_a + s) * max_tokens + slot[t,k] of the slot's buffer -- with its
+ * (s, t*K+k) metadata; then publishes cnt (this sender's counts, tagged with
+ * the epoch) to every expert GPU and releases their arrival counters.  No
+ * other sender's counts are needed before the payload moves.  `epoch` counts the
  * uses of `mb_slot` from 1; epoch 0 means "the slot's next use" as counted on
  * the device (msi_dispatch/msi_combine: attention side; msi_expert_ffn /
  * msi_expert_echo: expert side), which makes a whole step capturable in a CUDA
@@ -161,6 +163,21 @@ int msi_gate_topk_placed(const void* x, const void* wg, int T, int H, int E, int
 int msi_dispatch(msi_ctx* ctx, const void* x, const int32_t* cnt,
                  const int32_t* idx, const int32_t* slot, int T, int mb_slot,
                  uint32_t epoch, void* stream);
+
+/* ---- (1) fused router + M2N dispatch (top-K, counts,
+ * normalized weights and the scatter fused with the gating computation): one
+ * launch computes msi_gate_topk's outputs for x [T,H] (wg [E,H]) and stores
+ * every routed row into its receive region as msi_dispatch does -- each CTA
+ * sends its rows as soon as a decoupled look-back over the CTAs before it
+ * fixes their slots; the last CTA publishes the counts and releases the
+ * expert GPUs.  rep/R (may be NULL/0): replicated experts as in
+ * msi_gate_topk_placed (E = logical experts, the plan's experts = physical
+ * slots P, pidx [T,K] receives the physical slot); with rep == NULL, E must
+ * equal the plan's experts and pidx may be NULL.  Uses the context's router
+ * workspace.  Epoch rules as msi_dispatch. */
+int msi_route_dispatch(msi_ctx* ctx, const void* x, const void* wg, int T, int E, const int32_t* rep, int R,
+                       int32_t* idx, int32_t* pidx, float* w, int32_t* cnt, int32_t* slot, int mb_slot,
+                       uint32_t epoch, void* stream);
 
 /* Block `stream` (one spinning thread, no other SM use) until every sender
  * released `mb_slot`'s epoch -- the wait msi_expert_ffn performs itself --

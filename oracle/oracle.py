@@ -13,7 +13,8 @@ oracle restates the paper's semantics with the build's precision contract:
            ``place`` (bit-exact contract: idx, counts, slots, and weights via
            the deterministic exp in msi_oracle.c)
 * dispatch PAPER.md:396-411 (M2N sender/receiver), per-pair bytes
-           PAPER.md:632 -> ``dispatch_layout`` (bit-exact row placement)
+           PAPER.md:632 -> ``dispatch_rows`` (bit-exact receive rows),
+           ``dispatch_layout`` (the expert GEMM's virtual row order)
 * expert   PAPER.md:285-286 (FFN in/out GEMMs) + SwiGLU per BASELINE
            north_star -> ``expert_ffn`` (fp32 accumulate; bf16 rounding at
            X, H, Y; tolerance-checked)
@@ -179,7 +180,9 @@ def segment_starts(total: np.ndarray, align: int = ROW_ALIGN) -> np.ndarray:
 
 def dispatch_layout(cnt_all: np.ndarray, E_l: int):
     """cnt_all [n_a, E] -> per expert GPU q: (total [E_l], seg_start [E_l],
-    base [n_a, E_l]) with row(s, t, k) = seg_start[e_l] + base[s, e_l] + slot."""
+    base [n_a, E_l]): the expert GEMM's *virtual* rows -- expert e_l's rows
+    are its senders' rows in ascending (sender, slot) order, segments 128-row
+    aligned (the activation buffer hbuf uses this order)."""
     cnt_all = np.asarray(cnt_all, np.int64)
     n_a, E = cnt_all.shape
     out = []
@@ -191,14 +194,15 @@ def dispatch_layout(cnt_all: np.ndarray, E_l: int):
     return out
 
 
-def dispatch_rows(idx: np.ndarray, slot: np.ndarray, s: int, layout, E_l: int):
-    """Destination (expert GPU, row) of every (t, k) of sender s."""
+def dispatch_rows(idx: np.ndarray, slot: np.ndarray, s: int, E_l: int, n_a: int, cap_s: int):
+    """Destination (expert GPU, receive row) of every (t, k) of sender s
+    (PAPER.md:396-411): the receive buffer of an expert GPU has one region of
+    cap_s (= b_a) rows per (local expert e_l, sender), at row
+    (e_l * n_a + s) * cap_s; row (t, k) sits at its slot inside it.  A sender
+    therefore places its rows from its own counts alone."""
+    idx = np.asarray(idx, np.int64)
     q = idx // E_l
-    el = idx % E_l
-    rows = np.empty(idx.shape, np.int64)
-    for qq, (total, seg, base) in enumerate(layout):
-        m = q == qq
-        rows[m] = seg[el[m]] + base[s, el[m]] + slot[m]
+    rows = ((idx % E_l) * n_a + s) * cap_s + np.asarray(slot, np.int64)
     return q.astype(np.int32), rows
 
 

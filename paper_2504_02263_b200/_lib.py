@@ -66,6 +66,7 @@ SIGNATURES = {
     "msi_gate_topk": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
     "msi_gate_topk_placed": (_I, [_P, _P, _I, _I, _I, _I, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
     "msi_dispatch": (_I, [_P, _P, _P, _P, _P, _I, _I, _U32, _P]),
+    "msi_route_dispatch": (_I, [_P, _P, _P, _I, _I, _P, _I, _P, _P, _P, _P, _P, _I, _U32, _P]),
     "msi_expert_ffn": (_I, [_P, _P, _P, _I, _U32, _P]),
     "msi_expert_echo": (_I, [_P, _I, _U32, _P]),
     "msi_expert_wait": (_I, [_P, _I, _U32, _P]),

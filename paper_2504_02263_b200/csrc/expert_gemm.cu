@@ -65,7 +65,40 @@ struct SegInfo {
   int start[MAXE];
   int tile0[MAXE + 1];  // first tile of expert e
   int mtiles[MAXE];     // M tiles (CG=1) or M-tile pairs (CG=2)
+  int pre[MAXE][MSI_MAX_RANKS + 1];  // receive regions: first virtual row of sender s in expert e
 };
+
+// A-operand boxes of 128, 64, ..., 1 rows (SW128, 64 columns): a tile's rows
+// are loaded as runs of the (expert, sender) receive regions, each run split
+// into power-of-two boxes.  The 128-B swizzle is applied by shared-memory
+// address (scripts/probe_tma_runs.cu), so a box may land at any row offset.
+struct AMaps {
+  CUtensorMap m[8];  // m[i]: box of 128 >> i rows
+};
+constexpr int kMaxPieces = 64;
+
+// Row runs of this CTA's share [v0, v0 + nrows) of expert e's virtual rows:
+// pieces (smem row, global row, box index); returns the rows covered.
+template <int MAXE>
+__device__ __forceinline__ int plan_pieces(const SegInfo<MAXE>& sg, const GemmParams& p, int e, int v0, int nrows,
+                                           int4* pieces, int& npieces) {
+  npieces = 0;
+  const int end = min(v0 + nrows, sg.total[e]);
+  for (int s = 0; s < p.n_src; ++s) {
+    const int a = max(v0, sg.pre[e][s]), b = min(end, sg.pre[e][s + 1]);
+    if (a >= b) continue;
+    int off = a - v0, len = b - a;
+    long long row = ((long long)e * p.n_src + s) * p.cap_s + (a - sg.pre[e][s]);
+    while (len > 0 && npieces < kMaxPieces) {
+      const int lg = 31 - __clz(min(len, 128));  // largest power of two <= len
+      pieces[npieces++] = make_int4(off, (int)row, 7 - lg, 0);
+      off += 1 << lg;
+      row += 1 << lg;
+      len -= 1 << lg;
+    }
+  }
+  return max(0, end - v0);
+}
 
 template <int MAXE>
 __device__ __forceinline__ void decode_tile(const SegInfo<MAXE>& s, int E_l, int tau, int& e, int& n, int& m) {
@@ -95,8 +128,10 @@ __device__ __forceinline__ bool half_pair_rows(const SegInfo<MAXE>& s, int e, in
 
 template <int CG, int MAXE>
 __global__ void __launch_bounds__(kThreads, 1)
-grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const __grid_constant__ CUtensorMap tmA64, const GemmParams p) {
+grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CUtensorMap tmB,
+                    const GemmParams p) {
+  const CUtensorMap& tmA = am.m[0];
+  const CUtensorMap& tmA64 = am.m[1];
   using C = Cfg<CG, MAXE>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -118,7 +153,6 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;  // CTA within the pair
   const bool leader = rank == 0;
-  const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;  // pair / CTA index
   const int nunits = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   pdl_trigger();  // the next kernel (GEMM2 / combine) may launch and queue now
   pdl_wait();     // everything earlier on the stream is complete and visible
@@ -139,7 +173,8 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     s_abort = ok ? 0 : 1;
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
-    if (CG == 2) tma_prefetch(&tmA64);
+    if (CG == 2 || p.a_runs)
+      for (int i = 1; i < (p.a_runs ? 8 : 2); ++i) tma_prefetch(&am.m[i]);
     for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4 * CG); }
     // ring consumers: MMA thread + 4 epilogue warps (+ the peer's producer
@@ -185,10 +220,17 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       seg.total[i] = p.totals[i];
     } else {
       const int s = i / p.E_l, e = i - s * p.E_l;
-      atomicAdd(&seg.total[e], (int)(uint32_t)ld_relaxed_sys64(p.cntab + (size_t)s * p.E + p.e0 + e));
+      const int v = (int)(uint32_t)ld_relaxed_sys64(p.cntab + (size_t)s * p.E + p.e0 + e);
+      if (p.n_src) seg.pre[e][s + 1] = v;
+      atomicAdd(&seg.total[e], v);
     }
   }
   __syncthreads();
+  if (p.n_src)  // receive regions: exclusive prefix over senders per expert
+    for (int e = threadIdx.x; e < p.E_l; e += blockDim.x) {
+      seg.pre[e][0] = 0;
+      for (int s = 0; s < p.n_src; ++s) seg.pre[e][s + 1] += seg.pre[e][s];
+    }
   if (threadIdx.x == 0) {
     int run_start = 0, run_tile = 0;
     for (int e = 0; e < p.E_l; ++e) {
@@ -255,6 +297,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     // ===================== TMA producer (both CTAs of a pair) ==============
     int stage = 0;
     uint32_t phase = 0;
+    int4 pieces[kMaxPieces];
     for (int it = 0;; ++it) {
       const int tau = leader ? publish_tile(it) : take_tile(it, true);
       if (tau >= ntiles) break;
@@ -267,17 +310,38 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       const int rowA = seg.start[e] + m * CG * BM + (int)rank * (hp ? BM / 2 : BM);
       const int rowB = e * p.n_total + n * BN + (int)rank * C::B_ROWS;
       const CUtensorMap* mA = (CG == 2 && hp && p.a64) ? &tmA64 : &tmA;
-      const uint32_t a_bytes = (CG == 2 && hp && p.a64) ? C::A_BYTES / 2 : C::A_BYTES;
+      uint32_t a_bytes = (CG == 2 && hp && p.a64) ? C::A_BYTES / 2 : C::A_BYTES;
+      uint32_t a_bytes_pair = 2 * a_bytes;  // both CTAs' A bytes (the leader's barrier counts them)
+      int npieces = 0;
+      if (p.a_runs) {  // receive regions: only the rows present, as runs
+        const int nrows = hp ? BM / 2 : BM;
+        const int v0 = m * CG * BM + (int)rank * nrows;
+        a_bytes = (uint32_t)plan_pieces(seg, p, e, v0, nrows, pieces, npieces) * (BK * 2);
+        if constexpr (CG == 2) {
+          const int v1 = m * CG * BM + (int)(rank ^ 1) * nrows;
+          a_bytes_pair = a_bytes + (uint32_t)max(0, min(nrows, seg.total[e] - v1)) * (BK * 2);
+        }
+      }
       for (int kb = 0; kb < kblocks; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* st = sA + stage * C::STAGE_BYTES;
         if constexpr (CG == 2) {
-          if (leader) mbar_expect_tx(&full[stage], 2 * (a_bytes + C::B_BYTES));
-          tma_load_2d_pair(st, mA, kb * BK, rowA, &full[stage]);
+          if (leader) mbar_expect_tx(&full[stage], a_bytes_pair + 2 * C::B_BYTES);
+          if (p.a_runs) {
+            for (int i = 0; i < npieces; ++i)
+              tma_load_2d_pair(st + pieces[i].x * (BK * 2), &am.m[pieces[i].z], kb * BK, pieces[i].y, &full[stage]);
+          } else {
+            tma_load_2d_pair(st, mA, kb * BK, rowA, &full[stage]);
+          }
           tma_load_2d_pair(st + C::A_BYTES, &tmB, kb * BK, rowB, &full[stage]);
         } else {
-          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
-          tma_load_2d(st, &tmA, kb * BK, rowA, &full[stage]);
+          mbar_expect_tx(&full[stage], a_bytes + C::B_BYTES);
+          if (p.a_runs) {
+            for (int i = 0; i < npieces; ++i)
+              tma_load_2d(st + pieces[i].x * (BK * 2), &am.m[pieces[i].z], kb * BK, pieces[i].y, &full[stage]);
+          } else {
+            tma_load_2d(st, &tmA, kb * BK, rowA, &full[stage]);
+          }
           tma_load_2d(st + C::A_BYTES, &tmB, kb * BK, rowB, &full[stage]);
         }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -364,7 +428,13 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         if (p.mode == 0) {
           rowdst = reinterpret_cast<char*>(p.out) + ((size_t)row_global * p.out_ld + (size_t)n * (BN / 2) + colofs) * 2;
         } else if (p.meta) {
-          const int2 md = p.meta[row_global];
+          long long mrow = row_global;
+          if (p.n_src) {  // receive regions: (expert, sender) region row of virtual row row_local
+            int s = 0;
+            while (s + 1 < p.n_src && seg.pre[e][s + 1] <= row_local) ++s;
+            mrow = ((long long)e * p.n_src + s) * p.cap_s + (row_local - seg.pre[e][s]);
+          }
+          const int2 md = p.meta[mrow];
           const size_t drow = (size_t)md.y * (p.row_mul ? p.row_mul : 1) + p.row_add;
           rowdst = p.dst[md.x] + (drow * p.out_ld + (size_t)n * BN + colofs) * 2;
         } else {
@@ -551,11 +621,13 @@ int num_sms() {
 template <int CG, int MAXE>
 int launch_cg(const GemmLaunch& L, cudaStream_t st) {
   using C = Cfg<CG, MAXE>;
-  CUtensorMap ta, tb, ta64;
-  int rc = make_tmap(&ta, L.a, (uint64_t)L.p.kdim, (uint64_t)L.a_rows, BK, BM);
+  AMaps am;
+  CUtensorMap tb;
+  int rc = 0;
+  for (int i = 0; i < (L.p.a_runs ? 8 : 2) && !rc; ++i)  // 128-row boxes, 64 (half pairs), ... 1 (runs)
+    rc = make_tmap(&am.m[i], L.a, (uint64_t)L.p.kdim, (uint64_t)L.a_rows, BK, BM >> i);
   if (rc) return rc;
-  rc = make_tmap(&ta64, L.a, (uint64_t)L.p.kdim, (uint64_t)L.a_rows, BK, BM / 2);  // half-pair A boxes
-  if (rc) return rc;
+  if (!L.p.a_runs) memcpy(&am.m[2], &am.m[0], 6 * sizeof(CUtensorMap));  // unused
   rc = make_tmap(&tb, L.b, (uint64_t)L.p.kdim, (uint64_t)L.p.E_l * L.p.n_total, BK, C::B_ROWS);
   if (rc) return rc;
   if (int arc = smem_attr(reinterpret_cast<const void*>(grouped_gemm_kernel<CG, MAXE>), C::SMEM)) return arc;
@@ -588,7 +660,7 @@ int launch_cg(const GemmLaunch& L, cudaStream_t st) {
   cfg.numAttrs = na;
   GemmParams prm = L.p;
   prm.a64 = half_pair_box64();
-  MSI_CUDA(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<CG, MAXE>, ta, tb, ta64, prm));
+  MSI_CUDA(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<CG, MAXE>, am, tb, prm));
   return check_launch("grouped_gemm_kernel");
 }
 

@@ -43,6 +43,13 @@ struct GemmParams {
   uint32_t* tile_ctr;
   // half-pair tiles load A with the 64-row box (set by the launcher)
   int a64;
+  // receive regions (msi_expert_ffn): counts per (sender, expert) from cntab;
+  // virtual row v of expert e lives in region (e, s) of cap_s rows at offset
+  // v - pre[e][s].  a_runs = 1: GEMM1 loads A by runs of those regions; the
+  // mode 1 epilogue finds meta rows the same way.  n_src = 0: compact rows.
+  int n_src;
+  long long cap_s;
+  int a_runs;
   // mode 1 destination row = meta.y * row_mul + row_add (expert TP: the
   // partial of TP rank r of (t, k) goes to row (t*K + k)*tp + r); 0 = 1, 0
   int row_mul, row_add;

@@ -25,9 +25,15 @@
 //            stats[2] u64                   rows through the expert FFN, FFN calls
 //            cntab[slot][n_a][E] u64        (epoch << 32 | count), all-gathered
 //   ybuf   : (attention role) [slot][max_tokens * K][H] bf16 expert outputs
-//   recv   : (expert role)    [slot][cap][H] bf16 received rows
-//   meta   : (expert role)    [slot][cap] int2 (sender, t*K + k)
-//   cap = n_a * max_tokens * min(K, E_l) + E_l * (ROW_ALIGN - 1), rounded to 128.
+//   recv   : (expert role)    [slot][E_l][n_a][max_tokens][H] bf16 received rows:
+//            one region per (local expert, sender), so a sender places its
+//            rows from its own counts alone (no count exchange before the
+//            payload); the expert GEMM loads a tile's rows as runs of these
+//            regions (TMA boxes at any row offset)
+//   meta   : (expert role)    [slot][E_l][n_a][max_tokens] int2 (sender, t*K + k)
+//   hbuf   : (expert role, separate allocation) [cap][H'] SwiGLU activations,
+//            per-expert segments 128-row aligned in virtual (sender-major)
+//            row order; cap = n_a * max_tokens * min(K, E_l) + E_l * 127.
 #include <cstdarg>
 #include <cstdlib>
 #include <cstdio>
@@ -38,6 +44,7 @@
 
 #include "common.cuh"
 #include "gemm.h"
+#include "route.h"
 
 namespace msi {
 
@@ -105,7 +112,8 @@ struct Layout {
   size_t ybuf, ybuf_slot;
   size_t recv, recv_slot, meta, meta_slot;
   size_t total;
-  int64_t cap;
+  int64_t cap;       // hbuf rows (compact, 128-aligned segments)
+  int64_t recv_rows;  // recv / meta rows per slot: E_l * n_a * max_tokens
 };
 
 Layout make_layout(const msi_plan& p, bool attn, bool expert) {
@@ -128,13 +136,14 @@ Layout make_layout(const msi_plan& p, bool attn, bool expert) {
   const int per_tok = p.topk < E_l ? p.topk : E_l;
   int64_t cap = (int64_t)p.n_a * p.max_tokens * per_tok + (int64_t)E_l * (MSI_ROW_ALIGN - 1);
   L.cap = (cap + 127) / 128 * 128;
+  L.recv_rows = (int64_t)E_l * p.n_a * p.max_tokens;
   L.ybuf_slot = (size_t)p.max_tokens * p.topk * plan_tp(p) * p.hidden * 2;  // tp_e partials per (t, k)
   L.ybuf = off;
   if (attn) off += align_up(L.ybuf_slot * p.slots, ALIGN);
-  L.recv_slot = (size_t)L.cap * p.hidden * 2;
+  L.recv_slot = (size_t)L.recv_rows * p.hidden * 2;
   L.recv = off;
   if (expert) off += align_up(L.recv_slot * p.slots, ALIGN);
-  L.meta_slot = (size_t)L.cap * 8;
+  L.meta_slot = (size_t)L.recv_rows * 8;
   L.meta = off;
   if (expert) off += align_up(L.meta_slot * p.slots, ALIGN);
   L.total = off;
@@ -146,9 +155,10 @@ struct DevCtx {
   int n_a, n_e, n_world, E, K, H, Hp, E_l, slots, max_tokens;
   int my_a, my_e;
   int tp, nodes, my_node, my_tp;  // expert TP: node = tp GPUs; this GPU's node and rank in it
-  long long cap;
+  long long cap;        // hbuf rows
+  long long recv_rows;  // recv / meta rows per slot (E_l * n_a * max_tokens regions)
   uint64_t timeout_ns;
-  uint64_t* cntab_of[MSI_MAX_RANKS];   // count table on every rank of the world
+  uint64_t* ecntab_of[MSI_MAX_RANKS];  // count table per expert index q
   uint32_t* arrive_of[MSI_MAX_RANKS];  // per expert index q
   char* recv_of[MSI_MAX_RANKS];        // per expert index q
   int2* meta_of[MSI_MAX_RANKS];        // per expert index q
@@ -212,138 +222,33 @@ int validate(const msi_plan& p) {
 // ------------------------------------------------------------ dispatch ----
 constexpr int kDispThreads = 512;
 
-// Dynamic smem of the dispatch kernel: row bases [E] (i64), counts [n_a][E]
-// and padded sizes [E] (u32); the TMA variant adds one row buffer + mbarrier
-// per warp after a 128-B aligned offset.
-__host__ __device__ inline size_t disp_table_bytes(int E, int n_a) {
-  return ((size_t)E * 8 + (size_t)(n_a + 1) * E * 4 + 127) & ~size_t(127);
-}
-
-// Copy engine of the dispatch: MSI_DISPATCH=tma selects TMA bulk copies
-// (cp.async.bulk global->smem->peer), otherwise SM 16-B vector stores.
-bool dispatch_uses_tma() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("MSI_DISPATCH");
-    v = (e && e[0] == 't') ? 1 : 0;
-  }
-  return v == 1;
-}
-
-template <bool TMA>
+// Stand-alone M2N dispatch (msi_dispatch: router outputs given).  Row (t, k)
+// goes to region (e_l, s) of its expert GPU at its slot -- this sender's own
+// counts place it, so no other sender is waited for; the last CTA publishes
+// the counts (tagged with the epoch) to every expert GPU and releases their
+// arrival counters.  The fused router + dispatch (msi_route_dispatch,
+// router.cu) does the same from inside the router.
 __global__ void __launch_bounds__(kDispThreads)
 dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ cnt,
                 const int32_t* __restrict__ idx, const int32_t* __restrict__ slot, int T, int mb,
                 uint32_t epoch) {
-  extern __shared__ __align__(128) long long s_rowbase[];  // [E] first row of this sender in expert e's segment
-  __shared__ int s_abort;
+  __shared__ uint32_t s_epoch;
+  __shared__ int s_last;
   const int tid = threadIdx.x;
   pdl_trigger();
   pdl_wait();
-  epoch = resolve_epoch(epoch, c.my_ause + mb * CTR_STRIDE, 1u, c.my_status);
+  if (tid == 0) s_epoch = resolve_epoch(epoch, c.my_ause + mb * CTR_STRIDE, 1u, c.my_status);
+  __syncthreads();
+  epoch = s_epoch;
   if (epoch == 0) return;  // host/device epoch mismatch: status set, nothing sent
   const int s = c.my_a;
-  const size_t tab = (size_t)mb * c.n_a * c.E;
-
   if (blockIdx.x == 0 && tid == 0) trace_stamp(c.trace, 0);
-  // ---- publish this sender's counts to every rank (tagged with the epoch)
-  if (blockIdx.x == 0)
-    for (int i = tid; i < c.n_world * c.E; i += blockDim.x) {
-      const int r = i / c.E, e = i - r * c.E;
-      st_relaxed_sys64(c.cntab_of[r] + tab + (size_t)s * c.E + e,
-                       ((uint64_t)epoch << 32) | (uint32_t)cnt[e]);
-    }
-  // ---- wait for every sender's counts (local table), keep them in smem
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_rowbase + c.E);  // [n_a][E]
-  if (tid == 0) s_abort = 0;
-  __syncthreads();
-  for (int i = tid; i < c.n_a * c.E; i += blockDim.x) {
-    const uint64_t* p = c.my_cntab + tab + i;
-    uint64_t t0 = 0;
-    uint32_t spins = 0;
-    uint64_t v;
-    while ((uint32_t)((v = ld_acquire_sys64(p)) >> 32) != epoch) {
-      if ((++spins & 1023u) == 0) {
-        uint64_t now = globaltimer();
-        if (t0 == 0) t0 = now;
-        else if (now - t0 > c.timeout_ns) { atomicExch(c.my_status, MSI_ETIMEOUT); s_abort = 1; break; }
-      }
-      __nanosleep(32);
-    }
-    s_cnt[i] = (uint32_t)v;
-  }
-  __syncthreads();
-  if (s_abort) return;
-  if (blockIdx.x == 0 && tid == 0) trace_stamp(c.trace, 1);
-  // ---- row base per expert: 128-aligned segment start + rows of senders < s
-  //      (per expert in parallel, then a short prefix per expert GPU)
-  uint32_t* s_pad = s_cnt + c.n_a * c.E;  // [E] padded segment sizes
-  for (int e = tid; e < c.E; e += blockDim.x) {
-    long long total = 0, before = 0;
-    for (int s2 = 0; s2 < c.n_a; ++s2) {
-      const long long v = s_cnt[s2 * c.E + e];
-      total += v;
-      if (s2 < s) before += v;
-    }
-    s_rowbase[e] = before;
-    s_pad[e] = (uint32_t)((total + MSI_ROW_ALIGN - 1) / MSI_ROW_ALIGN * MSI_ROW_ALIGN);
-  }
-  __syncthreads();
-  for (int q = tid; q < c.nodes; q += blockDim.x) {  // per expert node (all its GPUs share the layout)
-    long long run = 0;
-    for (int el = 0; el < c.E_l; ++el) {
-      const int e = q * c.E_l + el;
-      s_rowbase[e] += run;
-      run += s_pad[e];
-    }
-  }
-  __syncthreads();
-
   const int lane = tid & 31;
   const int gwarp = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
   const int nwarps = gridDim.x * (blockDim.x >> 5);
   const size_t row_bytes = (size_t)c.H * 2;
-  if constexpr (TMA) {
-    // ---- copy rows with the TMA engine: one bulk load of x[t] into this
-    //      warp's smem buffer, then K bulk stores straight into the expert
-    //      GPUs' receive rows (NVLink peer memory); one lane per warp drives it
-    char* buf = reinterpret_cast<char*>(s_rowbase) + disp_table_bytes(c.E, c.n_a) + (size_t)(tid >> 5) * row_bytes;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(s_rowbase) + disp_table_bytes(c.E, c.n_a) +
-                                                (size_t)(blockDim.x >> 5) * row_bytes) + (tid >> 5);
-    if (lane == 0) {
-      mbar_init(bar, 1);
-      fence_barrier_init();
-    }
-    __syncwarp();
-    uint32_t phase = 0;
-    for (int t = gwarp; t < T; t += nwarps) {
-      if (lane < c.K) {  // metadata of (t, lane)
-        const int e = idx[(size_t)t * c.K + lane];
-        const long long row = s_rowbase[e] + slot[(size_t)t * c.K + lane];
-        c.meta_of[e / c.E_l][(size_t)mb * c.cap + row] = make_int2(s, t * c.K + lane);
-      }
-      if (lane == 0) {
-        bulk_wait_read0();  // the previous token's stores have read the buffer
-        mbar_expect_tx(bar, (uint32_t)row_bytes);
-        bulk_g2s(buf, x + (size_t)t * c.H, (uint32_t)row_bytes, bar);
-        mbar_wait(bar, phase);
-        for (int k = 0; k < c.K; ++k) {
-          const int e = idx[(size_t)t * c.K + k];
-          const long long row = s_rowbase[e] + slot[(size_t)t * c.K + k];
-          bulk_s2g(c.recv_of[e / c.E_l] + ((size_t)mb * c.cap + row) * row_bytes, buf, (uint32_t)row_bytes);
-        }
-        bulk_commit();
-      }
-      phase ^= 1;
-      __syncwarp();
-    }
-    if (lane == 0) {
-      bulk_wait0();                // every bulk store has completed its writes
-      fence_proxy_async_global();  // order them before the generic-proxy release below
-    }
-  } else {
-  // ---- copy rows: a warp moves one part of one token row (x read once,
-  //      written K times with 16 B stores, 8 x 512 B in flight per warp)
+  // a warp moves one part of one token row (x read once, written K * tp
+  // times with 16 B stores, 8 x 512 B in flight per warp)
   const int nchunk = c.H >> 8;  // 512 B warp-chunks per row
   int parts = T > 0 ? (nwarps + T - 1) / T : 1;
   parts = parts < 1 ? 1 : (parts > nchunk ? nchunk : parts);
@@ -358,9 +263,10 @@ dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32
       const int k = lane / c.tp, r = lane - (lane / c.tp) * c.tp;
       const int e = idx[(size_t)t * c.K + k];
       const int q = (e / c.E_l) * c.tp + r;
-      const long long row = s_rowbase[e] + slot[(size_t)t * c.K + k];
-      my_dst = c.recv_of[q] + ((size_t)mb * c.cap + row) * row_bytes;
-      if (part == 0) c.meta_of[q][(size_t)mb * c.cap + row] = make_int2(s, t * c.K + k);
+      const long long row = (long long)mb * c.recv_rows +
+                            ((long long)(e % c.E_l) * c.n_a + s) * c.max_tokens + slot[(size_t)t * c.K + k];
+      my_dst = c.recv_of[q] + (size_t)row * row_bytes;
+      if (part == 0) c.meta_of[q][row] = make_int2(s, t * c.K + k);
     }
     const char* src = reinterpret_cast<const char*>(x + (size_t)t * c.H) + lane * 16;
     const int j_end = min(nchunk, (part + 1) * per_part);
@@ -378,29 +284,37 @@ dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32
       }
     }
   }
-  }  // copy variant
 
-  // ---- release: the last CTA bumps every expert GPU's arrival counter
+  // ---- the last CTA: counts to every expert GPU, then release -------------
   __syncthreads();
   if (tid == 0) {
     __threadfence_system();
-    const uint32_t old = atomicAdd(c.my_dticket + mb * CTR_STRIDE, 1u);
-    if (old == gridDim.x - 1) {
-      c.my_dticket[mb * CTR_STRIDE] = 0;
-      c.my_ause[mb * CTR_STRIDE] = epoch;  // every CTA has read the old value
-      trace_stamp(c.trace, 2);
-      fence_sys();
-      for (int q = 0; q < c.n_e; ++q) red_release_sys_add(c.arrive_of[q] + mb * CTR_STRIDE, 1u);
-    }
+    s_last = atomicAdd(c.my_dticket + mb * CTR_STRIDE, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  const size_t tab = (size_t)mb * c.n_a * c.E;
+  for (int i = tid; i < c.n_e * c.E; i += blockDim.x) {
+    const int q = i / c.E, e = i - q * c.E;
+    st_relaxed_sys64(c.ecntab_of[q] + tab + (size_t)s * c.E + e, ((uint64_t)epoch << 32) | (uint32_t)cnt[e]);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    c.my_dticket[mb * CTR_STRIDE] = 0;
+    c.my_ause[mb * CTR_STRIDE] = epoch;  // every CTA has read the old value
+    trace_stamp(c.trace, 2);
+    fence_sys();
+    for (int q = 0; q < c.n_e; ++q) red_release_sys_add(c.arrive_of[q] + mb * CTR_STRIDE, 1u);
   }
 }
 
 // ---------------------------------------------------------------- echo ----
 // Identity expert: returns every received row to its sender's combine buffer
 // (the N2M leg without the FFN), so dispatch + echo + combine times the pure
-// M2N round trip.  Same waits, metadata, segment layout and signals as the
+// M2N round trip.  Same waits, metadata, receive regions and signals as the
 // real expert step.
 constexpr int kEchoThreads = 512;
+constexpr int kMaxPairs = MSI_MAX_LOCAL_EXPERTS * MSI_MAX_RANKS;
 
 // Expert-side wait for a slot's rows (one thread): spins until every sender
 // released the slot's epoch (device-resolved like msi_expert_ffn's), so the
@@ -418,8 +332,7 @@ __global__ void expert_wait_kernel(const DevCtx c, int mb, uint32_t epoch) {
 __global__ void __launch_bounds__(kEchoThreads)
 echo_kernel(const DevCtx c, int mb, uint32_t epoch) {
   __shared__ int s_ok, s_last;
-  __shared__ int s_start[MSI_MAX_LOCAL_EXPERTS], s_total[MSI_MAX_LOCAL_EXPERTS];
-  __shared__ int s_first[MSI_MAX_LOCAL_EXPERTS + 1];  // exclusive prefix of totals
+  __shared__ int s_first[kMaxPairs + 1];  // exclusive prefix of the (e_l, s) region counts
   const int tid = threadIdx.x, lane = tid & 31;
   const uint32_t* arrive = c.my_arrive + mb * CTR_STRIDE;
   pdl_trigger();
@@ -428,50 +341,45 @@ echo_kernel(const DevCtx c, int mb, uint32_t epoch) {
   if (epoch == 0) return;
   if (blockIdx.x == 0 && tid == 0) trace_stamp(c.trace, 3);
   if (tid == 0) s_ok = wait_geq(arrive, epoch * (uint32_t)c.n_a, c.timeout_ns, c.my_status);
-  if (tid < MSI_MAX_LOCAL_EXPERTS) s_total[tid] = 0;
   __syncthreads();
   if (!s_ok) return;
   if (blockIdx.x == 0 && tid == 0) trace_stamp(c.trace, 4);
   const size_t tab = (size_t)mb * c.n_a * c.E;
-  for (int i = tid; i < c.n_a * c.E_l; i += blockDim.x) {  // all entries in parallel
-    const int s = i / c.E_l, el = i - s * c.E_l;
-    atomicAdd(&s_total[el], (int)(uint32_t)ld_relaxed_sys64(c.my_cntab + tab + (size_t)s * c.E + c.my_node * c.E_l + el));
+  const int npairs = c.E_l * c.n_a;  // region (e_l, s) = pair e_l * n_a + s
+  for (int i = tid; i < npairs; i += blockDim.x) {  // all counts loaded in parallel
+    const int el = i / c.n_a, s = i - el * c.n_a;
+    s_first[i + 1] = (int)(uint32_t)ld_relaxed_sys64(c.my_cntab + tab + (size_t)s * c.E + c.my_node * c.E_l + el);
   }
   __syncthreads();
-  if (tid == 0) {  // 128-aligned segment starts and the flat row prefix
-    int run = 0, flat = 0;
-    for (int el = 0; el < c.E_l; ++el) {
-      s_start[el] = run;
-      s_first[el] = flat;
-      run += (s_total[el] + MSI_ROW_ALIGN - 1) / MSI_ROW_ALIGN * MSI_ROW_ALIGN;
-      flat += s_total[el];
-    }
-    s_first[c.E_l] = flat;
+  if (tid == 0) {
+    s_first[0] = 0;
+    for (int i = 1; i <= npairs; ++i) s_first[i] += s_first[i - 1];
   }
   __syncthreads();
   const int gwarp = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
   const int nwarps = gridDim.x * (blockDim.x >> 5);
   const size_t row_bytes = (size_t)c.H * 2;
   const int nchunk = c.H >> 8;
-  {
-    // one flat row index over all local experts: every warp has work
-    for (int i = gwarp; i < s_first[c.E_l]; i += nwarps) {
-      int el = 0;
-      while (i >= s_first[el + 1]) ++el;
-      const long long row = s_start[el] + (i - s_first[el]);
-      const int2 md = c.meta_of[c.my_e][(size_t)mb * c.cap + row];
-      const char* src = c.recv_of[c.my_e] + ((size_t)mb * c.cap + row) * row_bytes + lane * 16;
-      char* dst = c.ybuf_of[md.x] + (size_t)mb * c.max_tokens * c.K * c.tp * row_bytes +
-                  ((size_t)md.y * c.tp + c.my_tp) * row_bytes + lane * 16;
-      for (int j = 0; j < nchunk; j += 8) {
-        uint4 v[8];
+  for (int i = gwarp; i < s_first[npairs]; i += nwarps) {  // one flat row index over all regions
+    int lo = 0, hi = npairs - 1;  // last pair with s_first[pair] <= i
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_first[mid] <= i) lo = mid;
+      else hi = mid - 1;
+    }
+    const long long row = (long long)mb * c.recv_rows + (long long)lo * c.max_tokens + (i - s_first[lo]);
+    const int2 md = c.meta_of[c.my_e][row];
+    const char* src = c.recv_of[c.my_e] + (size_t)row * row_bytes + lane * 16;
+    char* dst = c.ybuf_of[md.x] + (size_t)mb * c.max_tokens * c.K * c.tp * row_bytes +
+                ((size_t)md.y * c.tp + c.my_tp) * row_bytes + lane * 16;
+    for (int j = 0; j < nchunk; j += 8) {
+      uint4 v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (j + u < nchunk) v[u] = __ldcg(reinterpret_cast<const uint4*>(src + (size_t)(j + u) * 512));
+      for (int u = 0; u < 8; ++u)
+        if (j + u < nchunk) v[u] = __ldcg(reinterpret_cast<const uint4*>(src + (size_t)(j + u) * 512));
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (j + u < nchunk) st_v4(dst + (size_t)(j + u) * 512, v[u]);
-      }
+      for (int u = 0; u < 8; ++u)
+        if (j + u < nchunk) st_v4(dst + (size_t)(j + u) * 512, v[u]);
     }
   }
   __syncthreads();
@@ -695,14 +603,12 @@ extern "C" int msi_ctx_finalize(msi_ctx* c) {
   d.my_node = c->my_e >= 0 ? c->my_e / d.tp : -1;
   d.my_tp = c->my_e >= 0 ? c->my_e % d.tp : 0;
   d.cap = c->my_layout.cap;
+  d.recv_rows = c->my_layout.recv_rows;
   d.timeout_ns = c->timeout_ns;
-  for (int r = 0; r < p.world; ++r) {
-    Layout L = make_layout(p, role_attn(p, r), role_expert(p, r));
-    d.cntab_of[r] = reinterpret_cast<uint64_t*>(c->peer[r] + L.cntab);
-  }
   for (int q = 0; q < p.n_e; ++q) {
     const int r = p.expert_ranks[q];
     Layout L = make_layout(p, role_attn(p, r), true);
+    d.ecntab_of[q] = reinterpret_cast<uint64_t*>(c->peer[r] + L.cntab);
     d.arrive_of[q] = reinterpret_cast<uint32_t*>(c->peer[r] + L.arrive);
     d.recv_of[q] = c->peer[r] + L.recv;
     d.meta_of[q] = reinterpret_cast<int2*>(c->peer[r] + L.meta);
@@ -812,29 +718,52 @@ extern "C" int msi_dispatch(msi_ctx* c, const void* x, const int32_t* cnt, const
   MSI_REQUIRE(T >= 0 && T <= c->plan.max_tokens, "msi_dispatch: T=%d exceeds max_tokens=%d", T, c->plan.max_tokens);
   MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots && epoch != 0xffffffffu, "msi_dispatch: bad slot/epoch");
   MSI_REQUIRE(cnt && (T == 0 || (x && idx && slot)), "msi_dispatch: null pointer");
-  // row bases [E] (long long) + the all-gathered count table [n_a][E] + padded sizes (u32)
-  const size_t table = disp_table_bytes(c->plan.experts, c->plan.n_a);
   const size_t bytes = (size_t)T * c->plan.topk * c->plan.hidden * 2;
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (dispatch_uses_tma() && plan_tp(c->plan) == 1) {
-    // TMA variant: 8 warps per CTA, one token row buffer each, a warp per token
-    constexpr int kThr = 256;
-    const size_t smem = table + (kThr / 32) * ((size_t)c->plan.hidden * 2 + 8);
-    if (int rc = smem_attr(reinterpret_cast<const void*>(dispatch_kernel<true>), smem)) return rc;
-    int grid = (T + kThr / 32 - 1) / (kThr / 32);
-    grid = grid < 1 ? 1 : (grid > 2 * num_sms() ? 2 * num_sms() : grid);
-    MSI_CUDA(launch_k(dispatch_kernel<true>, dim3(grid), dim3(kThr), smem, st, c->dev,
-                      reinterpret_cast<const __nv_bfloat16*>(x), cnt, idx, slot, T, mb_slot, epoch));
-    return check_launch("dispatch_kernel<tma>");
-  }
-  // SM-store variant: ~64 KB of row stores per CTA, at most one CTA per SM
-  // (rows are split into parts so every warp has work); small micro-batches
-  // use few CTAs, which keeps the last-CTA release cheap
+  // ~64 KB of row stores per CTA, at most one CTA per SM (rows are split into
+  // parts so every warp has work); small micro-batches use few CTAs, which
+  // keeps the last-CTA release cheap
   int grid = (int)((bytes + 65535) / 65536);
   grid = grid < 1 ? 1 : (grid > num_sms() ? num_sms() : grid);
-  MSI_CUDA(launch_k(dispatch_kernel<false>, dim3(grid), dim3(kDispThreads), table, st, c->dev,
-                    reinterpret_cast<const __nv_bfloat16*>(x), cnt, idx, slot, T, mb_slot, epoch));
+  MSI_CUDA(launch_k(dispatch_kernel, dim3(grid), dim3(kDispThreads), 0, reinterpret_cast<cudaStream_t>(stream),
+                    c->dev, reinterpret_cast<const __nv_bfloat16*>(x), cnt, idx, slot, T, mb_slot, epoch));
   return check_launch("dispatch_kernel");
+}
+
+extern "C" int msi_route_dispatch(msi_ctx* c, const void* x, const void* wg, int T, int E, const int32_t* rep,
+                                  int R, int32_t* idx, int32_t* pidx, float* w, int32_t* cnt, int32_t* slot,
+                                  int mb_slot, uint32_t epoch, void* stream) {
+  if (!c || !c->finalized) { set_error("msi_route_dispatch: context not finalized"); return MSI_ESTATE; }
+  if (!c->attn) { set_error("msi_route_dispatch: rank %d has no attention role", c->rank); return MSI_EINVAL; }
+  const msi_plan& p = c->plan;
+  MSI_REQUIRE(T >= 0 && T <= p.max_tokens, "msi_route_dispatch: T=%d exceeds max_tokens=%d", T, p.max_tokens);
+  MSI_REQUIRE(mb_slot >= 0 && mb_slot < p.slots && epoch != 0xffffffffu, "msi_route_dispatch: bad slot/epoch");
+  MSI_REQUIRE(rep ? (E >= 1 && E <= p.experts && pidx) : E == p.experts,
+              "msi_route_dispatch: E must equal the plan's experts (or its logical count with a replica table)");
+  const DevCtx& dv = c->dev;
+  DispatchArgs d{};
+  d.on = 1;
+  d.s = c->my_a;
+  d.n_send = p.n_a;
+  d.n_e = p.n_e;
+  d.E_l = dv.E_l;
+  d.tp = dv.tp;
+  d.H = p.hidden;
+  d.K = p.topk;
+  d.P = p.experts;
+  d.cap_s = p.max_tokens;
+  d.slot_row0 = (long long)mb_slot * dv.recv_rows;
+  for (int q = 0; q < p.n_e; ++q) {
+    d.recv[q] = dv.recv_of[q];
+    d.meta[q] = dv.meta_of[q];
+    d.cntab[q] = dv.ecntab_of[q] + (size_t)mb_slot * p.n_a * p.experts;
+    d.arrive[q] = dv.arrive_of[q] + mb_slot * CTR_STRIDE;
+  }
+  d.ause = dv.my_ause + mb_slot * CTR_STRIDE;
+  d.epoch = epoch;
+  d.status = dv.my_status;
+  d.trace = dv.trace;
+  return gate_topk(x, wg, T, p.hidden, E, p.topk, idx, w, cnt, slot, c->workspace, reinterpret_cast<cudaStream_t>(stream),
+                   rep, rep ? R : 0, rep ? p.experts : 0, c->my_a, rep ? pidx : nullptr, &d);
 }
 
 extern "C" int msi_expert_ffn(msi_ctx* c, const void* w13, const void* w2, int mb_slot,
@@ -852,7 +781,10 @@ extern "C" int msi_expert_ffn(msi_ctx* c, const void* w13, const void* w2, int m
   const int hp_l = p.inter / d.tp;  // this GPU's slice of h' (expert TP)
   GemmLaunch g1{};
   g1.a = c->heap + L.recv + mb_slot * L.recv_slot;
-  g1.a_rows = L.cap;
+  g1.a_rows = L.recv_rows;
+  g1.p.n_src = p.n_a;      // A rows: runs of the (expert, sender) receive regions
+  g1.p.cap_s = p.max_tokens;
+  g1.p.a_runs = 1;
   g1.b = w13;
   g1.p.E_l = d.E_l;
   g1.p.n_total = 2 * hp_l;
@@ -896,6 +828,8 @@ extern "C" int msi_expert_ffn(msi_ctx* c, const void* w13, const void* w2, int m
   g2.p.mode = 1;
   g2.p.out_ld = p.hidden;
   g2.p.meta = reinterpret_cast<const int2*>(c->heap + L.meta + mb_slot * L.meta_slot);
+  g2.p.n_src = p.n_a;      // meta of virtual row v: its (expert, sender) region row
+  g2.p.cap_s = p.max_tokens;
   for (int s = 0; s < p.n_a; ++s) g2.p.dst[s] = d.ybuf_of[s] + mb_slot * L.ybuf_slot;
   g2.p.ticket = d.my_fticket + mb_slot * CTR_STRIDE;
   g2.p.tile_ctr = d.my_fticket + mb_slot * CTR_STRIDE + 2;

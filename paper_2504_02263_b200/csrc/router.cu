@@ -1,28 +1,33 @@
 // router.cu -- fused gate GEMM + top-K + normalized weights + per-expert
-// counts + slot placement.
+// counts + slot placement, optionally fused
+// with the M2N dispatch of the routed rows (route.h).
 //
 // One kernel launch (fine-grained MoE at small T: a logits kernel on a
-// token x expert grid, then route_kernel for phases 2-4).  Each CTA owns BT
+// token x expert grid, then route_kernel for phases 2-5).  Each CTA takes a
+// virtual block id (atomic ticket: every lower block has started) and owns BT
 // consecutive tokens:
 //   1. logits[t,e] in the pinned fp32 order (lane l accumulates elements
 //      256j + 8l + c with fmaf, then an xor butterfly 16,8,4,2,1) -- the
 //      order oracle/msi_oracle.c restates, so routing is bit-exact;
 //   2. top-K per token (warp arg-max, ties to the lower expert), weights =
 //      softmax of the K chosen logits with det_expf (bit-exact as well);
-//   3. in-CTA ranks (BT <= 32 tokens, one warp): bit `lane` of mask[e] marks
-//      "token lane chose e", so rank = popc(mask[e] & lanes_below); the
-//      CTA's per-expert histogram goes to the workspace;
-//   4. the last CTA to finish (ticket) scans the histograms over CTAs
-//      (batched independent loads into shared memory) into per-CTA bases,
-//      writes cnt[E] and adds the bases to every slot (16-B vectors).
-// MSI_ROUTER_PROF=1 writes %globaltimer phase stamps into workspace words
-// 1..8 (scripts/router_phase_probe.py).
-// HBM-bound for small E (reads x once); FMA-bound for E = 256 (logits on
-// CUDA cores because the fixed reduction order is the bit-exactness contract).
+//   3. in-CTA ranks (BT <= 32 tokens, one warp): bit `lane` of mask[p] marks
+//      "token lane chose p", so rank = popc(mask[p] & lanes_below);
+//   4. decoupled look-back: the CTA publishes its per-slot histogram, sums the
+//      histograms (or the first inclusive prefix) of the blocks before it, and
+//      publishes its inclusive prefix -- every CTA gets its slot bases without
+//      a second pass or a serial last-CTA scan;
+//   5. (dispatch) the CTA's rows go straight to the expert GPUs' receive
+//      regions (16-B stores over NVLink peer memory); the last CTA to finish
+//      publishes the sender's counts and releases the arrival counters.
+// HBM-bound for small E (x read once; the dispatch re-reads the CTA's rows from
+// L2); FMA-bound for E = 256 (logits on CUDA cores because the fixed reduction
+// order is the bit-exactness contract).
 #include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
+#include "route.h"
 
 namespace msi {
 
@@ -42,9 +47,9 @@ constexpr int kWarps = 8;
 #endif
 constexpr uint32_t kTaken = 0x7fc0dead;  // NaN payload marking an already-selected expert
 
-// Shared memory: logits [max(BT,16)][E] fp32 (reused by the last CTA for
-// [8][E] masks + [8][E] counts), then -- when WS -- a copy of W_g [E][H] bf16
-// so the FMA loop reads the gate weights at shared-memory latency.
+// Shared memory: logits [max(BT,16)][E] fp32 (reused after top-K for the [P]
+// slot masks and [P] bases), then -- when WS -- a copy of W_g [E][H] bf16 so
+// the FMA loop reads the gate weights at shared-memory latency.
 __host__ __device__ inline size_t logit_smem_bytes(int BT, int E) {
   return (size_t)(BT > 16 ? BT : 16) * E * sizeof(float) + (size_t)E * sizeof(uint32_t);
 }
@@ -58,48 +63,56 @@ struct Placement {
   const int32_t* rep;
   int R, P, sender;
   int32_t* pidx;  // [T,K] physical slot per (t,k) (may alias idx when rep == nullptr)
-  int prof;       // MSI_ROUTER_PROF=1: %globaltimer phase stamps into ws[2..8] (diagnostics)
   int pfw;        // 1 = prefetch the next W_g chunk into L1 (MSI_ROUTER_PFW, unstaged W_g only)
 };
 
-__device__ __forceinline__ void rprof(const Placement& pl, int32_t* ws, int i) {
-  if (pl.prof) {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    ws[i] = (int32_t)(uint32_t)t;
-  }
+// Workspace: [0] finish ticket, [1] virtual-block ticket (both back to 0 at the
+// end of every launch), u64 at byte 64 = launch generation, u64 look-back
+// words [nblk][P] from byte 128: (generation << 32 | flag << 30 | count).
+constexpr size_t kLbOffset = 128;
+constexpr uint32_t kAgg = 1u, kInc = 2u;
+
+__device__ __forceinline__ uint64_t lb_word(uint32_t gen, uint32_t flag, uint32_t v) {
+  return ((uint64_t)gen << 32) | ((uint64_t)flag << 30) | (uint64_t)v;
+}
+__device__ __forceinline__ void st_volatile64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_volatile64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
-// All CTA histograms into shared memory with 16 independent L2 loads in
-// flight per thread (one at a time was a serial chain of L2 round trips:
-// ~30 us for 147 x 256 entries).
-__device__ __forceinline__ void load_hist(int32_t* s_hist, const int32_t* hist, size_t nh) {
-  constexpr int U = 16;
-  for (size_t i0 = threadIdx.x; i0 < nh; i0 += (size_t)blockDim.x * U) {
-    int32_t v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const size_t i = i0 + (size_t)u * blockDim.x;
-      v[u] = i < nh ? __ldcg(&hist[i]) : 0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const size_t i = i0 + (size_t)u * blockDim.x;
-      if (i < nh) s_hist[i] = v[u];
-    }
+// Virtual block id and launch generation of this CTA (thread 0 takes them).
+struct BlockId {
+  int vb;
+  uint32_t gen;
+};
+__device__ __forceinline__ BlockId take_block(int32_t* ws) {
+  __shared__ int s_vb;
+  __shared__ uint32_t s_gen;
+  if (threadIdx.x == 0) {
+    s_vb = atomicAdd(&ws[1], 1);
+    s_gen = (uint32_t)(*reinterpret_cast<volatile uint64_t*>(ws + 16)) + 1u;
   }
+  __syncthreads();
+  return BlockId{s_vb, s_gen};
 }
 
-// Phases 2-4 (shared by both logit kernels): s_logit [BT][E] holds this CTA's
-// logits; produces idx, w (and pidx), in-CTA ranks, and -- in the last CTA --
-// the counts and final slots.
-__device__ __forceinline__ void route_tail(float* s_logit, int t0, int BT, int T, int E, int K,
-                                           int32_t* __restrict__ idx_out, float* __restrict__ w_out,
-                                           int32_t* __restrict__ cnt_out, int32_t* __restrict__ slot_out,
-                                           int32_t* __restrict__ ws, const Placement& pl, size_t smem_cap) {
+// Phases 2-5 (shared by both logit kernels): s_logit [BT][E] holds this CTA's
+// logits; produces idx, w (and pidx), the final slots, the counts (the last
+// virtual block) and, with d.on, the dispatch of the CTA's rows.
+__device__ __forceinline__ void route_tail(const __nv_bfloat16* __restrict__ x, float* s_logit, BlockId b, int nblk,
+                                           int BT, int T, int E, int K, int32_t* __restrict__ idx_out,
+                                           float* __restrict__ w_out, int32_t* __restrict__ cnt_out,
+                                           int32_t* __restrict__ slot_out, int32_t* __restrict__ ws,
+                                           const Placement& pl, const DispatchArgs& d) {
   __shared__ int s_last;
+  __shared__ uint32_t s_epoch;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (blockIdx.x == 0 && threadIdx.x == 0) rprof(pl, ws, 3);
+  const int t0 = b.vb * BT;
+  if (d.on && b.vb == 0 && threadIdx.x == 0) trace_stamp(d.trace, 0);
   // ---- 2. top-K + weights (one warp per token) ----------------------------
   for (int lt = warp; lt < BT; lt += kWarps) {
     const int t = t0 + lt;
@@ -145,184 +158,123 @@ __device__ __forceinline__ void route_tail(float* s_logit, int t0, int BT, int T
   }
   __syncthreads();
 
-  if (blockIdx.x == 0 && threadIdx.x == 0) rprof(pl, ws, 4);
   // ---- 3. in-CTA ranks (BT <= 32 tokens = one warp chunk): lane = token,
-  //      bit `lane` of mask[p] says "this token chose physical slot p", so the
-  //      rank of (t,k) among the CTA's earlier tokens is popc(mask[p] & lanes_below)
+  //      bit `lane` of mask[p] says "this token chose physical slot p"
   const int P = pl.P;
   const int32_t* pidx = pl.rep ? pl.pidx : idx_out;
-  int32_t* hist = ws + 16;                                   // [nblk][P] CTA histograms
-  int32_t* base = hist + (size_t)gridDim.x * P;              // [nblk][P] CTA bases
-  uint32_t* mask = reinterpret_cast<uint32_t*>(s_logit);     // [P] (logits no longer needed)
+  uint32_t* mask = reinterpret_cast<uint32_t*>(s_logit);  // [P] (logits no longer needed)
+  int32_t* s_base = reinterpret_cast<int32_t*>(mask + P);  // [P] exclusive bases of this CTA
   for (int e = threadIdx.x; e < P; e += blockDim.x) mask[e] = 0u;
   __syncthreads();
   if (warp == 0) {
     const int t = t0 + lane;
-    const bool valid = lane < BT && t < T;
-    if (valid)
+    if (lane < BT && t < T)
       for (int k = 0; k < K; ++k) atomicOr(&mask[pidx[(size_t)t * K + k]], 1u << lane);
-    __syncwarp();
+  }
+  __syncthreads();
+
+  // ---- 4. decoupled look-back over the virtual blocks before this one -----
+  uint64_t* lb = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(ws) + kLbOffset);
+  uint64_t* mine = lb + (size_t)b.vb * P;
+  for (int p = threadIdx.x; p < P; p += blockDim.x)  // aggregate first (block 0: already inclusive)
+    st_volatile64(mine + p, lb_word(b.gen, b.vb == 0 ? kInc : kAgg, __popc(mask[p])));
+  for (int p = threadIdx.x; p < P; p += blockDim.x) {
+    uint32_t excl = 0;
+    for (int j = b.vb - 1; j >= 0; --j) {
+      uint64_t v;
+      do { v = ld_volatile64(lb + (size_t)j * P + p); } while ((uint32_t)(v >> 32) != b.gen);
+      excl += (uint32_t)v & 0x3fffffffu;
+      if (((uint32_t)v >> 30 & 3u) == kInc) break;
+    }
+    const uint32_t h = __popc(mask[p]);
+    if (b.vb > 0) st_volatile64(mine + p, lb_word(b.gen, kInc, excl + h));
+    s_base[p] = (int32_t)excl;
+    if (b.vb == nblk - 1) cnt_out[p] = (int32_t)(excl + h);
+  }
+  __syncthreads();
+  if (warp == 0) {  // final slots: rank among the sender's earlier tokens
+    const int t = t0 + lane;
     const uint32_t below = (1u << lane) - 1u;
-    if (valid)
-      for (int k = 0; k < K; ++k)
-        slot_out[(size_t)t * K + k] = __popc(mask[pidx[(size_t)t * K + k]] & below);
-    __syncwarp();
-    for (int e = lane; e < P; e += 32) hist[(size_t)blockIdx.x * P + e] = __popc(mask[e]);
+    if (lane < BT && t < T)
+      for (int k = 0; k < K; ++k) {
+        const int p = pidx[(size_t)t * K + k];
+        slot_out[(size_t)t * K + k] = s_base[p] + __popc(mask[p] & below);
+      }
   }
 
-  // ---- 4. the last CTA to finish turns CTA histograms into bases (exclusive
-  //      scan over CTAs per expert; independent loads, no serial L2 chain) and
-  //      adds them to every slot; its totals are this sender's counts --------
-  __threadfence();
+  // ---- 5. dispatch: this CTA's rows into the expert GPUs' receive regions --
+  if (d.on) {
+    if (threadIdx.x == 0) s_epoch = resolve_epoch(d.epoch, d.ause, 1u, d.status);  // 0 = mismatch: send nothing
+    __syncthreads();
+    if (s_epoch) {
+      const size_t row_bytes = (size_t)d.H * 2;
+      const int nchunk = d.H >> 8;  // 512-B warp chunks per row
+      const int ndst = K * d.tp;
+      for (int lt = warp; lt < BT; lt += kWarps) {
+        const int t = t0 + lt;
+        if (t >= T) break;
+        // lane j < K*tp resolves destination j: (t, k = j / tp) on GPU r = j % tp of the node
+        char* my_dst = nullptr;
+        if (lane < ndst) {
+          const int k = lane / d.tp, r = lane - k * d.tp;
+          const int p = pidx[(size_t)t * K + k];
+          const int q = (p / d.E_l) * d.tp + r;
+          const long long row = d.slot_row0 + ((long long)(p % d.E_l) * d.n_send + d.s) * d.cap_s +
+                                slot_out[(size_t)t * K + k];
+          my_dst = d.recv[q] + row * row_bytes;
+          d.meta[q][row] = make_int2(d.s, t * K + k);
+        }
+        const char* src = reinterpret_cast<const char*>(x + (size_t)t * d.H) + lane * 16;
+        constexpr int U = 8;
+        for (int j0 = 0; j0 < nchunk; j0 += U) {
+          uint4 v[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (j0 + u < nchunk) v[u] = ld_nc_v4(src + (size_t)(j0 + u) * 512);
+          for (int j = 0; j < ndst; ++j) {
+            char* dst = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(my_dst), j)) +
+                        lane * 16;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+              if (j0 + u < nchunk) st_v4(dst + (size_t)(j0 + u) * 512, v[u]);
+          }
+        }
+      }
+    }
+  }
+
+  // ---- 6. the last CTA to finish: counts to the receivers, release, reset --
   __syncthreads();
-  if (blockIdx.x == 0 && threadIdx.x == 0) rprof(pl, ws, 5);
-  if (threadIdx.x == 0) s_last = (atomicAdd(&ws[0], 1) == (int)gridDim.x - 1);
+  if (threadIdx.x == 0) {
+    if (d.on) __threadfence_system();  // this CTA's peer row stores before the ticket
+    else __threadfence();
+    s_last = atomicAdd(&ws[0], 1) == (int)gridDim.x - 1;
+  }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  if (threadIdx.x == 0) rprof(pl, ws, 6);
-  // The last CTA runs alone, so its L2 round trips must overlap: every
-  // histogram entry is loaded at once into shared memory (the logits area is
-  // free), each warp scans whole experts across CTAs there, and the slot
-  // fix-up issues all of a thread's loads before its stores.
-  const int nblk = gridDim.x;
-  const size_t nh = (size_t)nblk * P;
-  int32_t* s_hist = reinterpret_cast<int32_t*>(s_logit);  // [nblk][P] -> exclusive bases in place
-  const bool in_smem = nh * sizeof(int32_t) <= smem_cap;
-  if (in_smem && P >= 64 && P <= (int)blockDim.x) {
-    // many experts: one thread per expert walks the CTAs in shared memory
-    // (the warp-per-expert shuffle scan below costs ~80 us at P = 256)
-    load_hist(s_hist, hist, nh);
-    __syncthreads();
-    const int e = threadIdx.x;
-    if (e < P) {
-      int carry = 0;
-      for (int b = 0; b < nblk; ++b) {
-        const int v = s_hist[(size_t)b * P + e];
-        s_hist[(size_t)b * P + e] = carry;
-        carry += v;
-      }
-      cnt_out[e] = carry;
+  if (d.on && s_epoch) {
+    // the sender's counts (the last virtual block's inclusive prefix), tagged
+    // with the epoch, into every expert GPU's count table
+    const uint32_t ep = s_epoch;
+    for (int i = threadIdx.x; i < d.n_e * P; i += blockDim.x) {
+      const int q = i / P, p = i - q * P;
+      const uint32_t c = (uint32_t)ld_volatile64(lb + (size_t)(nblk - 1) * P + p) & 0x3fffffffu;
+      st_relaxed_sys64(d.cntab[q] + (size_t)d.s * P + p, ((uint64_t)ep << 32) | c);
     }
     __syncthreads();
-  } else if (in_smem) {
-    load_hist(s_hist, hist, nh);
-    __syncthreads();
-    for (int e = warp; e < P; e += kWarps) {  // warp-wide exclusive scan over CTAs
-      int carry = 0;
-      for (int b0 = 0; b0 < nblk; b0 += 32) {
-        const int b = b0 + lane;
-        const int v = b < nblk ? s_hist[(size_t)b * P + e] : 0;
-        int incl = v;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const int o = __shfl_up_sync(0xffffffffu, incl, off);
-          if (lane >= off) incl += o;
-        }
-        if (b < nblk) s_hist[(size_t)b * P + e] = carry + incl - v;
-        carry += __shfl_sync(0xffffffffu, incl, 31);
-      }
-      if (lane == 0) cnt_out[e] = carry;
-    }
-    __syncthreads();
-  } else if (P <= (int)blockDim.x && smem_cap >= (size_t)P * sizeof(int32_t)) {
-    // many CTAs: stream the [nblk][P] histograms through shared memory in
-    // chunks of cb CTAs (coalesced loads/stores); thread e carries expert e
-    const int cb = (int)(smem_cap / ((size_t)P * sizeof(int32_t)));
-    const int e = threadIdx.x;
-    int carry = 0;
-    for (int b0 = 0; b0 < nblk; b0 += cb) {
-      const int nb = min(cb, nblk - b0);
-      const size_t n = (size_t)nb * P;
-      for (size_t i = threadIdx.x; i < n; i += blockDim.x) s_hist[i] = __ldcg(&hist[(size_t)b0 * P + i]);
-      __syncthreads();
-      if (e < P)
-        for (int b = 0; b < nb; ++b) {
-          const int v = s_hist[(size_t)b * P + e];
-          s_hist[(size_t)b * P + e] = carry;
-          carry += v;
-        }
-      __syncthreads();
-      for (size_t i = threadIdx.x; i < n; i += blockDim.x) base[(size_t)b0 * P + i] = s_hist[i];
-      __syncthreads();
-    }
-    if (e < P) cnt_out[e] = carry;
-    __threadfence_block();
-    __syncthreads();
-  } else {  // replicated placements with P > 256: per-thread scans, 8 loads in flight
-    constexpr int U = 8;
-    for (int e = threadIdx.x; e < P; e += blockDim.x) {
-      int run = 0;
-      for (int b0 = 0; b0 < nblk; b0 += U) {
-        int c[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) c[u] = (b0 + u < nblk) ? __ldcg(&hist[(size_t)(b0 + u) * P + e]) : 0;
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (b0 + u < nblk) {
-            base[(size_t)(b0 + u) * P + e] = run;
-            run += c[u];
-          }
-      }
-      cnt_out[e] = run;
-    }
-    __threadfence_block();
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) rprof(pl, ws, 7);
-  const int32_t* bsrc = in_smem ? s_hist : base;
-  const int TK = T * K, stride = blockDim.x;
-  int done = 0;
-  if ((((uintptr_t)pidx | (uintptr_t)slot_out) & 15) == 0) {
-    // 16-B vectors: 4 (t, k) entries per load, 8 vectors in flight per thread
-    // (the single last CTA is latency-bound here: E = 256, T = 4096 took 38 us
-    // with scalar loads)
-    constexpr int V4 = 8;
-    const int n4 = TK / 4;
-    const int4* p4 = reinterpret_cast<const int4*>(pidx);
-    int4* s4 = reinterpret_cast<int4*>(slot_out);
-    for (int j0 = threadIdx.x; j0 < n4; j0 += stride * V4) {
-      int4 ex[V4], sl[V4];
-#pragma unroll
-      for (int u = 0; u < V4; ++u) {
-        const int j = j0 + u * stride;
-        ex[u] = j < n4 ? __ldcg(p4 + j) : make_int4(0, 0, 0, 0);
-        sl[u] = j < n4 ? __ldcg(s4 + j) : make_int4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int u = 0; u < V4; ++u) {
-        const int j = j0 + u * stride;
-        if (j < n4) {
-          const int i = 4 * j;
-          int4 o;
-          o.x = sl[u].x + bsrc[(size_t)(((i + 0) / K) / BT) * P + ex[u].x];
-          o.y = sl[u].y + bsrc[(size_t)(((i + 1) / K) / BT) * P + ex[u].y];
-          o.z = sl[u].z + bsrc[(size_t)(((i + 2) / K) / BT) * P + ex[u].z];
-          o.w = sl[u].w + bsrc[(size_t)(((i + 3) / K) / BT) * P + ex[u].w];
-          s4[j] = o;
-        }
-      }
-    }
-    done = n4 * 4;
-  }
-  constexpr int V = 16;
-  for (int i0 = done + threadIdx.x; i0 < TK; i0 += stride * V) {
-    int ex[V], sl[V];
-#pragma unroll
-    for (int u = 0; u < V; ++u) {
-      const int i = i0 + u * stride;
-      ex[u] = i < TK ? __ldcg(&pidx[i]) : 0;
-      sl[u] = i < TK ? __ldcg(&slot_out[i]) : 0;
-    }
-#pragma unroll
-    for (int u = 0; u < V; ++u) {
-      const int i = i0 + u * stride;
-      if (i < TK) slot_out[i] = sl[u] + bsrc[(size_t)((i / K) / BT) * P + ex[u]];
+    if (threadIdx.x == 0) {
+      *d.ause = ep;  // every CTA has read the old value
+      trace_stamp(d.trace, 2);
+      fence_sys();
+      for (int q = 0; q < d.n_e; ++q) red_release_sys_add(d.arrive[q], 1u);
     }
   }
-  __syncthreads();
-  if (threadIdx.x == 0) rprof(pl, ws, 8);
-  if (threadIdx.x == 0) ws[0] = 0;  // ticket ready for the next launch
+  if (threadIdx.x == 0) {
+    ws[0] = 0;
+    ws[1] = 0;
+    *reinterpret_cast<volatile uint64_t*>(ws + 16) = b.gen;
+  }
 }
 
 // Logits of one warp tile: TT tokens from t_first x TE experts from e_first.
@@ -455,10 +407,11 @@ __device__ __forceinline__ void tile_logits(const __nv_bfloat16* __restrict__ x,
     }
 }
 
+
 // Fine-grained MoE (E >= 64, FMA-bound): the logits get their own 2-D grid --
 // CTA (blockIdx.x, blockIdx.y) = BT tokens x EB experts, one TT x TE warp
 // tile per warp at a time, <= 128 registers so 2 CTAs share an SM -- into a
-// [T][E] fp32 scratch; route_kernel then runs phases 2-4 on 32-token blocks.
+// [T][E] fp32 scratch; route_kernel then runs phases 2-5 on 32-token blocks.
 // Same per-(token, expert) reduction order as the fused kernel: bit-identical.
 template <int TT, int TE>
 __global__ void __launch_bounds__(kWarps * 32, 2)
@@ -484,19 +437,20 @@ gate_logits_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __r
 }
 
 __global__ void __launch_bounds__(kWarps * 32)
-route_kernel(const float* __restrict__ logits, int T, int E, int K, int BT, int32_t* __restrict__ idx_out,
-             float* __restrict__ w_out, int32_t* __restrict__ cnt_out, int32_t* __restrict__ slot_out,
-             int32_t* __restrict__ ws, const Placement pl, size_t smem_cap) {
+route_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ logits, int T, int E, int K, int BT,
+             int32_t* __restrict__ idx_out, float* __restrict__ w_out, int32_t* __restrict__ cnt_out,
+             int32_t* __restrict__ slot_out, int32_t* __restrict__ ws, const Placement pl, const DispatchArgs d) {
   extern __shared__ __align__(16) float s_logit[];  // [BT][E]
   pdl_trigger();
   pdl_wait();
-  const int t0 = blockIdx.x * BT;
-  const int rows = min(BT, T - t0);
+  const BlockId b = take_block(ws);
+  const int t0 = b.vb * BT;
+  const int rows = max(0, min(BT, T - t0));
   const float4* src = reinterpret_cast<const float4*>(logits + (size_t)t0 * E);
   float4* dst = reinterpret_cast<float4*>(s_logit);
   for (int i = threadIdx.x; i < rows * E / 4; i += blockDim.x) dst[i] = __ldcg(src + i);
   __syncthreads();
-  route_tail(s_logit, t0, BT, T, E, K, idx_out, w_out, cnt_out, slot_out, ws, pl, smem_cap);
+  route_tail(x, s_logit, b, (int)gridDim.x, BT, T, E, K, idx_out, w_out, cnt_out, slot_out, ws, pl, d);
 }
 
 // Small warp tiles (TT * TE <= 16) are capped at 128 registers so two CTAs
@@ -507,14 +461,15 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
                  int T, int H, int E, int K, int BT, int32_t* __restrict__ idx_out,
                  float* __restrict__ w_out, int32_t* __restrict__ cnt_out,
                  int32_t* __restrict__ slot_out, int32_t* __restrict__ ws, const Placement pl,
-                 size_t smem_cap) {
+                 const DispatchArgs d) {
   extern __shared__ __align__(16) float s_logit[];         // [BT][E]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t0 = blockIdx.x * BT;
   pdl_trigger();
   pdl_wait();
-  if (blockIdx.x == 0 && threadIdx.x == 0) rprof(pl, ws, 1);
+  const BlockId b = take_block(ws);
+  const int t0 = b.vb * BT;
+  const __nv_bfloat16* wgs = wg;
   if (WS) {  // stage W_g (E*H*2 bytes) with one TMA bulk copy
     __shared__ __align__(8) uint64_t s_bar;
     char* dst = reinterpret_cast<char*>(s_logit) + ((logit_smem_bytes(BT, E) + 15) & ~size_t(15));
@@ -527,16 +482,15 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
     }
     __syncthreads();
     mbar_wait(&s_bar, 0);
-    wg = reinterpret_cast<const __nv_bfloat16*>(dst);
+    wgs = reinterpret_cast<const __nv_bfloat16*>(dst);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) rprof(pl, ws, 2);
 
   // ---- 1. logits ---------------------------------------------------------
   const int tgroups = BT / TT, egroups = E / TE;
   for (int tile = warp; tile < tgroups * egroups; tile += kWarps) {
     const int tg = tile % tgroups, eg = tile / tgroups;
     float acc[TT][TE];
-    tile_logits<TT, TE, WS>(x, wg, t0 + tg * TT, eg * TE, T, H, acc, pl.pfw);
+    tile_logits<TT, TE, WS>(x, wgs, t0 + tg * TT, eg * TE, T, H, acc, pl.pfw);
 #pragma unroll
     for (int i = 0; i < TT; ++i)
 #pragma unroll
@@ -545,44 +499,45 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
   }
   __syncthreads();
 
-  route_tail(s_logit, t0, BT, T, E, K, idx_out, w_out, cnt_out, slot_out, ws, pl, smem_cap);
+  route_tail(x, s_logit, b, (int)gridDim.x, BT, T, E, K, idx_out, w_out, cnt_out, slot_out, ws, pl, d);
 }
 
 constexpr size_t kMaxStagedW = 200 * 1024;  // W_g staged in smem up to this size
 
+// shared memory before the staged W_g: logits, or the [P] masks + [P] bases
+size_t tail_smem_bytes(int BT, int E, int P) {
+  size_t head = logit_smem_bytes(BT, E);
+  if (head < (size_t)P * 8) head = (size_t)P * 8;
+  return (head + 15) & ~size_t(15);
+}
+
 template <int TT, int TE>
 int launch(const void* x, const void* wg, int T, int H, int E, int K, int BT, int32_t* idx,
-           float* w, int32_t* cnt, int32_t* slot, void* ws, const Placement& pl, cudaStream_t st) {
-  const int nblk = (T + BT - 1) / BT;
+           float* w, int32_t* cnt, int32_t* slot, void* ws, const Placement& pl, const DispatchArgs& d,
+           cudaStream_t st) {
+  const int nblk = T > 0 ? (T + BT - 1) / BT : 1;
   const size_t wbytes = (size_t)E * H * 2;
   const bool stage = E <= 16 && wbytes <= kMaxStagedW;  // (unstaged measured 10-50 % slower)
-  size_t head = logit_smem_bytes(BT, E);
-  if (head < (size_t)pl.P * 4) head = (size_t)pl.P * 4;  // the [P] slot masks reuse this space
-  // Wide tiles run one CTA per SM anyway (registers): give the last CTA room
-  // to scan all [nblk][P] histograms in shared memory at once (E = 256,
-  // T = 4096: the chunked scan took 40 us of the 568 us kernel)
-  const size_t nh_bytes = (size_t)nblk * pl.P * 4;
-  if (!stage && TT * TE > 16 && nh_bytes > head && nh_bytes <= 200 * 1024) head = nh_bytes;
-  const size_t smem = ((head + 15) & ~size_t(15)) + (stage ? wbytes : 0);
+  const size_t smem = tail_smem_bytes(BT, E, pl.P) + (stage ? wbytes : 0);
   auto kern = stage ? gate_topk_kernel<TT, TE, true> : gate_topk_kernel<TT, TE, false>;
   if (int arc = smem_attr(reinterpret_cast<const void*>(kern), smem)) return arc;
   MSI_CUDA(launch_k(kern, dim3(nblk), dim3(kWarps * 32), smem, st, reinterpret_cast<const __nv_bfloat16*>(x),
                     reinterpret_cast<const __nv_bfloat16*>(wg), T, H, E, K, BT, idx, w, cnt, slot,
-                    reinterpret_cast<int32_t*>(ws), pl, smem));
+                    reinterpret_cast<int32_t*>(ws), pl, d));
   return check_launch("gate_topk_kernel");
 }
 
-
-// [T][E] fp32 logits scratch of the split path: after the ticket word and the
-// CTA histograms / bases (sized for the smallest BT = 4), 256-B aligned.
+// look-back words for the smallest BT (4) and the [T][E] fp32 logits scratch
+// of the split path after them, 256-B aligned
 size_t split_logits_offset(int T, int P) {
-  const size_t nblk = ((size_t)T + 3) / 4;
-  return (64 + 2 * nblk * (size_t)P * sizeof(int32_t) + 255) & ~size_t(255);
+  const size_t nblk = ((size_t)T + 3) / 4 + 1;
+  return (kLbOffset + nblk * (size_t)P * sizeof(uint64_t) + 255) & ~size_t(255);
 }
 
 template <int TT>
 int launch_split(const void* x, const void* wg, int T, int H, int E, int K, int BTL, int EB, int32_t* idx,
-                 float* w, int32_t* cnt, int32_t* slot, void* ws, const Placement& pl, cudaStream_t st) {
+                 float* w, int32_t* cnt, int32_t* slot, void* ws, const Placement& pl, const DispatchArgs& d,
+                 cudaStream_t st) {
   constexpr int TE = 8;
   MSI_REQUIRE(BTL % TT == 0 && EB % TE == 0 && E % EB == 0, "gate_topk: bad split tile %dx%d", BTL, EB);
   float* logits = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + split_logits_offset(T, pl.P));
@@ -591,12 +546,11 @@ int launch_split(const void* x, const void* wg, int T, int H, int E, int K, int 
                     reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<const __nv_bfloat16*>(wg), T, H, E,
                     BTL, EB, logits, pl.pfw));
   constexpr int BT = 32;
-  size_t head = logit_smem_bytes(BT, E);
-  if (head < (size_t)pl.P * 4) head = (size_t)pl.P * 4;
-  const size_t smem = (head + 15) & ~size_t(15);
+  const size_t smem = tail_smem_bytes(BT, E, pl.P);
   if (int arc = smem_attr(reinterpret_cast<const void*>(route_kernel), smem)) return arc;
-  MSI_CUDA(launch_k(route_kernel, dim3((T + BT - 1) / BT), dim3(kWarps * 32), smem, st, (const float*)logits, T, E, K,
-                    BT, idx, w, cnt, slot, reinterpret_cast<int32_t*>(ws), pl, smem));
+  MSI_CUDA(launch_k(route_kernel, dim3((T + BT - 1) / BT), dim3(kWarps * 32), smem, st,
+                    reinterpret_cast<const __nv_bfloat16*>(x), (const float*)logits, T, E, K, BT, idx, w, cnt, slot,
+                    reinterpret_cast<int32_t*>(ws), pl, d));
   return check_launch("gate_logits_kernel + route_kernel");
 }
 
@@ -604,7 +558,7 @@ int launch_split(const void* x, const void* wg, int T, int H, int E, int K, int 
 // experts per CTA.  MSI_ROUTER_SPLIT=TTxBTLxEB forces the split path with that
 // tile (any T), =0 forces the fused kernel.
 int route_split(const void* x, const void* wg, int T, int H, int E, int K, int32_t* idx, float* w, int32_t* cnt,
-                int32_t* slot, void* ws, const Placement& pl, cudaStream_t st) {
+                int32_t* slot, void* ws, const Placement& pl, const DispatchArgs& d, cudaStream_t st) {
   // measured best at small T (scripts/sweep_router_split.py, T = 128: 2x4x32)
   int tt = 2, btl = 4, eb = 32;
   if (const char* ov = getenv("MSI_ROUTER_SPLIT")) {
@@ -612,9 +566,9 @@ int route_split(const void* x, const void* wg, int T, int H, int E, int K, int32
     if (sscanf(ov, "%dx%dx%d", &a, &b, &c) == 3) { tt = a; btl = b; eb = c; }
   }
   if (E % eb) eb = 8;
-  if (tt == 4) return launch_split<4>(x, wg, T, H, E, K, btl, eb, idx, w, cnt, slot, ws, pl, st);
-  if (tt == 2) return launch_split<2>(x, wg, T, H, E, K, btl, eb, idx, w, cnt, slot, ws, pl, st);
-  return launch_split<1>(x, wg, T, H, E, K, btl, eb, idx, w, cnt, slot, ws, pl, st);
+  if (tt == 4) return launch_split<4>(x, wg, T, H, E, K, btl, eb, idx, w, cnt, slot, ws, pl, d, st);
+  if (tt == 2) return launch_split<2>(x, wg, T, H, E, K, btl, eb, idx, w, cnt, slot, ws, pl, d, st);
+  return launch_split<1>(x, wg, T, H, E, K, btl, eb, idx, w, cnt, slot, ws, pl, d, st);
 }
 
 // The split path wins only at small T (T = 128: 92 -> 71 us); from T ~ 512 on
@@ -629,29 +583,31 @@ bool split_enabled(int E, int T) {
 }  // namespace
 
 int gate_topk(const void* x, const void* wg, int T, int H, int E, int K, int32_t* idx, float* w,
-              int32_t* cnt, int32_t* slot, void* ws, cudaStream_t st, const int32_t* rep = nullptr,
-              int R = 0, int P = 0, int sender = 0, int32_t* pidx = nullptr) {
+              int32_t* cnt, int32_t* slot, void* ws, cudaStream_t st, const int32_t* rep, int R, int P, int sender,
+              int32_t* pidx, const DispatchArgs* dp) {
   MSI_REQUIRE(T >= 0 && H > 0 && H % 256 == 0, "gate_topk: H must be a positive multiple of 256 (got %d)", H);
   MSI_REQUIRE(E >= 1 && E <= 1024 && K >= 1 && K <= E && K <= 32, "gate_topk: need 1 <= K <= min(E, 32), E <= 1024");
   // an empty micro-batch (T = 0) may pass null token / output buffers
   MSI_REQUIRE((x || T == 0) && wg && (T == 0 || (idx && w && slot)) && cnt && ws, "gate_topk: null pointer");
   MSI_REQUIRE(!rep || (R >= 1 && P >= E && P <= 4096 && pidx && sender >= 0),
               "gate_topk: replica table needs R >= 1, E <= P <= 4096, pidx and sender >= 0");
-  const char* pe = getenv("MSI_ROUTER_PROF");
   const char* pf = getenv("MSI_ROUTER_PFW");
-  const Placement pl{rep, R, rep ? P : E, sender, rep ? pidx : idx, (pe && pe[0] == '1') ? 1 : 0,
-                     (pf && pf[0] == '1') ? 1 : 0};
-  if (T == 0) {
+  const Placement pl{rep, R, rep ? P : E, sender, rep ? pidx : idx, (pf && pf[0] == '1') ? 1 : 0};
+  DispatchArgs d{};
+  if (dp) d = *dp;
+  if (T == 0 && !d.on) {
     MSI_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * pl.P, st));
     return 0;
   }
+  if (T == 0)  // empty micro-batch with dispatch: one CTA still runs the protocol (zero counts, release)
+    return launch<1, 1>(x, wg, 0, H, E, K, 8, idx, w, cnt, slot, ws, pl, d, st);
   // Tile shapes: TE experts x TT tokens per warp; BT tokens per CTA.  Small E
   // is HBM-bound (want many CTAs); large E is FMA-bound (want token reuse).
   // MSI_ROUTER_TILE=TTxTExBT overrides the choice (tuning experiments).
   if (const char* ov = getenv("MSI_ROUTER_TILE")) {
     int tt = 0, te = 0, bt = 0;
     if (sscanf(ov, "%dx%dx%d", &tt, &te, &bt) == 3 && bt >= 4 && bt >= tt && bt <= 32 && bt % tt == 0 && E % te == 0) {
-#define MSI_RT(A, B) if (tt == A && te == B) return launch<A, B>(x, wg, T, H, E, K, bt, idx, w, cnt, slot, ws, pl, st);
+#define MSI_RT(A, B) if (tt == A && te == B) return launch<A, B>(x, wg, T, H, E, K, bt, idx, w, cnt, slot, ws, pl, d, st);
       MSI_RT(1, 8) MSI_RT(2, 8) MSI_RT(4, 8) MSI_RT(8, 8) MSI_RT(1, 16) MSI_RT(2, 16) MSI_RT(4, 16) MSI_RT(8, 4)
       MSI_RT(4, 4) MSI_RT(2, 4)
 #undef MSI_RT
@@ -659,7 +615,7 @@ int gate_topk(const void* x, const void* wg, int T, int H, int E, int K, int32_t
   }
   // fine-grained MoE at small T: logits on their own 2-D grid, then top-K /
   // placement (route_split)
-  if (split_enabled(E, T) && E >= 64 && E % 8 == 0) return route_split(x, wg, T, H, E, K, idx, w, cnt, slot, ws, pl, st);
+  if (split_enabled(E, T) && E >= 64 && E % 8 == 0) return route_split(x, wg, T, H, E, K, idx, w, cnt, slot, ws, pl, d, st);
   // One CTA per SM fits (255 registers): BT = the smallest multiple of 4 that
   // covers T in one wave of num_sms() CTAs (<= 32), so no second partial wave
   // (T = 4096: BT 16 -> 28, 256 -> 147 CTAs) and W_g is re-read by as few
@@ -667,7 +623,7 @@ int gate_topk(const void* x, const void* wg, int T, int H, int E, int K, int32_t
   if (E % 16 == 0 && E > 16) {
     int bt = 4 * ((T + 4 * num_sms() - 1) / (4 * num_sms()));
     bt = bt < 4 ? 4 : (bt > 32 ? 32 : bt);
-    return launch<4, 16>(x, wg, T, H, E, K, bt, idx, w, cnt, slot, ws, pl, st);
+    return launch<4, 16>(x, wg, T, H, E, K, bt, idx, w, cnt, slot, ws, pl, d, st);
   }
   // E = 8 / 16: W_g staged once per CTA (TMA bulk copy) and amortised over 32
   // tokens (4 per warp); x is the only HBM stream
@@ -675,25 +631,25 @@ int gate_topk(const void* x, const void* wg, int T, int H, int E, int K, int32_t
   //  scripts/sweep_router_tiles.py -- DBRX T=1024: 50 -> 32 us at BT = 8)
   const int bt = T >= 96 * 32 ? 32 : (T >= 96 * 16 ? 16 : 8);
   if (E % 16 == 0) {
-    if (bt == 32) return launch<4, 16>(x, wg, T, H, E, K, 32, idx, w, cnt, slot, ws, pl, st);
-    if (bt == 16) return launch<2, 16>(x, wg, T, H, E, K, 16, idx, w, cnt, slot, ws, pl, st);
-    return launch<1, 16>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, pl, st);
+    if (bt == 32) return launch<4, 16>(x, wg, T, H, E, K, 32, idx, w, cnt, slot, ws, pl, d, st);
+    if (bt == 16) return launch<2, 16>(x, wg, T, H, E, K, 16, idx, w, cnt, slot, ws, pl, d, st);
+    return launch<1, 16>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, pl, d, st);
   }
   if (E % 8 == 0) {
-    if (bt == 32) return launch<4, 8>(x, wg, T, H, E, K, 32, idx, w, cnt, slot, ws, pl, st);
-    if (bt == 16) return launch<2, 8>(x, wg, T, H, E, K, 16, idx, w, cnt, slot, ws, pl, st);
-    return launch<1, 8>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, pl, st);
+    if (bt == 32) return launch<4, 8>(x, wg, T, H, E, K, 32, idx, w, cnt, slot, ws, pl, d, st);
+    if (bt == 16) return launch<2, 8>(x, wg, T, H, E, K, 16, idx, w, cnt, slot, ws, pl, d, st);
+    return launch<1, 8>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, pl, d, st);
   }
-  if (E % 4 == 0) return launch<1, 4>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, pl, st);
-  if (E % 2 == 0) return launch<1, 2>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, pl, st);
-  return launch<1, 1>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, pl, st);
+  if (E % 4 == 0) return launch<1, 4>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, pl, d, st);
+  if (E % 2 == 0) return launch<1, 2>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, pl, d, st);
+  return launch<1, 1>(x, wg, T, H, E, K, 8, idx, w, cnt, slot, ws, pl, d, st);
 }
 
 size_t gate_topk_workspace(int T, int E) {
-  const size_t nblk = ((size_t)T + 3) / 4;  // smallest BT used above
-  const size_t base = 64 /* ticket + pad */ + 2 * nblk * (size_t)E * sizeof(int32_t);  // CTA histograms + bases
-  // split path (E >= 64): + [T][E] fp32 logits (E here is the physical slot count P >= logical E)
-  return E >= 64 ? split_logits_offset(T, E) + (size_t)T * E * sizeof(float) : base;
+  // look-back words for the smallest BT (4); split path (E >= 64): + [T][E]
+  // fp32 logits (E here is the physical slot count P >= logical E)
+  const size_t lb = split_logits_offset(T, E);
+  return E >= 64 ? lb + (size_t)T * E * sizeof(float) : lb;
 }
 
 }  // namespace msi

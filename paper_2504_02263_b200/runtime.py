@@ -277,6 +277,28 @@ class MoEDecodeLayer:
         r.T, r.mb = T, mb
         return r
 
+    # -- (1) fused router + M2N dispatch ---------------------
+    def route_dispatch(self, x: torch.Tensor, mb: int = 0, stream=None) -> Route:
+        """router(x) and dispatch in one launch (msi_route_dispatch): every
+        routed row is stored into its expert GPU's receive region by the CTA
+        that routed it.  Same outputs as router() + dispatch()."""
+        m = self.g.model
+        T = x.shape[0]
+        if T > self.g.plan.b_a:
+            raise ValueError(f"micro-batch of {T} tokens exceeds plan.b_a={self.g.plan.b_a}")
+        r = self._routes[mb]
+        self.epoch_a[mb] += 1
+        r.T, r.mb, r.epoch = T, mb, (0 if self.device_epochs else self.epoch_a[mb])
+        if self._rep is None:
+            _lib.call("msi_route_dispatch", self.g.ctx, ops._ptr(x), ops._ptr(self.wg), T, m.experts, None, 0,
+                      ops._ptr(r.idx), None, ops._ptr(r.w), ops._ptr(r.cnt), ops._ptr(r.slot), mb, r.epoch,
+                      ops._stream(stream))
+        else:
+            _lib.call("msi_route_dispatch", self.g.ctx, ops._ptr(x), ops._ptr(self.wg), T, m.experts,
+                      ops._ptr(self._rep), self.g.slots.R, ops._ptr(r.idx), ops._ptr(r.pidx), ops._ptr(r.w),
+                      ops._ptr(r.cnt), ops._ptr(r.slot), mb, r.epoch, ops._stream(stream))
+        return r
+
     # -- (1) M2N dispatch -----------------------------------------------------
     def dispatch(self, x: torch.Tensor, route: Route, mb: int | None = None, stream=None) -> Route:
         mb = route.mb if mb is None else mb
@@ -364,12 +386,23 @@ class PingPongRunner:
                          for _ in range(g.plan.m)]
         self.record = record_timeline
         self.events = []
+        self.fused = os.environ.get("MSI_FUSED_DISPATCH", "1") != "0"
 
     def _attn(self, j, l, x):
         """Attention stage of micro-batch j, layer l -> the MoE layer's input."""
         if self.attn is not None:
             return self.attn[j].forward(x, l)
         return x
+
+    def _route_dispatch(self, h, j):
+        """Router + M2N dispatch of micro-batch j: one fused launch by default
+        (MSI_FUSED_DISPATCH=0: router and dispatch kernels, for A/B runs)."""
+        lay = self.layer
+        if self.fused:
+            return lay.route_dispatch(h, j)
+        r = lay.router(h, j)
+        lay.dispatch(h, r, j)
+        return r
 
     def _out(self, xs, j):
         return xs[j] if self.chain else self.outs[j][: xs[j].shape[0]]
@@ -392,8 +425,7 @@ class PingPongRunner:
                 for j in range(m):
                     self._ev(("attn", j, l, 0)); h = self._attn(j, l, xs[j]); self._ev(("attn", j, l, 1))
                     self._ev(("disp", j, l, 0))
-                    r = lay.router(h, j)
-                    lay.dispatch(h, r, j)
+                    r = self._route_dispatch(h, j)
                     self._ev(("disp", j, l, 1))
                     lay.expert_wait(j); self._ev(("ffn", j, l, 0)); lay.expert_ffn(j); self._ev(("ffn", j, l, 1))
                     self._ev(("comb", j, l, 0)); lay.combine(r, resid=h, out=self._out(xs, j)); self._ev(("comb", j, l, 1))
@@ -407,8 +439,7 @@ class PingPongRunner:
                     self._ev(("comb", j, l - 1, 1))
                 self._ev(("attn", j, l, 0)); hs[j] = self._attn(j, l, xs[j]); self._ev(("attn", j, l, 1))
                 self._ev(("disp", j, l, 0))
-                routes[j] = lay.router(hs[j], j)
-                lay.dispatch(hs[j], routes[j], j)
+                routes[j] = self._route_dispatch(hs[j], j)
                 self._ev(("disp", j, l, 1))
             for j in range(m):
                 self._ev(("comb", j, L - 1, 0))

@@ -64,8 +64,11 @@ def _worker(rank, world, port, n_a, n_e, colo, shape, tokens, m, layers, outdir,
                 s = g.attn_index
                 x = O.synth_tokens(tokens[s], model.hidden, seed=1000 * l + 10 * j + s)
                 xd = dev(x)
-                r = layer.router(xd, j)
-                layer.dispatch(xd, r, j)
+                if (l + j) % 2 == 0:  # the fused router + dispatch launch
+                    r = layer.route_dispatch(xd, j)
+                else:  # router, then the stand-alone dispatch
+                    r = layer.router(xd, j)
+                    layer.dispatch(xd, r, j)
             if g.is_expert:
                 layer.expert_step(j)
             if g.is_attention:
@@ -159,7 +162,7 @@ def test_m2n_multi_gpu(lib, tmp_path, n_a, n_e, colo, shape, tokens, m, layers, 
                 assert_close_bf16(a[f"out_{l}_{j}"], ref.out[s], f"layer output s={s}")
                 # placement: every (t, k) row landed at the oracle's row on the right GPU
                 np.testing.assert_array_equal(a[f"dest_{l}_{j}"], ref.pidx[s])
-                q, rows = O.dispatch_rows(ref.pidx[s], ref.slot[s], s, ref.layout, E_l)
+                q, rows = O.dispatch_rows(ref.pidx[s], ref.slot[s], s, E_l, n_a, max(tokens))
                 T = tokens[s]
                 for t in range(T):
                     for k in range(model.topk):

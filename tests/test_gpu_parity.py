@@ -178,7 +178,7 @@ def test_colocated_layer_tiny(lib, T):
     np.testing.assert_array_equal(r.idx[:T].cpu().numpy(), ref.idx[0])
     np.testing.assert_array_equal(r.cnt.cpu().numpy(), ref.cnt[0])
     np.testing.assert_array_equal(r.slot[:T].cpu().numpy(), ref.slot[0])
-    q, rows = O.dispatch_rows(ref.idx[0], ref.slot[0], 0, ref.layout, model.experts)
+    q, rows = O.dispatch_rows(ref.idx[0], ref.slot[0], 0, model.experts, 1, g.plan.b_a)
     recv = to_host(g.recv_view(0))
     meta = g.meta_view(0).cpu().numpy()
     t_idx, k_idx = np.nonzero(np.ones_like(ref.idx[0], bool))
@@ -540,3 +540,86 @@ def test_colocated_layer_empty_microbatch(lib):
         else:
             assert int(r.cnt.sum()) == 0
     g.close()
+
+
+# ------------------------------------------- fused router + M2N dispatch --
+@pytest.mark.parametrize("shape,T,b_a", [("tiny", 64, 64), ("tiny", 1, 64), ("dbrx", 333, 400),
+                                         ("mixtral-8x22b", 3072, 3072),
+                                         ({"name": "fine256", "layers": 1, "hidden": 7168, "intermediate": 256,
+                                           "experts": 256, "topk": 8}, 700, 700),
+                                         ({"name": "fine256s", "layers": 1, "hidden": 7168, "intermediate": 256,
+                                           "experts": 256, "topk": 8}, 130, 130)])
+def test_route_dispatch_fused_matches_oracle(lib, shape, T, b_a):
+    """msi_route_dispatch (router + dispatch in one launch, decoupled
+    look-back slots) places every row where the oracle says, with the same
+    idx / w / cnt / slot bit-exact, and the echo round trip returns them."""
+    from paper_2504_02263_b200 import runtime
+    from paper_2504_02263_b200.config import DeploymentPlan, as_model_spec
+
+    model = as_model_spec(shape)
+    g = runtime.M2NGroup(model, DeploymentPlan(n_a=1, n_e=1, m=2, b_a=b_a, colocated=True), rank=0)
+    wg = O.synth_weights(model.hidden, 128, model.experts, seed=2, experts=[]).wg
+    layer = runtime.MoEDecodeLayer(g, wg=to_dev(wg))
+    for j, seed in enumerate((5, 6)):
+        x = O.synth_tokens(T, model.hidden, seed=seed)
+        xd = to_dev(x)
+        r = layer.route_dispatch(xd, j)
+        layer.expert_echo(j)
+        out = layer.combine(r)
+        torch.cuda.synchronize()
+        assert g.status() == 0
+        idx_r, w_r = O.router(x, wg, model.topk)
+        cnt_r, slot_r = O.place(idx_r, model.experts)
+        np.testing.assert_array_equal(r.idx[:T].cpu().numpy(), idx_r)
+        np.testing.assert_array_equal(r.w[:T].cpu().numpy().view(np.uint32), w_r.view(np.uint32))
+        np.testing.assert_array_equal(r.cnt.cpu().numpy(), cnt_r)
+        np.testing.assert_array_equal(r.slot[:T].cpu().numpy(), slot_r)
+        _, rows = O.dispatch_rows(idx_r, slot_r, 0, model.experts, 1, b_a)
+        recv = to_host(g.recv_view(j))
+        meta = g.meta_view(j).cpu().numpy()
+        for k in range(model.topk):
+            np.testing.assert_array_equal(recv[rows[:, k]], x)
+            np.testing.assert_array_equal(meta[rows[:, k], 1], np.arange(T) * model.topk + k)
+        y = np.repeat(x[:, None, :], model.topk, axis=1)
+        np.testing.assert_array_equal(to_host(out), O.combine(y, w_r))
+    g.close()
+
+
+def test_route_dispatch_fused_empty_and_replicated(lib):
+    """T = 0 still runs the protocol (zero counts, release); replicated slots
+    route through the fused kernel bit-exactly and give the same output as the
+    unreplicated layer."""
+    from paper_2504_02263_b200 import ops, runtime
+    from paper_2504_02263_b200.config import DeploymentPlan, as_model_spec
+
+    model = as_model_spec("tiny")
+    wts = O.synth_weights(model.hidden, model.intermediate, model.experts, seed=0)
+    x = O.synth_tokens(64, model.hidden, seed=41)
+    outs = {}
+    for name, sl in (("plain", None), ("rep", _replicated_slots())):
+        g = runtime.M2NGroup(model, DeploymentPlan(n_a=1, n_e=1, m=1, b_a=64, colocated=True), rank=0, slots=sl)
+        ex = runtime.local_experts(g)
+        w13 = ops.pack_w13(to_dev(wts.w_gate[ex]), to_dev(wts.w_up[ex]))
+        layer = runtime.MoEDecodeLayer(g, wg=to_dev(wts.wg), w13=w13, w2=to_dev(wts.w_down[ex]))
+        empty = torch.empty((0, model.hidden), dtype=torch.bfloat16, device="cuda")
+        r = layer.route_dispatch(empty, 0)
+        layer.expert_step(0)
+        layer.combine(r)
+        torch.cuda.synchronize()
+        assert g.status() == 0 and int(r.cnt.sum()) == 0
+        xd = to_dev(x)
+        r = layer.route_dispatch(xd, 0)
+        layer.expert_step(0)
+        out = layer.combine(r, resid=xd)
+        torch.cuda.synchronize()
+        assert g.status() == 0
+        outs[name] = to_host(out)
+        ref = O.moe_layer([x], wts, model.topk, n_e=1, resid=True,
+                          rep=None if sl is None else sl.rep, phys2log=None if sl is None else sl.phys2log)
+        np.testing.assert_array_equal(r.idx.cpu().numpy(), ref.idx[0])
+        np.testing.assert_array_equal(r.dest.cpu().numpy(), ref.pidx[0])
+        np.testing.assert_array_equal(r.cnt.cpu().numpy(), ref.cnt[0])
+        np.testing.assert_array_equal(r.slot.cpu().numpy(), ref.slot[0])
+        assert_close_bf16(outs[name], ref.out[0], f"layer output ({name})")
+        g.close()
+    np.testing.assert_array_equal(outs["rep"], outs["plain"])

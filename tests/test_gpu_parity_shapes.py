@@ -85,8 +85,7 @@ def test_bench_config_n1_mixtral_8x22b(lib):
     np.testing.assert_array_equal(r.slot.cpu().numpy(), slot_r)
     assert cnt_r.min() >= 512, "every expert should see a full multi-tile segment at this shape"
     # placement: every (t, k) row at the oracle's receive row
-    layout = O.dispatch_layout(cnt_r[None, :], model.experts)
-    _, rows = O.dispatch_rows(idx_r, slot_r, 0, layout, model.experts)
+    _, rows = O.dispatch_rows(idx_r, slot_r, 0, model.experts, 1, T)
     recv = to_host(g.recv_view(0))
     np.testing.assert_array_equal(recv[rows[:, 0]], x)
     np.testing.assert_array_equal(recv[rows[:, 1]], x)

@@ -109,6 +109,9 @@ def test_place_invariants():
 
 
 def test_dispatch_layout_invariants():
+    """Receive rows: distinct per expert GPU, inside region (e_l, s) of cap_s
+    rows, and dense from the region start (slots 0..cnt-1); the virtual
+    order of the expert GEMM is 128-row aligned per expert."""
     rng = np.random.default_rng(1)
     n_a, T, K, E, n_e = 3, 100, 2, 8, 2
     E_l = E // n_e
@@ -118,17 +121,18 @@ def test_dispatch_layout_invariants():
     layout = O.dispatch_layout(cnt, E_l)
     seen = {q: set() for q in range(n_e)}
     for s in range(n_a):
-        q, rows = O.dispatch_rows(idxs[s], pl[s][1], s, layout, E_l)
+        q, rows = O.dispatch_rows(idxs[s], pl[s][1], s, E_l, n_a, T)
         for t in range(T):
             for k in range(K):
                 key = int(rows[t, k])
                 assert key not in seen[q[t, k]]
                 seen[q[t, k]].add(key)
                 e_l = idxs[s][t, k] % E_l
-                total, seg, base = layout[q[t, k]]
-                assert seg[e_l] <= key < seg[e_l] + total[e_l]
-                assert seg[e_l] % O.ROW_ALIGN == 0
-    assert sum(len(v) for v in seen.values()) == n_a * T * K
+                region = (e_l * n_a + s) * T
+                assert region <= key < region + cnt[s, idxs[s][t, k]]
+    for q in range(n_e):
+        total, seg, base = layout[q]
+        assert (seg % O.ROW_ALIGN == 0).all() and (np.diff(seg) >= total[:-1]).all()
 
 
 def test_combine_matches_float64():
