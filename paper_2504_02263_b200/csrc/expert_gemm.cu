@@ -65,8 +65,20 @@ struct SegInfo {
   int start[MAXE];
   int tile0[MAXE + 1];  // first tile of expert e
   int mtiles[MAXE];     // M tiles (CG=1) or M-tile pairs (CG=2)
-  int pre[MAXE][MSI_MAX_RANKS + 1];  // receive regions: first virtual row of sender s in expert e
 };
+
+// Receive regions: first virtual row of each sender in local expert e (the
+// exclusive prefix of its per-sender counts, read from the count table -- a
+// few L2 hits per tile; shared memory has no room left for a table).
+__device__ __forceinline__ void load_pre(const GemmParams& p, int e, int (&pre)[MSI_MAX_RANKS + 1]) {
+  uint32_t c[MSI_MAX_RANKS];
+#pragma unroll
+  for (int s = 0; s < MSI_MAX_RANKS; ++s)
+    c[s] = s < p.n_src ? (uint32_t)ld_relaxed_sys64(p.cntab + (size_t)s * p.E + p.e0 + e) : 0u;
+  pre[0] = 0;
+#pragma unroll
+  for (int s = 0; s < MSI_MAX_RANKS; ++s) pre[s + 1] = pre[s] + (int)c[s];
+}
 
 // A-operand boxes of 128, 64, ..., 1 rows (SW128, 64 columns): a tile's rows
 // are loaded as runs of the (expert, sender) receive regions, each run split
@@ -80,15 +92,15 @@ constexpr int kMaxPieces = 64;
 // Row runs of this CTA's share [v0, v0 + nrows) of expert e's virtual rows:
 // pieces (smem row, global row, box index); returns the rows covered.
 template <int MAXE>
-__device__ __forceinline__ int plan_pieces(const SegInfo<MAXE>& sg, const GemmParams& p, int e, int v0, int nrows,
-                                           int4* pieces, int& npieces) {
+__device__ __forceinline__ int plan_pieces(const SegInfo<MAXE>& sg, const GemmParams& p, int e, const int (&pre)[MSI_MAX_RANKS + 1],
+                                           int v0, int nrows, int4* pieces, int& npieces) {
   npieces = 0;
   const int end = min(v0 + nrows, sg.total[e]);
   for (int s = 0; s < p.n_src; ++s) {
-    const int a = max(v0, sg.pre[e][s]), b = min(end, sg.pre[e][s + 1]);
+    const int a = max(v0, pre[s]), b = min(end, pre[s + 1]);
     if (a >= b) continue;
     int off = a - v0, len = b - a;
-    long long row = ((long long)e * p.n_src + s) * p.cap_s + (a - sg.pre[e][s]);
+    long long row = ((long long)e * p.n_src + s) * p.cap_s + (a - pre[s]);
     while (len > 0 && npieces < kMaxPieces) {
       const int lg = 31 - __clz(min(len, 128));  // largest power of two <= len
       pieces[npieces++] = make_int4(off, (int)row, 7 - lg, 0);
@@ -220,17 +232,9 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
       seg.total[i] = p.totals[i];
     } else {
       const int s = i / p.E_l, e = i - s * p.E_l;
-      const int v = (int)(uint32_t)ld_relaxed_sys64(p.cntab + (size_t)s * p.E + p.e0 + e);
-      if (p.n_src) seg.pre[e][s + 1] = v;
-      atomicAdd(&seg.total[e], v);
+      atomicAdd(&seg.total[e], (int)(uint32_t)ld_relaxed_sys64(p.cntab + (size_t)s * p.E + p.e0 + e));
     }
   }
-  __syncthreads();
-  if (p.n_src)  // receive regions: exclusive prefix over senders per expert
-    for (int e = threadIdx.x; e < p.E_l; e += blockDim.x) {
-      seg.pre[e][0] = 0;
-      for (int s = 0; s < p.n_src; ++s) seg.pre[e][s + 1] += seg.pre[e][s];
-    }
   if (threadIdx.x == 0) {
     int run_start = 0, run_tile = 0;
     for (int e = 0; e < p.E_l; ++e) {
@@ -316,7 +320,9 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
       if (p.a_runs) {  // receive regions: only the rows present, as runs
         const int nrows = hp ? BM / 2 : BM;
         const int v0 = m * CG * BM + (int)rank * nrows;
-        a_bytes = (uint32_t)plan_pieces(seg, p, e, v0, nrows, pieces, npieces) * (BK * 2);
+        int pre[MSI_MAX_RANKS + 1];
+        load_pre(p, e, pre);
+        a_bytes = (uint32_t)plan_pieces(seg, p, e, pre, v0, nrows, pieces, npieces) * (BK * 2);
         if constexpr (CG == 2) {
           const int v1 = m * CG * BM + (int)(rank ^ 1) * nrows;
           a_bytes_pair = a_bytes + (uint32_t)max(0, min(nrows, seg.total[e] - v1)) * (BK * 2);
@@ -430,9 +436,11 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
         } else if (p.meta) {
           long long mrow = row_global;
           if (p.n_src) {  // receive regions: (expert, sender) region row of virtual row row_local
+            int pre[MSI_MAX_RANKS + 1];
+            load_pre(p, e, pre);
             int s = 0;
-            while (s + 1 < p.n_src && seg.pre[e][s + 1] <= row_local) ++s;
-            mrow = ((long long)e * p.n_src + s) * p.cap_s + (row_local - seg.pre[e][s]);
+            while (s + 1 < p.n_src && pre[s + 1] <= row_local) ++s;
+            mrow = ((long long)e * p.n_src + s) * p.cap_s + (row_local - pre[s]);
           }
           const int2 md = p.meta[mrow];
           const size_t drow = (size_t)md.y * (p.row_mul ? p.row_mul : 1) + p.row_add;
