@@ -87,29 +87,67 @@ __device__ __forceinline__ void load_pre(const GemmParams& p, int e, int (&pre)[
 struct AMaps {
   CUtensorMap m[8];  // m[i]: box of 128 >> i rows
 };
-constexpr int kMaxPieces = 64;
+constexpr int kMaxPieces = 48;
 
-// Row runs of this CTA's share [v0, v0 + nrows) of expert e's virtual rows:
-// pieces (smem row, global row, box index); returns the rows covered.
+__device__ __forceinline__ const CUtensorMap* a_box_map(const AMaps& am, uint32_t z) {
+  switch (z) {  // constant indices (once per tile)
+    case 0: return &am.m[0]; case 1: return &am.m[1]; case 2: return &am.m[2]; case 3: return &am.m[3];
+    case 4: return &am.m[4]; case 5: return &am.m[5]; case 6: return &am.m[6]; default: return &am.m[7];
+  }
+}
+
+// TMA load of A box `z` (128 >> z rows), for tiles made of several runs.
+// The producer is one thread whose per-k-block issue cost bounds the MMA
+// rate, so single-run tiles (the common case) resolve their box once per
+// tile and take the same two-load path as compact rows.
+template <bool PAIR>
+__device__ __forceinline__ void tma_a_box(const AMaps& am, uint32_t z, void* dst, int c0, int c1, uint64_t* bar) {
+#define MSI_TMA_A(I)                                                  \
+  case I:                                                             \
+    if constexpr (PAIR) tma_load_2d_pair(dst, &am.m[I], c0, c1, bar); \
+    else tma_load_2d(dst, &am.m[I], c0, c1, bar);                     \
+    break;
+  switch (z) { MSI_TMA_A(0) MSI_TMA_A(1) MSI_TMA_A(2) MSI_TMA_A(3) MSI_TMA_A(4) MSI_TMA_A(5) MSI_TMA_A(6) MSI_TMA_A(7) }
+#undef MSI_TMA_A
+}  // >= the most power-of-two runs 8 senders can cut 128 rows into
+
+// Row runs of this CTA's share [v0, v0 + nrows) of expert e's virtual rows,
+// as power-of-two boxes written to shared memory: piece = (smem row | box
+// index << 8, global row).  Runs before the last are cut exactly; the last
+// run takes one box rounded up to a power of two when it fits the tile (the
+// rows past the run are never stored by the epilogue -- the same over-read
+// as compact rows' tail tiles), so a tile of one run is one box.  Returns
+// the bytes the boxes load (pieces == nullptr: only that, for the peer CTA).
+// 8 senders cut 128 rows into at most ~36 boxes.
 template <int MAXE>
-__device__ __forceinline__ int plan_pieces(const SegInfo<MAXE>& sg, const GemmParams& p, int e, const int (&pre)[MSI_MAX_RANKS + 1],
-                                           int v0, int nrows, int4* pieces, int& npieces) {
+__device__ __forceinline__ uint32_t plan_pieces(const SegInfo<MAXE>& sg, const GemmParams& p, int e,
+                                                const int (&pre)[MSI_MAX_RANKS + 1], int v0, int nrows, uint2* pieces,
+                                                int& npieces) {
   npieces = 0;
+  uint32_t rows = 0;
   const int end = min(v0 + nrows, sg.total[e]);
-  for (int s = 0; s < p.n_src; ++s) {
+#pragma unroll
+  for (int s = 0; s < MSI_MAX_RANKS; ++s) {
+    if (s >= p.n_src) break;
     const int a = max(v0, pre[s]), b = min(end, pre[s + 1]);
     if (a >= b) continue;
     int off = a - v0, len = b - a;
     long long row = ((long long)e * p.n_src + s) * p.cap_s + (a - pre[s]);
+    if (b == end) {  // the tile's last run: one box if the rounded-up size fits
+      const int up = len <= 1 ? 1 : 1 << (32 - __clz(len - 1));
+      if (off + up <= nrows && up <= 128) len = up;
+    }
     while (len > 0 && npieces < kMaxPieces) {
       const int lg = 31 - __clz(min(len, 128));  // largest power of two <= len
-      pieces[npieces++] = make_int4(off, (int)row, 7 - lg, 0);
+      if (pieces) pieces[npieces] = make_uint2((uint32_t)off | ((uint32_t)(7 - lg) << 8), (uint32_t)row);
+      ++npieces;
       off += 1 << lg;
       row += 1 << lg;
       len -= 1 << lg;
+      rows += 1u << lg;
     }
   }
-  return max(0, end - v0);
+  return rows * (BK * 2);
 }
 
 template <int MAXE>
@@ -161,6 +199,7 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
   __shared__ uint32_t s_tmem;
   __shared__ SegInfo<MAXE> seg;
   __shared__ int s_last, s_abort;
+  __shared__ uint2 s_pieces[kMaxPieces];  // producer: A runs of the current tile
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;  // CTA within the pair
@@ -185,8 +224,11 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
     s_abort = ok ? 0 : 1;
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
-    if (CG == 2 || p.a_runs)
-      for (int i = 1; i < (p.a_runs ? 8 : 2); ++i) tma_prefetch(&am.m[i]);
+    if (CG == 2 || p.a_runs) tma_prefetch(&am.m[1]);
+    if (p.a_runs) {
+      tma_prefetch(&am.m[2]); tma_prefetch(&am.m[3]); tma_prefetch(&am.m[4]);
+      tma_prefetch(&am.m[5]); tma_prefetch(&am.m[6]); tma_prefetch(&am.m[7]);
+    }
     for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4 * CG); }
     // ring consumers: MMA thread + 4 epilogue warps (+ the peer's producer
@@ -301,7 +343,9 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
     // ===================== TMA producer (both CTAs of a pair) ==============
     int stage = 0;
     uint32_t phase = 0;
-    int4 pieces[kMaxPieces];
+    uint2* pieces = s_pieces;
+    int pre[MSI_MAX_RANKS + 1];
+    int pre_e = -1;  // expert whose sender prefix is in pre (tiles arrive expert-major)
     for (int it = 0;; ++it) {
       const int tau = leader ? publish_tile(it) : take_tile(it, true);
       if (tau >= ntiles) break;
@@ -311,21 +355,30 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
       // last 128-row tile of a segment split 64/64 over the pair, moved with
       // a 64-row box so the half-cost MMA is not fed a full tile's bytes)
       const bool hp = half_pair(seg, e, m);
-      const int rowA = seg.start[e] + m * CG * BM + (int)rank * (hp ? BM / 2 : BM);
+      int rowA = seg.start[e] + m * CG * BM + (int)rank * (hp ? BM / 2 : BM);
       const int rowB = e * p.n_total + n * BN + (int)rank * C::B_ROWS;
-      const CUtensorMap* mA = (CG == 2 && hp && p.a64) ? &tmA64 : &tmA;
+      const CUtensorMap* mA = (CG == 2 && hp && p.a64) ? &tmA64 : &tmA;  // compact rows
       uint32_t a_bytes = (CG == 2 && hp && p.a64) ? C::A_BYTES / 2 : C::A_BYTES;
       uint32_t a_bytes_pair = 2 * a_bytes;  // both CTAs' A bytes (the leader's barrier counts them)
       int npieces = 0;
+      bool multi = false;  // receive regions: this tile's rows come in several runs
       if (p.a_runs) {  // receive regions: only the rows present, as runs
         const int nrows = hp ? BM / 2 : BM;
         const int v0 = m * CG * BM + (int)rank * nrows;
-        int pre[MSI_MAX_RANKS + 1];
-        load_pre(p, e, pre);
-        a_bytes = (uint32_t)plan_pieces(seg, p, e, pre, v0, nrows, pieces, npieces) * (BK * 2);
-        if constexpr (CG == 2) {
+        if (e != pre_e) {
+          load_pre(p, e, pre);
+          pre_e = e;
+        }
+        a_bytes = plan_pieces(seg, p, e, pre, v0, nrows, pieces, npieces);
+        if constexpr (CG == 2) {  // the peer CTA's boxes (same plan, its rows)
           const int v1 = m * CG * BM + (int)(rank ^ 1) * nrows;
-          a_bytes_pair = a_bytes + (uint32_t)max(0, min(nrows, seg.total[e] - v1)) * (BK * 2);
+          int n1 = 0;
+          a_bytes_pair = a_bytes + plan_pieces(seg, p, e, pre, v1, nrows, nullptr, n1);
+        }
+        multi = npieces > 1;
+        if (npieces == 1) {  // one run from the tile's first row: the compact path with its box
+          mA = a_box_map(am, pieces[0].x >> 8);
+          rowA = (int)pieces[0].y;
         }
       }
       for (int kb = 0; kb < kblocks; ++kb) {
@@ -333,20 +386,24 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
         uint8_t* st = sA + stage * C::STAGE_BYTES;
         if constexpr (CG == 2) {
           if (leader) mbar_expect_tx(&full[stage], a_bytes_pair + 2 * C::B_BYTES);
-          if (p.a_runs) {
-            for (int i = 0; i < npieces; ++i)
-              tma_load_2d_pair(st + pieces[i].x * (BK * 2), &am.m[pieces[i].z], kb * BK, pieces[i].y, &full[stage]);
-          } else {
+          if (multi) {
+            for (int i = 0; i < npieces; ++i) {
+              const uint2 pc = pieces[i];
+              tma_a_box<true>(am, pc.x >> 8, st + (pc.x & 0xff) * (BK * 2), kb * BK, (int)pc.y, &full[stage]);
+            }
+          } else if (a_bytes) {
             tma_load_2d_pair(st, mA, kb * BK, rowA, &full[stage]);
           }
           tma_load_2d_pair(st + C::A_BYTES, &tmB, kb * BK, rowB, &full[stage]);
         } else {
           mbar_expect_tx(&full[stage], a_bytes + C::B_BYTES);
-          if (p.a_runs) {
-            for (int i = 0; i < npieces; ++i)
-              tma_load_2d(st + pieces[i].x * (BK * 2), &am.m[pieces[i].z], kb * BK, pieces[i].y, &full[stage]);
-          } else {
-            tma_load_2d(st, &tmA, kb * BK, rowA, &full[stage]);
+          if (multi) {
+            for (int i = 0; i < npieces; ++i) {
+              const uint2 pc = pieces[i];
+              tma_a_box<false>(am, pc.x >> 8, st + (pc.x & 0xff) * (BK * 2), kb * BK, (int)pc.y, &full[stage]);
+            }
+          } else if (a_bytes) {
+            tma_load_2d(st, mA, kb * BK, rowA, &full[stage]);
           }
           tma_load_2d(st + C::A_BYTES, &tmB, kb * BK, rowB, &full[stage]);
         }
@@ -397,6 +454,8 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
     // every 128-column half holds matching gate/up features.
     const int q = warp & 3;  // TMEM lanes [32q, 32q+32)
     uint8_t* stg = sEpi + q * EPI_WARP_BYTES;
+    int pre[MSI_MAX_RANKS + 1];
+    int pre_e = -1;  // receive regions: sender prefix of expert pre_e
     for (int it = 0;; ++it) {
       int tau = 0;
       if (lane == 0) tau = take_tile(it, false);
@@ -436,11 +495,15 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
         } else if (p.meta) {
           long long mrow = row_global;
           if (p.n_src) {  // receive regions: (expert, sender) region row of virtual row row_local
-            int pre[MSI_MAX_RANKS + 1];
-            load_pre(p, e, pre);
-            int s = 0;
-            while (s + 1 < p.n_src && pre[s + 1] <= row_local) ++s;
-            mrow = ((long long)e * p.n_src + s) * p.cap_s + (row_local - pre[s]);
+            if (e != pre_e) {
+              load_pre(p, e, pre);
+              pre_e = e;
+            }
+            int s = 0, base = 0;
+#pragma unroll
+            for (int j = 1; j < MSI_MAX_RANKS; ++j)  // last sender whose first row is <= row_local
+              if (j < p.n_src && pre[j] <= row_local) { s = j; base = pre[j]; }
+            mrow = ((long long)e * p.n_src + s) * p.cap_s + (row_local - base);
           }
           const int2 md = p.meta[mrow];
           const size_t drow = (size_t)md.y * (p.row_mul ? p.row_mul : 1) + p.row_add;
