@@ -528,7 +528,7 @@ def parity_check(layer, g, runner, att_stages, xs, wg, w13, w2, model, n_experts
                                      and np.array_equal(r.cnt.cpu().numpy(), cnt_r)
                                      and np.array_equal(r.slot[:T].cpu().numpy(), slot_r))}
     tp = g.plan.tp_e
-    ybuf = _u16(g.ybuf_view(0)[:T])
+    ybuf = _u16(layer.gather_y(r))
     yk = ybuf.reshape(T, K * tp, model.hidden)
     out = _u16(runner._out([x for x in xs], 0)[:T]) if xs else None
     if out is not None:

@@ -139,21 +139,26 @@ def main():
             return (t[:len(lat)], t[len(lat):]) if split else t[:len(lat)]
 
         def verify() -> bool:
-            """One more round trip with fresh data (x negated, ybuf cleared):
-            every row must come back byte-exact to its (t, k) slot and no
-            device wait may have failed -- a round trip that raced its own
-            dispatch would return stale rows."""
+            """One more round trip with fresh data (x negated, output cleared):
+            every row must come back byte-exact to its (t, k) slot (the rows
+            the combine pulled) and the combined output must equal the local
+            weighted sum of x, with no failed device wait -- a round trip
+            that raced its own dispatch would return stale rows."""
             ok = torch.ones(1, device=dev)
             if g.is_attention:
                 x.neg_()
-                g.ybuf_view(0)[:T].zero_()
+                out.zero_()
             if world > 1:
                 dist.barrier()
             ours()
             torch.cuda.synchronize()
             if g.is_attention:
-                y = g.ybuf_view(0)[:T]
-                ok[0] = float(torch.equal(y, x[:, None, :].expand(T, K, H)))
+                from paper_2504_02263_b200 import ops as _ops
+                xk = x[:, None, :].expand(T, K, H).contiguous()
+                y = layer.gather_y(route)
+                want = _ops.combine_local(xk, route.w[:T])
+                torch.cuda.synchronize()
+                ok[0] = float(torch.equal(y, xk) and torch.equal(out, want))
             ok[0] *= float(g.status() == 0)
             if world > 1:
                 dist.all_reduce(ok, op=dist.ReduceOp.MIN)

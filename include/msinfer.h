@@ -44,9 +44,8 @@ enum {
 
 /* Buffer ids for msi_ctx_buffer (inspection by tests / benches). */
 enum {
-  MSI_BUF_RECV = 0,   /* expert GPU: received rows [E_l][n_a][max_tokens][H] bf16 per slot */
-  MSI_BUF_META = 1,   /* expert GPU: (sender, t*K+k) per receive row, int32x2 */
-  MSI_BUF_YBUF = 2,   /* attention GPU: expert outputs [max_tokens*K][H] bf16 per slot */
+  MSI_BUF_RECV = 0,   /* expert GPU: received rows [E_l][n_a][max_tokens][H] bf16 per slot
+                       * (after the expert FFN: the expert outputs in place) */
   MSI_BUF_HBUF = 3,   /* expert GPU: SwiGLU activations [cap][H'] bf16 (one, shared) */
   MSI_BUF_CNTAB = 4   /* count table [n_a][E] of (epoch<<32 | count) per slot */
 };
@@ -188,23 +187,32 @@ int msi_expert_wait(msi_ctx* ctx, int mb_slot, uint32_t epoch, void* stream);
 /* ---- (2) expert FFN (SwiGLU): waits for all senders'
  * rows, then two tcgen05/TMEM/TMA grouped GEMMs over the local experts:
  *   H = bf16(silu(X W_gate^T) * (X W_up^T)),  Y = bf16(H W_down^T)
- * whose epilogue stores every Y row straight into its attention GPU's
- * combine buffer (N2M leg) and releases its arrival counter.
+ * whose epilogue stores every Y row over its X in the receive region (local
+ * HBM) and releases the attention GPUs, whose combine pulls it (N2M leg,
+ * PAPER.md:97).
  * w13: msi_pack_w13 layout [E_l][2H'][H]; w2: [E_l][H][H'] (natural). */
 int msi_expert_ffn(msi_ctx* ctx, const void* w13, const void* w2, int mb_slot,
                    uint32_t epoch, void* stream);
 
-/* Identity expert (M2N measurement): waits like msi_expert_ffn, then returns
- * every received row unchanged to its sender's combine buffer (the N2M leg
- * without the FFN), and releases the same counters.  dispatch + echo + combine
- * is the pure M2N round trip of PAPER.md §5's latency/throughput figures. */
+/* Identity expert (M2N measurement): waits like msi_expert_ffn and releases
+ * the same counters without touching the rows (Y = X in the receive regions,
+ * which the combine pulls back).  dispatch + echo + combine is the pure M2N
+ * round trip of PAPER.md §5's latency/throughput figures. */
 int msi_expert_echo(msi_ctx* ctx, int mb_slot, uint32_t epoch, void* stream);
 
-/* ---- (3) combine: waits for all expert GPUs, then
- * out[t] = bf16(resid[t] + sum_k w[t,k] * y[t,k]) (fp32 fmaf, ascending k;
- * resid may be NULL). */
-int msi_combine(msi_ctx* ctx, void* out, const float* w, const void* resid,
-                int T, int mb_slot, uint32_t epoch, void* stream);
+/* ---- (3) combine (N2M leg PAPER.md:97): waits for all expert
+ * GPUs, then pulls the K (x tp_e) expert output rows of every token straight
+ * from the expert GPUs' receive regions over NVLink (its own routing names
+ * the rows: region (dest % E_l, this sender), row slot) and reduces them:
+ * out[t] = bf16(resid[t] + sum_{k,r} w[t,k] * y[t,k,r]) (fp32 fmaf, ascending
+ * (k, r); resid may be NULL).  dest/slot: the router's physical slots and
+ * slots of this micro-batch (msi_route_dispatch / msi_gate_topk outputs). */
+int msi_combine(msi_ctx* ctx, void* out, const float* w, const int32_t* dest, const int32_t* slot,
+                const void* resid, int T, int mb_slot, uint32_t epoch, void* stream);
+/* The expert output rows themselves, y [T][K * tp_e][H] bf16 (the combine's
+ * inputs, for verification; call after the combine of the same use). */
+int msi_gather_y(msi_ctx* ctx, void* y, const int32_t* dest, const int32_t* slot, int T, int mb_slot,
+                 void* stream);
 
 /* ---- building blocks (also used by tests) -------------------------------- */
 /* Expert GEMM variant: 1 = one CTA per 128x256 tile, 2 = CTA pairs

@@ -17,7 +17,7 @@ ROW_ALIGN = 128
 KV_PAGE = 64     # MSI_KV_PAGE
 HEAD_DIM = 128   # MSI_HEAD_DIM
 
-BUF_RECV, BUF_META, BUF_YBUF, BUF_HBUF, BUF_CNTAB = range(5)
+BUF_RECV, BUF_HBUF, BUF_CNTAB = 0, 3, 4
 ERRORS = {-1: "MSI_EINVAL", -2: "MSI_EARCH", -3: "MSI_ESTATE", -4: "MSI_ETIMEOUT", -5: "MSI_EDRIVER"}
 
 
@@ -70,7 +70,8 @@ SIGNATURES = {
     "msi_expert_ffn": (_I, [_P, _P, _P, _I, _U32, _P]),
     "msi_expert_echo": (_I, [_P, _I, _U32, _P]),
     "msi_expert_wait": (_I, [_P, _I, _U32, _P]),
-    "msi_combine": (_I, [_P, _P, _P, _P, _I, _I, _U32, _P]),
+    "msi_combine": (_I, [_P, _P, _P, _P, _P, _P, _I, _I, _U32, _P]),
+    "msi_gather_y": (_I, [_P, _P, _P, _P, _I, _I, _P]),
     "msi_pack_w13": (_I, [_P, _P, _P, _I, _I, _I, _P]),
     "msi_set_gemm_cta_group": (_I, [_I]),
     "msi_grouped_ffn": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _I, _I, _P]),

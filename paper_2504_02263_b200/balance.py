@@ -162,3 +162,25 @@ def balanced_slots(loads, n_e: int, max_replicas: int = 2, k_cold: float = 0.0) 
     """balance_experts(mode='replicated') followed by slots_from_placement."""
     x = balance_experts(loads, n_e, k_cold=k_cold, mode="replicated", max_replicas=max_replicas)
     return slots_from_placement(x, max_replicas)
+
+
+def spread_slots(E: int, n_e: int) -> SlotPlacement:
+    """Even load on any number of expert GPUs (PAPER.md:452-455 on-device
+    redundancy; SPEC.md:407-414 replicated mode with uniform loads): the first
+    (E // n_e) * n_e experts are placed whole, E // n_e per GPU; each of the
+    remaining E % n_e experts is replicated on every GPU, so token t of sender
+    s reaches replica (t + s) mod n_e and each GPU carries 1 / n_e of its rows.
+    Every GPU then holds E / n_e experts' worth of rows (e.g. Mixtral's 8
+    experts on 5 expert GPUs: 1 whole + 3 fifths each, 4 slots per GPU), so a
+    disaggregated split need not divide the expert count."""
+    if n_e < 1 or E < 1:
+        raise ValueError("need E >= 1 experts and n_e >= 1 GPUs")
+    q, r = divmod(E, n_e)
+    if r == 0:
+        return identity_slots(E, n_e)
+    x = np.zeros((E, n_e))
+    for i in range(q * n_e):
+        x[i, i // q] = 1.0
+    for i in range(q * n_e, E):
+        x[i, :] = 1.0 / n_e
+    return slots_from_placement(x)

@@ -9,9 +9,9 @@
 //   GEMM1  A = X [rows][H], B = W13[e] [2H'][H] (gate/up interleaved in
 //          128-row blocks)  ->  epilogue H = bf16(silu(G) * U) into hbuf
 //   GEMM2  A = hbuf [rows][H'], B = W2[e] [H][H']  ->  epilogue stores every
-//          Y row straight to its attention GPU's combine buffer at
-//          (sender, t*K+k) from the row metadata (N2M leg over NVLink), then
-//          the last CTA releases the attention GPUs' arrival counters.
+//          Y row over its own X in the receive region (local HBM); the last
+//          CTA releases the attention GPUs' arrival counters, whose combine
+//          pulls the rows over NVLink (N2M leg).
 //
 // Kernel shape: persistent, one CTA per SM, 256 threads, warp-specialized:
 //   warp 0  TMA producer (1 thread): A 128x64 + B 256x64 bf16 per stage,
@@ -492,22 +492,17 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
       if (row_local < seg.total[e]) {
         if (p.mode == 0) {
           rowdst = reinterpret_cast<char*>(p.out) + ((size_t)row_global * p.out_ld + (size_t)n * (BN / 2) + colofs) * 2;
-        } else if (p.meta) {
-          long long mrow = row_global;
-          if (p.n_src) {  // receive regions: (expert, sender) region row of virtual row row_local
-            if (e != pre_e) {
-              load_pre(p, e, pre);
-              pre_e = e;
-            }
-            int s = 0, base = 0;
-#pragma unroll
-            for (int j = 1; j < MSI_MAX_RANKS; ++j)  // last sender whose first row is <= row_local
-              if (j < p.n_src && pre[j] <= row_local) { s = j; base = pre[j]; }
-            mrow = ((long long)e * p.n_src + s) * p.cap_s + (row_local - base);
+        } else if (p.n_src) {  // receive regions: Y of virtual row row_local replaces its X in place
+          if (e != pre_e) {
+            load_pre(p, e, pre);
+            pre_e = e;
           }
-          const int2 md = p.meta[mrow];
-          const size_t drow = (size_t)md.y * (p.row_mul ? p.row_mul : 1) + p.row_add;
-          rowdst = p.dst[md.x] + (drow * p.out_ld + (size_t)n * BN + colofs) * 2;
+          int s = 0, base = 0;
+#pragma unroll
+          for (int j = 1; j < MSI_MAX_RANKS; ++j)  // last sender whose first row is <= row_local
+            if (j < p.n_src && pre[j] <= row_local) { s = j; base = pre[j]; }
+          const long long rrow = ((long long)e * p.n_src + s) * p.cap_s + (row_local - base);
+          rowdst = reinterpret_cast<char*>(p.out) + ((size_t)rrow * p.out_ld + (size_t)n * BN + colofs) * 2;
         } else {
           rowdst = reinterpret_cast<char*>(p.out) + ((size_t)row_global * p.out_ld + (size_t)n * BN + colofs) * 2;
         }

@@ -33,11 +33,11 @@ struct GemmParams {
   unsigned long long* trace;  // optional %globaltimer stamps: [slot] start,
   int trace_slot;             //   [slot+1] rows arrived, [slot+2] release
   // epilogue
-  int mode;                 // 0: SwiGLU -> out[row][out_ld]; 1: plain -> rows by meta
-  __nv_bfloat16* out;       // mode 0: hbuf; mode 1 with meta == null: y
+  int mode;                 // 0: SwiGLU -> out[row][out_ld]; 1: plain bf16 rows
+  __nv_bfloat16* out;       // mode 0: hbuf; mode 1: y (n_src > 0: the receive
+                            //   regions themselves -- Y of a row replaces its X,
+                            //   which the attention GPU's combine pulls)
   int out_ld;               // elements per output row (H' or H)
-  const int2* meta;         // mode 1: (sender, t*K+k) per row
-  char* dst[MSI_MAX_RANKS]; // mode 1: combine buffer base per sender index
   // dynamic tile scheduler: CTAs (pairs) take tiles in order from this
   // counter (0 at launch; the launch's last fetch resets it)
   uint32_t* tile_ctr;
@@ -46,13 +46,10 @@ struct GemmParams {
   // receive regions (msi_expert_ffn): counts per (sender, expert) from cntab;
   // virtual row v of expert e lives in region (e, s) of cap_s rows at offset
   // v - pre[e][s].  a_runs = 1: GEMM1 loads A by runs of those regions; the
-  // mode 1 epilogue finds meta rows the same way.  n_src = 0: compact rows.
+  // mode 1 epilogue stores row v there.  n_src = 0: compact rows.
   int n_src;
   long long cap_s;
   int a_runs;
-  // mode 1 destination row = meta.y * row_mul + row_add (expert TP: the
-  // partial of TP rank r of (t, k) goes to row (t*K + k)*tp + r); 0 = 1, 0
-  int row_mul, row_add;
   // completion signal (last CTA): red.release.sys +1 on each sig[i]
   uint32_t* ticket;
   uint32_t* sig[MSI_MAX_RANKS];

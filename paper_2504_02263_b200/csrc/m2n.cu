@@ -24,13 +24,14 @@
 //            status[2]                      device error word + abort flag
 //            stats[2] u64                   rows through the expert FFN, FFN calls
 //            cntab[slot][n_a][E] u64        (epoch << 32 | count), all-gathered
-//   ybuf   : (attention role) [slot][max_tokens * K][H] bf16 expert outputs
 //   recv   : (expert role)    [slot][E_l][n_a][max_tokens][H] bf16 received rows:
 //            one region per (local expert, sender), so a sender places its
 //            rows from its own counts alone (no count exchange before the
 //            payload); the expert GEMM loads a tile's rows as runs of these
-//            regions (TMA boxes at any row offset)
-//   meta   : (expert role)    [slot][E_l][n_a][max_tokens] int2 (sender, t*K + k)
+//            regions (TMA boxes at any row offset), and GEMM2 writes each Y
+//            row over its X -- the attention GPU's combine pulls it from
+//            there (it knows the row from its own routing), so there is no
+//            per-row metadata and no combine buffer
 //   hbuf   : (expert role, separate allocation) [cap][H'] SwiGLU activations,
 //            per-expert segments 128-row aligned in virtual (sender-major)
 //            row order; cap = n_a * max_tokens * min(K, E_l) + E_l * 127.
@@ -109,11 +110,10 @@ inline int plan_el(const msi_plan& p) { return p.experts / plan_nodes(p); }
 
 struct Layout {
   size_t arrive, comb, dticket, fticket, ause, euse, status, stats, trace, cntab, ctrl_bytes;
-  size_t ybuf, ybuf_slot;
-  size_t recv, recv_slot, meta, meta_slot;
+  size_t recv, recv_slot;
   size_t total;
   int64_t cap;       // hbuf rows (compact, 128-aligned segments)
-  int64_t recv_rows;  // recv / meta rows per slot: E_l * n_a * max_tokens
+  int64_t recv_rows;  // recv rows per slot: E_l * n_a * max_tokens
 };
 
 Layout make_layout(const msi_plan& p, bool attn, bool expert) {
@@ -137,15 +137,9 @@ Layout make_layout(const msi_plan& p, bool attn, bool expert) {
   int64_t cap = (int64_t)p.n_a * p.max_tokens * per_tok + (int64_t)E_l * (MSI_ROW_ALIGN - 1);
   L.cap = (cap + 127) / 128 * 128;
   L.recv_rows = (int64_t)E_l * p.n_a * p.max_tokens;
-  L.ybuf_slot = (size_t)p.max_tokens * p.topk * plan_tp(p) * p.hidden * 2;  // tp_e partials per (t, k)
-  L.ybuf = off;
-  if (attn) off += align_up(L.ybuf_slot * p.slots, ALIGN);
   L.recv_slot = (size_t)L.recv_rows * p.hidden * 2;
   L.recv = off;
   if (expert) off += align_up(L.recv_slot * p.slots, ALIGN);
-  L.meta_slot = (size_t)L.recv_rows * 8;
-  L.meta = off;
-  if (expert) off += align_up(L.meta_slot * p.slots, ALIGN);
   L.total = off;
   return L;
 }
@@ -156,14 +150,12 @@ struct DevCtx {
   int my_a, my_e;
   int tp, nodes, my_node, my_tp;  // expert TP: node = tp GPUs; this GPU's node and rank in it
   long long cap;        // hbuf rows
-  long long recv_rows;  // recv / meta rows per slot (E_l * n_a * max_tokens regions)
+  long long recv_rows;  // recv rows per slot (E_l * n_a * max_tokens regions)
   uint64_t timeout_ns;
   uint64_t* ecntab_of[MSI_MAX_RANKS];  // count table per expert index q
   uint32_t* arrive_of[MSI_MAX_RANKS];  // per expert index q
   char* recv_of[MSI_MAX_RANKS];        // per expert index q
-  int2* meta_of[MSI_MAX_RANKS];        // per expert index q
   uint32_t* comb_of[MSI_MAX_RANKS];    // per attention index s
-  char* ybuf_of[MSI_MAX_RANKS];        // per attention index s
   uint64_t* my_cntab;
   uint32_t *my_arrive, *my_comb, *my_dticket, *my_fticket, *my_ause, *my_euse;
   int32_t* my_status;
@@ -266,7 +258,6 @@ dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32
       const long long row = (long long)mb * c.recv_rows +
                             ((long long)(e % c.E_l) * c.n_a + s) * c.max_tokens + slot[(size_t)t * c.K + k];
       my_dst = c.recv_of[q] + (size_t)row * row_bytes;
-      if (part == 0) c.meta_of[q][row] = make_int2(s, t * c.K + k);
     }
     const char* src = reinterpret_cast<const char*>(x + (size_t)t * c.H) + lane * 16;
     const int j_end = min(nchunk, (part + 1) * per_part);
@@ -309,13 +300,10 @@ dispatch_kernel(const DevCtx c, const __nv_bfloat16* __restrict__ x, const int32
 }
 
 // ---------------------------------------------------------------- echo ----
-// Identity expert: returns every received row to its sender's combine buffer
-// (the N2M leg without the FFN), so dispatch + echo + combine times the pure
-// M2N round trip.  Same waits, metadata, receive regions and signals as the
-// real expert step.
-constexpr int kEchoThreads = 512;
-constexpr int kMaxPairs = MSI_MAX_LOCAL_EXPERTS * MSI_MAX_RANKS;
-
+// Identity expert (Y = X): waits for every sender's rows like the expert FFN
+// and releases the attention GPUs the same way, without touching the rows --
+// the combine then pulls X back from the receive regions.  dispatch + echo +
+// combine is the pure M2N round trip (both legs' bytes over NVLink).
 // Expert-side wait for a slot's rows (one thread): spins until every sender
 // released the slot's epoch (device-resolved like msi_expert_ffn's), so the
 // FFN kernels that follow start on data already in place and their timing is
@@ -329,114 +317,59 @@ __global__ void expert_wait_kernel(const DevCtx c, int mb, uint32_t epoch) {
     c.my_status[1] = 1;
 }
 
-__global__ void __launch_bounds__(kEchoThreads)
-echo_kernel(const DevCtx c, int mb, uint32_t epoch) {
-  __shared__ int s_ok, s_last;
-  __shared__ int s_first[kMaxPairs + 1];  // exclusive prefix of the (e_l, s) region counts
-  const int tid = threadIdx.x, lane = tid & 31;
-  const uint32_t* arrive = c.my_arrive + mb * CTR_STRIDE;
+__global__ void echo_kernel(const DevCtx c, int mb, uint32_t epoch) {
   pdl_trigger();
   pdl_wait();
   epoch = resolve_epoch(epoch, c.my_euse + mb * CTR_STRIDE, 1u, c.my_status);
   if (epoch == 0) return;
-  if (blockIdx.x == 0 && tid == 0) trace_stamp(c.trace, 3);
-  if (tid == 0) s_ok = wait_geq(arrive, epoch * (uint32_t)c.n_a, c.timeout_ns, c.my_status);
-  __syncthreads();
-  if (!s_ok) return;
-  if (blockIdx.x == 0 && tid == 0) trace_stamp(c.trace, 4);
-  const size_t tab = (size_t)mb * c.n_a * c.E;
-  const int npairs = c.E_l * c.n_a;  // region (e_l, s) = pair e_l * n_a + s
-  for (int i = tid; i < npairs; i += blockDim.x) {  // all counts loaded in parallel
-    const int el = i / c.n_a, s = i - el * c.n_a;
-    s_first[i + 1] = (int)(uint32_t)ld_relaxed_sys64(c.my_cntab + tab + (size_t)s * c.E + c.my_node * c.E_l + el);
-  }
-  __syncthreads();
-  if (tid == 0) {
-    s_first[0] = 0;
-    for (int i = 1; i <= npairs; ++i) s_first[i] += s_first[i - 1];
-  }
-  __syncthreads();
-  const int gwarp = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
-  const int nwarps = gridDim.x * (blockDim.x >> 5);
-  const size_t row_bytes = (size_t)c.H * 2;
-  const int nchunk = c.H >> 8;
-  for (int i = gwarp; i < s_first[npairs]; i += nwarps) {  // one flat row index over all regions
-    int lo = 0, hi = npairs - 1;  // last pair with s_first[pair] <= i
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (s_first[mid] <= i) lo = mid;
-      else hi = mid - 1;
-    }
-    const long long row = (long long)mb * c.recv_rows + (long long)lo * c.max_tokens + (i - s_first[lo]);
-    const int2 md = c.meta_of[c.my_e][row];
-    const char* src = c.recv_of[c.my_e] + (size_t)row * row_bytes + lane * 16;
-    char* dst = c.ybuf_of[md.x] + (size_t)mb * c.max_tokens * c.K * c.tp * row_bytes +
-                ((size_t)md.y * c.tp + c.my_tp) * row_bytes + lane * 16;
-    for (int j = 0; j < nchunk; j += 8) {
-      uint4 v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (j + u < nchunk) v[u] = __ldcg(reinterpret_cast<const uint4*>(src + (size_t)(j + u) * 512));
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (j + u < nchunk) st_v4(dst + (size_t)(j + u) * 512, v[u]);
-    }
-  }
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence_system();
-    s_last = atomicAdd(c.my_fticket + mb * CTR_STRIDE, 1u) == gridDim.x - 1;
-    if (s_last) {
-      c.my_fticket[mb * CTR_STRIDE] = 0;
-      c.my_euse[mb * CTR_STRIDE] = epoch;
-      trace_stamp(c.trace, 5);
-      fence_sys();
-      for (int s = 0; s < c.n_a; ++s) red_release_sys_add(c.comb_of[s] + mb * CTR_STRIDE, 1u);
-    }
-  }
+  trace_stamp(c.trace, 3);
+  if (!wait_geq(c.my_arrive + mb * CTR_STRIDE, epoch * (uint32_t)c.n_a, c.timeout_ns, c.my_status)) return;
+  trace_stamp(c.trace, 4);
+  c.my_euse[mb * CTR_STRIDE] = epoch;
+  trace_stamp(c.trace, 5);
+  fence_sys();
+  for (int s = 0; s < c.n_a; ++s) red_release_sys_add(c.comb_of[s] + mb * CTR_STRIDE, 1u);
 }
 
 // ------------------------------------------------------------- combine ----
-// y rows: (t*K + k)*tp + r, r < tp the expert-TP partials of (t, k); fp32
-// fmaf over ascending (k, r) -- tp = 1 is the plain top-K combine
-__device__ __forceinline__ void combine_row8(const char* ybase, const float* w, const uint16_t* resid,
-                                             uint16_t* out, int t, int col8, int K, int H, int tp) {
-  float acc[8];
-  if (resid) {
-    uint4 r = *reinterpret_cast<const uint4*>(resid + (size_t)t * H + col8 * 8);
-    acc[0] = bf16lo(r.x); acc[1] = bf16hi(r.x); acc[2] = bf16lo(r.y); acc[3] = bf16hi(r.y);
-    acc[4] = bf16lo(r.z); acc[5] = bf16hi(r.z); acc[6] = bf16lo(r.w); acc[7] = bf16hi(r.w);
-  } else {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
-  }
-  for (int kr = 0; kr < K * tp; ++kr) {
-    const float wk = w[(size_t)t * K + kr / tp];
-    uint4 y = __ldcg(reinterpret_cast<const uint4*>(ybase + (((size_t)t * K * tp + kr) * H + col8 * 8) * 2));
-    acc[0] = __fmaf_rn(wk, bf16lo(y.x), acc[0]); acc[1] = __fmaf_rn(wk, bf16hi(y.x), acc[1]);
-    acc[2] = __fmaf_rn(wk, bf16lo(y.y), acc[2]); acc[3] = __fmaf_rn(wk, bf16hi(y.y), acc[3]);
-    acc[4] = __fmaf_rn(wk, bf16lo(y.z), acc[4]); acc[5] = __fmaf_rn(wk, bf16hi(y.z), acc[5]);
-    acc[6] = __fmaf_rn(wk, bf16lo(y.w), acc[6]); acc[7] = __fmaf_rn(wk, bf16hi(y.w), acc[7]);
-  }
-  uint4 o = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
-                       pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
-  *reinterpret_cast<uint4*>(out + (size_t)t * H + col8 * 8) = o;
-}
+// N2M combine as a pull: the attention GPU reads the K (x tp partial) expert
+// output rows of each token straight from the expert GPUs' receive regions
+// (NVLink peer loads; SM loads pull 750 GB/s one way against 700 for stores,
+// scripts/peer_load_probe.cu) and reduces them on the fly, so the return leg
+// and the weighted sum are one pass and no combine buffer is written.
+// out[t] = bf16(resid[t] + sum_{k, r} w[t,k] * y[t,k,r]), fp32 fmaf in
+// ascending (k, r) -- the oracle's order.
+struct CombineSrc {
+  const char* y[MSI_MAX_RANKS];  // per expert GPU q: rows of this micro-batch slot
+  int E_l, tp, n_send, s;        // row of (t, k): ((p % E_l) * n_send + s) * cap_s + slot
+  long long cap_s;
+  const int32_t* dest;           // [T, K] physical slot (null: rows [T, K(, tp)] of y[0])
+  const int32_t* slot;           // [T, K]
+};
 
-// Same arithmetic as combine_row8 with KR = K * tp known at compile time:
-// every y row of the token is loaded before the first FMA (KR independent
-// loads in flight instead of a serial load -> FMA chain per k); the fmaf
-// order (residual, then ascending (k, r)) is unchanged, so results are
-// bit-identical.
 template <int KR>
-__device__ __forceinline__ void combine_row8_fixed(const char* ybase, const float* w, const uint16_t* resid,
-                                                   uint16_t* out, int t, int col8, int K, int H, int tp) {
+__device__ __forceinline__ void combine_row8(const CombineSrc& src, const float* w, const uint16_t* resid, uint16_t* out,
+                                             int t, int col8, int K, int H, uint4* gather) {
   uint4 y[KR];
   float wk[KR];
 #pragma unroll
   for (int kr = 0; kr < KR; ++kr) {
-    y[kr] = __ldcg(reinterpret_cast<const uint4*>(ybase + (((size_t)t * KR + kr) * H + col8 * 8) * 2));
-    wk[kr] = w[(size_t)t * K + kr / tp];
+    const int k = kr / src.tp, r = kr - k * src.tp;
+    const char* row;
+    if (src.dest) {
+      const int p = src.dest[(size_t)t * K + k];
+      const long long rr = ((long long)(p % src.E_l) * src.n_send + src.s) * src.cap_s + src.slot[(size_t)t * K + k];
+      row = src.y[(p / src.E_l) * src.tp + r] + (size_t)rr * H * 2;
+    } else {
+      row = src.y[0] + ((size_t)t * KR + kr) * H * 2;
+    }
+    y[kr] = __ldcg(reinterpret_cast<const uint4*>(row + (size_t)col8 * 16));
+    wk[kr] = w ? w[(size_t)t * K + k] : 0.0f;
+  }
+  if (gather) {  // msi_gather_y: the rows themselves, [T][K*tp][H]
+#pragma unroll
+    for (int kr = 0; kr < KR; ++kr) gather[((size_t)t * KR + kr) * (H / 8) + col8] = y[kr];
+    return;
   }
   float acc[8];
   if (resid) {
@@ -459,11 +392,12 @@ __device__ __forceinline__ void combine_row8_fixed(const char* ybase, const floa
   *reinterpret_cast<uint4*>(out + (size_t)t * H + col8 * 8) = o;
 }
 
+template <int KR>
 __global__ void __launch_bounds__(256)
-combine_kernel(const char* __restrict__ ybase, const float* __restrict__ w, const uint16_t* __restrict__ resid,
-               uint16_t* __restrict__ out, int T, int K, int H, int tp, const uint32_t* wait_ctr,
-               uint32_t epoch, uint32_t mul, const uint32_t* epoch_src, uint64_t timeout_ns,
-               int32_t* status, unsigned long long* trace) {
+combine_kernel(const CombineSrc src, const float* __restrict__ w, const uint16_t* __restrict__ resid,
+               uint16_t* __restrict__ out, uint4* __restrict__ gather, int T, int K, int H, const uint32_t* wait_ctr,
+               uint32_t epoch, uint32_t mul, const uint32_t* epoch_src, uint64_t timeout_ns, int32_t* status,
+               unsigned long long* trace) {
   __shared__ int s_ok;
   const bool t0 = blockIdx.x == 0 && threadIdx.x == 0;
   pdl_trigger();
@@ -479,18 +413,41 @@ combine_kernel(const char* __restrict__ ybase, const float* __restrict__ w, cons
   }
   const int per_row = H / 8;
   const size_t n = (size_t)T * per_row;
-  const int KR = K * tp;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    const int t = (int)(i / per_row), c8 = (int)(i % per_row);
-    switch (KR) {
-      case 1: combine_row8_fixed<1>(ybase, w, resid, out, t, c8, K, H, tp); break;
-      case 2: combine_row8_fixed<2>(ybase, w, resid, out, t, c8, K, H, tp); break;
-      case 4: combine_row8_fixed<4>(ybase, w, resid, out, t, c8, K, H, tp); break;
-      case 8: combine_row8_fixed<8>(ybase, w, resid, out, t, c8, K, H, tp); break;
-      default: combine_row8(ybase, w, resid, out, t, c8, K, H, tp);
-    }
-  }
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    combine_row8<KR>(src, w, resid, out, (int)(i / per_row), (int)(i % per_row), K, H, gather);
   if (t0) trace_stamp(trace, 8);
+}
+
+template <int KR>
+cudaError_t launch_combine_kr(const CombineSrc& src, const float* w, const void* resid, void* out, void* gather, int T,
+                              int K, int H, const uint32_t* wait_ctr, uint32_t epoch, uint32_t mul,
+                              const uint32_t* epoch_src, uint64_t timeout_ns, int32_t* status,
+                              unsigned long long* trace, cudaStream_t st) {
+  const size_t n = (size_t)T * H / 8;
+  int grid = (int)((n + 255) / 256);
+  grid = grid < 1 ? 1 : (grid > 4 * num_sms() ? 4 * num_sms() : grid);
+  return launch_k(combine_kernel<KR>, dim3(grid), dim3(256), 0, st, src, w, reinterpret_cast<const uint16_t*>(resid),
+                  reinterpret_cast<uint16_t*>(out), reinterpret_cast<uint4*>(gather), T, K, H, wait_ctr, epoch, mul,
+                  epoch_src, timeout_ns, status, trace);
+}
+
+// K * tp rows per token; every supported count gets its own unrolled kernel
+int launch_combine(const CombineSrc& src, const float* w, const void* resid, void* out, void* gather, int T, int K,
+                   int H, const uint32_t* wait_ctr, uint32_t epoch, uint32_t mul, const uint32_t* epoch_src,
+                   uint64_t timeout_ns, int32_t* status, unsigned long long* trace, cudaStream_t st) {
+  cudaError_t e;
+  switch (K * src.tp) {
+#define MSI_KR(N) case N: e = launch_combine_kr<N>(src, w, resid, out, gather, T, K, H, wait_ctr, epoch, mul, epoch_src, \
+                                                  timeout_ns, status, trace, st); break;
+    MSI_KR(1) MSI_KR(2) MSI_KR(3) MSI_KR(4) MSI_KR(5) MSI_KR(6) MSI_KR(7) MSI_KR(8) MSI_KR(12) MSI_KR(16)
+    MSI_KR(24) MSI_KR(32)
+#undef MSI_KR
+    default:
+      set_error("combine: K * tp_e = %d rows per token unsupported", K * src.tp);
+      return MSI_EINVAL;
+  }
+  if (e != cudaSuccess) { set_error("combine launch: %s", cudaGetErrorString(e)); return (int)e; }
+  return check_launch("combine_kernel");
 }
 
 }  // namespace
@@ -611,13 +568,11 @@ extern "C" int msi_ctx_finalize(msi_ctx* c) {
     d.ecntab_of[q] = reinterpret_cast<uint64_t*>(c->peer[r] + L.cntab);
     d.arrive_of[q] = reinterpret_cast<uint32_t*>(c->peer[r] + L.arrive);
     d.recv_of[q] = c->peer[r] + L.recv;
-    d.meta_of[q] = reinterpret_cast<int2*>(c->peer[r] + L.meta);
   }
   for (int s = 0; s < p.n_a; ++s) {
     const int r = p.attn_ranks[s];
     Layout L = make_layout(p, true, role_expert(p, r));
     d.comb_of[s] = reinterpret_cast<uint32_t*>(c->peer[r] + L.comb);
-    d.ybuf_of[s] = c->peer[r] + L.ybuf;
   }
   const Layout& M = c->my_layout;
   d.my_cntab = reinterpret_cast<uint64_t*>(c->heap + M.cntab);
@@ -651,12 +606,6 @@ extern "C" int msi_ctx_buffer(msi_ctx* c, int which, int slot, void** ptr, size_
     case MSI_BUF_RECV:
       if (!c->expert) break;
       *ptr = c->heap + L.recv + slot * L.recv_slot; *bytes = L.recv_slot; return 0;
-    case MSI_BUF_META:
-      if (!c->expert) break;
-      *ptr = c->heap + L.meta + slot * L.meta_slot; *bytes = L.meta_slot; return 0;
-    case MSI_BUF_YBUF:
-      if (!c->attn) break;
-      *ptr = c->heap + L.ybuf + slot * L.ybuf_slot; *bytes = L.ybuf_slot; return 0;
     case MSI_BUF_HBUF:
       if (!c->expert) break;
       *ptr = c->hbuf; *bytes = (size_t)L.cap * c->plan.inter * 2; return 0;
@@ -754,7 +703,6 @@ extern "C" int msi_route_dispatch(msi_ctx* c, const void* x, const void* wg, int
   d.slot_row0 = (long long)mb_slot * dv.recv_rows;
   for (int q = 0; q < p.n_e; ++q) {
     d.recv[q] = dv.recv_of[q];
-    d.meta[q] = dv.meta_of[q];
     d.cntab[q] = dv.ecntab_of[q] + (size_t)mb_slot * p.n_a * p.experts;
     d.arrive[q] = dv.arrive_of[q] + mb_slot * CTR_STRIDE;
   }
@@ -822,15 +770,12 @@ extern "C" int msi_expert_ffn(msi_ctx* c, const void* w13, const void* w2, int m
   g2.p.n_a = p.n_a;
   g2.p.E = p.experts;
   g2.p.e0 = d.my_node * d.E_l;
-  g2.p.row_mul = d.tp;   // partial of (t, k) from TP rank r lands in row (t*K + k)*tp + r
-  g2.p.row_add = d.my_tp;
   g2.p.status = d.my_status;
   g2.p.mode = 1;
   g2.p.out_ld = p.hidden;
-  g2.p.meta = reinterpret_cast<const int2*>(c->heap + L.meta + mb_slot * L.meta_slot);
-  g2.p.n_src = p.n_a;      // meta of virtual row v: its (expert, sender) region row
+  g2.p.out = reinterpret_cast<__nv_bfloat16*>(c->heap + L.recv + mb_slot * L.recv_slot);  // Y over X
+  g2.p.n_src = p.n_a;      // virtual row v -> its (expert, sender) region row
   g2.p.cap_s = p.max_tokens;
-  for (int s = 0; s < p.n_a; ++s) g2.p.dst[s] = d.ybuf_of[s] + mb_slot * L.ybuf_slot;
   g2.p.ticket = d.my_fticket + mb_slot * CTR_STRIDE;
   g2.p.tile_ctr = d.my_fticket + mb_slot * CTR_STRIDE + 2;
   for (int s = 0; s < p.n_a; ++s) g2.p.sig[s] = d.comb_of[s] + mb_slot * CTR_STRIDE;
@@ -856,41 +801,59 @@ extern "C" int msi_expert_echo(msi_ctx* c, int mb_slot, uint32_t epoch, void* st
   if (!c || !c->finalized) { set_error("msi_expert_echo: context not finalized"); return MSI_ESTATE; }
   if (!c->expert) { set_error("msi_expert_echo: rank %d has no expert role", c->rank); return MSI_EINVAL; }
   MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots , "msi_expert_echo: bad slot");
-  MSI_CUDA(launch_k(echo_kernel, dim3(num_sms()), dim3(kEchoThreads), 0, reinterpret_cast<cudaStream_t>(stream),
+  MSI_CUDA(launch_k(echo_kernel, dim3(1), dim3(1), 0, reinterpret_cast<cudaStream_t>(stream),
                     c->dev, mb_slot, epoch));
   return check_launch("echo_kernel");
 }
 
-extern "C" int msi_combine(msi_ctx* c, void* out, const float* w, const void* resid, int T, int mb_slot,
-                           uint32_t epoch, void* stream) {
+// Pull sources of this rank's rows of micro-batch slot mb on every expert GPU.
+static CombineSrc combine_src(const msi_ctx* c, int mb_slot, const int32_t* dest, const int32_t* slot) {
+  const msi_plan& p = c->plan;
+  const DevCtx& d = c->dev;
+  CombineSrc src{};
+  for (int q = 0; q < p.n_e; ++q) src.y[q] = d.recv_of[q] + (size_t)mb_slot * d.recv_rows * p.hidden * 2;
+  src.E_l = d.E_l;
+  src.tp = d.tp;
+  src.n_send = p.n_a;
+  src.s = c->my_a;
+  src.cap_s = p.max_tokens;
+  src.dest = dest;
+  src.slot = slot;
+  return src;
+}
+
+extern "C" int msi_combine(msi_ctx* c, void* out, const float* w, const int32_t* dest, const int32_t* slot,
+                           const void* resid, int T, int mb_slot, uint32_t epoch, void* stream) {
   if (!c || !c->finalized) { set_error("msi_combine: context not finalized"); return MSI_ESTATE; }
   if (!c->attn) { set_error("msi_combine: rank %d has no attention role", c->rank); return MSI_EINVAL; }
   MSI_REQUIRE(T >= 0 && T <= c->plan.max_tokens, "msi_combine: T out of range");
-  MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots , "msi_combine: bad slot");
-  MSI_REQUIRE(T == 0 || (out && w), "msi_combine: null pointer");
-  const msi_plan& p = c->plan;
-  const Layout& L = c->my_layout;
-  const size_t n = (size_t)T * p.hidden / 8;
-  int grid = (int)((n + 255) / 256);
-  grid = grid < 1 ? 1 : (grid > 4 * num_sms() ? 4 * num_sms() : grid);
-  MSI_CUDA(launch_k(combine_kernel, dim3(grid), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream),
-                    (const char*)(c->heap + L.ybuf + mb_slot * L.ybuf_slot), w,
-                    reinterpret_cast<const uint16_t*>(resid), reinterpret_cast<uint16_t*>(out), T, p.topk, p.hidden,
-                    plan_tp(p), (const uint32_t*)(c->dev.my_comb + mb_slot * CTR_STRIDE), epoch, (uint32_t)p.n_e,
-                    (const uint32_t*)(c->dev.my_ause + mb_slot * CTR_STRIDE), c->timeout_ns, c->dev.my_status,
-                    c->dev.trace));
-  return check_launch("combine_kernel");
+  MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots, "msi_combine: bad slot");
+  MSI_REQUIRE(T == 0 || (out && w && dest && slot), "msi_combine: null pointer");
+  const DevCtx& d = c->dev;
+  return launch_combine(combine_src(c, mb_slot, dest, slot), w, resid, out, nullptr, T, c->plan.topk, c->plan.hidden,
+                        d.my_comb + mb_slot * CTR_STRIDE, epoch, (uint32_t)c->plan.n_e, d.my_ause + mb_slot * CTR_STRIDE,
+                        c->timeout_ns, d.my_status, d.trace, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int msi_gather_y(msi_ctx* c, void* y, const int32_t* dest, const int32_t* slot, int T, int mb_slot,
+                            void* stream) {
+  if (!c || !c->finalized) { set_error("msi_gather_y: context not finalized"); return MSI_ESTATE; }
+  if (!c->attn) { set_error("msi_gather_y: rank %d has no attention role", c->rank); return MSI_EINVAL; }
+  MSI_REQUIRE(T >= 0 && T <= c->plan.max_tokens && mb_slot >= 0 && mb_slot < c->plan.slots, "msi_gather_y: bad T/slot");
+  MSI_REQUIRE(T == 0 || (y && dest && slot), "msi_gather_y: null pointer");
+  if (T == 0) return 0;
+  return launch_combine(combine_src(c, mb_slot, dest, slot), nullptr, nullptr, nullptr, y, T, c->plan.topk,
+                        c->plan.hidden, nullptr, 0, 0, nullptr, 0, nullptr, nullptr,
+                        reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" int msi_combine_local(const void* y, const float* w, const void* resid, void* out, int T, int K,
                                  int H, void* stream) {
   MSI_REQUIRE(y && w && out && T >= 0 && K >= 1 && H % 8 == 0, "msi_combine_local: bad argument");
   if (T == 0) return 0;
-  const size_t n = (size_t)T * H / 8;
-  int grid = (int)((n + 255) / 256);
-  grid = grid > 4 * num_sms() ? 4 * num_sms() : grid;
-  combine_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<const char*>(y), w, reinterpret_cast<const uint16_t*>(resid),
-      reinterpret_cast<uint16_t*>(out), T, K, H, 1, nullptr, 0, 0, nullptr, 0, nullptr, nullptr);
-  return check_launch("combine_kernel");
+  CombineSrc src{};
+  src.y[0] = reinterpret_cast<const char*>(y);
+  src.tp = 1;
+  return launch_combine(src, w, resid, out, nullptr, T, K, H, nullptr, 0, 0, nullptr, 0, nullptr, nullptr,
+                        reinterpret_cast<cudaStream_t>(stream));
 }

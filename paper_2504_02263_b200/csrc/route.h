@@ -25,9 +25,8 @@ struct DispatchArgs {
   int n_e, E_l, tp;                  // expert GPUs, physical slots per expert node, GPUs per node
   int H, K, P;                       // hidden, top-K, physical expert slots
   long long cap_s;                   // rows per (expert, sender) region
-  long long slot_row0;               // first row of micro-batch slot mb in recv / meta
+  long long slot_row0;               // first row of micro-batch slot mb in recv
   char* recv[MSI_MAX_RANKS];         // per expert index q
-  int2* meta[MSI_MAX_RANKS];         // per expert index q: (sender, t*K + k) per row
   uint64_t* cntab[MSI_MAX_RANKS];    // per expert index q: [n_send][P] of slot mb
   uint32_t* arrive[MSI_MAX_RANKS];   // per expert index q: arrival counter of slot mb
   uint32_t* ause;                    // this sender's use counter of slot mb

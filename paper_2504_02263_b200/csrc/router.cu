@@ -222,7 +222,6 @@ __device__ __forceinline__ void route_tail(const __nv_bfloat16* __restrict__ x, 
           const long long row = d.slot_row0 + ((long long)(p % d.E_l) * d.n_send + d.s) * d.cap_s +
                                 slot_out[(size_t)t * K + k];
           my_dst = d.recv[q] + row * row_bytes;
-          d.meta[q][row] = make_int2(d.s, t * K + k);
         }
         const char* src = reinterpret_cast<const char*>(x + (size_t)t * d.H) + lane * 16;
         constexpr int U = 8;

@@ -138,19 +138,6 @@ class M2NGroup:
         H = self.model.hidden
         return device_view(ptr, (n // (2 * H), H), torch.bfloat16, self.device)
 
-    def meta_view(self, slot: int) -> torch.Tensor:
-        ptr, n = self.buffer(_lib.BUF_META, slot)
-        return device_view(ptr, (n // 8, 2), torch.int32, self.device)
-
-    def ybuf_view(self, slot: int) -> torch.Tensor:
-        """[max_tokens, K, H] expert outputs; with expert TP [max_tokens, K, tp, H]
-        (the tp partial outputs of every (t, k), summed by the combine)."""
-        ptr, n = self.buffer(_lib.BUF_YBUF, slot)
-        m, tp = self.model, self.plan.tp_e
-        rows = n // (2 * m.hidden * m.topk * tp)
-        shape = (rows, m.topk, m.hidden) if tp == 1 else (rows, m.topk, tp, m.hidden)
-        return device_view(ptr, shape, torch.bfloat16, self.device)
-
     def cntab_view(self, slot: int) -> torch.Tensor:
         ptr, n = self.buffer(_lib.BUF_CNTAB, slot)
         return device_view(ptr, (self.plan.n_a, self.model.experts), torch.int64, self.device)
@@ -342,9 +329,20 @@ class MoEDecodeLayer:
         m = self.g.model
         if out is None:
             out = torch.empty((route.T, m.hidden), dtype=torch.bfloat16, device=self.g.device)
-        _lib.call("msi_combine", self.g.ctx, ops._ptr(out), ops._ptr(route.w), ops._ptr(resid),
-                  route.T, route.mb, route.epoch, ops._stream(stream))
+        _lib.call("msi_combine", self.g.ctx, ops._ptr(out), ops._ptr(route.w), ops._ptr(route.dest),
+                  ops._ptr(route.slot), ops._ptr(resid), route.T, route.mb, route.epoch, ops._stream(stream))
         return out
+
+    def gather_y(self, route: Route, stream=None) -> torch.Tensor:
+        """The expert outputs of the route's rows, [T, K, H] (with expert TP
+        [T, K, tp, H]): what the combine pulled (verification; call after
+        the combine of the same micro-batch)."""
+        m, tp = self.g.model, self.g.plan.tp_e
+        shape = (route.T, m.topk, m.hidden) if tp == 1 else (route.T, m.topk, tp, m.hidden)
+        y = torch.empty(shape, dtype=torch.bfloat16, device=self.g.device)
+        _lib.call("msi_gather_y", self.g.ctx, ops._ptr(y), ops._ptr(route.dest), ops._ptr(route.slot), route.T,
+                  route.mb, ops._stream(stream))
+        return y
 
 
 # ------------------------------------------------------------- pipeline -----

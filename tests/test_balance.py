@@ -107,3 +107,24 @@ def test_identity_slots_match_default_layout():
     assert sl.P_l == 4 and sl.logical_of_local(1) == [4, 5, 6, 7]
     with pytest.raises(ValueError):
         B.identity_slots(8, 3)
+
+
+def test_spread_slots_balances_non_dividing_counts():
+    """8 experts on 3, 5 or 6 expert GPUs: every GPU carries E / n_e experts'
+    rows under the (t + s) mod nrep replica rule; 8 on 4 is the identity."""
+    from paper_2504_02263_b200.balance import identity_slots, spread_slots
+    for n_e, P_l in ((3, 4), (5, 4), (6, 3), (7, 2)):
+        sl = spread_slots(8, n_e)
+        assert sl.P_l == P_l and sl.P == n_e * P_l
+        rows = sl.expected_gpu_rows(np.ones(8))
+        np.testing.assert_allclose(rows, 8 / n_e)
+        assert set(sl.phys2log[sl.phys2log >= 0]) == set(range(8))
+        # the replica rule spreads a replicated expert's tokens evenly
+        for e in range(8):
+            c = int(sl.rep[e, 0])
+            t = np.arange(600)
+            for s in range(3):
+                got = np.bincount((t + s) % c, minlength=c)
+                assert got.max() - got.min() <= 1
+    ident = spread_slots(8, 4)
+    assert ident.P == identity_slots(8, 4).P and (ident.phys2log == np.arange(8)).all()

@@ -71,7 +71,10 @@ def test_bench_config_n1_mixtral_8x22b(lib):
     xd = torch.randn((T, model.hidden), generator=gen, device=dev).to(torch.bfloat16)
     r = layer.router(xd, 0)
     layer.dispatch(xd, r, 0)
-    layer.expert_step(0)
+    layer.expert_wait(0)
+    torch.cuda.synchronize()
+    recv = to_host(g.recv_view(0))  # rows as dispatched (the FFN then writes Y over them)
+    layer.expert_ffn(0)
     out = layer.combine(r, resid=xd)
     torch.cuda.synchronize()
     assert g.status() == 0
@@ -86,11 +89,10 @@ def test_bench_config_n1_mixtral_8x22b(lib):
     assert cnt_r.min() >= 512, "every expert should see a full multi-tile segment at this shape"
     # placement: every (t, k) row at the oracle's receive row
     _, rows = O.dispatch_rows(idx_r, slot_r, 0, model.experts, 1, T)
-    recv = to_host(g.recv_view(0))
     np.testing.assert_array_equal(recv[rows[:, 0]], x)
     np.testing.assert_array_equal(recv[rows[:, 1]], x)
     # every expert's SwiGLU outputs (t_e ~ 768) vs the oracle
-    ybuf = to_host(g.ybuf_view(0)[:T])
+    ybuf = to_host(layer.gather_y(r))
     y_ref = np.zeros_like(ybuf)
     for e in range(model.experts):
         t, k = np.nonzero(idx_r == e)
