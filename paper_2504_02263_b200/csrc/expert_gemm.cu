@@ -339,15 +339,20 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
     return t;
   };
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 0) {
     // ===================== TMA producer (both CTAs of a pair) ==============
+    // Lane 0 takes tiles, plans them and issues the loads of single-run
+    // tiles; a tile of several receive-region runs has its boxes issued by
+    // lanes 0..n-1 at once (the single issuing thread bounds the MMA rate).
     int stage = 0;
     uint32_t phase = 0;
     uint2* pieces = s_pieces;
     int pre[MSI_MAX_RANKS + 1];
     int pre_e = -1;  // expert whose sender prefix is in pre (tiles arrive expert-major)
     for (int it = 0;; ++it) {
-      const int tau = leader ? publish_tile(it) : take_tile(it, true);
+      int tau = 0;
+      if (lane == 0) tau = leader ? publish_tile(it) : take_tile(it, true);
+      tau = __shfl_sync(0xffffffffu, tau, 0);
       if (tau >= ntiles) break;
       int e, n, m;
       decode_tile(seg, p.E_l, tau, e, n, m);
@@ -361,8 +366,7 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
       uint32_t a_bytes = (CG == 2 && hp && p.a64) ? C::A_BYTES / 2 : C::A_BYTES;
       uint32_t a_bytes_pair = 2 * a_bytes;  // both CTAs' A bytes (the leader's barrier counts them)
       int npieces = 0;
-      bool multi = false;  // receive regions: this tile's rows come in several runs
-      if (p.a_runs) {  // receive regions: only the rows present, as runs
+      if (p.a_runs && lane == 0) {  // receive regions: only the rows present, as runs
         const int nrows = hp ? BM / 2 : BM;
         const int v0 = m * CG * BM + (int)rank * nrows;
         if (e != pre_e) {
@@ -375,40 +379,38 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
           int n1 = 0;
           a_bytes_pair = a_bytes + plan_pieces(seg, p, e, pre, v1, nrows, nullptr, n1);
         }
-        multi = npieces > 1;
         if (npieces == 1) {  // one run from the tile's first row: the compact path with its box
           mA = a_box_map(am, pieces[0].x >> 8);
           rowA = (int)pieces[0].y;
         }
       }
+      if (p.a_runs) npieces = __shfl_sync(0xffffffffu, npieces, 0);
+      const bool multi = npieces > 1;
+      __syncwarp();  // the pieces in shared memory are visible to every lane
       for (int kb = 0; kb < kblocks; ++kb) {
-        mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* st = sA + stage * C::STAGE_BYTES;
-        if constexpr (CG == 2) {
-          if (leader) mbar_expect_tx(&full[stage], a_bytes_pair + 2 * C::B_BYTES);
-          if (multi) {
-            for (int i = 0; i < npieces; ++i) {
-              const uint2 pc = pieces[i];
-              tma_a_box<true>(am, pc.x >> 8, st + (pc.x & 0xff) * (BK * 2), kb * BK, (int)pc.y, &full[stage]);
-            }
-          } else if (a_bytes) {
-            tma_load_2d_pair(st, mA, kb * BK, rowA, &full[stage]);
+        if (lane == 0) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if constexpr (CG == 2) {
+            if (leader) mbar_expect_tx(&full[stage], a_bytes_pair + 2 * C::B_BYTES);
+            if (!multi && a_bytes) tma_load_2d_pair(st, mA, kb * BK, rowA, &full[stage]);
+            tma_load_2d_pair(st + C::A_BYTES, &tmB, kb * BK, rowB, &full[stage]);
+          } else {
+            mbar_expect_tx(&full[stage], a_bytes + C::B_BYTES);
+            if (!multi && a_bytes) tma_load_2d(st, mA, kb * BK, rowA, &full[stage]);
+            tma_load_2d(st + C::A_BYTES, &tmB, kb * BK, rowB, &full[stage]);
           }
-          tma_load_2d_pair(st + C::A_BYTES, &tmB, kb * BK, rowB, &full[stage]);
-        } else {
-          mbar_expect_tx(&full[stage], a_bytes + C::B_BYTES);
-          if (multi) {
-            for (int i = 0; i < npieces; ++i) {
-              const uint2 pc = pieces[i];
-              tma_a_box<false>(am, pc.x >> 8, st + (pc.x & 0xff) * (BK * 2), kb * BK, (int)pc.y, &full[stage]);
-            }
-          } else if (a_bytes) {
-            tma_load_2d(st, mA, kb * BK, rowA, &full[stage]);
+        }
+        if (multi) {
+          __syncwarp();  // the stage is free (lane 0 waited for it)
+          for (int i = lane; i < npieces; i += 32) {
+            const uint2 pc = pieces[i];
+            tma_a_box<CG == 2>(am, pc.x >> 8, st + (pc.x & 0xff) * (BK * 2), kb * BK, (int)pc.y, &full[stage]);
           }
-          tma_load_2d(st + C::A_BYTES, &tmB, kb * BK, rowB, &full[stage]);
         }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
+      __syncwarp();  // the pieces may be rewritten for the next tile
     }
   } else if (warp == 1 && lane == 0 && leader) {
     // ===================== MMA issuer (leader only) =====================
