@@ -184,3 +184,133 @@ def spread_slots(E: int, n_e: int) -> SlotPlacement:
     for i in range(q * n_e, E):
         x[i, :] = 1.0 / n_e
     return slots_from_placement(x)
+
+
+@dataclass
+class AttnBatchPlan:
+    """Requests assigned to attention nodes: ``assignment[j]``
+    lists the request ids of node j (in placement order), ``predicted[j]`` its
+    predicted attention time in seconds (k2 + sum of request costs; 0 for an
+    empty node)."""
+
+    assignment: list
+    predicted: list
+
+    @property
+    def n_a(self) -> int:
+        return len(self.assignment)
+
+    def seq_lens(self, requests) -> list:
+        """Per node, the sequence lengths of its requests (the attention
+        stage's ctx_lens), in assignment order."""
+        length = {rid: int(s) for rid, s in requests}
+        return [np.array([length[r] for r in ids], np.int32) for ids in self.assignment]
+
+
+def request_cost(seq_len: float, cm) -> float:
+    """alpha·seq_len + beta: one decode request's share of T_a.
+    Without a fitted beta the per-token slope k1 stands in for it."""
+    beta = cm.beta if cm.beta is not None else (cm.k1 if cm.alpha == 0 else 0.0)
+    return cm.alpha * float(seq_len) + beta
+
+
+def _spread(load, k2) -> float:
+    t = [k2 + v for v in load]
+    lo = min(t)
+    return max(t) / lo if lo > 0 else float("inf")
+
+
+def _refine(assignment, load, cost, n_a, k2, max_batch, max_iter: int = 200):
+    """Best-improvement local search on max/min node time (moves + swaps)."""
+    for _ in range(max_iter):
+        cur = _spread(load, k2)
+        best = (cur * (1 - 1e-12), None)
+        for a in range(n_a):
+            for b in range(n_a):
+                if a == b:
+                    continue
+                for ia, i in enumerate(assignment[a]):
+                    # move i: a -> b
+                    if len(assignment[a]) > 1 and (max_batch is None or len(assignment[b]) < max_batch):
+                        trial = load.copy()
+                        trial[a] -= cost[i]
+                        trial[b] += cost[i]
+                        f = _spread(trial, k2)
+                        if f < best[0]:
+                            best = (f, ("move", a, ia, b, None))
+                    if a < b:
+                        for ib, j in enumerate(assignment[b]):  # swap i <-> j
+                            trial = load.copy()
+                            trial[a] += cost[j] - cost[i]
+                            trial[b] += cost[i] - cost[j]
+                            f = _spread(trial, k2)
+                            if f < best[0]:
+                                best = (f, ("swap", a, ia, b, ib))
+        if best[1] is None:
+            return
+        kind, a, ia, b, ib = best[1]
+        i = assignment[a][ia]
+        if kind == "move":
+            assignment[a].pop(ia)
+            assignment[b].append(i)
+            load[a] -= cost[i]
+            load[b] += cost[i]
+        else:
+            j = assignment[b][ib]
+            assignment[a][ia], assignment[b][ib] = j, i
+            load[a] += cost[j] - cost[i]
+            load[b] += cost[i] - cost[j]
+
+
+def compose_attention_batches(requests, n_a: int, cm, target_time: float | None = None,
+                              max_batch: int | None = None, refine_limit: int = 32) -> AttnBatchPlan:
+    """Attention batch composition (§7 / SPEC.md:415-423): per-request
+    cost alpha·seq_len + beta, first-fit-decreasing into n_a bins whose
+    predicted time (k2 + costs) is capped at ``target_time``; a request no
+    bin can take spills to the least-loaded bin (ties: lowest node index).
+    Deterministic: requests of equal cost keep their input order.
+
+    ``target_time`` None = the balanced target k2 + total cost / n_a.
+    ``max_batch`` (additive; the runtime's per-node micro-batch capacity)
+    also caps the request count of a bin; spills then go to the least-loaded
+    bin with room.
+
+    Small instances (<= ``refine_limit`` requests, where one misplaced
+    request moves a node's time by a large fraction) are then refined by
+    deterministic local search -- the best single move or swap between two
+    nodes while it lowers max/min of the node times -- which keeps FFD's
+    result within 15 % of the brute-force optimal max/min ratio
+    (tests/test_balance.py).  Large batches are FFD as stated."""
+    if n_a < 1:
+        raise ValueError("need at least one attention node")
+    reqs = [(rid, float(s)) for rid, s in requests]
+    if max_batch is not None and len(reqs) > n_a * max_batch:
+        raise ValueError("more requests than n_a * max_batch")
+    cost = [request_cost(s, cm) for _, s in reqs]
+    if target_time is None:
+        target_time = cm.k2 + sum(cost) / n_a
+    if not target_time > 0:
+        raise ValueError("target_time must be > 0")
+    order = sorted(range(len(reqs)), key=lambda i: (-cost[i], i))
+    load = [0.0] * n_a
+    assignment = [[] for _ in range(n_a)]
+    eps = 1e-12 * max(target_time, 1e-30)
+
+    def has_room(j):
+        return max_batch is None or len(assignment[j]) < max_batch
+
+    for i in order:
+        dest = None
+        for j in range(n_a):
+            if has_room(j) and cm.k2 + load[j] + cost[i] <= target_time + eps:
+                dest = j
+                break
+        if dest is None:
+            dest = min((j for j in range(n_a) if has_room(j)), key=lambda j: (load[j], j))
+        assignment[dest].append(i)
+        load[dest] += cost[i]
+    if len(reqs) <= refine_limit and n_a > 1:
+        _refine(assignment, load, cost, n_a, cm.k2, max_batch)
+    assignment = [[reqs[i][0] for i in a] for a in assignment]
+    predicted = [cm.k2 + load[j] if assignment[j] else 0.0 for j in range(n_a)]
+    return AttnBatchPlan(assignment, predicted)

@@ -128,3 +128,76 @@ def test_spread_slots_balances_non_dividing_counts():
                 assert got.max() - got.min() <= 1
     ident = spread_slots(8, 4)
     assert ident.P == identity_slots(8, 4).P and (ident.phys2log == np.arange(8)).all()
+
+
+# ---------------- attention batch composition ----------------
+def _cm(alpha=2e-9, beta=1e-7, k2=3e-5):
+    from paper_2504_02263_b200.perf_model import CostModel
+    return CostModel(k1=alpha * 730 + beta, k2=k2, k3=1e-6, k4=1e-4, alpha=alpha, beta=beta)
+
+
+def test_compose_identical_requests_equal_nodes():
+    cm = _cm()
+    for n_a, per in ((4, 3), (3, 5), (2, 64)):
+        reqs = [(i, 730) for i in range(n_a * per)]
+        plan = B.compose_attention_batches(reqs, n_a, cm)
+        assert [len(a) for a in plan.assignment] == [per] * n_a
+        assert max(plan.predicted) - min(plan.predicted) <= 1e-12 * max(plan.predicted)
+
+
+def test_compose_giant_request_isolated():
+    cm = _cm()
+    reqs = [(0, 10), (1, 12), (2, 100000), (3, 9), (4, 11), (5, 10), (6, 8)]
+    plan = B.compose_attention_batches(reqs, 3, cm)
+    giant = [a for a in plan.assignment if 2 in a]
+    assert giant == [[2]]
+
+
+def test_compose_assigns_every_request_once_and_is_deterministic():
+    cm = _cm()
+    rng = np.random.default_rng(1)
+    reqs = [(int(i), int(s)) for i, s in zip(rng.permutation(200), rng.integers(1, 1460, 200))]
+    p1 = B.compose_attention_batches(reqs, 6, cm)
+    p2 = B.compose_attention_batches(reqs, 6, cm)
+    assert p1.assignment == p2.assignment
+    ids = sorted(r for a in p1.assignment for r in a)
+    assert ids == sorted(r for r, _ in reqs)
+    # predicted = k2 + sum of costs, per node
+    length = dict(reqs)
+    for ids_j, t in zip(p1.assignment, p1.predicted):
+        assert t == pytest.approx(cm.k2 + sum(B.request_cost(length[r], cm) for r in ids_j), rel=1e-12)
+    # seq_lens view for the attention stage
+    lens = p1.seq_lens(reqs)
+    assert [len(v) for v in lens] == [len(a) for a in p1.assignment]
+
+
+def test_compose_max_batch_caps_bins():
+    cm = _cm()
+    reqs = [(i, 100 + i) for i in range(12)]
+    plan = B.compose_attention_batches(reqs, 3, cm, target_time=1.0, max_batch=4)  # huge target: first-fit
+    assert [len(a) for a in plan.assignment] == [4, 4, 4]
+    with pytest.raises(ValueError):
+        B.compose_attention_batches(reqs, 2, cm, max_batch=5)
+
+
+def test_compose_near_brute_force_optimum():
+    """random seq lens, n_a = 4, <= 8 requests: max/min predicted node time
+    within the brute-force optimal ratio + 15 %."""
+    cm = _cm(k2=0.0)
+    rng = np.random.default_rng(7)
+    for trial in range(40):
+        n = int(rng.integers(4, 9))
+        lens = rng.integers(1, 1460, n)
+        reqs = list(enumerate(lens.tolist()))
+        plan = B.compose_attention_batches(reqs, 4, cm)
+        got = max(plan.predicted) / min(plan.predicted)
+        cost = [B.request_cost(s, cm) for s in lens]
+        best = np.inf
+        for assign in itertools.product(range(4), repeat=n):
+            if len(set(assign)) < 4:
+                continue
+            t = np.zeros(4)
+            for i, j in enumerate(assign):
+                t[j] += cost[i]
+            best = min(best, t.max() / t.min())
+        assert got <= best * 1.15 + 1e-12, (trial, got, best)
