@@ -120,6 +120,8 @@ def parse():
                     help="every GPU is both an attention and an expert GPU (DeepSeek-V3-shaped config 5)")
     ap.add_argument("--no-merge", dest="merge", action="store_false",
                     help="co-located layouts (any N): keep m separate micro-batches instead of one merged batch")
+    ap.add_argument("--no-pingpong", dest="pingpong", action="store_false",
+                    help="N > 1 co-located headline: skip the secondary disaggregated ping-pong measurement")
     ap.add_argument("--no-m2n", action="store_true", help="skip the M2N round-trip p50 measurement")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch eagerly from Python instead of replaying a captured CUDA graph")
@@ -636,23 +638,54 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------- GPU leg ----
-def main():
-    args = parse()
-    if args.impl == "reference":
-        run_reference(args)
-        return
+def disaggregated_layout(args, world: int, expert_share: float):
+    """Best disaggregated split of `world` GPUs for the ping-pong line:
+    n_e = round(world * T_e / (T_a + T_e)) in [1, world - 1] (the balance
+    condition T_a ~ T_e of PAPER.md:296 with the measured per-token costs),
+    m = --micro-batches separate micro-batches of --b-a tokens per attention
+    GPU.  When n_e does not divide E the experts are spread over slots
+    (balance.spread_slots: whole experts plus replicas of the remainder on
+    every expert GPU)."""
+    from paper_2504_02263_b200.balance import spread_slots
+    from paper_2504_02263_b200.config import as_model_spec
+
+    model = as_model_spec(args.shape)
+    n_e = int(min(max(round(world * expert_share), 1), world - 1))
+    n_a = world - n_e
+    slots = spread_slots(model.experts, n_e) if model.experts % n_e else None
+    src = (f"disaggregated {n_a}+{n_e}: n_e = round({world} x T_e/(T_a+T_e) = {expert_share:.3f}) from the "
+           "co-located headline's stage times" + (f"; {slots.P} expert slots (spread_slots)" if slots else ""))
+    return (n_a, n_e, False, src, 1, model, args.m, args.b_a), slots
+
+
+def pingpong_summary(sub: dict | None, expert_share: float) -> dict | None:
+    """The secondary (disaggregated ping-pong) line, reduced to what compares
+    with the headline."""
+    if sub is None:
+        return None
+    keep = ("value", "value_per_gpu", "ms_per_step", "stage_times", "clocks", "gpu_launches", "attention")
+    out = {k: sub.get(k) for k in keep}
+    out["config"] = sub["config"]
+    out["expert_share"] = expert_share
+    rf = sub.get("roofline") or {}
+    out["expert_ffn"] = {k: rf.get(k) for k in ("achieved", "frac", "frac_burst", "avg_launch_pair_ms", "unit")}
+    par = sub.get("parity") or {}
+    out["parity"] = {"routing_bit_exact": par.get("routing_bit_exact"),
+                     "combine_bit_exact": par.get("combine_bit_exact")}
+    return out
+
+
+def measure(args, rank: int, world: int, local: int, layout, full: bool = True, slots_override=None):
+    """Set up one layout, run the warm-up and the K timed steps, and return
+    rank 0's JSON line (None on other ranks).  full=False (the secondary
+    ping-pong measurement) skips the e2e, M2N latency and CPU legs."""
     import torch
     import torch.distributed as dist
 
     from paper_2504_02263_b200 import runtime
-    from paper_2504_02263_b200.config import DeploymentPlan, WorkloadSpec, as_model_spec
+    from paper_2504_02263_b200.config import DeploymentPlan, WorkloadSpec
 
-    rank, world, local = runtime.init_distributed_from_env("gloo" if _over() else "nccl")
-    if world != args.gpus:
-        if rank == 0:
-            print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}))
-        sys.exit(2)
-    n_a, n_e, colo, plan_source, tp_e, model, m_eff, b_a = resolve_layout(args, world)
+    n_a, n_e, colo, plan_source, tp_e, model, m_eff, b_a = layout
     args.b_a = b_a
     plan = DeploymentPlan(n_a=n_a, n_e=n_e, m=m_eff, b_a=b_a, colocated=colo, tp_e=tp_e)
     dev = torch.device(f"cuda:{local}")
@@ -687,7 +720,7 @@ def main():
         w_att = attn_mod.AttentionWeights(model, dev, seed=0)
         att_stages = [attn_mod.AttentionStage(model, args.b_a, args.layers, dev, weights=w_att,
                                           avg_seq_len=wl.avg_seq_len, seed=1000 * rank + j) for j in range(plan.m)]
-    slots, loads = None, None
+    slots, loads = slots_override, None
     if args.balance or args.skew > 0:
         # calibration: this step's routing counts (all attention ranks), placement
         # by balance_experts(mode="replicated"), agreed by all ranks
@@ -849,7 +882,7 @@ def main():
 
     # ---- e2e through the public API with host buffers -------------------
     e2e = None
-    if not args.no_e2e:
+    if full and not args.no_e2e:
         # Host-resident inputs and results, every step: step i+1's inputs go
         # H2D and step i's results go D2H on a copy stream while step i
         # computes (double-buffered pinned host buffers + device staging; the
@@ -920,7 +953,7 @@ def main():
 
     # ---- the metric's M2N dispatch+combine p50 (this config's micro-batch) ----
     m2n = None
-    if not args.no_m2n:
+    if full and not args.no_m2n:
         xm = None
         if g.is_attention:
             xm = att_stages[0].y if att_stages else xs[0]
@@ -928,9 +961,7 @@ def main():
 
     if rank != 0:
         g.close()
-        if world > 1:
-            dist.destroy_process_group()
-        return
+        return None
 
     peaks = measured_peaks()
     traffic = ncu_traffic(model.name, args.b_a, n_a, n_e, colo)
@@ -943,15 +974,17 @@ def main():
     flops_per_call = 6.0 * (rows_total / max(calls_total, 1)) * model.hidden * model.intermediate / plan.tp_e
     achieved = flops_per_call / ffn_avg_s / 1e12 if ffn_n else None
     peak = peaks.get("bf16_tflops_sustained") or 1404.8
-    # our kernels per (micro-batch, layer): attention (stand-in 1; real: rope_append +
-    # decode_attn [+ split combine]; its two projections are cuBLAS), router,
-    # dispatch, expert wait + 2 GEMMs, combine
+    # our kernels per (micro-batch, layer): attention (real: QKV GEMM with
+    # RoPE/append epilogue + decode_attn [+ split combine] + O GEMM with the
+    # residual), router + dispatch (one fused launch; E >= 64 at T <= 256:
+    # logits + route kernels), expert wait + [region gather when several
+    # senders share an expert] + 2 GEMMs, combine
     attn_launches = 0
     if att_stages:
-        attn_launches = 2 + (1 if att_stages[0].ws is not None else 0)
-    # router: one fused kernel, or logits + route kernels (E >= 64 at T <= 256)
+        attn_launches = 3 + (1 if att_stages[0].ws is not None else 0)
     router_launches = 2 if (model.experts >= 64 and model.experts % 8 == 0 and args.b_a <= 256) else 1
-    launches_per_mbl = attn_launches + router_launches + 1 + 3 + 1  # expert: wait + 2 GEMMs
+    expert_launches = 3 + (1 if n_a > 1 else 0)
+    launches_per_mbl = attn_launches + router_launches + expert_launches + 1
     line = {
         "metric": "decode tokens/s/GPU (MoE layer, ping-pong); M2N dispatch+combine p50 µs",
         "value": value, "unit": "layer-tokens/s", "value_per_gpu": value / world,
@@ -986,17 +1019,57 @@ def main():
     # our kernels inside the timed region (per rank, summed over roles)
     per_step = plan.m * args.layers * (launches_per_mbl * world if colo else 0)
     if not colo:
-        per_step = plan.m * args.layers * (n_a * (attn_launches + router_launches + 2) + n_e * 3)
+        per_step = plan.m * args.layers * (n_a * (attn_launches + router_launches + 1) + n_e * expert_launches)
     line["gpu_launches"] = per_step * args.steps
-    if not args.no_cpu and world == 1:  # the CPU baseline is timed at N = 1 only
+    if full and not args.no_cpu and world == 1:  # the CPU baseline is timed at N = 1 only
         threads = len(os.sched_getaffinity(0))
         cs = cpu_layer(model, plan.m * args.b_a, attn=args.attn == "real", steps=1, warmup=1)
         line["cpu_baseline"] = {"value": cs["tokens_per_s"], "unit": "layer-tokens/s", "cores": threads,
                                 "kind": "port", "sample": cs["sample"], "cpu": cpu_model_name(),
                                 "t_layer_s": cs["t_layer_s"], "t_attention_s": cs["t_attention_s"],
                                 "t_moe_s": cs["t_moe_s"]}
-    print(json.dumps(line), flush=True)
     g.close()
+    return line
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_2504_02263_b200 import runtime
+
+    rank, world, local = runtime.init_distributed_from_env("gloo" if _over() else "nccl")
+    if world != args.gpus:
+        if rank == 0:
+            print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}))
+        sys.exit(2)
+    import copy
+    args0 = copy.copy(args)  # measure() folds merged micro-batches into args.b_a
+    layout = resolve_layout(args, world)
+    line = measure(args, rank, world, local, layout, full=True)
+    if world > 1 and layout[2] and args.pingpong:
+        # The paper's disaggregated ping-pong layout, measured beside the
+        # co-located headline with the same tokens per attention GPU per
+        # micro-batch: n_e from the headline's own per-token stage costs
+        # (T_e / (T_a + T_e) of the GPUs), experts spread over n_e GPUs.
+        import gc
+        gc.collect()
+        torch.cuda.empty_cache()
+        share = [None]
+        if rank == 0:
+            st = line["stage_times"]
+            share[0] = st["T_e_ms"] / (st["T_a_ms"] + st["T_e_ms"])
+        dist.broadcast_object_list(share, src=0)
+        alt, slots = disaggregated_layout(args0, world, share[0])
+        sub = measure(args0, rank, world, local, alt, full=False, slots_override=slots)
+        if rank == 0:
+            line["pingpong"] = pingpong_summary(sub, share[0])
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 

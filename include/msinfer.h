@@ -252,6 +252,43 @@ int msi_rope_append(const void* qkv, int64_t qkv_ld, const int32_t* pos, int T,
                     const int32_t* block_table, int max_pages,
                     void* k_cache, void* v_cache, int64_t num_pages,
                     void* q_out, void* stream);
+/* The expert FFN on (expert, sender) receive regions without a context (the
+ * layout msi_expert_ffn reads; tests and A/B runs): region (e, s) of cap_s
+ * rows at row (e*n_src + s)*cap_s of x_reg, cntab [n_src][E_l] uint64 with
+ * the region's row count in the low 32 bits.  a_runs = 1: GEMM1 loads each
+ * 128-row tile as runs of the regions (one power-of-two TMA box per piece).
+ * xcomp != NULL (>= hbuf_rows x hidden): the regions are first gathered into
+ * compact 128-aligned per-expert segments of xcomp and GEMM1 reads those
+ * (msi_expert_ffn's path when several senders share an expert).  Y of every
+ * row is stored at its own row of y_reg (may alias x_reg).  hbuf >=
+ * hbuf_rows x inter, hbuf_rows >= sum over experts of the 128-rounded totals. */
+int msi_grouped_ffn_regions(const void* x_reg, const uint64_t* cntab, int n_src,
+                            int64_t cap_s, int E_l, const void* w13, const void* w2,
+                            void* hbuf, int64_t hbuf_rows, void* y_reg, int hidden,
+                            int inter, int a_runs, void* xcomp, void* stream);
+/* The attention stage's two projections (Table 3, "QKV
+ * Project" and "Attn Output") on the expert GEMM's tcgen05 kernel, run as
+ * one dense "expert" of T rows (CTA-pair 256x256 tiles, TMA, TMEM).
+ * tile_ctr: a caller-owned zeroed uint32 in device memory (the launch's
+ * dynamic tile counter; each call leaves it at 0; one in-flight call per
+ * counter).
+ *
+ * out[t][0:N] = bf16(a[t] . b[0:N]^T (+ resid[t][0:N])) -- a bf16 [T][K],
+ * b bf16 [N][K] (K-major), N % 256 == 0, K % 64 == 0, fp32 accumulation and
+ * one rounding (the residual is added in fp32). */
+int msi_dense_gemm(const void* a, int64_t T, const void* b, int N, int K,
+                   void* out, int64_t out_ld, const void* resid, int64_t resid_ld,
+                   uint32_t* tile_ctr, void* stream);
+/* QKV projection with RoPE and the paged-KV append in the GEMM epilogue:
+ * qkv = bf16(x . wqkv^T) (wqkv bf16 [(n_heads + 2 n_kv) 128][hidden]), then
+ * exactly what msi_rope_append does with that qkv -- q heads rotated into
+ * q_out [T][n_heads][128], k heads rotated and v heads copied into the cache
+ * slot (page block_table[t][pos[t]/64], row pos[t]%64).  No qkv buffer. */
+int msi_qkv_rope_append(const void* x, int64_t T, int hidden, const void* wqkv,
+                        int n_heads, int n_kv, const int32_t* pos, float theta,
+                        const int32_t* block_table, int max_pages,
+                        void* k_cache, void* v_cache, void* q_out,
+                        uint32_t* tile_ctr, void* stream);
 /* Workspace bytes msi_decode_attention needs for T sequences (split-KV
  * partials; 0 when no split is used). */
 size_t msi_decode_attention_workspace(int T, int n_heads, int n_kv, int max_pages);

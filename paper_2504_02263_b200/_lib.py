@@ -78,6 +78,11 @@ SIGNATURES = {
     "msi_combine_local": (_I, [_P, _P, _P, _P, _I, _I, _I, _P]),
     "msi_rope_append": (_I, [_P, ctypes.c_int64, _P, _I, _I, _I, ctypes.c_float, _P, _I, _P, _P,
                              ctypes.c_int64, _P, _P]),
+    "msi_grouped_ffn_regions": (_I, [_P, _P, _I, ctypes.c_int64, _I, _P, _P, _P, ctypes.c_int64, _P, _I, _I, _I,
+                                     _P, _P]),
+    "msi_dense_gemm": (_I, [_P, ctypes.c_int64, _P, _I, _I, _P, ctypes.c_int64, _P, ctypes.c_int64, _P, _P]),
+    "msi_qkv_rope_append": (_I, [_P, ctypes.c_int64, _I, _P, _I, _I, _P, ctypes.c_float, _P, _I, _P, _P, _P,
+                                 _P, _P]),
     "msi_decode_attention_workspace": (_SZ, [_I, _I, _I, _I]),
     "msi_decode_attention": (_I, [_P, _P, _P, ctypes.c_int64, _P, _I, _P, _I, _I, _I, ctypes.c_float, _P, _P,
                                   _SZ, _P]),

@@ -5,12 +5,14 @@ with k1 proportional to the KV bytes read, 2 b s h bytes / g
 (Table 3 GEMMs: QKV projection
 h -> h(1 + 2/g), output projection h -> h).  Here it is a real decode layer:
 
-    qkv = x W_qkv^T                       (cuBLAS: plain library GEMM)
-    q, k = RoPE(q, k at pos); append k, v into the paged KV cache
-                                          (msi_rope_append)
+    q, k = RoPE(x W_qkv^T at pos); append k, v into the paged KV cache
+                                          (msi_qkv_rope_append: the tcgen05
+                                           GEMM with RoPE + append in its
+                                           epilogue, no qkv buffer)
     o = softmax(q K^T / sqrt(128)) V      (msi_decode_attention: paged,
                                            GQA, TMA-streamed, HBM-bound)
-    y = x + o W_o^T                       (cuBLAS, residual in the epilogue)
+    y = x + o W_o^T                       (msi_dense_gemm, residual added in
+                                           fp32 in the epilogue)
 
 ``y`` is the MoE layer's input (router + M2N dispatch) and its residual.
 
@@ -146,7 +148,8 @@ class AttentionStage:
             ctx_lens = batch_composition(T, avg_seq_len, seed, composition)
         self.cache = PagedKVCache(T, self.n_kv, ctx_lens, layers, device, seed, headroom=headroom)
         D = _lib.HEAD_DIM
-        self.qkv = torch.empty((T, (self.n_heads + 2 * self.n_kv) * D), dtype=torch.bfloat16, device=device)
+        self.qkv_width = (self.n_heads + 2 * self.n_kv) * D
+        self.ctr = ops.TileCounter(2, device)  # tile counters of the two projection GEMMs
         self.q = torch.empty((T, self.n_heads, D), dtype=torch.bfloat16, device=device)
         self.o = torch.empty((T, self.n_heads * D), dtype=torch.bfloat16, device=device)
         self.y = torch.empty((T, model.hidden), dtype=torch.bfloat16, device=device)
@@ -157,9 +160,8 @@ class AttentionStage:
         """x bf16 [T, h] -> x + Attn(x) W_o^T (bf16 [T, h]) on the current stream."""
         c = self.cache
         out = self.y if out is None else out
-        torch.matmul(x, self.w.wqkv.t(), out=self.qkv)
-        ops.rope_append(self.qkv, c.pos, self.n_heads, self.n_kv, self.theta, c.block_table, c.k[layer],
-                        c.v[layer], self.q)
+        ops.qkv_rope_append(x, self.w.wqkv, c.pos, self.n_heads, self.n_kv, self.theta, c.block_table,
+                            c.k[layer], c.v[layer], self.q, self.ctr, 0)
         if self.timing is not None:  # (start, end) events around the attention kernel
             e0, e1 = torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True)
             e0.record()
@@ -167,13 +169,13 @@ class AttentionStage:
         if self.timing is not None:
             e1.record()
             self.timing.append((e0, e1))
-        torch.addmm(x, self.o, self.w.wo.t(), out=out)
+        ops.dense_gemm(self.o, self.w.wo, out, resid=x, ctr=self.ctr, slot=1)
         return out
 
     def flops(self) -> float:
         """Projection GEMM FLOPs per layer (Table 3: QKV + output)."""
         h = self.model.hidden
-        return 2.0 * self.T * h * (self.qkv.shape[1] + self.o.shape[1])
+        return 2.0 * self.T * h * (self.qkv_width + self.o.shape[1])
 
     def attn_bytes(self) -> int:
         """Algorithmic bytes of msi_decode_attention per layer: K/V read + q read + o write."""

@@ -269,8 +269,10 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
   // of system-scope loads), summed in shared memory
   for (int e = threadIdx.x; e < p.E_l; e += blockDim.x) seg.total[e] = 0;
   __syncthreads();
-  for (int i = threadIdx.x; i < (p.totals ? p.E_l : p.n_a * p.E_l); i += blockDim.x) {
-    if (p.totals) {
+  for (int i = threadIdx.x; i < (p.dense_rows ? 1 : p.totals ? p.E_l : p.n_a * p.E_l); i += blockDim.x) {
+    if (p.dense_rows) {
+      seg.total[0] = (int)p.dense_rows;
+    } else if (p.totals) {
       seg.total[i] = p.totals[i];
     } else {
       const int s = i / p.E_l, e = i - s * p.E_l;
@@ -491,9 +493,14 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
       const int colofs = (p.mode == 0) ? nh * 64 : nh * 128;
 
       char* rowdst = nullptr;
+      int pos_t = 0, page_t = 0;  // mode 2: the row's token position and its KV page
       if (row_local < seg.total[e]) {
         if (p.mode == 0) {
           rowdst = reinterpret_cast<char*>(p.out) + ((size_t)row_global * p.out_ld + (size_t)n * (BN / 2) + colofs) * 2;
+        } else if (p.mode == 2) {  // per-head destinations below
+          pos_t = p.pos[row_global];
+          page_t = p.block_table[(size_t)row_global * p.max_pages + pos_t / MSI_KV_PAGE];
+          rowdst = reinterpret_cast<char*>(p.q_out);
         } else if (p.n_src) {  // receive regions: Y of virtual row row_local replaces its X in place
           if (e != pre_e) {
             load_pre(p, e, pre);
@@ -509,11 +516,42 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
           rowdst = reinterpret_cast<char*>(p.out) + ((size_t)row_global * p.out_ld + (size_t)n * BN + colofs) * 2;
         }
       }
-      // 256-byte row segments (mode 1 full: 2, mode 1 half / mode 0 full: 1)
+      // 256-byte row segments (mode 1/2 full: 2, mode 1/2 half / mode 0 full: 1)
       // or one 128-byte segment (mode 0 half)
-      const int segs = (p.mode == 1 && !hp) ? 2 : 1;
+      const int segs = (p.mode != 0 && !hp) ? 2 : 1;
       const bool narrow = (p.mode == 0 && hp);
+      auto stage = [&](int cc, const uint32_t (&pk)[16]) {  // 32 bf16 of the lane's row -> swizzled staging
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int u = cc * 4 + j;
+          uint4 val = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          const int sw = narrow ? (u ^ (lane & 7)) : (u ^ (lane & 15));
+          *reinterpret_cast<uint4*>(stg + lane * 256 + sw * 16) = val;
+        }
+      };
       for (int sgi = 0; sgi < segs; ++sgi) {
+        // mode 2: the segment's 128 columns are one head of q | k | v
+        const int head = p.mode == 2 ? n * 2 + (hp ? nh : sgi) : 0;
+        const bool rope = p.mode == 2 && head < p.n_heads + p.n_kv;
+        char* segdst = nullptr;
+        if (rowdst) {
+          if (p.mode == 2) {
+            __nv_bfloat16* d;
+            if (head < p.n_heads) {
+              d = p.q_out + ((size_t)row_global * p.n_heads + head) * 128;
+            } else {
+              const bool isk = head < p.n_heads + p.n_kv;
+              const int kvh = head - p.n_heads - (isk ? 0 : p.n_kv);
+              d = (isk ? p.k_cache : p.v_cache) +
+                  (((size_t)page_t * p.n_kv + kvh) * MSI_KV_PAGE + pos_t % MSI_KV_PAGE) * 128;
+            }
+            segdst = reinterpret_cast<char*>(d);
+          } else {
+            segdst = rowdst + sgi * 256;
+          }
+        }
+        const __nv_bfloat16* rsrc = (p.mode == 1 && p.resid && rowdst)
+            ? p.resid + (size_t)row_global * p.resid_ld + (size_t)n * BN + colofs + sgi * 128 : nullptr;
         if (valid_rows > 0) {
           const int nchunk = narrow ? 2 : 4;
 #pragma unroll 1
@@ -535,21 +573,59 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
                 float h1 = g1 / (1.0f + __expf(-g1)) * u1;
                 packed[j] = pack_bf16x2(h0, h1);
               }
+            } else if (rope) {
+              // rotate-half RoPE pairs dims (i, i + 64): chunks c and c + 2
+              // together; same arithmetic as rope_append_kernel on the
+              // bf16-rounded projection (attention.cu)
+              if (c >= 2) continue;
+              uint32_t lo[32], hi[32], rh[16];
+              tmem_ld32(tbase + sgi * 128 + c * 32, lo);
+              tmem_ld32(tbase + sgi * 128 + 64 + c * 32, hi);
+              tmem_wait_ld();
+              const float fp = (float)pos_t;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                float r0[2], r1[2];
+#pragma unroll
+                for (int b = 0; b < 2; ++b) {
+                  const int i = c * 32 + 2 * j + b;
+                  const float inv = 1.0f / powf(p.theta, (float)(2 * i) / 128.0f);
+                  float sn, cs;
+                  sincosf(fp * inv, &sn, &cs);
+                  const float x0 = __bfloat162float(__float2bfloat16_rn(__uint_as_float(lo[2 * j + b])));
+                  const float x1 = __bfloat162float(__float2bfloat16_rn(__uint_as_float(hi[2 * j + b])));
+                  r0[b] = x0 * cs - x1 * sn;
+                  r1[b] = x1 * cs + x0 * sn;
+                }
+                packed[j] = pack_bf16x2(r0[0], r0[1]);
+                rh[j] = pack_bf16x2(r1[0], r1[1]);
+              }
+              stage(c + 2, rh);
             } else {
               uint32_t v[32];
               tmem_ld32(tbase + sgi * 128 + c * 32, v);
-              tmem_wait_ld();
+              if (p.resid) {  // residual (O projection): out = bf16(acc + x), one rounding
+                // (warp-uniform branch: tcgen05.wait::ld is .sync.aligned;
+                // lanes past the last row load nothing)
+                uint32_t r[16];
 #pragma unroll
-              for (int j = 0; j < 16; ++j)
-                packed[j] = pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
-            }
+                for (int j = 0; j < 4; ++j) {
+                  const uint4 q4 = rsrc ? ld_nc_v4(rsrc + c * 32 + 8 * j) : make_uint4(0u, 0u, 0u, 0u);
+                  r[4 * j] = q4.x; r[4 * j + 1] = q4.y; r[4 * j + 2] = q4.z; r[4 * j + 3] = q4.w;
+                }
+                tmem_wait_ld();
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int u = c * 4 + j;
-              uint4 val = make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
-              const int sw = narrow ? (u ^ (lane & 7)) : (u ^ (lane & 15));
-              *reinterpret_cast<uint4*>(stg + lane * 256 + sw * 16) = val;
+                for (int j = 0; j < 16; ++j)
+                  packed[j] = pack_bf16x2(__uint_as_float(v[2 * j]) + bf16lo(r[j]),
+                                          __uint_as_float(v[2 * j + 1]) + bf16hi(r[j]));
+              } else {
+                tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                  packed[j] = pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+              }
             }
+            stage(c, packed);
           }
         }
         if (sgi == segs - 1) {
@@ -568,10 +644,10 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
           const int u = lane & 15;
           for (int r0 = 0; r0 < valid_rows; r0 += 2) {
             const int r = r0 + (lane >> 4);
-            char* dst = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(rowdst), r & 31));
+            char* dst = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(segdst), r & 31));
             if (r < valid_rows) {
               uint4 val = *reinterpret_cast<const uint4*>(stg + r * 256 + ((u ^ (r & 15)) * 16));
-              st_v4(dst + sgi * 256 + u * 16, val);
+              st_v4(dst + u * 16, val);
             }
           }
         } else {
@@ -579,7 +655,7 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
           const int u = lane & 7;
           for (int r0 = 0; r0 < valid_rows; r0 += 4) {
             const int r = r0 + (lane >> 3);
-            char* dst = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(rowdst), r & 31));
+            char* dst = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(segdst), r & 31));
             if (r < valid_rows) {
               uint4 val = *reinterpret_cast<const uint4*>(stg + r * 256 + ((u ^ (r & 7)) * 16));
               st_v4(dst + u * 16, val);
@@ -609,6 +685,87 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
       fence_sys();
       for (int i = 0; i < p.n_sig; ++i) red_release_sys_add(p.sig[i], 1u);
     }
+  }
+}
+
+// ------------------------------------------------ region gather ----------
+// Several senders' receive regions per expert -> one compact 128-row aligned
+// segment per expert, so GEMM1 loads every A tile with one 128-row box.
+// (Loading a tile that straddles two regions as runs of power-of-two boxes
+// costs ~8 TMA issues per k-block; measured 1.25-2x slower GEMM1 at 2-8
+// senders, scripts/ab_ffn_regions_1gpu.py.)  HBM-bound copy of the rows
+// (2 * rows * H * 2 bytes), one warp per row; optionally waits for the
+// senders' arrivals first (the expert_wait of msi_expert_ffn).
+constexpr int kGatherThreads = 512;
+
+__global__ void __launch_bounds__(kGatherThreads)
+gather_regions_kernel(const __nv_bfloat16* __restrict__ recv, const uint64_t* cntab, int E, int e0, int n_src,
+                      int E_l, long long cap_s, int H, __nv_bfloat16* __restrict__ xc, const uint32_t* wait_ctr,
+                      uint32_t epoch, const uint32_t* epoch_src, uint32_t wait_mul, uint64_t timeout_ns,
+                      int32_t* status) {
+  extern __shared__ int g_sm[];
+  int* vpre = g_sm;                    // [E_l + 1] exclusive prefix of expert totals (virtual rows)
+  int* cstart = vpre + E_l + 1;        // [E_l] compact 128-aligned segment start
+  int* spre = cstart + E_l;            // [E_l][n_src + 1] sender prefix within the expert
+  __shared__ int s_abort;
+  pdl_trigger();
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    bool ok = true;
+    if (wait_ctr) {
+      if (epoch_src) epoch = resolve_epoch(epoch, epoch_src, 1u, status);
+      ok = epoch != 0 && wait_geq(wait_ctr, epoch * wait_mul, timeout_ns, status);
+      if (!ok) status[1] = 1;
+    }
+    s_abort = ok ? 0 : 1;
+  }
+  __syncthreads();
+  if (s_abort) return;
+  for (int e = threadIdx.x; e < E_l; e += blockDim.x) {
+    int* sp = spre + e * (n_src + 1);
+    int run = 0;
+    sp[0] = 0;
+    for (int s = 0; s < n_src; ++s) {
+      run += (int)(uint32_t)ld_relaxed_sys64(cntab + (size_t)s * E + e0 + e);
+      sp[s + 1] = run;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // E_l <= 256: serial scan
+    int v = 0, c = 0;
+    for (int e = 0; e < E_l; ++e) {
+      const int t = spre[e * (n_src + 1) + n_src];
+      vpre[e] = v;
+      cstart[e] = c;
+      v += t;
+      c += (t + 127) / 128 * 128;
+    }
+    vpre[E_l] = v;
+  }
+  __syncthreads();
+  const int total = vpre[E_l];
+  const int lane = threadIdx.x & 31;
+  const int nvec = H / 8;  // 16-byte vectors per row
+  for (int v = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); v < total;
+       v += gridDim.x * (blockDim.x >> 5)) {
+    int lo = 0, hi = E_l - 1;  // last expert with vpre[e] <= v
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (vpre[mid] <= v) lo = mid;
+      else hi = mid - 1;
+    }
+    const int e = lo, ve = v - vpre[e];
+    const int* sp = spre + e * (n_src + 1);
+    int s = 0;
+    while (s + 1 < n_src && sp[s + 1] <= ve) ++s;
+    const uint4* src = reinterpret_cast<const uint4*>(recv + ((size_t)(e * n_src + s) * cap_s + (ve - sp[s])) * H);
+    uint4* dst = reinterpret_cast<uint4*>(xc + ((size_t)cstart[e] + ve) * H);
+    int i = lane;
+    for (; i + 96 < nvec; i += 128) {  // 4 loads in flight per lane
+      const uint4 a = src[i], b = src[i + 32], c = src[i + 64], d = src[i + 96];
+      dst[i] = a; dst[i + 32] = b; dst[i + 64] = c; dst[i + 96] = d;
+    }
+    for (; i < nvec; i += 32) dst[i] = src[i];
   }
 }
 
@@ -684,6 +841,19 @@ int num_sms() {
   if (dev < 0 || dev >= 64) dev = 0;
   if (!n[dev]) cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev);
   return n[dev];
+}
+
+int gather_regions(const void* recv, const uint64_t* cntab, int E, int e0, int n_src, int E_l, long long cap_s,
+                   int H, void* xc, const uint32_t* wait_ctr, uint32_t epoch, const uint32_t* epoch_src,
+                   uint32_t wait_mul, uint64_t timeout_ns, int32_t* status, cudaStream_t st) {
+  MSI_REQUIRE(E_l >= 1 && E_l <= MSI_MAX_LOCAL_EXPERTS && n_src >= 1 && n_src <= MSI_MAX_RANKS && H % 8 == 0,
+              "gather_regions: bad shape");
+  const size_t smem = (size_t)(E_l + 1 + E_l + E_l * (n_src + 1)) * sizeof(int);
+  if (int arc = smem_attr(reinterpret_cast<const void*>(gather_regions_kernel), smem)) return arc;
+  MSI_CUDA(launch_k(gather_regions_kernel, dim3(2 * num_sms()), dim3(kGatherThreads), smem, st,
+                    reinterpret_cast<const __nv_bfloat16*>(recv), cntab, E, e0, n_src, E_l, cap_s, H,
+                    reinterpret_cast<__nv_bfloat16*>(xc), wait_ctr, epoch, epoch_src, wait_mul, timeout_ns, status));
+  return check_launch("gather_regions_kernel");
 }
 
 template <int CG, int MAXE>
@@ -822,7 +992,153 @@ int grouped_ffn_local(const void* x, const int32_t* total, int E_l, int rows, co
   return grouped_gemm_launch(g2, st);
 }
 
+// The expert FFN on receive regions without a context (tests and A/B runs):
+// x_reg holds n_src regions of cap_s rows per local expert (region (e, s) at
+// row (e * n_src + s) * cap_s), cntab [n_src][E_l] uint64 whose low 32 bits
+// are the rows of region (e, s).  GEMM1 reads A as region runs (a_runs = 0:
+// one 128-row box per tile from the expert's first region -- only valid
+// when every expert has one non-empty region), GEMM2 stores Y over X in the
+// regions of y_reg (may alias x_reg).  hbuf >= rows x H' (compact per expert).
+int grouped_ffn_regions(const void* x_reg, const uint64_t* cntab, int n_src, int64_t cap_s, int E_l,
+                        const void* w13, const void* w2, void* hbuf, int64_t hbuf_rows, void* y_reg, int hidden,
+                        int inter, int a_runs, void* xcomp, cudaStream_t st) {
+  MSI_REQUIRE(hidden % 256 == 0 && inter % 128 == 0, "grouped_ffn_regions: hidden %% 256 and inter %% 128 required");
+  MSI_REQUIRE(n_src >= 1 && n_src <= MSI_MAX_RANKS && cap_s >= 1, "grouped_ffn_regions: bad n_src / cap_s");
+  int crc = 0;
+  uint32_t* ctrs = local_tile_counters(&crc);
+  if (!ctrs) return crc;
+  const int64_t rows = (int64_t)E_l * n_src * cap_s;
+  GemmLaunch g1{};
+  g1.a = x_reg;
+  g1.a_rows = rows;
+  if (xcomp) {  // gather the regions into compact segments first (msi_expert_ffn's path for n_a > 1)
+    int grc = gather_regions(x_reg, cntab, E_l, 0, n_src, E_l, cap_s, hidden, xcomp, nullptr, 0, nullptr, 0, 0,
+                             nullptr, st);
+    if (grc) return grc;
+    g1.a = xcomp;
+    g1.a_rows = hbuf_rows;
+    a_runs = 0;
+  }
+  g1.b = w13;
+  g1.p.E_l = E_l;
+  g1.p.n_total = 2 * inter;
+  g1.p.nt = 2 * inter / BN;
+  g1.p.kdim = hidden;
+  g1.p.cntab = cntab;
+  g1.p.n_a = n_src;
+  g1.p.E = E_l;
+  g1.p.n_src = a_runs ? n_src : 0;
+  g1.p.cap_s = cap_s;
+  g1.p.a_runs = a_runs;
+  g1.p.mode = 0;
+  g1.p.out = reinterpret_cast<__nv_bfloat16*>(hbuf);
+  g1.p.out_ld = inter;
+  g1.p.tile_ctr = ctrs;
+  int rc = grouped_gemm_launch(g1, st);
+  if (rc) return rc;
+  GemmLaunch g2{};
+  g2.a = hbuf;
+  g2.a_rows = hbuf_rows;
+  g2.b = w2;
+  g2.p.E_l = E_l;
+  g2.p.n_total = hidden;
+  g2.p.nt = hidden / BN;
+  g2.p.kdim = inter;
+  g2.p.cntab = cntab;
+  g2.p.n_a = n_src;
+  g2.p.E = E_l;
+  g2.p.n_src = n_src;
+  g2.p.cap_s = cap_s;
+  g2.p.mode = 1;
+  g2.p.out = reinterpret_cast<__nv_bfloat16*>(y_reg);
+  g2.p.out_ld = hidden;
+  g2.p.tile_ctr = ctrs + 32;
+  return grouped_gemm_launch(g2, st);
+}
+
+// Dense GEMM of the attention stage on the same kernel: one "expert" of
+// `rows` compact rows (E_l = 1, no count table).  tile_ctr: the caller's
+// zeroed counter word (each launch leaves it at 0).
+static GemmLaunch dense_launch(const void* a, int64_t rows, const void* b, int n, int k, uint32_t* tile_ctr) {
+  GemmLaunch g{};
+  g.a = a;
+  g.a_rows = rows;
+  g.b = b;
+  g.p.E_l = 1;
+  g.p.n_total = n;
+  g.p.nt = n / BN;
+  g.p.kdim = k;
+  g.p.dense_rows = rows;
+  g.p.mode = 1;
+  g.p.tile_ctr = tile_ctr;
+  return g;
+}
+
+int dense_gemm(const void* a, int64_t rows, const void* b, int n, int k, void* out, int64_t out_ld,
+               const void* resid, int64_t resid_ld, uint32_t* tile_ctr, cudaStream_t st) {
+  MSI_REQUIRE(rows >= 0 && rows < (1ll << 31), "dense_gemm: rows out of range");
+  if (rows == 0) return 0;
+  MSI_REQUIRE(a && b && out && tile_ctr, "dense_gemm: null pointer");
+  MSI_REQUIRE(n > 0 && n % BN == 0 && k > 0 && k % BK == 0, "dense_gemm: N %% 256 and K %% 64 required");
+  MSI_REQUIRE(out_ld >= n && out_ld % 8 == 0, "dense_gemm: out_ld must be >= N and a multiple of 8");
+  MSI_REQUIRE(!resid || (resid_ld >= n && resid_ld % 8 == 0), "dense_gemm: resid_ld must be >= N and a multiple of 8");
+  if (rows == 0) return 0;
+  GemmLaunch g = dense_launch(a, rows, b, n, k, tile_ctr);
+  g.p.out = reinterpret_cast<__nv_bfloat16*>(out);
+  g.p.out_ld = (int)out_ld;
+  g.p.resid = reinterpret_cast<const __nv_bfloat16*>(resid);
+  g.p.resid_ld = resid_ld;
+  return grouped_gemm_launch(g, st);
+}
+
+int qkv_rope_append(const void* x, int64_t rows, int hidden, const void* wqkv, int n_heads, int n_kv,
+                    const int32_t* pos, float theta, const int32_t* block_table, int max_pages, void* k_cache,
+                    void* v_cache, void* q_out, uint32_t* tile_ctr, cudaStream_t st) {
+  MSI_REQUIRE(rows >= 0 && rows < (1ll << 31), "qkv_rope_append: rows out of range");
+  if (rows == 0) return 0;
+  MSI_REQUIRE(x && wqkv && pos && block_table && k_cache && v_cache && q_out && tile_ctr,
+              "qkv_rope_append: null pointer");
+  MSI_REQUIRE(n_kv > 0 && n_heads > 0 && n_heads % n_kv == 0, "qkv_rope_append: bad head counts");
+  const int n = (n_heads + 2 * n_kv) * MSI_HEAD_DIM;
+  MSI_REQUIRE(n % BN == 0, "qkv_rope_append: n_heads + 2 n_kv must be even (256-column N tiles)");
+  MSI_REQUIRE(hidden > 0 && hidden % BK == 0, "qkv_rope_append: hidden %% 64 required");
+  MSI_REQUIRE(theta > 0.f && max_pages > 0, "qkv_rope_append: bad theta / max_pages");
+  if (rows == 0) return 0;
+  GemmLaunch g = dense_launch(x, rows, wqkv, n, hidden, tile_ctr);
+  g.p.mode = 2;
+  g.p.pos = pos;
+  g.p.theta = theta;
+  g.p.block_table = block_table;
+  g.p.max_pages = max_pages;
+  g.p.n_heads = n_heads;
+  g.p.n_kv = n_kv;
+  g.p.q_out = reinterpret_cast<__nv_bfloat16*>(q_out);
+  g.p.k_cache = reinterpret_cast<__nv_bfloat16*>(k_cache);
+  g.p.v_cache = reinterpret_cast<__nv_bfloat16*>(v_cache);
+  return grouped_gemm_launch(g, st);
+}
+
 }  // namespace msi
+
+extern "C" int msi_grouped_ffn_regions(const void* x_reg, const uint64_t* cntab, int n_src, int64_t cap_s, int E_l,
+                                       const void* w13, const void* w2, void* hbuf, int64_t hbuf_rows, void* y_reg,
+                                       int hidden, int inter, int a_runs, void* xcomp, void* stream) {
+  return msi::grouped_ffn_regions(x_reg, cntab, n_src, cap_s, E_l, w13, w2, hbuf, hbuf_rows, y_reg, hidden, inter,
+                                  a_runs, xcomp, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int msi_dense_gemm(const void* a, int64_t rows, const void* b, int n, int k, void* out, int64_t out_ld,
+                              const void* resid, int64_t resid_ld, uint32_t* tile_ctr, void* stream) {
+  return msi::dense_gemm(a, rows, b, n, k, out, out_ld, resid, resid_ld, tile_ctr,
+                         reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int msi_qkv_rope_append(const void* x, int64_t T, int hidden, const void* wqkv, int n_heads, int n_kv,
+                                   const int32_t* pos, float theta, const int32_t* block_table, int max_pages,
+                                   void* k_cache, void* v_cache, void* q_out, uint32_t* tile_ctr, void* stream) {
+  return msi::qkv_rope_append(x, T, hidden, wqkv, n_heads, n_kv, pos, theta, block_table, max_pages, k_cache,
+                              v_cache, q_out, tile_ctr, reinterpret_cast<cudaStream_t>(stream));
+}
 
 extern "C" int msi_pack_w13(const void* w_gate, const void* w_up, void* w13, int E_l, int inter,
                             int hidden, void* stream) {

@@ -33,7 +33,7 @@ struct GemmParams {
   unsigned long long* trace;  // optional %globaltimer stamps: [slot] start,
   int trace_slot;             //   [slot+1] rows arrived, [slot+2] release
   // epilogue
-  int mode;                 // 0: SwiGLU -> out[row][out_ld]; 1: plain bf16 rows
+  int mode;                 // 0: SwiGLU -> out[row][out_ld]; 1: plain bf16 rows; 2: QKV + RoPE/append
   __nv_bfloat16* out;       // mode 0: hbuf; mode 1: y (n_src > 0: the receive
                             //   regions themselves -- Y of a row replaces its X,
                             //   which the attention GPU's combine pulls)
@@ -54,6 +54,20 @@ struct GemmParams {
   uint32_t* ticket;
   uint32_t* sig[MSI_MAX_RANKS];
   int n_sig;
+  // dense GEMMs of the attention stage (E_l = 1, rows = dense_rows, no
+  // segment table): mode 1 adds resid[row][resid_ld] before the bf16
+  // rounding (O projection + residual); mode 2 is the QKV projection with
+  // RoPE on q/k heads and the paged-KV append in the epilogue (msi_qkv_rope_append)
+  long long dense_rows;
+  const __nv_bfloat16* resid;
+  long long resid_ld;
+  const int32_t* pos;          // mode 2: position of row t's new token
+  const int32_t* block_table;  // mode 2: [rows][max_pages]
+  int max_pages, n_heads, n_kv;
+  float theta;
+  __nv_bfloat16* q_out;        // [rows][n_heads][128]
+  __nv_bfloat16* k_cache;      // [pages][n_kv][64][128]
+  __nv_bfloat16* v_cache;
 };
 
 struct GemmLaunch {
@@ -67,5 +81,11 @@ struct GemmLaunch {
 
 int grouped_gemm_launch(const GemmLaunch& L, cudaStream_t st);
 int num_sms();
+// Rows of the (expert, sender) receive regions -> compact 128-aligned
+// per-expert segments of xc (GEMM1's A when several senders share an
+// expert); wait_ctr != null: first wait for *wait_ctr >= epoch * wait_mul.
+int gather_regions(const void* recv, const uint64_t* cntab, int E, int e0, int n_src, int E_l, long long cap_s,
+                   int H, void* xc, const uint32_t* wait_ctr, uint32_t epoch, const uint32_t* epoch_src,
+                   uint32_t wait_mul, uint64_t timeout_ns, int32_t* status, cudaStream_t st);
 
 }  // namespace msi

@@ -87,6 +87,13 @@ int smem_attr(const void* fn, size_t bytes) {
   return 0;
 }
 
+// MSI_REGION_RUNS=1: GEMM1 loads several senders' regions as box runs
+// instead of gathering them first (A/B runs; measured slower).
+bool region_runs_forced() {
+  const char* e = getenv("MSI_REGION_RUNS");
+  return e && e[0] == '1';
+}
+
 bool pdl_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -172,6 +179,7 @@ struct msi_ctx {
   int my_a, my_e;
   char* heap = nullptr;
   char* hbuf = nullptr;       // expert role: SwiGLU activations [cap][H']
+  char* xcomp = nullptr;      // expert role with n_a > 1: gathered rows [cap][H] (GEMM1's A)
   void* workspace = nullptr;  // router workspace for the runtime (zeroed)
   size_t ws_bytes = 0;
   size_t heap_bytes = 0;
@@ -492,6 +500,7 @@ extern "C" int msi_ctx_create(const msi_plan* plan, int rank, msi_ctx** out) {
     set_error("msi_ctx_create: %s: %s", what, cudaGetErrorString(e));
     if (c->heap) cudaFree(c->heap);
     if (c->hbuf) cudaFree(c->hbuf);
+    if (c->xcomp) cudaFree(c->xcomp);
     if (c->workspace) cudaFree(c->workspace);
     delete c;
     return (int)e;
@@ -502,6 +511,10 @@ extern "C" int msi_ctx_create(const msi_plan* plan, int rank, msi_ctx** out) {
   if (c->expert) {
     e = cudaMalloc(&c->hbuf, (size_t)c->my_layout.cap * plan->inter * 2);
     if (e != cudaSuccess) return fail("hbuf cudaMalloc", e);
+    if (plan->n_a > 1) {
+      e = cudaMalloc(&c->xcomp, (size_t)c->my_layout.cap * plan->hidden * 2);
+      if (e != cudaSuccess) return fail("xcomp cudaMalloc", e);
+    }
   }
   c->ws_bytes = msi_gate_topk_workspace(plan->max_tokens, plan->experts);
   if ((e = cudaMalloc(&c->workspace, c->ws_bytes)) != cudaSuccess) return fail("workspace cudaMalloc", e);
@@ -519,6 +532,7 @@ extern "C" int msi_ctx_destroy(msi_ctx* c) {
     if (r != c->rank && c->opened[r] && c->peer[r]) cudaIpcCloseMemHandle(c->peer[r]);
   if (c->heap) cudaFree(c->heap);
   if (c->hbuf) cudaFree(c->hbuf);
+  if (c->xcomp) cudaFree(c->xcomp);
   if (c->workspace) cudaFree(c->workspace);
   delete c;
   return 0;
@@ -733,6 +747,18 @@ extern "C" int msi_expert_ffn(msi_ctx* c, const void* w13, const void* w2, int m
   g1.p.n_src = p.n_a;      // A rows: runs of the (expert, sender) receive regions
   g1.p.cap_s = p.max_tokens;
   g1.p.a_runs = 1;
+  if (c->xcomp && !region_runs_forced()) {
+    // several senders: wait for their rows and gather the regions into
+    // compact per-expert segments, so every GEMM1 tile is one 128-row box
+    int grc = gather_regions(g1.a, d.my_cntab + tab, p.experts, d.my_node * d.E_l, p.n_a, d.E_l, p.max_tokens,
+                             p.hidden, c->xcomp, d.my_arrive + mb_slot * CTR_STRIDE, epoch,
+                             d.my_euse + mb_slot * CTR_STRIDE, (uint32_t)p.n_a, c->timeout_ns, d.my_status, st);
+    if (grc) return grc;
+    g1.a = c->xcomp;
+    g1.a_rows = L.cap;
+    g1.p.n_src = 0;
+    g1.p.a_runs = 0;
+  }
   g1.b = w13;
   g1.p.E_l = d.E_l;
   g1.p.n_total = 2 * hp_l;

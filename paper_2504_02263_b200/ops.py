@@ -166,3 +166,85 @@ def decode_attention(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tens
               block_table.shape[1], _ptr(seq_lens), T, n_heads, n_kv, ctypes.c_float(scale), _ptr(out),
               _ptr(workspace), ws_bytes, _stream(stream))
     return out
+
+
+class TileCounter:
+    """Zeroed device words for the dense GEMM launches' dynamic tile
+    scheduler (each launch leaves its word at 0; one in-flight launch per word)."""
+
+    def __init__(self, n: int = 1, device=None):
+        self.buf = torch.zeros(n * 32, dtype=torch.int32, device=device or "cuda")  # 128 B apart
+
+    def __getitem__(self, i: int):
+        return ctypes.c_void_p(self.buf.data_ptr() + 128 * i)
+
+
+def dense_gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None,
+               resid: torch.Tensor | None = None, ctr: TileCounter | None = None, slot: int = 0,
+               stream=None) -> torch.Tensor:
+    """out = bf16(a b^T (+ resid)) on the tcgen05 GEMM (msi_dense_gemm):
+    a bf16 [T, K], b bf16 [N, K]; out/resid bf16 [T, >= N] row-major."""
+    _check_bf16("a", a, 2)
+    _check_bf16("b", b, 2)
+    T, K = a.shape
+    N = b.shape[0]
+    if b.shape[1] != K:
+        raise ValueError("dense_gemm: b must be [N, K]")
+    if out is None:
+        out = torch.empty((T, N), dtype=torch.bfloat16, device=a.device)
+    for name, t in (("out", out), ("resid", resid)):
+        if t is not None and (t.dtype != torch.bfloat16 or not t.is_cuda or t.stride(1) != 1 or t.shape[0] != T):
+            raise ValueError(f"dense_gemm: {name} must be a row-major CUDA bfloat16 [T, >= N] matrix")
+    ctr = ctr or TileCounter(1, a.device)
+    _lib.call("msi_dense_gemm", _ptr(a), T, _ptr(b), N, K, _ptr(out), out.stride(0), _ptr(resid),
+              0 if resid is None else resid.stride(0), ctr[slot], _stream(stream))
+    return out
+
+
+def qkv_rope_append(x: torch.Tensor, wqkv: torch.Tensor, pos: torch.Tensor, n_heads: int, n_kv: int,
+                    theta: float, block_table: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
+                    q_out: torch.Tensor, ctr: TileCounter | None = None, slot: int = 0, stream=None) -> torch.Tensor:
+    """QKV projection with RoPE + paged-KV append in the GEMM epilogue
+    (msi_qkv_rope_append): the result msi_rope_append gives on bf16(x wqkv^T)."""
+    _check_bf16("x", x, 2)
+    _check_bf16("wqkv", wqkv, 2)
+    _check_i32("pos", pos)
+    _check_i32("block_table", block_table)
+    for n, t in (("k_cache", k_cache), ("v_cache", v_cache), ("q_out", q_out)):
+        _check_bf16(n, t)
+    T, H = x.shape
+    if wqkv.shape != ((n_heads + 2 * n_kv) * _lib.HEAD_DIM, H):
+        raise ValueError("qkv_rope_append: wqkv must be [(n_heads + 2 n_kv) 128, hidden]")
+    ctr = ctr or TileCounter(1, x.device)
+    _lib.call("msi_qkv_rope_append", _ptr(x), T, H, _ptr(wqkv), n_heads, n_kv, _ptr(pos), ctypes.c_float(theta),
+              _ptr(block_table), block_table.shape[1], _ptr(k_cache), _ptr(v_cache), _ptr(q_out), ctr[slot],
+              _stream(stream))
+    return q_out
+
+
+def grouped_ffn_regions(x_reg: torch.Tensor, counts, cap_s: int, w13: torch.Tensor, w2: torch.Tensor,
+                        y_reg: torch.Tensor | None = None, hbuf: torch.Tensor | None = None, a_runs: bool = True,
+                        gather: bool = False, stream=None) -> torch.Tensor:
+    """The expert FFN on (expert, sender) receive regions (msi_grouped_ffn_regions):
+    x_reg bf16 [E_l * n_src * cap_s, H], region (e, s) = rows
+    [(e n_src + s) cap_s, + counts[s][e]).  Returns y_reg (Y of each row at
+    its own row; may be x_reg itself).  gather=True: regions gathered into
+    compact per-expert segments first (msi_expert_ffn with several senders)."""
+    _check_bf16("x_reg", x_reg, 2)
+    E_l, two_hp, H = w13.shape
+    Hp = two_hp // 2
+    cnt = torch.as_tensor(counts, dtype=torch.int64)
+    n_src = cnt.shape[0]
+    if cnt.shape != (n_src, E_l) or x_reg.shape[0] < E_l * n_src * cap_s or (cnt > cap_s).any():
+        raise ValueError("grouped_ffn_regions: counts must be [n_src, E_l] <= cap_s over E_l*n_src*cap_s rows")
+    tab = cnt.to(x_reg.device).contiguous()
+    tot = cnt.sum(0).tolist()
+    rows = sum((int(t) + ROW_ALIGN - 1) // ROW_ALIGN * ROW_ALIGN for t in tot) + ROW_ALIGN
+    if hbuf is None:
+        hbuf = torch.empty((rows, Hp), dtype=torch.bfloat16, device=x_reg.device)
+    if y_reg is None:
+        y_reg = torch.zeros_like(x_reg)
+    xcomp = torch.empty((hbuf.shape[0], H), dtype=torch.bfloat16, device=x_reg.device) if gather else None
+    _lib.call("msi_grouped_ffn_regions", _ptr(x_reg), _ptr(tab), n_src, cap_s, E_l, _ptr(w13), _ptr(w2),
+              _ptr(hbuf), hbuf.shape[0], _ptr(y_reg), H, Hp, int(a_runs), _ptr(xcomp), _stream(stream))
+    return y_reg

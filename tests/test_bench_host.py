@@ -58,3 +58,29 @@ def test_reference_arm_runs_whole_layer_and_reports_bench_config():
     args = types.SimpleNamespace(layers=4, merge=True, attn="real", graph=True)
     want = bench.bench_config(args, as_model_spec("tiny"), 1, 1, True, "1 GPU: co-located", 1, 1, 96, 1)
     assert line["config"] == want
+
+
+def test_disaggregated_layout_for_the_pingpong_line():
+    import argparse
+
+    args = argparse.Namespace(shape="mixtral-8x22b", m=3, b_a=1024)
+    # expert share of the per-token GPU time ~0.65 (T_e 3.3 ms vs T_a 1.8 ms per merged micro-batch)
+    (n_a, n_e, colo, src, tp, model, m, b_a), slots = bench.disaggregated_layout(args, 8, 0.65)
+    assert (n_a, n_e, colo, tp, m, b_a) == (3, 5, False, 1, 3, 1024)
+    assert slots is not None and slots.n_e == 5 and slots.P % 5 == 0  # 8 experts over 5 GPUs
+    assert "3+5" in src
+    (n_a, n_e, *_), slots = bench.disaggregated_layout(args, 4, 0.65)
+    assert (n_a, n_e) == (1, 3) and slots.P == 12
+    (n_a, n_e, *_), slots = bench.disaggregated_layout(args, 2, 0.65)
+    assert (n_a, n_e) == (1, 1) and slots is None
+    (n_a, n_e, *_), slots = bench.disaggregated_layout(args, 8, 0.99)  # at least one attention GPU
+    assert (n_a, n_e) == (1, 7)
+
+
+def test_pingpong_summary_keeps_the_comparable_fields():
+    sub = {"value": 1.0, "value_per_gpu": 0.5, "ms_per_step": 3.0, "stage_times": {"T_a_ms": 1}, "clocks": {},
+           "gpu_launches": 7, "attention": None, "config": {"n_a": 1}, "roofline": {"achieved": 900.0, "frac": 0.6},
+           "parity": {"routing_bit_exact": True, "combine_bit_exact": True}, "e2e": None}
+    out = bench.pingpong_summary(sub, 0.6)
+    assert out["value"] == 1.0 and out["expert_ffn"]["achieved"] == 900.0 and out["parity"]["routing_bit_exact"]
+    assert "e2e" not in out and bench.pingpong_summary(None, 0.5) is None

@@ -108,6 +108,8 @@ PLANS = [
     (2, 2, False, "tiny", [64, 48], 2, 1, "skew"),  # replicated hot experts (load balancing)
     (1, 2, False, "tiny", [64], 2, 2, None, 2),     # expert TP: one node of 2 GPUs (h' split)
     (2, 4, False, "tiny", [48, 33], 2, 1, None, 2),  # 2 attention + 2 expert nodes x 2 GPUs
+    (1, 3, False, "tiny", [64], 2, 1, "spread"),    # 8 experts on 3 expert GPUs (spread_slots)
+    (3, 5, False, "tiny", [64, 40, 17], 2, 1, "spread"),  # the 8-GPU 3+5 split: 8 experts on 5 GPUs
 ]
 
 
@@ -133,6 +135,9 @@ def test_m2n_multi_gpu(lib, tmp_path, n_a, n_e, colo, shape, tokens, m, layers, 
         loads = np.ones(model.experts)
         loads[0], loads[4] = 20.0, 15.0
         slots = balanced_slots(loads, n_e, max_replicas=2)
+    elif balanced == "spread":  # a split whose expert-GPU count does not divide E
+        from paper_2504_02263_b200.balance import spread_slots
+        slots = spread_slots(model.experts, n_e)
     port = _free_port()
     mp.spawn(_worker, args=(world, port, n_a, n_e, colo, shape, tokens, m, layers, str(tmp_path), slots, tp),
              nprocs=world, join=True)

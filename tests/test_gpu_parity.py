@@ -620,3 +620,49 @@ def test_route_dispatch_fused_empty_and_replicated(lib):
         assert_close_bf16(outs[name], ref.out[0], f"layer output ({name})")
         g.close()
     np.testing.assert_array_equal(outs["rep"], outs["plain"])
+
+
+@pytest.mark.parametrize("n_src,E_l,per", [(1, 3, 300), (2, 4, 200), (3, 2, 130), (8, 2, 70), (5, 5, 40)])
+def test_expert_ffn_regions_equal_compact(lib, n_src, E_l, per):
+    """The receive-region layout msi_expert_ffn reads (n_src regions per
+    expert, A loaded as region runs; ragged, empty and one-row regions) gives
+    bit-identical expert outputs to the same rows packed compactly per
+    expert: every row's MMAs and epilogue are the same."""
+    import torch
+
+    from paper_2504_02263_b200 import ops, runtime
+    from paper_2504_02263_b200.config import MoeModelSpec
+
+    model = MoeModelSpec("regions", 1, 512, 768, E_l, 1)
+    rng = np.random.default_rng(n_src * 31 + E_l)
+    counts = rng.integers(0, 2 * per, size=(n_src, E_l))
+    counts[0, 0] = 0
+    if n_src > 1:
+        counts[1, 0] = 1
+    cap = int(counts.max()) + 5
+    _, w13, w2 = runtime.synth_device_weights(model, list(range(E_l)), seed=3, device="cuda")
+    x_reg = torch.randn((E_l * n_src * cap, model.hidden), device="cuda").to(torch.bfloat16)
+    tot = counts.sum(0)
+    starts = ops.segment_starts(tot.tolist())
+    rows = starts[-1] + (int(tot[-1]) + 127) // 128 * 128 + 128
+    xc = torch.zeros((rows, model.hidden), dtype=torch.bfloat16, device="cuda")
+    for e in range(E_l):
+        o = starts[e]
+        for s in range(n_src):
+            b = (e * n_src + s) * cap
+            xc[o:o + counts[s, e]] = x_reg[b:b + counts[s, e]]
+            o += counts[s, e]
+    yc = ops.grouped_ffn(xc, torch.tensor(tot, dtype=torch.int32), w13, w2)
+    y_reg = ops.grouped_ffn_regions(x_reg, counts, cap, w13, w2)
+    xr = x_reg.clone()
+    y_inplace = ops.grouped_ffn_regions(xr, counts, cap, w13, w2, y_reg=xr)  # Y over X
+    y_gather = ops.grouped_ffn_regions(x_reg, counts, cap, w13, w2, gather=True)  # gathered, compact GEMM1
+    torch.cuda.synchronize()
+    for e in range(E_l):
+        o = starts[e]
+        for s in range(n_src):
+            b = (e * n_src + s) * cap
+            assert torch.equal(y_reg[b:b + counts[s, e]], yc[o:o + counts[s, e]]), (e, s)
+            assert torch.equal(y_inplace[b:b + counts[s, e]], yc[o:o + counts[s, e]]), (e, s)
+            assert torch.equal(y_gather[b:b + counts[s, e]], yc[o:o + counts[s, e]]), (e, s)
+            o += counts[s, e]
