@@ -592,6 +592,9 @@ def bench_config(args, model, n_a: int, n_e: int, colo: bool, plan_source: str, 
             "microbatching": ("co-located: m micro-batches merged into one batch (no ping-pong partner)"
                               if colo and args.merge else "ping-pong, m micro-batches"),
             "L_sim": args.layers, "attention_stage": args.attn,
+            "attention_batches": ("uniform context lengths (mean 730)" if n_a == 1 else
+                                  "compose_attention_batches over the attention GPUs (SPEC.md:415-423; "
+                                  "uniform request lengths, mean 730)"),
             "l2": (f"working set (expert weights {model.experts * 3 * model.hidden * model.intermediate * 2 / 1e9:.1f} GB"
                    " + KV cache) >> 126 MB L2; no flush needed"),
             "parallelism": f"dp{n_a}-ep{n_e}" + (f"-etp{tp_e}" if tp_e > 1 else ""),
@@ -718,8 +721,16 @@ def measure(args, rank: int, world: int, local: int, layout, full: bool = True, 
         # real decode attention layer per micro-batch (paged KV at s = avg_seq_len)
         from paper_2504_02263_b200 import attention as attn_mod
         w_att = attn_mod.AttentionWeights(model, dev, seed=0)
-        att_stages = [attn_mod.AttentionStage(model, args.b_a, args.layers, dev, weights=w_att,
-                                          avg_seq_len=wl.avg_seq_len, seed=1000 * rank + j) for j in range(plan.m)]
+        ctx = [None] * plan.m
+        if n_a > 1:
+            # the micro-batch's n_a * b_a requests composed over the attention
+            # GPUs for equal predicted attention time
+            ai = plan.attention_ranks().index(rank)
+            ctx = [attn_mod.composed_ctx_lens(model, n_a, args.b_a, wl.avg_seq_len, seed=j)[0][ai]
+                   for j in range(plan.m)]
+        att_stages = [attn_mod.AttentionStage(model, args.b_a, args.layers, dev, weights=w_att, ctx_lens=ctx[j],
+                                              avg_seq_len=wl.avg_seq_len, seed=1000 * rank + j)
+                      for j in range(plan.m)]
     slots, loads = slots_override, None
     if args.balance or args.skew > 0:
         # calibration: this step's routing counts (all attention ranks), placement

@@ -180,3 +180,30 @@ class AttentionStage:
     def attn_bytes(self) -> int:
         """Algorithmic bytes of msi_decode_attention per layer: K/V read + q read + o write."""
         return self.cache.kv_bytes_read() + 2 * self.T * self.n_heads * _lib.HEAD_DIM * 2
+
+
+def request_cost_model(model, hbm_gbs: float = 6546.6, tflops: float = 1400.0):
+    """perf_model.CostModel whose per-request attention cost is
+    alpha * seq_len + beta: alpha = the KV bytes one cached token adds to the
+    decode read (2 n_kv 128 x 2 B) at the HBM rate, beta = the request's
+    projection FLOPs at the tensor rate."""
+    from .perf_model import CostModel
+
+    n_heads, n_kv = head_layout(model)
+    alpha = 2 * n_kv * _lib.HEAD_DIM * 2 / (hbm_gbs * 1e9)
+    beta = 2.0 * model.hidden * (n_heads + 2 * n_kv + n_heads) * _lib.HEAD_DIM / (tflops * 1e12)
+    return CostModel(k1=alpha * 730 + beta, k2=0.0, k3=1e-6, k4=1e-4, alpha=alpha, beta=beta)
+
+
+def composed_ctx_lens(model, n_a: int, b_a: int, avg_seq_len: int, seed: int = 0):
+    """Attention batch composition over the data-parallel attention GPUs
+    (balance.compose_attention_batches): a pool of n_a * b_a
+    decode requests (uniform lengths, mean avg_seq_len, identical on every
+    rank for a seed) is split into n_a batches of b_a requests whose predicted
+    attention times are balanced (largest first onto the least-loaded GPU).  Returns (per-GPU ctx_lens, AttnBatchPlan)."""
+    from .balance import compose_attention_batches
+
+    lens = batch_composition(n_a * b_a, avg_seq_len, seed, "uniform")
+    reqs = list(enumerate(lens.tolist()))
+    plan = compose_attention_batches(reqs, n_a, request_cost_model(model), max_batch=b_a, mode="lpt")
+    return plan.seq_lens(reqs), plan

@@ -263,7 +263,8 @@ def _refine(assignment, load, cost, n_a, k2, max_batch, max_iter: int = 200):
 
 
 def compose_attention_batches(requests, n_a: int, cm, target_time: float | None = None,
-                              max_batch: int | None = None, refine_limit: int = 32) -> AttnBatchPlan:
+                              max_batch: int | None = None, refine_limit: int = 32,
+                              mode: str = "ffd") -> AttnBatchPlan:
     """Attention batch composition (§7 / SPEC.md:415-423): per-request
     cost alpha·seq_len + beta, first-fit-decreasing into n_a bins whose
     predicted time (k2 + costs) is capped at ``target_time``; a request no
@@ -273,7 +274,11 @@ def compose_attention_batches(requests, n_a: int, cm, target_time: float | None 
     ``target_time`` None = the balanced target k2 + total cost / n_a.
     ``max_batch`` (additive; the runtime's per-node micro-batch capacity)
     also caps the request count of a bin; spills then go to the least-loaded
-    bin with room.
+    bin with room.  ``mode="lpt"`` (additive) skips the first-fit step: every
+    request, largest first, goes to the least-loaded bin with room -- the
+    right rule when max_batch fixes every bin's request count (the runtime's
+    equal micro-batches), where first-fit would fill the first bins with the
+    largest requests and leave the spill to the count cap.
 
     Small instances (<= ``refine_limit`` requests, where one misplaced
     request moves a node's time by a large fraction) are then refined by
@@ -283,6 +288,8 @@ def compose_attention_batches(requests, n_a: int, cm, target_time: float | None 
     (tests/test_balance.py).  Large batches are FFD as stated."""
     if n_a < 1:
         raise ValueError("need at least one attention node")
+    if mode not in ("ffd", "lpt"):
+        raise ValueError("mode must be 'ffd' or 'lpt'")
     reqs = [(rid, float(s)) for rid, s in requests]
     if max_batch is not None and len(reqs) > n_a * max_batch:
         raise ValueError("more requests than n_a * max_batch")
@@ -301,7 +308,7 @@ def compose_attention_batches(requests, n_a: int, cm, target_time: float | None 
 
     for i in order:
         dest = None
-        for j in range(n_a):
+        for j in range(n_a if mode == "ffd" else 0):
             if has_room(j) and cm.k2 + load[j] + cost[i] <= target_time + eps:
                 dest = j
                 break

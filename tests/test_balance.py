@@ -201,3 +201,16 @@ def test_compose_near_brute_force_optimum():
                 t[j] += cost[i]
             best = min(best, t.max() / t.min())
         assert got <= best * 1.15 + 1e-12, (trial, got, best)
+
+
+def test_compose_lpt_with_equal_batches():
+    """mode='lpt' + max_batch: equal request counts per node and balanced
+    predicted times (the bench's per-GPU micro-batches)."""
+    cm = _cm()
+    rng = np.random.default_rng(3)
+    reqs = list(enumerate(rng.integers(1, 1460, 3 * 512).tolist()))
+    plan = B.compose_attention_batches(reqs, 3, cm, max_batch=512, mode="lpt")
+    assert [len(a) for a in plan.assignment] == [512] * 3
+    assert max(plan.predicted) / min(plan.predicted) < 1.001
+    with pytest.raises(ValueError):
+        B.compose_attention_batches(reqs, 3, cm, mode="best")
