@@ -84,7 +84,9 @@ def choose_split(world: int, shape: str, plan_arg: str, split: str = "", colocat
                 src = "planner.search_box (calibrated B200 costs, profiles/r01_calibration_8x22b.json)"
                 if p.tp_e > 1:  # expert nodes of tp_e GPUs
                     src += f"; expert TP {p.tp_e}"
-                return p.n_a, p.n_e * p.tp_e, bool(p.colocated), src, p.tp_e
+                if p.tp_a > 1:  # attention nodes of tp_a GPUs: the runtime counts attention GPUs
+                    src += f"; attention TP {p.tp_a} (use --tp-a {p.tp_a})"
+                return p.n_a * p.tp_a, p.n_e * p.tp_e, bool(p.colocated), src, p.tp_e
     n_a, n_e, colo = SPLITS[world]
     return n_a, n_e, colo, "BASELINE.json config split", tp_e
 
@@ -104,6 +106,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--split", default="", help="attention+expert GPUs, e.g. 6+2 (disaggregated)")
+    ap.add_argument("--tp-a", dest="tp_a", type=int, default=1,
+                    help="attention GPUs per attention node (tensor parallel over heads; all-gather/reduce-scatter "
+                         "fused into the projection GEMMs)")
     ap.add_argument("--tp-e", dest="tp_e", type=int, default=1,
                     help="expert GPUs per expert node (tensor parallel over h'; disaggregated layouts)")
     ap.add_argument("--plan-json", default="", help="a planner output (python -m paper_2504_02263_b200.planner "
@@ -579,6 +584,10 @@ def resolve_layout(args, world: int):
     return n_a, n_e, colo, plan_source, (1 if colo else tp_e), model, m_eff, b_a
 
 
+def args_tp_a(args) -> int:
+    return int(getattr(args, "tp_a", 1) or 1)
+
+
 def bench_config(args, model, n_a: int, n_e: int, colo: bool, plan_source: str, tp_e: int, m: int, b_a: int,
                  world: int) -> dict:
     """The workload the line describes (identical in both arms' lines)."""
@@ -597,7 +606,9 @@ def bench_config(args, model, n_a: int, n_e: int, colo: bool, plan_source: str, 
                                   "uniform request lengths, mean 730)"),
             "l2": (f"working set (expert weights {model.experts * 3 * model.hidden * model.intermediate * 2 / 1e9:.1f} GB"
                    " + KV cache) >> 126 MB L2; no flush needed"),
-            "parallelism": f"dp{n_a}-ep{n_e}" + (f"-etp{tp_e}" if tp_e > 1 else ""),
+            "parallelism": (f"dp{n_a // args_tp_a(args)}-atp{args_tp_a(args)}" if args_tp_a(args) > 1 else f"dp{n_a}")
+                           + f"-ep{n_e}" + (f"-etp{tp_e}" if tp_e > 1 else ""),
+            "tp_a": args_tp_a(args),
             "launch": "CUDA graph per rank (device-tracked epochs)" if args.graph else "eager"}
 
 
@@ -690,7 +701,10 @@ def measure(args, rank: int, world: int, local: int, layout, full: bool = True, 
 
     n_a, n_e, colo, plan_source, tp_e, model, m_eff, b_a = layout
     args.b_a = b_a
-    plan = DeploymentPlan(n_a=n_a, n_e=n_e, m=m_eff, b_a=b_a, colocated=colo, tp_e=tp_e)
+    tp_a = getattr(args, "tp_a", 1) or 1
+    plan = DeploymentPlan(n_a=n_a, n_e=n_e, m=m_eff, b_a=b_a, colocated=colo, tp_e=tp_e, tp_a=tp_a)
+    if tp_a > 1 and (args.balance or args.skew > 0):
+        raise SystemExit("--tp-a > 1 with --balance/--skew is not supported")
     dev = torch.device(f"cuda:{local}")
     gen = torch.Generator(device=dev)
     gen.manual_seed(1 + rank)
@@ -717,7 +731,7 @@ def measure(args, rank: int, world: int, local: int, layout, full: bool = True, 
         xs = [x.to(torch.bfloat16) for x in xs]
     wl = WorkloadSpec()
     att_stages = None
-    if args.attn == "real" and is_attn_rank:
+    if args.attn == "real" and is_attn_rank and tp_a == 1:
         # real decode attention layer per micro-batch (paged KV at s = avg_seq_len)
         from paper_2504_02263_b200 import attention as attn_mod
         w_att = attn_mod.AttentionWeights(model, dev, seed=0)
@@ -748,6 +762,17 @@ def measure(args, rank: int, world: int, local: int, layout, full: bool = True, 
             from paper_2504_02263_b200.balance import balanced_slots
             slots = balanced_slots(loads, n_e, max_replicas=min(n_e, 2))
     g = runtime.M2NGroup(model, plan, rank=rank, device=dev, slots=slots)
+    if args.attn == "real" and is_attn_rank and tp_a > 1:
+        # attention nodes of tp_a GPUs: heads split, all-gather fused into the
+        # QKV GEMM, reduce-scatter into the O projection (attn_tp.cu); the
+        # node's tp_a * b_a requests composed over the attention nodes
+        from paper_2504_02263_b200 import attention as attn_mod
+        w_att = attn_mod.AttentionWeights(model, dev, seed=0)
+        node = g.attn_index // tp_a
+        att_stages = [attn_mod.AttentionTPStage(
+            model, args.b_a, args.layers, g, j, w_att,
+            attn_mod.composed_ctx_lens(model, n_a // tp_a, tp_a * args.b_a, wl.avg_seq_len, seed=j)[0][node],
+            seed=1000 * node + j) for j in range(plan.m)]
     _, w13, w2 = runtime.synth_device_weights(model, runtime.local_experts(g), seed=0, device=dev, tp=g.tp,
                                               tp_rank=g.tp_rank)
     layer = runtime.MoEDecodeLayer(g, wg=wg if g.is_attention else None,
@@ -991,8 +1016,8 @@ def measure(args, rank: int, world: int, local: int, layout, full: bool = True, 
     # logits + route kernels), expert wait + [region gather when several
     # senders share an expert] + 2 GEMMs, combine
     attn_launches = 0
-    if att_stages:
-        attn_launches = 3 + (1 if att_stages[0].ws is not None else 0)
+    if att_stages:  # TP node: publish, QKV, attention [+ combine], O projection, reduce
+        attn_launches = (5 if tp_a > 1 else 3) + (1 if att_stages[0].ws is not None else 0)
     router_launches = 2 if (model.experts >= 64 and model.experts % 8 == 0 and args.b_a <= 256) else 1
     expert_launches = 3 + (1 if n_a > 1 else 0)
     launches_per_mbl = attn_launches + router_launches + expert_launches + 1

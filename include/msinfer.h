@@ -47,7 +47,8 @@ enum {
   MSI_BUF_RECV = 0,   /* expert GPU: received rows [E_l][n_a][max_tokens][H] bf16 per slot
                        * (after the expert FFN: the expert outputs in place) */
   MSI_BUF_HBUF = 3,   /* expert GPU: SwiGLU activations [cap][H'] bf16 (one, shared) */
-  MSI_BUF_CNTAB = 4   /* count table [n_a][E] of (epoch<<32 | count) per slot */
+  MSI_BUF_CNTAB = 4,  /* count table [n_a][E] of (epoch<<32 | count) per slot */
+  MSI_BUF_TP_X = 5    /* attention TP: this GPU's token shard [max_tokens][H] bf16 per slot */
 };
 
 /* Deployment plan.  Vocabulary of SPEC.md:311 (n_a, m) plus n_e; tp = 1.
@@ -71,6 +72,12 @@ typedef struct {
                                          /* all of the node's rows and holds h'/  */
                                          /* tp_e features of each local expert;   */
                                          /* the combine sums the tp_e partials.   */
+  int32_t tp_a;                          /* attention GPUs per attention node     */
+                                         /* (tensor parallel over heads; 0 or 1 = */
+                                         /* none).  Node i = attention indices    */
+                                         /* [i tp_a, (i+1) tp_a); every GPU keeps */
+                                         /* its own max_tokens token shard (its   */
+                                         /* M2N batch) and 1/tp_a of the heads.   */
 } msi_plan;
 
 typedef struct msi_ctx msi_ctx;
@@ -266,6 +273,36 @@ int msi_grouped_ffn_regions(const void* x_reg, const uint64_t* cntab, int n_src,
                             int64_t cap_s, int E_l, const void* w13, const void* w2,
                             void* hbuf, int64_t hbuf_rows, void* y_reg, int hidden,
                             int inter, int a_runs, void* xcomp, void* stream);
+/* ---- attention-node tensor parallelism (plan.tp_a > 1)
+ * Per layer and micro-batch slot, on every attention GPU of a node, in this
+ * order on one stream (epoch 0 = device-tracked, as for the M2N calls):
+ *   msi_tp_publish  x shard [T][H] -> this GPU's symmetric shard buffer, then
+ *                   release the node peers (x may be that buffer itself:
+ *                   msi_ctx_buffer(MSI_BUF_TP_X)).
+ *   msi_tp_qkv      all-gather fused into the QKV GEMM: the tcgen05 GEMM
+ *                   reads every peer's shard over NVLink with its own TMA
+ *                   map; wqkv_l = this GPU's [q heads | k heads | v heads]
+ *                   rows [(n_heads_l + 2 n_kv_l) 128][H]; epilogue = RoPE +
+ *                   paged-KV append for all tp_a*T node tokens (node token
+ *                   s*T + t = peer s's token t), q_out [tp_a*T][n_heads_l][128].
+ *   (msi_decode_attention over this GPU's heads, o [tp_a*T][n_heads_l*128])
+ *   msi_tp_oproj    row-parallel O projection, wo_l = W_o[:, this GPU's head
+ *                   columns] [H][n_heads_l*128]; the epilogue stores each
+ *                   token's partial row into its owner's partial buffer over
+ *                   NVLink (reduce-scatter fused into the GEMM).
+ *   msi_tp_reduce   out[t] = bf16(resid[t] + sum_r partial_r[t]) (fp32, r
+ *                   ascending) once every peer's partials landed.
+ * T <= max_tokens, the same T on every GPU of the node. */
+int msi_tp_publish(msi_ctx* ctx, const void* x, int T, int mb_slot, uint32_t epoch,
+                   void* stream);
+int msi_tp_qkv(msi_ctx* ctx, const void* wqkv_l, int n_heads_l, int n_kv_l, const int32_t* pos,
+               float theta, const int32_t* block_table, int max_pages, void* k_cache,
+               void* v_cache, void* q_out, int T, int mb_slot, uint32_t epoch, void* stream);
+int msi_tp_oproj(msi_ctx* ctx, const void* o, const void* wo_l, int k_l, int T, int mb_slot,
+                 uint32_t epoch, void* stream);
+int msi_tp_reduce(msi_ctx* ctx, const void* resid, void* out, int T, int mb_slot, uint32_t epoch,
+                  void* stream);
+
 /* The attention stage's two projections (Table 3, "QKV
  * Project" and "Attn Output") on the expert GEMM's tcgen05 kernel, run as
  * one dense "expert" of T rows (CTA-pair 256x256 tiles, TMA, TMEM).

@@ -17,7 +17,7 @@ ROW_ALIGN = 128
 KV_PAGE = 64     # MSI_KV_PAGE
 HEAD_DIM = 128   # MSI_HEAD_DIM
 
-BUF_RECV, BUF_HBUF, BUF_CNTAB = 0, 3, 4
+BUF_RECV, BUF_HBUF, BUF_CNTAB, BUF_TP_X = 0, 3, 4, 5
 ERRORS = {-1: "MSI_EINVAL", -2: "MSI_EARCH", -3: "MSI_ESTATE", -4: "MSI_ETIMEOUT", -5: "MSI_EDRIVER"}
 
 
@@ -35,7 +35,7 @@ class Plan(ctypes.Structure):
         ("attn_ranks", ctypes.c_int32 * MAX_RANKS), ("expert_ranks", ctypes.c_int32 * MAX_RANKS),
         ("hidden", ctypes.c_int32), ("inter", ctypes.c_int32), ("experts", ctypes.c_int32),
         ("topk", ctypes.c_int32), ("max_tokens", ctypes.c_int32), ("slots", ctypes.c_int32),
-        ("tp_e", ctypes.c_int32),
+        ("tp_e", ctypes.c_int32), ("tp_a", ctypes.c_int32),
     ]
 
 
@@ -80,6 +80,10 @@ SIGNATURES = {
                              ctypes.c_int64, _P, _P]),
     "msi_grouped_ffn_regions": (_I, [_P, _P, _I, ctypes.c_int64, _I, _P, _P, _P, ctypes.c_int64, _P, _I, _I, _I,
                                      _P, _P]),
+    "msi_tp_publish": (_I, [_P, _P, _I, _I, _U32, _P]),
+    "msi_tp_qkv": (_I, [_P, _P, _I, _I, _P, ctypes.c_float, _P, _I, _P, _P, _P, _I, _I, _U32, _P]),
+    "msi_tp_oproj": (_I, [_P, _P, _P, _I, _I, _I, _U32, _P]),
+    "msi_tp_reduce": (_I, [_P, _P, _P, _I, _I, _U32, _P]),
     "msi_dense_gemm": (_I, [_P, ctypes.c_int64, _P, _I, _I, _P, ctypes.c_int64, _P, ctypes.c_int64, _P, _P]),
     "msi_qkv_rope_append": (_I, [_P, ctypes.c_int64, _I, _P, _I, _I, _P, ctypes.c_float, _P, _I, _P, _P, _P,
                                  _P, _P]),

@@ -32,6 +32,7 @@ step (stationary work); ``advance()`` moves every sequence on by one token.
 
 from __future__ import annotations
 
+import ctypes
 import math
 
 import numpy as np
@@ -207,3 +208,83 @@ def composed_ctx_lens(model, n_a: int, b_a: int, avg_seq_len: int, seed: int = 0
     reqs = list(enumerate(lens.tolist()))
     plan = compose_attention_batches(reqs, n_a, request_cost_model(model), max_batch=b_a, mode="lpt")
     return plan.seq_lens(reqs), plan
+
+
+class AttentionTPStage:
+    """One micro-batch's attention stage on an attention node of tp_a GPUs
+    (DeploymentPlan.tp_a > 1; PAPER.md:192, 441-443; csrc/attn_tp.cu).
+
+    This GPU (rank r of its node) holds heads [r nh_l, (r+1) nh_l) and KV heads
+    [r kv_l, (r+1) kv_l) of every node sequence (tp_a * T sequences: node
+    token s*T + t is peer s's token t), and its own T-token shard of the
+    residual stream -- its M2N batch.  forward(x_shard):
+
+        msi_tp_publish   x -> symmetric shard buffer, release the node peers
+        msi_tp_qkv       all-gather + QKV GEMM + RoPE/append in one kernel
+        msi_decode_attention  this GPU's heads, all node tokens
+        msi_tp_oproj     O projection, reduce-scatter in the epilogue
+        msi_tp_reduce    y = bf16(x + sum of the tp_a partials)
+
+    ``weights`` are the full AttentionWeights (identical on every node GPU);
+    each GPU slices its heads.  ``ctx_lens`` are the node's tp_a * T cached
+    lengths (identical on every node GPU, and so is the block table)."""
+
+    def __init__(self, model, T: int, layers: int, group, slot: int, weights: AttentionWeights,
+                 ctx_lens: np.ndarray, seed: int = 0, theta: float = ROPE_THETA, headroom: int = 0):
+        g = group
+        self.tp = g.plan.tp_a
+        if self.tp < 2 or not g.is_attention:
+            raise ValueError("AttentionTPStage needs an attention rank of a tp_a > 1 plan")
+        if T > g.plan.b_a:
+            raise ValueError("T exceeds the plan's b_a")
+        self.g, self.model, self.T, self.slot, self.theta = g, model, T, slot, theta
+        self.r = g.attn_index % self.tp
+        n_heads, n_kv = weights.n_heads, weights.n_kv
+        if n_kv % self.tp:
+            raise ValueError(f"tp_a={self.tp} must divide the {n_kv} KV heads")
+        self.n_heads, self.n_kv = n_heads // self.tp, n_kv // self.tp  # this GPU's heads
+        D = _lib.HEAD_DIM
+        r, hl, kl = self.r, self.n_heads, self.n_kv
+        wq = weights.wqkv[:n_heads * D]
+        wk = weights.wqkv[n_heads * D:(n_heads + n_kv) * D]
+        wv = weights.wqkv[(n_heads + n_kv) * D:]
+        self.wqkv = torch.cat([wq[r * hl * D:(r + 1) * hl * D], wk[r * kl * D:(r + 1) * kl * D],
+                               wv[r * kl * D:(r + 1) * kl * D]]).contiguous()
+        self.wo = weights.wo[:, r * hl * D:(r + 1) * hl * D].contiguous()
+        ctx = np.asarray(ctx_lens, np.int32)
+        if ctx.shape != (self.tp * T,):
+            raise ValueError("ctx_lens must hold the node's tp_a * T sequences")
+        # same seed on every node GPU -> same block table; KV contents per head slice
+        self.cache = PagedKVCache(self.tp * T, kl, ctx, layers, g.device, seed, headroom=headroom)
+        self.q = torch.empty((self.tp * T, hl, D), dtype=torch.bfloat16, device=g.device)
+        self.o = torch.empty((self.tp * T, hl * D), dtype=torch.bfloat16, device=g.device)
+        self.y = torch.empty((T, model.hidden), dtype=torch.bfloat16, device=g.device)
+        self.ws = ops.decode_attention_workspace(self.tp * T, hl, kl, self.cache.max_pages, g.device)
+        self.timing = None
+        self.qkv_width = self.wqkv.shape[0]
+
+    def forward(self, x: torch.Tensor, layer: int, out: torch.Tensor | None = None) -> torch.Tensor:
+        """x bf16 [T, h] (this GPU's shard) -> x + Attn(x) W_o^T for the shard."""
+        c, g, s = self.cache, self.g, ops._stream()
+        out = self.y if out is None else out
+        ctx = g.ctx
+        _lib.call("msi_tp_publish", ctx, ops._ptr(x), self.T, self.slot, 0, s)
+        _lib.call("msi_tp_qkv", ctx, ops._ptr(self.wqkv), self.n_heads, self.n_kv, ops._ptr(c.pos),
+                  ctypes.c_float(self.theta), ops._ptr(c.block_table), c.block_table.shape[1], ops._ptr(c.k[layer]),
+                  ops._ptr(c.v[layer]), ops._ptr(self.q), self.T, self.slot, 0, s)
+        if self.timing is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True)
+            e0.record()
+        ops.decode_attention(self.q, c.k[layer], c.v[layer], c.block_table, c.lens, self.o, self.ws)
+        if self.timing is not None:
+            e1.record()
+            self.timing.append((e0, e1))
+        _lib.call("msi_tp_oproj", ctx, ops._ptr(self.o), ops._ptr(self.wo), self.o.shape[1], self.T, self.slot, 0, s)
+        _lib.call("msi_tp_reduce", ctx, ops._ptr(x), ops._ptr(out), self.T, self.slot, 0, s)
+        return out
+
+    def flops(self) -> float:
+        return 2.0 * self.tp * self.T * self.model.hidden * (self.qkv_width + self.o.shape[1])
+
+    def attn_bytes(self) -> int:
+        return self.cache.kv_bytes_read() + 2 * self.tp * self.T * self.n_heads * _lib.HEAD_DIM * 2

@@ -363,7 +363,7 @@ def save_config(bundle: ConfigBundle, path) -> None:
 class DeploymentPlan:
     """Roles of one decode deployment on a single NVSwitch box.
 
-    SPEC.md:311 vocabulary: ``tp_a`` (fixed to 1 here), ``tp_e``, ``n_a``
+    SPEC.md:311 vocabulary: ``tp_a``, ``tp_e``, ``n_a``
     attention GPUs (data-parallel replicas), ``m`` micro-batches
     (ping-pong), ``B`` = global batch per micro-batch
     (= n_a * b_a).  Added: ``n_e`` expert GPUs and ``b_a``.  Expert GPUs form
@@ -371,7 +371,12 @@ class DeploymentPlan:
     over tp_e GPUs); expert e lives on node
     e // (E / nodes), contiguous blocks, and every GPU of the node holds h'/tp_e
     features of each of the node's experts (tensor parallel over h'; the
-    combine sums the tp_e partial outputs).  ``colocated`` puts both roles on
+    combine sums the tp_e partial outputs).  Attention GPUs form n_a / tp_a
+    attention nodes of tp_a GPUs (tensor parallel over heads, PAPER.md:192,
+    441-443): every GPU keeps its own b_a-token shard (its M2N batch) and
+    1/tp_a of the heads; the QKV GEMM all-gathers the node's shards over
+    NVLink and the O projection reduce-scatters them back (attn_tp.cu).
+    ``colocated`` puts both roles on
     every GPU (the 1-GPU report point, and the DeepSeek-shaped 8->8 case); then
     n_a == n_e == world size and tp_e == 1.
     """
@@ -386,8 +391,8 @@ class DeploymentPlan:
 
     def __post_init__(self):
         _positive("plan", self, ("n_a", "n_e", "m", "b_a"))
-        if self.tp_a != 1:
-            raise ConfigError("plan: only tp_a = 1 is supported")
+        if self.tp_a < 1 or self.n_a % self.tp_a or self.tp_a > 8:
+            raise ConfigError(f"plan: tp_a ({self.tp_a}) must divide n_a ({self.n_a}) and be <= 8")
         if self.tp_e < 1 or self.n_e % self.tp_e:
             raise ConfigError(f"plan: tp_e ({self.tp_e}) must divide n_e ({self.n_e})")
         if self.colocated and self.n_a != self.n_e:

@@ -318,7 +318,8 @@ __global__ void attn_split_combine_kernel(const float* __restrict__ part_o, cons
 // thread with 16 B loads/stores (pairs (i, i+64)); q to q_out, k and v into
 // the cache slot.
 __global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld, const int* __restrict__ pos,
-                                   int n_heads, int n_kv, float theta, const int* __restrict__ bt, int max_pages,
+                                   int n_heads, int n_kv, const __grid_constant__ RopeInv rope,
+                                   const int* __restrict__ bt, int max_pages,
                                    __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
                                    __nv_bfloat16* __restrict__ q_out) {
   __shared__ float s_cos[kD / 2], s_sin[kD / 2];
@@ -328,8 +329,7 @@ __global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv, int64_
   const int p = pos[t];
   if (threadIdx.x < kD / 2) {
     const int i = threadIdx.x;
-    const float inv = 1.0f / powf(theta, (float)(2 * i) / (float)kD);
-    sincosf((float)p * inv, &s_sin[i], &s_cos[i]);
+    sincosf((float)p * rope.v[i], &s_sin[i], &s_cos[i]);
   }
   __syncthreads();
   const int page = bt[(size_t)t * max_pages + p / kPage];
@@ -425,7 +425,7 @@ extern "C" int msi_rope_append(const void* qkv, int64_t qkv_ld, const int32_t* p
   MSI_REQUIRE(qkv && pos && block_table && k_cache && v_cache && q_out, "rope_append: null pointer");
   if (T == 0) return 0;
   MSI_CUDA(launch_k(rope_append_kernel, dim3(T), dim3(128), 0, (cudaStream_t)stream, (const __nv_bfloat16*)qkv,
-                    (int64_t)qkv_ld, pos, n_heads, n_kv, theta, block_table, max_pages, (__nv_bfloat16*)k_cache,
+                    (int64_t)qkv_ld, pos, n_heads, n_kv, rope_inv_table(theta), block_table, max_pages, (__nv_bfloat16*)k_cache,
                     (__nv_bfloat16*)v_cache, (__nv_bfloat16*)q_out));
   return check_launch("rope_append_kernel");
 }

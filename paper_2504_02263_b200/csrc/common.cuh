@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cmath>
 #include <utility>
 
 #include "../../include/msinfer.h"
@@ -53,6 +54,18 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 bool pdl_enabled();  // MSI_PDL=1 enables (A/B switch)
+
+// RoPE inverse frequencies theta^(-2i/128), i = 0..63, computed once on the
+// host and passed by value to both RoPE kernels (rope_append_kernel and the
+// QKV GEMM epilogue), which then rotate with identical arithmetic.
+struct RopeInv {
+  float v[64];
+};
+inline RopeInv rope_inv_table(float theta) {
+  RopeInv r;
+  for (int i = 0; i < 64; ++i) r.v[i] = 1.0f / powf(theta, (float)(2 * i) / 128.0f);
+  return r;
+}
 
 // Raise kernel `fn`'s dynamic shared-memory limit to >= bytes on the current
 // device.  The attribute is per (function, device context), so the cache is

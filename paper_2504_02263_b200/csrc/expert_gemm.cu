@@ -179,7 +179,7 @@ __device__ __forceinline__ bool half_pair_rows(const SegInfo<MAXE>& s, int e, in
 template <int CG, int MAXE>
 __global__ void __launch_bounds__(kThreads, 1)
 grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CUtensorMap tmB,
-                    const GemmParams p) {
+                    const __grid_constant__ GemmParams p) {
   const CUtensorMap& tmA = am.m[0];
   const CUtensorMap& tmA64 = am.m[1];
   using C = Cfg<CG, MAXE>;
@@ -224,8 +224,8 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
     s_abort = ok ? 0 : 1;
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
-    if (CG == 2 || p.a_runs) tma_prefetch(&am.m[1]);
-    if (p.a_runs) {
+    if (CG == 2 || p.a_runs || p.a_shards > 1) tma_prefetch(&am.m[1]);
+    if (p.a_runs || p.a_shards > 2) {
       tma_prefetch(&am.m[2]); tma_prefetch(&am.m[3]); tma_prefetch(&am.m[4]);
       tma_prefetch(&am.m[5]); tma_prefetch(&am.m[6]); tma_prefetch(&am.m[7]);
     }
@@ -269,8 +269,11 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
   // of system-scope loads), summed in shared memory
   for (int e = threadIdx.x; e < p.E_l; e += blockDim.x) seg.total[e] = 0;
   __syncthreads();
-  for (int i = threadIdx.x; i < (p.dense_rows ? 1 : p.totals ? p.E_l : p.n_a * p.E_l); i += blockDim.x) {
-    if (p.dense_rows) {
+  for (int i = threadIdx.x; i < (p.a_shards ? p.E_l : p.dense_rows ? 1 : p.totals ? p.E_l : p.n_a * p.E_l);
+       i += blockDim.x) {
+    if (p.a_shards) {
+      seg.total[i] = p.shard_rows;
+    } else if (p.dense_rows) {
       seg.total[0] = (int)p.dense_rows;
     } else if (p.totals) {
       seg.total[i] = p.totals[i];
@@ -362,10 +365,11 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
       // last 128-row tile of a segment split 64/64 over the pair, moved with
       // a 64-row box so the half-cost MMA is not fed a full tile's bytes)
       const bool hp = half_pair(seg, e, m);
-      int rowA = seg.start[e] + m * CG * BM + (int)rank * (hp ? BM / 2 : BM);
-      const int rowB = e * p.n_total + n * BN + (int)rank * C::B_ROWS;
-      const CUtensorMap* mA = (CG == 2 && hp && p.a64) ? &tmA64 : &tmA;  // compact rows
-      uint32_t a_bytes = (CG == 2 && hp && p.a64) ? C::A_BYTES / 2 : C::A_BYTES;
+      int rowA = (p.a_shards ? 0 : seg.start[e]) + m * CG * BM + (int)rank * (hp ? BM / 2 : BM);
+      const int rowB = (p.a_shards ? 0 : e * p.n_total) + n * BN + (int)rank * C::B_ROWS;
+      const CUtensorMap* mA = p.a_shards ? a_box_map(am, (uint32_t)e)                 // shard e's own map
+                              : (CG == 2 && hp && p.a64) ? &tmA64 : &tmA;               // compact rows
+      uint32_t a_bytes = (CG == 2 && hp && p.a64 && !p.a_shards) ? C::A_BYTES / 2 : C::A_BYTES;
       uint32_t a_bytes_pair = 2 * a_bytes;  // both CTAs' A bytes (the leader's barrier counts them)
       int npieces = 0;
       if (p.a_runs && lane == 0) {  // receive regions: only the rows present, as runs
@@ -486,7 +490,7 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       const int row_local = rowbase + rowsub + lane;                // row within expert segment
-      const int row_global = seg.start[e] + row_local;              // row in recv / hbuf
+      const int row_global = (p.a_shards ? e * p.shard_rows : seg.start[e]) + row_local;  // row in recv / hbuf
       const int valid_rows = min(32, max(0, seg.total[e] - (rowbase + rowsub)));
       // output columns of this warp: mode 0 writes 128 features per tile
       // (64 per N half), mode 1 writes 256 columns (128 per N half)
@@ -497,6 +501,10 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
       if (row_local < seg.total[e]) {
         if (p.mode == 0) {
           rowdst = reinterpret_cast<char*>(p.out) + ((size_t)row_global * p.out_ld + (size_t)n * (BN / 2) + colofs) * 2;
+        } else if (p.mode == 3) {  // attention-TP reduce-scatter: the token's shard owner
+          const int sh = row_global / p.shard_rows;
+          rowdst = reinterpret_cast<char*>(p.peer_out[sh]) +
+                   ((size_t)(row_global - sh * p.shard_rows) * p.out_ld + (size_t)n * BN + colofs) * 2;
         } else if (p.mode == 2) {  // per-head destinations below
           pos_t = p.pos[row_global];
           page_t = p.block_table[(size_t)row_global * p.max_pages + pos_t / MSI_KV_PAGE];
@@ -589,7 +597,7 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
 #pragma unroll
                 for (int b = 0; b < 2; ++b) {
                   const int i = c * 32 + 2 * j + b;
-                  const float inv = 1.0f / powf(p.theta, (float)(2 * i) / 128.0f);
+                  const float inv = p.rope.v[i];
                   float sn, cs;
                   sincosf(fp * inv, &sn, &cs);
                   const float x0 = __bfloat162float(__float2bfloat16_rn(__uint_as_float(lo[2 * j + b])));
@@ -862,11 +870,17 @@ int launch_cg(const GemmLaunch& L, cudaStream_t st) {
   AMaps am;
   CUtensorMap tb;
   int rc = 0;
-  for (int i = 0; i < (L.p.a_runs ? 8 : 2) && !rc; ++i)  // 128-row boxes, 64 (half pairs), ... 1 (runs)
-    rc = make_tmap(&am.m[i], L.a, (uint64_t)L.p.kdim, (uint64_t)L.a_rows, BK, BM >> i);
+  if (L.p.a_shards) {  // one 128-row-box map per shard (node peer)
+    MSI_REQUIRE(L.p.a_shards == L.p.E_l && L.p.a_shards <= 8 && !L.p.a_runs, "grouped_gemm: bad shard setup");
+    for (int i = 0; i < 8 && !rc; ++i)
+      rc = make_tmap(&am.m[i], L.a_shard[i < L.p.a_shards ? i : 0], (uint64_t)L.p.kdim, (uint64_t)L.a_rows, BK, BM);
+  } else {
+    for (int i = 0; i < (L.p.a_runs ? 8 : 2) && !rc; ++i)  // 128-row boxes, 64 (half pairs), ... 1 (runs)
+      rc = make_tmap(&am.m[i], L.a, (uint64_t)L.p.kdim, (uint64_t)L.a_rows, BK, BM >> i);
+    if (!rc && !L.p.a_runs) memcpy(&am.m[2], &am.m[0], 6 * sizeof(CUtensorMap));  // unused
+  }
   if (rc) return rc;
-  if (!L.p.a_runs) memcpy(&am.m[2], &am.m[0], 6 * sizeof(CUtensorMap));  // unused
-  rc = make_tmap(&tb, L.b, (uint64_t)L.p.kdim, (uint64_t)L.p.E_l * L.p.n_total, BK, C::B_ROWS);
+  rc = make_tmap(&tb, L.b, (uint64_t)L.p.kdim, (uint64_t)(L.p.a_shards ? 1 : L.p.E_l) * L.p.n_total, BK, C::B_ROWS);
   if (rc) return rc;
   if (int arc = smem_attr(reinterpret_cast<const void*>(grouped_gemm_kernel<CG, MAXE>), C::SMEM)) return arc;
   int grid = L.grid > 0 ? L.grid : num_sms();
@@ -1103,11 +1117,12 @@ int qkv_rope_append(const void* x, int64_t rows, int hidden, const void* wqkv, i
   MSI_REQUIRE(n % BN == 0, "qkv_rope_append: n_heads + 2 n_kv must be even (256-column N tiles)");
   MSI_REQUIRE(hidden > 0 && hidden % BK == 0, "qkv_rope_append: hidden %% 64 required");
   MSI_REQUIRE(theta > 0.f && max_pages > 0, "qkv_rope_append: bad theta / max_pages");
+  const RopeInv rope = rope_inv_table(theta);
   if (rows == 0) return 0;
   GemmLaunch g = dense_launch(x, rows, wqkv, n, hidden, tile_ctr);
   g.p.mode = 2;
   g.p.pos = pos;
-  g.p.theta = theta;
+  g.p.rope = rope;
   g.p.block_table = block_table;
   g.p.max_pages = max_pages;
   g.p.n_heads = n_heads;

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include "../../include/msinfer.h"
+#include "common.cuh"
 
 #define MSI_MAX_LOCAL_EXPERTS 256  /* DeepSeek-V3 shape on one GPU */
 #define MSI_SMALL_LOCAL_EXPERTS 64 /* GEMM variant with the deeper pipeline */
@@ -33,7 +34,8 @@ struct GemmParams {
   unsigned long long* trace;  // optional %globaltimer stamps: [slot] start,
   int trace_slot;             //   [slot+1] rows arrived, [slot+2] release
   // epilogue
-  int mode;                 // 0: SwiGLU -> out[row][out_ld]; 1: plain bf16 rows; 2: QKV + RoPE/append
+  int mode;                 // 0: SwiGLU -> out[row][out_ld]; 1: plain bf16 rows; 2: QKV + RoPE/append;
+                            // 3: plain rows to peer_out (attention-TP reduce-scatter)
   __nv_bfloat16* out;       // mode 0: hbuf; mode 1: y (n_src > 0: the receive
                             //   regions themselves -- Y of a row replaces its X,
                             //   which the attention GPU's combine pulls)
@@ -64,10 +66,19 @@ struct GemmParams {
   const int32_t* pos;          // mode 2: position of row t's new token
   const int32_t* block_table;  // mode 2: [rows][max_pages]
   int max_pages, n_heads, n_kv;
-  float theta;
+  RopeInv rope;                // mode 2: theta^(-2i/128) (rope_inv_table)
   __nv_bfloat16* q_out;        // [rows][n_heads][128]
   __nv_bfloat16* k_cache;      // [pages][n_kv][64][128]
   __nv_bfloat16* v_cache;
+  // attention TP (msi_tp_qkv / msi_tp_oproj): a_shards > 0 -> "expert" e is
+  // node peer e's token shard of shard_rows rows, loaded from its own tensor
+  // map (am.m[e], the peer's symmetric buffer) at the shard's rows; every
+  // shard uses the same B (shared weights); output row = e * shard_rows + r.
+  // mode 3: output row t goes to peer_out[t / shard_rows] at row
+  // t % shard_rows (the O projection's reduce-scatter over NVLink).
+  int a_shards;
+  int shard_rows;
+  __nv_bfloat16* peer_out[MSI_MAX_RANKS];
 };
 
 struct GemmLaunch {
@@ -76,6 +87,7 @@ struct GemmLaunch {
   const void* b;   // [E_l * n_total][kdim] bf16
   int grid;        // 0 = one CTA per SM
   int cta_group;   // 1: 128x256 tiles per CTA; 2: 256x256 tiles per CTA pair; 0 = default
+  const void* a_shard[MSI_MAX_RANKS];  // p.a_shards > 0: shard e's A ([a_rows][kdim] each)
   GemmParams p;
 };
 

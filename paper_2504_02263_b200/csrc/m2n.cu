@@ -46,6 +46,7 @@
 #include "common.cuh"
 #include "gemm.h"
 #include "route.h"
+#include "tp.h"
 
 namespace msi {
 
@@ -114,9 +115,12 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 inline int plan_tp(const msi_plan& p) { return p.tp_e > 1 ? p.tp_e : 1; }
 inline int plan_nodes(const msi_plan& p) { return p.n_e / plan_tp(p); }
 inline int plan_el(const msi_plan& p) { return p.experts / plan_nodes(p); }
+inline int plan_tpa(const msi_plan& p) { return p.tp_a > 1 ? p.tp_a : 1; }
 
 struct Layout {
   size_t arrive, comb, dticket, fticket, ause, euse, status, stats, trace, cntab, ctrl_bytes;
+  size_t tpready, tprs, tpuse, tpticket;  // attention TP counters (per slot lines)
+  size_t tpx, tpx_slot, tprsb, tprsb_slot;  // attention TP: shard [cap][H], partials [tp][cap][H] per slot
   size_t recv, recv_slot;
   size_t total;
   int64_t cap;       // hbuf rows (compact, 128-aligned segments)
@@ -137,8 +141,18 @@ Layout make_layout(const msi_plan& p, bool attn, bool expert) {
   L.stats = off; off += line;
   L.trace = off; off += 2 * line;  // 32 x u64 %globaltimer stamps
   L.cntab = off; off += (size_t)p.slots * p.n_a * p.experts * 8;
+  L.tpready = off; off += p.slots * line;
+  L.tprs = off; off += p.slots * line;
+  L.tpuse = off; off += p.slots * line;
+  L.tpticket = off; off += p.slots * line;
   L.ctrl_bytes = align_up(off, ALIGN);
   off = L.ctrl_bytes;
+  if (attn && plan_tpa(p) > 1) {  // before the expert buffers: same offsets on every attention GPU
+    L.tpx_slot = (size_t)p.max_tokens * p.hidden * 2;
+    L.tpx = off; off += align_up(L.tpx_slot * p.slots, ALIGN);
+    L.tprsb_slot = (size_t)plan_tpa(p) * L.tpx_slot;
+    L.tprsb = off; off += align_up(L.tprsb_slot * p.slots, ALIGN);
+  }
   const int E_l = plan_el(p);  // experts per expert node (tp_e GPUs share them)
   const int per_tok = p.topk < E_l ? p.topk : E_l;
   int64_t cap = (int64_t)p.n_a * p.max_tokens * per_tok + (int64_t)E_l * (MSI_ROW_ALIGN - 1);
@@ -167,6 +181,13 @@ struct DevCtx {
   uint32_t *my_arrive, *my_comb, *my_dticket, *my_fticket, *my_ause, *my_euse;
   int32_t* my_status;
   unsigned long long* trace;  // null = tracing off
+  // attention TP (plan.tp_a > 1): this GPU's node peers j = 0..tp_a-1
+  int tp_a, my_ta;
+  char* tpx_of[MSI_MAX_RANKS];        // peer j's shard buffers (slot 0)
+  char* tprsb_of[MSI_MAX_RANKS];      // peer j's partial buffers (slot 0)
+  uint32_t* tpready_of[MSI_MAX_RANKS];
+  uint32_t* tprs_of[MSI_MAX_RANKS];
+  uint32_t *my_tpready, *my_tprs, *my_tpuse, *my_tpticket;
 };
 
 }  // namespace
@@ -207,6 +228,7 @@ int validate(const msi_plan& p) {
   MSI_REQUIRE(p.world >= 1 && p.world <= MSI_MAX_RANKS, "plan: world must be in [1, %d]", MSI_MAX_RANKS);
   MSI_REQUIRE(p.n_a >= 1 && p.n_a <= p.world && p.n_e >= 1 && p.n_e <= p.world, "plan: bad n_a/n_e");
   MSI_REQUIRE(p.tp_e >= 0 && p.tp_e <= p.n_e && p.n_e % plan_tp(p) == 0, "plan: tp_e must divide n_e");
+  MSI_REQUIRE(p.tp_a >= 0 && p.tp_a <= MSI_MAX_RANKS && p.n_a % plan_tpa(p) == 0, "plan: tp_a must divide n_a");
   MSI_REQUIRE(p.experts >= 1 && p.experts % plan_nodes(p) == 0, "plan: experts must divide over the expert nodes");
   MSI_REQUIRE(plan_el(p) <= MSI_MAX_LOCAL_EXPERTS, "plan: at most %d experts per GPU", MSI_MAX_LOCAL_EXPERTS);
   MSI_REQUIRE(p.inter % (128 * plan_tp(p)) == 0, "plan: inter must split into tp_e multiples of 128");
@@ -598,6 +620,23 @@ extern "C" int msi_ctx_finalize(msi_ctx* c) {
   d.my_euse = reinterpret_cast<uint32_t*>(c->heap + M.euse);
   d.my_status = reinterpret_cast<int32_t*>(c->heap + M.status);
   d.trace = nullptr;
+  d.tp_a = plan_tpa(p);
+  d.my_tpready = reinterpret_cast<uint32_t*>(c->heap + M.tpready);
+  d.my_tprs = reinterpret_cast<uint32_t*>(c->heap + M.tprs);
+  d.my_tpuse = reinterpret_cast<uint32_t*>(c->heap + M.tpuse);
+  d.my_tpticket = reinterpret_cast<uint32_t*>(c->heap + M.tpticket);
+  if (c->attn && d.tp_a > 1) {
+    const int node0 = c->my_a / d.tp_a * d.tp_a;
+    d.my_ta = c->my_a - node0;
+    for (int j = 0; j < d.tp_a; ++j) {
+      const int r = p.attn_ranks[node0 + j];
+      Layout L = make_layout(p, true, role_expert(p, r));
+      d.tpx_of[j] = c->peer[r] + L.tpx;
+      d.tprsb_of[j] = c->peer[r] + L.tprsb;
+      d.tpready_of[j] = reinterpret_cast<uint32_t*>(c->peer[r] + L.tpready);
+      d.tprs_of[j] = reinterpret_cast<uint32_t*>(c->peer[r] + L.tprs);
+    }
+  }
   MSI_CUDA(cudaMemset(c->heap, 0, M.ctrl_bytes));
   MSI_CUDA(cudaDeviceSynchronize());
   c->finalized = true;
@@ -623,6 +662,9 @@ extern "C" int msi_ctx_buffer(msi_ctx* c, int which, int slot, void** ptr, size_
     case MSI_BUF_HBUF:
       if (!c->expert) break;
       *ptr = c->hbuf; *bytes = (size_t)L.cap * c->plan.inter * 2; return 0;
+    case MSI_BUF_TP_X:
+      if (!c->attn || plan_tpa(c->plan) < 2) break;
+      *ptr = c->heap + L.tpx + slot * L.tpx_slot; *bytes = L.tpx_slot; return 0;
     case MSI_BUF_CNTAB: {
       const size_t per = (size_t)c->plan.n_a * c->plan.experts * 8;
       *ptr = c->heap + L.cntab + slot * per; *bytes = per; return 0;
@@ -882,4 +924,115 @@ extern "C" int msi_combine_local(const void* y, const float* w, const void* resi
   src.tp = 1;
   return launch_combine(src, w, resid, out, nullptr, T, K, H, nullptr, 0, 0, nullptr, 0, nullptr, nullptr,
                         reinterpret_cast<cudaStream_t>(stream));
+}
+
+// ------------------------------------------------- attention-node TP ----
+static int tp_check(msi_ctx* c, const char* fn, int T, int mb_slot) {
+  if (!c || !c->finalized) { set_error("%s: context not finalized", fn); return MSI_ESTATE; }
+  if (!c->attn || c->dev.tp_a < 2) { set_error("%s: rank %d is not in an attention TP node", fn, c->rank); return MSI_EINVAL; }
+  MSI_REQUIRE(T >= 1 && T <= c->plan.max_tokens, "%s: T=%d outside [1, max_tokens=%d]", fn, T, c->plan.max_tokens);
+  MSI_REQUIRE(mb_slot >= 0 && mb_slot < c->plan.slots, "%s: bad slot", fn);
+  return 0;
+}
+
+extern "C" int msi_tp_publish(msi_ctx* c, const void* x, int T, int mb_slot, uint32_t epoch, void* stream) {
+  if (int rc = tp_check(c, "msi_tp_publish", T, mb_slot)) return rc;
+  (void)epoch;  // every use publishes once: the cumulative ready counter is the epoch
+  const DevCtx& d = c->dev;
+  const Layout& L = c->my_layout;
+  TpSignal sig{};
+  sig.ticket = d.my_tpticket + mb_slot * CTR_STRIDE;
+  for (int j = 0; j < d.tp_a; ++j) sig.ctr[j] = d.tpready_of[j] + mb_slot * CTR_STRIDE;
+  sig.n = d.tp_a;
+  char* xin = c->heap + L.tpx + mb_slot * L.tpx_slot;
+  return tp_publish(x ? x : xin, xin, T, c->plan.hidden, sig, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int msi_tp_qkv(msi_ctx* c, const void* wqkv_l, int n_heads_l, int n_kv_l, const int32_t* pos, float theta,
+                          const int32_t* block_table, int max_pages, void* k_cache, void* v_cache, void* q_out, int T,
+                          int mb_slot, uint32_t epoch, void* stream) {
+  if (int rc = tp_check(c, "msi_tp_qkv", T, mb_slot)) return rc;
+  MSI_REQUIRE(wqkv_l && pos && block_table && k_cache && v_cache && q_out, "msi_tp_qkv: null pointer");
+  MSI_REQUIRE(n_kv_l > 0 && n_heads_l > 0 && n_heads_l % n_kv_l == 0, "msi_tp_qkv: bad head counts");
+  const int n = (n_heads_l + 2 * n_kv_l) * MSI_HEAD_DIM;
+  MSI_REQUIRE(n % 256 == 0, "msi_tp_qkv: n_heads_l + 2 n_kv_l must be even");
+  MSI_REQUIRE(theta > 0.f && max_pages > 0, "msi_tp_qkv: bad theta / max_pages");
+  const DevCtx& d = c->dev;
+  const Layout& L = c->my_layout;
+  GemmLaunch g{};
+  g.p.a_shards = d.tp_a;
+  g.p.E_l = d.tp_a;
+  g.p.shard_rows = T;
+  for (int j = 0; j < d.tp_a; ++j) g.a_shard[j] = d.tpx_of[j] + mb_slot * L.tpx_slot;
+  g.a = g.a_shard[0];
+  g.a_rows = T;
+  g.b = wqkv_l;
+  g.p.n_total = n;
+  g.p.nt = n / 256;
+  g.p.kdim = c->plan.hidden;
+  g.p.mode = 2;
+  g.p.pos = pos;
+  g.p.rope = rope_inv_table(theta);
+  g.p.block_table = block_table;
+  g.p.max_pages = max_pages;
+  g.p.n_heads = n_heads_l;
+  g.p.n_kv = n_kv_l;
+  g.p.q_out = reinterpret_cast<__nv_bfloat16*>(q_out);
+  g.p.k_cache = reinterpret_cast<__nv_bfloat16*>(k_cache);
+  g.p.v_cache = reinterpret_cast<__nv_bfloat16*>(v_cache);
+  g.p.wait_ctr = d.my_tpready + mb_slot * CTR_STRIDE;  // every node peer's shard published
+  g.p.wait_mul = (uint32_t)d.tp_a;
+  g.p.epoch = epoch;
+  g.p.epoch_src = d.my_tpuse + mb_slot * CTR_STRIDE;
+  g.p.timeout_ns = c->timeout_ns;
+  g.p.status = d.my_status;
+  g.p.tile_ctr = d.my_tpticket + mb_slot * CTR_STRIDE + 1;
+  return grouped_gemm_launch(g, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int msi_tp_oproj(msi_ctx* c, const void* o, const void* wo_l, int k_l, int T, int mb_slot, uint32_t epoch,
+                            void* stream) {
+  if (int rc = tp_check(c, "msi_tp_oproj", T, mb_slot)) return rc;
+  MSI_REQUIRE(o && wo_l && k_l > 0 && k_l % 64 == 0, "msi_tp_oproj: bad arguments");
+  const DevCtx& d = c->dev;
+  const Layout& L = c->my_layout;
+  GemmLaunch g{};
+  g.a = o;
+  g.a_rows = (int64_t)d.tp_a * T;
+  g.b = wo_l;
+  g.p.E_l = 1;
+  g.p.dense_rows = (long long)d.tp_a * T;
+  g.p.n_total = c->plan.hidden;
+  g.p.nt = c->plan.hidden / 256;
+  g.p.kdim = k_l;
+  g.p.mode = 3;
+  g.p.shard_rows = T;
+  g.p.out_ld = c->plan.hidden;
+  for (int j = 0; j < d.tp_a; ++j)  // this GPU's partial slot in peer j's buffer
+    g.p.peer_out[j] = reinterpret_cast<__nv_bfloat16*>(d.tprsb_of[j] + mb_slot * L.tprsb_slot + d.my_ta * L.tpx_slot);
+  g.p.epoch = epoch;
+  g.p.epoch_src = d.my_tpuse + mb_slot * CTR_STRIDE;
+  g.p.status = d.my_status;
+  g.p.tile_ctr = d.my_tpticket + mb_slot * CTR_STRIDE + 2;
+  g.p.ticket = d.my_tpticket + mb_slot * CTR_STRIDE + 3;
+  for (int j = 0; j < d.tp_a; ++j) g.p.sig[j] = d.tprs_of[j] + mb_slot * CTR_STRIDE;
+  g.p.n_sig = d.tp_a;
+  return grouped_gemm_launch(g, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int msi_tp_reduce(msi_ctx* c, const void* resid, void* out, int T, int mb_slot, uint32_t epoch,
+                             void* stream) {
+  if (int rc = tp_check(c, "msi_tp_reduce", T, mb_slot)) return rc;
+  MSI_REQUIRE(resid && out, "msi_tp_reduce: null pointer");
+  const DevCtx& d = c->dev;
+  const Layout& L = c->my_layout;
+  TpWait wt{};
+  wt.ctr = d.my_tprs + mb_slot * CTR_STRIDE;
+  wt.use = d.my_tpuse + mb_slot * CTR_STRIDE;
+  wt.use_store = d.my_tpuse + mb_slot * CTR_STRIDE;
+  wt.epoch = epoch;
+  wt.timeout_ns = c->timeout_ns;
+  wt.status = d.my_status;
+  return tp_reduce(resid, out, c->heap + L.tprsb + mb_slot * L.tprsb_slot, (long long)c->plan.max_tokens * c->plan.hidden,
+                   d.tp_a, T, c->plan.hidden, wt, reinterpret_cast<cudaStream_t>(stream));
 }

@@ -221,36 +221,51 @@ def search(model: MoeModelSpec, gpu_a: GpuSpec, gpu_e: GpuSpec, cm: PM.CostModel
     return best if best is not None else NoPlan(reasons)
 
 
+def _head_layout(model) -> tuple[int, int]:
+    """(n_heads, n_kv) as the attention stage lays them out (attention.head_layout)."""
+    n_heads = max(1, model.hidden // 128)
+    g = max(1, min(int(getattr(model, "gqa_group", 8)), n_heads, 16))
+    while n_heads % g:
+        g -= 1
+    return n_heads, n_heads // g
+
+
 def search_box(model: MoeModelSpec, gpu: GpuSpec, cm_for, workload: WorkloadSpec, n_gpus: int = 8,
                max_microbatches: int = 4, balance_slack: float = 0.25, swiglu: bool = True,
-               explain: list | None = None, tp_choices=(1, 2, 4)) -> Plan | NoPlan:
+               explain: list | None = None, tp_choices=(1, 2, 4), tp_a_choices=(1, 2, 4)) -> Plan | NoPlan:
     """One B200 box: n_a attention GPUs + n_e expert nodes of tp_e GPUs
     (n_a + n_e tp_e = n_gpus, E divisible by n_e) with m in {2..N_m}, or all
     GPUs co-located (m = 1, merged batch).  ``cm_for(E_l)`` returns the cost
     model calibrated for E_l local experts per expert GPU (the expert
     intercept is the weight stream of those E_l experts); with expert TP each
     GPU streams E_l / tp_e experts' weights and does 1 / tp_e of the per-row
-    work.  The returned Plan's n_e counts expert nodes (GPUs = n_e tp_e)."""
+    work.  The returned Plan's n_e counts expert nodes (GPUs = n_e tp_e) and
+    its n_a attention nodes of tp_a GPUs (heads split; the attention slope
+    k1 divides by tp_a -- the all-gather / reduce-scatter ride on NVLink
+    inside the projection GEMMs, attn_tp.cu)."""
     best, reasons = None, []
     E = model.experts
-    cands = [(n_gpus - nodes * tp, nodes, tp, False) for tp in tp_choices for nodes in range(1, n_gpus)
-             if 0 < nodes * tp < n_gpus and E % nodes == 0 and model.intermediate % (128 * tp) == 0]
+    _, n_kv = _head_layout(model)
+    cands = [((n_gpus - nodes * tp) // tpa, nodes, tp, tpa, False)
+             for tp in tp_choices for tpa in tp_a_choices for nodes in range(1, n_gpus)
+             if 0 < nodes * tp < n_gpus and (n_gpus - nodes * tp) % tpa == 0 and n_kv % tpa == 0
+             and E % nodes == 0 and model.intermediate % (128 * tp) == 0]
     if E % n_gpus == 0:
-        cands.append((n_gpus, n_gpus, 1, True))
-    for n_a, n_e, tp, colo in cands:
+        cands.append((n_gpus, n_gpus, 1, 1, True))
+    for n_a, n_e, tp, tpa, colo in cands:
         E_l = E // n_e
         cm = cm_for(E_l / tp)
-        cm = PM.CostModel(k1=cm.k1, k2=cm.k2, k3=cm.k3 / tp, k4=cm.k4, util_curve=cm.util_curve,
+        cm = PM.CostModel(k1=cm.k1 / tpa, k2=cm.k2, k3=cm.k3 / tp, k4=cm.k4, util_curve=cm.util_curve,
                           comm_backend=cm.comm_backend)
         for m in ([1] if colo else range(2, max_microbatches + 1)):
-            p, r = max_batch_under_slo(model, gpu, gpu, cm, workload, 1, tp, n_a, n_e, m,
+            p, r = max_batch_under_slo(model, gpu, gpu, cm, workload, tpa, tp, n_a, n_e, m,
                                        balance_slack=balance_slack, colocated=colo, swiglu=swiglu,
                                        expert_nodes_hold=E_l)
             if explain is not None:
-                explain.append({"n_a": n_a, "n_e": n_e, "tp_e": tp, "colocated": colo, "m": m,
+                explain.append({"n_a": n_a, "tp_a": tpa, "n_e": n_e, "tp_e": tp, "colocated": colo, "m": m,
                                 "tpuc": p.tpuc if p else None, "B": p.B if p else None, "reason": r})
             if p is None:
-                reasons.append(((n_a, n_e, tp, m), r))
+                reasons.append(((n_a, tpa, n_e, tp, m), r))
             elif _better(p, best):
                 best = p
     return best if best is not None else NoPlan(reasons)
@@ -279,7 +294,9 @@ def to_deployment(p: Plan, b_a: int | None = None):
     ba = int(b_a if b_a is not None else max(1, round(p.b_a)))
     if p.colocated:
         return DeploymentPlan(n_a=p.n_a, n_e=p.n_a, m=p.m, b_a=ba, colocated=True)
-    return DeploymentPlan(n_a=p.n_a, n_e=p.n_e * p.tp_e, m=p.m, b_a=ba, tp_e=p.tp_e)
+    if b_a is None:  # the plan's b_a is per attention node: each of its tp_a GPUs holds a shard
+        ba = max(1, round(p.b_a / p.tp_a))
+    return DeploymentPlan(n_a=p.n_a * p.tp_a, n_e=p.n_e * p.tp_e, m=p.m, b_a=ba, tp_e=p.tp_e, tp_a=p.tp_a)
 
 
 def main(argv=None) -> int:

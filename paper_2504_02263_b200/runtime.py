@@ -63,6 +63,7 @@ def make_plan_struct(model: MoeModelSpec, plan: DeploymentPlan, slots=None) -> _
     p.experts, p.topk = (model.experts if slots is None else slots.P), model.topk
     p.max_tokens, p.slots = plan.b_a, plan.m
     p.tp_e = plan.tp_e
+    p.tp_a = plan.tp_a
     return p
 
 

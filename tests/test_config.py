@@ -123,8 +123,11 @@ def test_plan_expert_tp_validation():
         C.DeploymentPlan(n_a=2, n_e=3, tp_e=2)
     with pytest.raises(C.ConfigError, match="expert TP"):
         C.DeploymentPlan(n_a=2, n_e=2, tp_e=2, colocated=True)
+    assert C.DeploymentPlan(n_a=2, n_e=2, tp_a=2).tp_a == 2  # attention node of 2 GPUs
     with pytest.raises(C.ConfigError, match="tp_a"):
-        C.DeploymentPlan(n_a=2, n_e=2, tp_a=2)
+        C.DeploymentPlan(n_a=3, n_e=2, tp_a=2)
+    with pytest.raises(C.ConfigError, match="tp_a"):
+        C.DeploymentPlan(n_a=2, n_e=2, tp_a=0)
     with pytest.raises(C.ConfigError, match="divide evenly"):
         C.DeploymentPlan(n_a=1, n_e=6, tp_e=2).check_model(m)  # 3 nodes for 8 experts
     tiny = C.as_model_spec("tiny")  # h' = 1536 = 12 x 128: tp 4 -> 384 = 3 x 128
