@@ -1,30 +1,38 @@
-// expert_gemm.cu -- expert FFN as two grouped GEMMs on tcgen05 / TMEM / TMA.
+// expert_gemm.cu -- expert FFN as two grouped GEMMs on tcgen05 / TMEM / TMA,
+// and the attention stage's dense projections on the same kernel.
 //
 // PAPER.md:285-286 (FFN Input (b_e,h)x(h,h'), FFN Output (b_e,h')x(h',h)),
-// SwiGLU per BASELINE north_star.  Rows of local expert e are a contiguous
-// segment of the receive buffer starting at a 128-row aligned seg_start[e]
-// (written there by the dispatch kernel), so every 128-row M tile belongs to
-// exactly one expert.
+// SwiGLU per BASELINE north_star.  Rows of local expert e are one compact
+// segment starting at a 128-row aligned seg_start[e] (several senders'
+// receive regions are gathered there first, gather_regions_kernel), so every
+// 128-row M tile belongs to exactly one expert.
 //
 //   GEMM1  A = X [rows][H], B = W13[e] [2H'][H] (gate/up interleaved in
-//          128-row blocks)  ->  epilogue H = bf16(silu(G) * U) into hbuf
+//          64-row blocks, msi_pack_w13)  ->  epilogue H = bf16(silu(G) * U)
 //   GEMM2  A = hbuf [rows][H'], B = W2[e] [H][H']  ->  epilogue stores every
 //          Y row over its own X in the receive region (local HBM); the last
 //          CTA releases the attention GPUs' arrival counters, whose combine
 //          pulls the rows over NVLink (N2M leg).
+//   dense  (E_l = 1) the attention projections: QKV with RoPE + paged-KV
+//          append in the epilogue (mode 2), O projection + residual (mode 1),
+//          attention-TP all-gather (per-shard A maps over NVLink) and
+//          reduce-scatter (mode 3, peer stores).
 //
-// Kernel shape: persistent, one CTA per SM, 256 threads, warp-specialized:
-//   warp 0  TMA producer (1 thread): A 128x64 + B 256x64 bf16 per stage,
-//           128B swizzle, 4-stage mbarrier ring (48 KB / stage)
-//   warp 1  MMA issuer (1 thread): tcgen05.mma.cta_group::1.kind::f16
-//           M=128 N=256 K=16, fp32 accumulators in TMEM, 2 accumulator
-//           buffers (512 TMEM columns) so the epilogue of tile i overlaps the
-//           MMAs of tile i+1
+// Kernel shape: persistent, one CTA (CG=1) or CTA pair (CG=2, the default:
+// tcgen05.mma.cta_group::2, 256x256 tiles, half pairs for odd 128-row
+// tails) per SM (pair), 256 threads, warp-specialized:
+//   warp 0  TMA producer: A 128x64 + B (256/CG)x64 bf16 per stage, 128B
+//           swizzle, 6-stage (CG=2) / 4-stage (CG=1) mbarrier ring
+//   warp 1  MMA issuer (one thread of the leader CTA): kind::f16 M=128/256
+//           N=256 K=16, fp32 accumulators in TMEM, 2 accumulator buffers
+//           (512 TMEM columns) so the epilogue of tile i overlaps the MMAs of
+//           tile i+1
 //   warp 2  TMEM allocator
 //   warps 4-7 epilogue: tcgen05.ld 32x32b -> registers -> swizzled smem
 //           staging -> coalesced 256 B row stores (local or NVLink peer)
-// Tile order: expert-major, then N tile, then M tile (fastest), so CTAs that
-// run concurrently share one expert's B tiles and its A rows stay in L2.
+// Tiles are taken in order (expert-major, then N tile, then M tile) from a
+// dynamic scheduler, so CTAs that run together share one expert's B tiles
+// in L2.
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>

@@ -9,7 +9,7 @@
 set -u
 mkdir -p gpurun_out
 ARGS="--steps ${STEPS:-10} --warmup ${WARMUP:-3}"
-timeout 600 python bench.py $ARGS > gpurun_out/bench_n1.log 2>&1 || { echo "bench failed"; tail -20 gpurun_out/bench_n1.log; exit 1; }
+timeout 600 python bench.py $ARGS --timeline-csv gpurun_out/timeline_n1_r{rank}.csv > gpurun_out/bench_n1.log 2>&1 || { echo "bench failed"; tail -20 gpurun_out/bench_n1.log; exit 1; }
 grep '^{' gpurun_out/bench_n1.log | tail -1 > gpurun_out/bench_n1.json
 NCU=/usr/local/cuda/bin/ncu
 SMALL="--steps 1 --warmup 3 --no-e2e --no-cpu --no-graph --no-m2n"
@@ -19,4 +19,6 @@ timeout 1200 $NCU --set full --clock-control none --import-source on -k regex:gr
     -o gpurun_out/full_gemm -f python bench.py $SMALL > gpurun_out/ncu_gemm.log 2>&1 || echo "gemm capture failed"
 timeout 900 $NCU --set full --clock-control none --import-source on -k regex:decode_attn -s 12 -c 1 \
     -o gpurun_out/full_attn -f python bench.py $SMALL > gpurun_out/ncu_attn.log 2>&1 || echo "attn capture failed"
+python scripts/summarize_launches.py gpurun_out/launches_n1.csv 4 "N=1 launch list" > gpurun_out/launches_n1_summary.txt 2>&1
+cat gpurun_out/launches_n1_summary.txt
 ls -la gpurun_out/
