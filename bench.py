@@ -584,6 +584,17 @@ def resolve_layout(args, world: int):
     return n_a, n_e, colo, plan_source, (1 if colo else tp_e), model, m_eff, b_a
 
 
+def router_launch_count(E: int, T: int) -> int:
+    """Launches of one router (+ dispatch) call (router.cu's path choice):
+    tensor-core logits for E % 256 == 0 at T >= 2048 (expert norms, logits
+    GEMM, route), the split path for E >= 64 at T <= 256 (logits, route),
+    else the fused kernel."""
+    env = os.environ.get("MSI_ROUTER_TC")
+    if E % 256 == 0 and E <= 512 and (env == "1" or (env is None and T >= 2048)):
+        return 3
+    return 2 if (E >= 64 and E % 8 == 0 and T <= 256) else 1
+
+
 def args_tp_a(args) -> int:
     return int(getattr(args, "tp_a", 1) or 1)
 
@@ -1018,7 +1029,7 @@ def measure(args, rank: int, world: int, local: int, layout, full: bool = True, 
     attn_launches = 0
     if att_stages:  # TP node: publish, QKV, attention [+ combine], O projection, reduce
         attn_launches = (5 if tp_a > 1 else 3) + (1 if att_stages[0].ws is not None else 0)
-    router_launches = 2 if (model.experts >= 64 and model.experts % 8 == 0 and args.b_a <= 256) else 1
+    router_launches = router_launch_count(model.experts, args.b_a)
     expert_launches = 3 + (1 if n_a > 1 else 0)
     launches_per_mbl = attn_launches + router_launches + expert_launches + 1
     line = {

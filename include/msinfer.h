@@ -316,6 +316,11 @@ int msi_tp_reduce(msi_ctx* ctx, const void* resid, void* out, int T, int mb_slot
 int msi_dense_gemm(const void* a, int64_t T, const void* b, int N, int K,
                    void* out, int64_t out_ld, const void* resid, int64_t resid_ld,
                    uint32_t* tile_ctr, void* stream);
+/* fp32 out[t][e] = x[t] . wg[e] on the tensor cores (the router's candidate
+ * pass for fine-grained MoE; accumulation order of the MMA, not the pinned
+ * one): E % 256 == 0, H % 64 == 0. */
+int msi_dense_logits(const void* x, int64_t T, const void* wg, int E, int H, float* out,
+                     uint32_t* tile_ctr, void* stream);
 /* QKV projection with RoPE and the paged-KV append in the GEMM epilogue:
  * qkv = bf16(x . wqkv^T) (wqkv bf16 [(n_heads + 2 n_kv) 128][hidden]), then
  * exactly what msi_rope_append does with that qkv -- q heads rotated into

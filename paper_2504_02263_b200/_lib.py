@@ -84,6 +84,7 @@ SIGNATURES = {
     "msi_tp_qkv": (_I, [_P, _P, _I, _I, _P, ctypes.c_float, _P, _I, _P, _P, _P, _I, _I, _U32, _P]),
     "msi_tp_oproj": (_I, [_P, _P, _P, _I, _I, _I, _U32, _P]),
     "msi_tp_reduce": (_I, [_P, _P, _P, _I, _I, _U32, _P]),
+    "msi_dense_logits": (_I, [_P, ctypes.c_int64, _P, _I, _I, _P, _P, _P]),
     "msi_dense_gemm": (_I, [_P, ctypes.c_int64, _P, _I, _I, _P, ctypes.c_int64, _P, ctypes.c_int64, _P, _P]),
     "msi_qkv_rope_append": (_I, [_P, ctypes.c_int64, _I, _P, _I, _I, _P, ctypes.c_float, _P, _I, _P, _P, _P,
                                  _P, _P]),

@@ -589,6 +589,19 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
                 float h1 = g1 / (1.0f + __expf(-g1)) * u1;
                 packed[j] = pack_bf16x2(h0, h1);
               }
+            } else if (p.mode == 4) {
+              // fp32 rows (router logits): the lane's 32 consecutive columns
+              // straight from registers, 128 B per lane and chunk
+              uint32_t v[32];
+              tmem_ld32(tbase + sgi * 128 + c * 32, v);
+              tmem_wait_ld();
+              if (row_local < seg.total[e]) {
+                uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<float*>(p.out) + (size_t)row_global * p.out_ld +
+                                                      (size_t)n * BN + colofs + sgi * 128 + c * 32);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) dst[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+              }
+              continue;
             } else if (rope) {
               // rotate-half RoPE pairs dims (i, i + 64): chunks c and c + 2
               // together; same arithmetic as rope_append_kernel on the
@@ -655,6 +668,7 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
           }
         }
         __syncwarp();
+        if (p.mode == 4) continue;  // fp32 rows were stored from registers
         if (!narrow) {
           // ---- coalesced row stores: 2 rows per instruction, 256 B per row ----
           const int u = lane & 15;
@@ -1096,6 +1110,19 @@ static GemmLaunch dense_launch(const void* a, int64_t rows, const void* b, int n
   return g;
 }
 
+// fp32 logits = x . wg^T on the tensor cores (the router's candidate pass,
+// router.cu): E % 256 == 0, H % 64 == 0; out [rows][E] fp32.
+int dense_logits_f32(const void* x, int64_t rows, const void* wg, int E, int H, float* out, uint32_t* tile_ctr,
+                     cudaStream_t st) {
+  MSI_REQUIRE(E % BN == 0 && H % BK == 0 && rows >= 0, "dense_logits: E %% 256 and H %% 64 required");
+  if (rows == 0) return 0;
+  GemmLaunch g = dense_launch(x, rows, wg, E, H, tile_ctr);
+  g.p.mode = 4;
+  g.p.out = reinterpret_cast<__nv_bfloat16*>(out);
+  g.p.out_ld = E;
+  return grouped_gemm_launch(g, st);
+}
+
 int dense_gemm(const void* a, int64_t rows, const void* b, int n, int k, void* out, int64_t out_ld,
                const void* resid, int64_t resid_ld, uint32_t* tile_ctr, cudaStream_t st) {
   MSI_REQUIRE(rows >= 0 && rows < (1ll << 31), "dense_gemm: rows out of range");
@@ -1148,6 +1175,12 @@ extern "C" int msi_grouped_ffn_regions(const void* x_reg, const uint64_t* cntab,
                                        int hidden, int inter, int a_runs, void* xcomp, void* stream) {
   return msi::grouped_ffn_regions(x_reg, cntab, n_src, cap_s, E_l, w13, w2, hbuf, hbuf_rows, y_reg, hidden, inter,
                                   a_runs, xcomp, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int msi_dense_logits(const void* x, int64_t T, const void* wg, int E, int H, float* out, uint32_t* tile_ctr,
+                                void* stream) {
+  MSI_REQUIRE(T == 0 || (x && wg && out && tile_ctr), "msi_dense_logits: null pointer");
+  return msi::dense_logits_f32(x, T, wg, E, H, out, tile_ctr, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" int msi_dense_gemm(const void* a, int64_t rows, const void* b, int n, int k, void* out, int64_t out_ld,

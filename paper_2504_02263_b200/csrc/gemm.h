@@ -35,7 +35,8 @@ struct GemmParams {
   int trace_slot;             //   [slot+1] rows arrived, [slot+2] release
   // epilogue
   int mode;                 // 0: SwiGLU -> out[row][out_ld]; 1: plain bf16 rows; 2: QKV + RoPE/append;
-                            // 3: plain rows to peer_out (attention-TP reduce-scatter)
+                            // 3: plain rows to peer_out (attention-TP reduce-scatter);
+                            // 4: fp32 rows (router logits)
   __nv_bfloat16* out;       // mode 0: hbuf; mode 1: y (n_src > 0: the receive
                             //   regions themselves -- Y of a row replaces its X,
                             //   which the attention GPU's combine pulls)
@@ -96,6 +97,8 @@ int num_sms();
 // Rows of the (expert, sender) receive regions -> compact 128-aligned
 // per-expert segments of xc (GEMM1's A when several senders share an
 // expert); wait_ctr != null: first wait for *wait_ctr >= epoch * wait_mul.
+int dense_logits_f32(const void* x, int64_t rows, const void* wg, int E, int H, float* out, uint32_t* tile_ctr,
+                     cudaStream_t st);
 int gather_regions(const void* recv, const uint64_t* cntab, int E, int e0, int n_src, int E_l, long long cap_s,
                    int H, void* xc, const uint32_t* wait_ctr, uint32_t epoch, const uint32_t* epoch_src,
                    uint32_t wait_mul, uint64_t timeout_ns, int32_t* status, cudaStream_t st);

@@ -27,6 +27,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "gemm.h"
 #include "route.h"
 
 namespace msi {
@@ -435,10 +436,158 @@ gate_logits_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __r
   }
 }
 
+// Exact (pinned-order) logits of token row xr against up to 4 experts
+// ex[0..n) -- the per-lane accumulation of tile_logits (elements 256j + 8l + c,
+// j ascending, c = 0..7, fmaf from +0), then the same xor butterfly: the
+// values are bit-identical to the CUDA-core logits kernels'.  Warp-collective.
+__device__ __forceinline__ void exact_logits4(const __nv_bfloat16* __restrict__ xr, const __nv_bfloat16* __restrict__ wg,
+                                              int H, const int (&ex)[4], int n, float (&out)[4]) {
+  const int lane = threadIdx.x & 31;
+  float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  const int nchunk = H >> 8;
+  const __nv_bfloat16* wq[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) wq[q] = wg + (size_t)ex[q < n ? q : 0] * H + 8 * lane;
+  constexpr int U = 4;  // chunks whose loads are all issued before the FMAs (L2 latency)
+  for (int j0 = 0; j0 < nchunk; j0 += U) {
+    uint4 xv4[U], wv4[U][4];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool ok = j0 + u < nchunk;
+      xv4[u] = ok ? __ldg(reinterpret_cast<const uint4*>(xr + 256 * (j0 + u) + 8 * lane)) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        wv4[u][q] = (ok && q < n) ? __ldg(reinterpret_cast<const uint4*>(wq[q] + 256 * (j0 + u))) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (j0 + u >= nchunk) break;
+      const uint4 xa = xv4[u];
+      const float xv[8] = {bf16lo(xa.x), bf16hi(xa.x), bf16lo(xa.y), bf16hi(xa.y),
+                           bf16lo(xa.z), bf16hi(xa.z), bf16lo(xa.w), bf16hi(xa.w)};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 v = wv4[u][q];
+        const float wv[8] = {bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y),
+                             bf16lo(v.z), bf16hi(v.z), bf16lo(v.w), bf16hi(v.w)};
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[q] = __fmaf_rn(xv[c], wv[c], acc[q]);  // q >= n: unused
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    float v = acc[q];
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+    out[q] = (v != v) ? -INFINITY : v;
+  }
+}
+
+// Tensor-core candidate pass (route_tc): s_logit holds logits computed on
+// the tensor cores (fp32 accumulation in the MMA's order).  For every token:
+// |tc - pinned| <= eps_e = c ||x_t|| ||w_e|| (c = 4 H 2^-24, a margin over
+// the worst-case fp32 summation bound of both orders), so with theta = the
+// K-th largest of (tc_e - eps_e) only experts with tc_e + eps_e >= theta can
+// be in the pinned top-K.  Those candidates get their logits recomputed in
+// the pinned order (bit-identical), every other expert -inf; non-finite
+// norms or bounds recompute all E.  Top-K, weights and placement then run
+// unchanged on exact values.
+template <int EPL>  // experts per lane (E <= 32 * EPL)
+__device__ void exactify(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
+                         const float* __restrict__ wnorm, float* s_logit, int t0, int rows, int E, int K, int H) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float cb = 4.0f * (float)H * 5.9604645e-8f * 1.01f;
+  for (int lt = warp; lt < rows; lt += kWarps) {
+    const __nv_bfloat16* xr = x + (size_t)(t0 + lt) * H;
+    float* lg = s_logit + (size_t)lt * E;
+    float ss = 0.0f;
+    for (int i0 = 8 * lane; i0 < H; i0 += 256 * 4) {
+      uint4 v4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        v4[u] = i0 + 256 * u < H ? __ldg(reinterpret_cast<const uint4*>(xr + i0 + 256 * u)) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint4 v = v4[u];
+        const float f[8] = {bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y),
+                            bf16lo(v.z), bf16hi(v.z), bf16lo(v.w), bf16hi(v.w)};
+#pragma unroll
+        for (int c = 0; c < 8; ++c) ss = fmaf(f[c], f[c], ss);
+      }
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    const float xn = sqrtf(ss) * 1.001f;
+    float lo[EPL], hi[EPL];
+    bool finite = isfinite(xn);
+#pragma unroll
+    for (int q = 0; q < EPL; ++q) {
+      const int e = lane + 32 * q;
+      if (e < E) {
+        const float a = lg[e], eps = cb * xn * wnorm[e];
+        lo[q] = a - eps;
+        hi[q] = a + eps;
+        finite &= isfinite(lo[q]) && isfinite(hi[q]);
+      } else {
+        lo[q] = -INFINITY;
+        hi[q] = -INFINITY;
+      }
+    }
+    finite = __all_sync(0xffffffffu, finite);
+    float theta = -INFINITY;
+    if (finite) {  // K-th largest lower bound: K rounds of a warp max (one removal per round)
+      float cur[EPL];
+#pragma unroll
+      for (int q = 0; q < EPL; ++q) cur[q] = lo[q];
+      for (int k = 0; k < K; ++k) {
+        float bv = -INFINITY;
+        int bq = -1;
+#pragma unroll
+        for (int q = 0; q < EPL; ++q)
+          if (cur[q] > bv) { bv = cur[q]; bq = q; }
+        float mv = bv;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) mv = fmaxf(mv, __shfl_xor_sync(0xffffffffu, mv, off));
+        const unsigned own = __ballot_sync(0xffffffffu, bv == mv && bq >= 0);
+        if (lane == __ffs(own) - 1) cur[bq] = -INFINITY;  // remove one instance
+        theta = mv;
+      }
+    }
+    // candidate list, 4 experts per exact pass
+    int ex[4], n = 0;
+#pragma unroll
+    for (int q = 0; q < EPL; ++q) {
+      const bool cand = (lane + 32 * q < E) && (!finite || hi[q] >= theta);
+      unsigned m = __ballot_sync(0xffffffffu, cand);
+      if (!cand && lane + 32 * q < E) lg[lane + 32 * q] = -INFINITY;
+      while (m) {
+        const int bit = __ffs(m) - 1;
+        m &= m - 1;
+        ex[n++] = bit + 32 * q;
+        if (n == 4) {
+          float v[4];
+          exact_logits4(xr, wg, H, ex, 4, v);
+          if (lane < 4) lg[ex[lane]] = v[lane];  // lane 0..3 write their own expert's value
+          n = 0;
+        }
+      }
+    }
+    if (n) {
+      float v[4];
+      exact_logits4(xr, wg, H, ex, n, v);
+      if (lane < n) lg[ex[lane]] = v[lane];
+    }
+    __syncwarp();
+  }
+}
+
+template <int EPL>
 __global__ void __launch_bounds__(kWarps * 32)
 route_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ logits, int T, int E, int K, int BT,
              int32_t* __restrict__ idx_out, float* __restrict__ w_out, int32_t* __restrict__ cnt_out,
-             int32_t* __restrict__ slot_out, int32_t* __restrict__ ws, const Placement pl, const DispatchArgs d) {
+             int32_t* __restrict__ slot_out, int32_t* __restrict__ ws, const Placement pl, const DispatchArgs d,
+             const __nv_bfloat16* __restrict__ wg, const float* __restrict__ wnorm, int H) {
   extern __shared__ __align__(16) float s_logit[];  // [BT][E]
   pdl_trigger();
   pdl_wait();
@@ -449,7 +598,34 @@ route_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ logi
   float4* dst = reinterpret_cast<float4*>(s_logit);
   for (int i = threadIdx.x; i < rows * E / 4; i += blockDim.x) dst[i] = __ldcg(src + i);
   __syncthreads();
+  if (wnorm) {  // tensor-core logits: exact values for the candidates
+    exactify<EPL>(x, wg, wnorm, s_logit, t0, rows, E, K, H);
+    __syncthreads();
+  }
   route_tail(x, s_logit, b, (int)gridDim.x, BT, T, E, K, idx_out, w_out, cnt_out, slot_out, ws, pl, d);
+}
+
+// ||w_e||_2 per expert (rounded up) for the candidate bound of route_tc.
+__global__ void __launch_bounds__(256) wg_norm_kernel(const __nv_bfloat16* __restrict__ wg, int H, float* wnorm) {
+  __shared__ float s[8];
+  const __nv_bfloat16* w = wg + (size_t)blockIdx.x * H;
+  float ss = 0.0f;
+  for (int i = 8 * threadIdx.x; i < H; i += 8 * blockDim.x) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(w + i));
+    const float f[8] = {bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y),
+                        bf16lo(v.z), bf16hi(v.z), bf16lo(v.w), bf16hi(v.w)};
+#pragma unroll
+    for (int c = 0; c < 8; ++c) ss = fmaf(f[c], f[c], ss);
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.0f;
+    for (int i = 0; i < 8; ++i) t += s[i];
+    wnorm[blockIdx.x] = sqrtf(t) * 1.001f;
+  }
 }
 
 // Small warp tiles (TT * TE <= 16) are capped at 128 registers so two CTAs
@@ -546,11 +722,49 @@ int launch_split(const void* x, const void* wg, int T, int H, int E, int K, int 
                     BTL, EB, logits, pl.pfw));
   constexpr int BT = 32;
   const size_t smem = tail_smem_bytes(BT, E, pl.P);
-  if (int arc = smem_attr(reinterpret_cast<const void*>(route_kernel), smem)) return arc;
-  MSI_CUDA(launch_k(route_kernel, dim3((T + BT - 1) / BT), dim3(kWarps * 32), smem, st,
+  if (int arc = smem_attr(reinterpret_cast<const void*>(route_kernel<1>), smem)) return arc;
+  MSI_CUDA(launch_k(route_kernel<1>, dim3((T + BT - 1) / BT), dim3(kWarps * 32), smem, st,
                     reinterpret_cast<const __nv_bfloat16*>(x), (const float*)logits, T, E, K, BT, idx, w, cnt, slot,
-                    reinterpret_cast<int32_t*>(ws), pl, d));
+                    reinterpret_cast<int32_t*>(ws), pl, d, (const __nv_bfloat16*)nullptr, (const float*)nullptr, H));
   return check_launch("gate_logits_kernel + route_kernel");
+}
+
+// Tensor-core router for fine-grained MoE (E % 256 == 0, E <= 512): fp32
+// logits on tcgen05 (dense_logits_f32, ~15 us for 4096 x 7168 x 256), then
+// route_kernel recomputes only the candidate experts of every token in the
+// pinned order (exactify) -- routing stays bit-exact with the oracle.
+size_t tc_norm_offset(int T, int P, int E) {
+  return split_logits_offset(T, P) + (((size_t)T * E * sizeof(float) + 255) & ~size_t(255));
+}
+
+int route_tc(const void* x, const void* wg, int T, int H, int E, int K, int32_t* idx, float* w, int32_t* cnt,
+             int32_t* slot, void* ws, const Placement& pl, const DispatchArgs& d, cudaStream_t st) {
+  char* wsb = reinterpret_cast<char*>(ws);
+  float* logits = reinterpret_cast<float*>(wsb + split_logits_offset(T, pl.P));
+  float* wnorm = reinterpret_cast<float*>(wsb + tc_norm_offset(T, pl.P, E));
+  MSI_CUDA(launch_k(wg_norm_kernel, dim3(E), dim3(256), 0, st, reinterpret_cast<const __nv_bfloat16*>(wg), H, wnorm));
+  if (int rc = check_launch("wg_norm_kernel")) return rc;
+  // ws word 4: the GEMM's tile counter (0 at rest; the launch's last fetch resets it)
+  if (int rc = dense_logits_f32(x, T, wg, E, H, logits, reinterpret_cast<uint32_t*>(wsb) + 4, st)) return rc;
+  int BT = 16;  // tokens per CTA (warp per token in the candidate pass)
+  if (const char* ov = getenv("MSI_ROUTER_TC_BT")) BT = atoi(ov) == 32 ? 32 : (atoi(ov) == 8 ? 8 : 16);
+  const size_t smem = tail_smem_bytes(BT, E, pl.P);
+  auto kern = E <= 256 ? route_kernel<8> : route_kernel<16>;
+  if (int arc = smem_attr(reinterpret_cast<const void*>(kern), smem)) return arc;
+  MSI_CUDA(launch_k(kern, dim3((T + BT - 1) / BT), dim3(kWarps * 32), smem, st,
+                    reinterpret_cast<const __nv_bfloat16*>(x), (const float*)logits, T, E, K, BT, idx, w, cnt, slot,
+                    reinterpret_cast<int32_t*>(ws), pl, d, reinterpret_cast<const __nv_bfloat16*>(wg),
+                    (const float*)wnorm, H));
+  return check_launch("route_kernel (tensor-core logits)");
+}
+
+// MSI_ROUTER_TC=1 forces the tensor-core path (when the shape allows), =0
+// disables it; default: on for E % 256 == 0 from T >= 2048 (measured crossover)
+bool tc_enabled(int E, int T, int H) {
+  if (E % 256 || E > 512 || H % 64) return false;
+  const char* ov = getenv("MSI_ROUTER_TC");
+  if (ov) return ov[0] == '1';
+  return T >= 2048;
 }
 
 // Split-path tiles: TT tokens per warp tile (TE = 8 experts), BTL tokens x EB
@@ -614,6 +828,7 @@ int gate_topk(const void* x, const void* wg, int T, int H, int E, int K, int32_t
   }
   // fine-grained MoE at small T: logits on their own 2-D grid, then top-K /
   // placement (route_split)
+  if (tc_enabled(E, T, H)) return route_tc(x, wg, T, H, E, K, idx, w, cnt, slot, ws, pl, d, st);
   if (split_enabled(E, T) && E >= 64 && E % 8 == 0) return route_split(x, wg, T, H, E, K, idx, w, cnt, slot, ws, pl, d, st);
   // One CTA per SM fits (255 registers): BT = the smallest multiple of 4 that
   // covers T in one wave of num_sms() CTAs (<= 32), so no second partial wave
@@ -648,7 +863,8 @@ size_t gate_topk_workspace(int T, int E) {
   // look-back words for the smallest BT (4); split path (E >= 64): + [T][E]
   // fp32 logits (E here is the physical slot count P >= logical E)
   const size_t lb = split_logits_offset(T, E);
-  return E >= 64 ? lb + (size_t)T * E * sizeof(float) : lb;
+  // + the tensor-core path's per-expert norms after the logits
+  return E >= 64 ? tc_norm_offset(T, E, E) + (size_t)E * sizeof(float) : lb;
 }
 
 }  // namespace msi

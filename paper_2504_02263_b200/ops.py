@@ -248,3 +248,14 @@ def grouped_ffn_regions(x_reg: torch.Tensor, counts, cap_s: int, w13: torch.Tens
     _lib.call("msi_grouped_ffn_regions", _ptr(x_reg), _ptr(tab), n_src, cap_s, E_l, _ptr(w13), _ptr(w2),
               _ptr(hbuf), hbuf.shape[0], _ptr(y_reg), H, Hp, int(a_runs), _ptr(xcomp), _stream(stream))
     return y_reg
+
+
+def dense_logits(x: torch.Tensor, wg: torch.Tensor, ctr: TileCounter | None = None, stream=None) -> torch.Tensor:
+    """fp32 x wg^T on the tensor cores (msi_dense_logits; E % 256 == 0)."""
+    _check_bf16("x", x, 2)
+    _check_bf16("wg", wg, 2)
+    out = torch.empty((x.shape[0], wg.shape[0]), dtype=torch.float32, device=x.device)
+    ctr = ctr or TileCounter(1, x.device)
+    _lib.call("msi_dense_logits", _ptr(x), x.shape[0], _ptr(wg), wg.shape[0], wg.shape[1], _ptr(out), ctr[0],
+              _stream(stream))
+    return out

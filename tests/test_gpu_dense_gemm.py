@@ -169,3 +169,21 @@ def test_qkv_rope_append_equals_unfused_gpu_path(lib):
     assert torch.equal(q1.view(torch.int16), q2.view(torch.int16))
     assert torch.equal(k1.view(torch.int16), k2.view(torch.int16))
     assert torch.equal(v1.view(torch.int16), v2.view(torch.int16))
+
+
+@pytest.mark.parametrize("T,E,H", [(5, 256, 512), (130, 256, 7168), (1000, 512, 4096)])
+def test_dense_logits_fp32_vs_torch(lib, T, E, H):
+    """The router's tensor-core candidate logits (fp32 out) vs torch fp32:
+    within the fp32 summation bound used by the router (4 H 2^-24 |x| |w|)."""
+    from paper_2504_02263_b200 import ops
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(T + E)
+    x = bf16_randn((T, H), g)
+    wg = bf16_randn((E, H), g, H ** -0.5)
+    got = ops.dense_logits(x, wg)
+    torch.cuda.synchronize()
+    ref = (x.double() @ wg.double().t())
+    bound = 4 * H * 2.0 ** -24 * x.double().norm(dim=1, keepdim=True) * wg.double().norm(dim=1)[None, :]
+    assert ((got.double() - ref).abs() <= bound).all()
+    assert (got.double() - ref).abs().max() < 1e-3

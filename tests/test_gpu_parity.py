@@ -666,3 +666,39 @@ def test_expert_ffn_regions_equal_compact(lib, n_src, E_l, per):
             assert torch.equal(y_inplace[b:b + counts[s, e]], yc[o:o + counts[s, e]]), (e, s)
             assert torch.equal(y_gather[b:b + counts[s, e]], yc[o:o + counts[s, e]]), (e, s)
             o += counts[s, e]
+
+
+@pytest.mark.parametrize("T,H,E,K,mode", [(130, 7168, 256, 8, "rand"), (2400, 7168, 256, 8, "rand"),
+                                          (4096, 7168, 256, 8, "rand"), (515, 4096, 512, 8, "rand"),
+                                          (300, 7168, 256, 8, "ties"), (64, 7168, 256, 8, "nonfinite")])
+def test_router_tensor_core_path_bit_exact(lib, monkeypatch, T, H, E, K, mode):
+    """Fine-grained router with the logits on tcgen05 (MSI_ROUTER_TC=1): the
+    candidate experts of every token (within the fp32 error bound of the
+    K-th) are recomputed in the pinned order, so idx / weights / counts /
+    slots stay bit-exact vs the oracle -- including exact ties (duplicated
+    gate rows: ties go to the lower expert) and non-finite rows (all experts
+    recomputed)."""
+    from paper_2504_02263_b200 import ops
+
+    monkeypatch.setenv("MSI_ROUTER_TC", "1")
+    x = O.synth_tokens(T, H, seed=11 + T)
+    wg = O.synth_weights(H, 128, E, seed=6, experts=[]).wg
+    if mode == "ties":  # experts 2k and 2k+1 identical: every logit ties with a neighbour
+        wg = wg.copy()
+        wg[1::2] = wg[0::2]
+    if mode == "nonfinite":
+        x = x.copy()
+        x[3, 7] = 0x7FC0
+        x[5, :] = 0x7F80
+        x[9, 100] = 0xFF80
+    idx_r, w_r = O.router(x, wg, K)
+    cnt_r, slot_r = O.place(idx_r, E)
+    idx, w, cnt, slot = ops.gate_topk(to_dev(x), to_dev(wg), K)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(idx.cpu().numpy(), idx_r)
+    np.testing.assert_array_equal(cnt.cpu().numpy(), cnt_r)
+    np.testing.assert_array_equal(slot.cpu().numpy(), slot_r)
+    wgot = w.cpu().numpy()
+    fin = np.isfinite(w_r)
+    np.testing.assert_array_equal(np.isnan(wgot), np.isnan(w_r))
+    np.testing.assert_array_equal(wgot[fin].view(np.uint32), w_r[fin].view(np.uint32))
