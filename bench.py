@@ -586,11 +586,11 @@ def resolve_layout(args, world: int):
 
 def router_launch_count(E: int, T: int) -> int:
     """Launches of one router (+ dispatch) call (router.cu's path choice):
-    tensor-core logits for E % 256 == 0 at T >= 2048 (expert norms, logits
+    tensor-core logits for E % 256 == 0 at T >= 1024 (expert norms, logits
     GEMM, route), the split path for E >= 64 at T <= 256 (logits, route),
     else the fused kernel."""
     env = os.environ.get("MSI_ROUTER_TC")
-    if E % 256 == 0 and E <= 512 and (env == "1" or (env is None and T >= 2048)):
+    if E % 256 == 0 and E <= 512 and (env == "1" or (env is None and T >= 1024)):
         return 3
     return 2 if (E >= 64 and E % 8 == 0 and T <= 256) else 1
 

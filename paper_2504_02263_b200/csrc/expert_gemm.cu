@@ -311,8 +311,12 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
     }
   }
   __syncthreads();
-  const int ntiles = seg.tile0[p.E_l];
-  const int kblocks = p.kdim / BK;
+  // split-K (mode 4 only): unit tau covers tile tau % ntiles1 over the K
+  // range of split tau / ntiles1, written to its own fp32 plane
+  const int ksplit = p.ksplit > 1 ? p.ksplit : 1;
+  const int ntiles1 = seg.tile0[p.E_l];
+  const int ntiles = ntiles1 * ksplit;
+  const int kblocks = p.kdim / BK / ksplit;
   auto half_pair = [&](const SegInfo<MAXE>& sg, int e, int m) -> bool {
     if constexpr (CG == 2) return half_pair_rows(sg, e, m);
     else return false;
@@ -367,8 +371,9 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
       if (lane == 0) tau = leader ? publish_tile(it) : take_tile(it, true);
       tau = __shfl_sync(0xffffffffu, tau, 0);
       if (tau >= ntiles) break;
+      const int kb0 = (tau / ntiles1) * kblocks;  // split-K: first k-block of this unit
       int e, n, m;
-      decode_tile(seg, p.E_l, tau, e, n, m);
+      decode_tile(seg, p.E_l, tau % ntiles1, e, n, m);
       // this CTA's A rows: 128 (full tile / pair) or 64 (half pair: the odd
       // last 128-row tile of a segment split 64/64 over the pair, moved with
       // a 64-row box so the half-cost MMA is not fed a full tile's bytes)
@@ -407,12 +412,12 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
           mbar_wait(&empty[stage], phase ^ 1);
           if constexpr (CG == 2) {
             if (leader) mbar_expect_tx(&full[stage], a_bytes_pair + 2 * C::B_BYTES);
-            if (!multi && a_bytes) tma_load_2d_pair(st, mA, kb * BK, rowA, &full[stage]);
-            tma_load_2d_pair(st + C::A_BYTES, &tmB, kb * BK, rowB, &full[stage]);
+            if (!multi && a_bytes) tma_load_2d_pair(st, mA, (kb0 + kb) * BK, rowA, &full[stage]);
+            tma_load_2d_pair(st + C::A_BYTES, &tmB, (kb0 + kb) * BK, rowB, &full[stage]);
           } else {
             mbar_expect_tx(&full[stage], a_bytes + C::B_BYTES);
-            if (!multi && a_bytes) tma_load_2d(st, mA, kb * BK, rowA, &full[stage]);
-            tma_load_2d(st + C::A_BYTES, &tmB, kb * BK, rowB, &full[stage]);
+            if (!multi && a_bytes) tma_load_2d(st, mA, (kb0 + kb) * BK, rowA, &full[stage]);
+            tma_load_2d(st + C::A_BYTES, &tmB, (kb0 + kb) * BK, rowB, &full[stage]);
           }
         }
         if (multi) {
@@ -436,7 +441,7 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
       const int tau = take_tile(it, true);
       if (tau >= ntiles) break;
       int e_, n_, m_;
-      decode_tile(seg, p.E_l, tau, e_, n_, m_);
+      decode_tile(seg, p.E_l, tau % ntiles1, e_, n_, m_);
       const uint32_t idesc = half_pair(seg, e_, m_) ? idesc_half : idesc_full;
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
@@ -487,8 +492,9 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
         }
       }
       if (tau >= ntiles) break;
+      const int ks = tau / ntiles1;  // split-K plane (mode 4)
       int e, n, m;
-      decode_tile(seg, p.E_l, tau, e, n, m);
+      decode_tile(seg, p.E_l, tau % ntiles1, e, n, m);
       const bool hp = half_pair(seg, e, m);
       const int rowbase = hp ? m * CG * BM + (int)rank * (BM / 2) : (m * CG + (int)rank) * BM;
       const int rowsub = hp ? (q & 1) * 32 : q * 32;
@@ -596,8 +602,9 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
               tmem_ld32(tbase + sgi * 128 + c * 32, v);
               tmem_wait_ld();
               if (row_local < seg.total[e]) {
-                uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<float*>(p.out) + (size_t)row_global * p.out_ld +
-                                                      (size_t)n * BN + colofs + sgi * 128 + c * 32);
+                uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<float*>(p.out) + (size_t)ks * p.plane +
+                                                      (size_t)row_global * p.out_ld + (size_t)n * BN + colofs +
+                                                      sgi * 128 + c * 32);
 #pragma unroll
                 for (int j = 0; j < 8; ++j) dst[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
               }
@@ -1113,13 +1120,16 @@ static GemmLaunch dense_launch(const void* a, int64_t rows, const void* b, int n
 // fp32 logits = x . wg^T on the tensor cores (the router's candidate pass,
 // router.cu): E % 256 == 0, H % 64 == 0; out [rows][E] fp32.
 int dense_logits_f32(const void* x, int64_t rows, const void* wg, int E, int H, float* out, uint32_t* tile_ctr,
-                     cudaStream_t st) {
+                     cudaStream_t st, int ksplit) {
   MSI_REQUIRE(E % BN == 0 && H % BK == 0 && rows >= 0, "dense_logits: E %% 256 and H %% 64 required");
+  MSI_REQUIRE(ksplit >= 1 && (H / BK) % ksplit == 0, "dense_logits: ksplit must divide H / 64");
   if (rows == 0) return 0;
   GemmLaunch g = dense_launch(x, rows, wg, E, H, tile_ctr);
   g.p.mode = 4;
   g.p.out = reinterpret_cast<__nv_bfloat16*>(out);
   g.p.out_ld = E;
+  g.p.ksplit = ksplit;
+  g.p.plane = (long long)rows * E;
   return grouped_gemm_launch(g, st);
 }
 
@@ -1180,7 +1190,7 @@ extern "C" int msi_grouped_ffn_regions(const void* x_reg, const uint64_t* cntab,
 extern "C" int msi_dense_logits(const void* x, int64_t T, const void* wg, int E, int H, float* out, uint32_t* tile_ctr,
                                 void* stream) {
   MSI_REQUIRE(T == 0 || (x && wg && out && tile_ctr), "msi_dense_logits: null pointer");
-  return msi::dense_logits_f32(x, T, wg, E, H, out, tile_ctr, reinterpret_cast<cudaStream_t>(stream));
+  return msi::dense_logits_f32(x, T, wg, E, H, out, tile_ctr, reinterpret_cast<cudaStream_t>(stream), 1);
 }
 
 extern "C" int msi_dense_gemm(const void* a, int64_t rows, const void* b, int n, int k, void* out, int64_t out_ld,

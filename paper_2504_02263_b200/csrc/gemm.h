@@ -79,6 +79,9 @@ struct GemmParams {
   // t % shard_rows (the O projection's reduce-scatter over NVLink).
   int a_shards;
   int shard_rows;
+  // split-K (mode 4): ksplit planes of plane floats each, summed by the reader
+  int ksplit;
+  long long plane;
   __nv_bfloat16* peer_out[MSI_MAX_RANKS];
 };
 
@@ -98,7 +101,7 @@ int num_sms();
 // per-expert segments of xc (GEMM1's A when several senders share an
 // expert); wait_ctr != null: first wait for *wait_ctr >= epoch * wait_mul.
 int dense_logits_f32(const void* x, int64_t rows, const void* wg, int E, int H, float* out, uint32_t* tile_ctr,
-                     cudaStream_t st);
+                     cudaStream_t st, int ksplit);
 int gather_regions(const void* recv, const uint64_t* cntab, int E, int e0, int n_src, int E_l, long long cap_s,
                    int H, void* xc, const uint32_t* wait_ctr, uint32_t epoch, const uint32_t* epoch_src,
                    uint32_t wait_mul, uint64_t timeout_ns, int32_t* status, cudaStream_t st);

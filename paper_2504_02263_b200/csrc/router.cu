@@ -440,15 +440,15 @@ gate_logits_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __r
 // ex[0..n) -- the per-lane accumulation of tile_logits (elements 256j + 8l + c,
 // j ascending, c = 0..7, fmaf from +0), then the same xor butterfly: the
 // values are bit-identical to the CUDA-core logits kernels'.  Warp-collective.
-__device__ __forceinline__ void exact_logits4(const __nv_bfloat16* __restrict__ xr, const __nv_bfloat16* __restrict__ wg,
-                                              int H, const int (&ex)[4], int n, float (&out)[4]) {
+__device__ __noinline__ void exact_logits4(const __nv_bfloat16* __restrict__ xr, const __nv_bfloat16* __restrict__ wg,
+                                           int H, const int (&ex)[4], int n, float (&out)[4]) {
   const int lane = threadIdx.x & 31;
   float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
   const int nchunk = H >> 8;
   const __nv_bfloat16* wq[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) wq[q] = wg + (size_t)ex[q < n ? q : 0] * H + 8 * lane;
-  constexpr int U = 4;  // chunks whose loads are all issued before the FMAs (L2 latency)
+  constexpr int U = 2;  // chunks whose loads are all issued before the FMAs (L2 latency)
   for (int j0 = 0; j0 < nchunk; j0 += U) {
     uint4 xv4[U], wv4[U][4];
 #pragma unroll
@@ -554,40 +554,49 @@ __device__ void exactify(const __nv_bfloat16* __restrict__ x, const __nv_bfloat1
         theta = mv;
       }
     }
-    // candidate list, 4 experts per exact pass
-    int ex[4], n = 0;
+    // candidate masks (bit l of mask[q]: expert l + 32 q), non-candidates -inf
+    unsigned mask[EPL];
 #pragma unroll
     for (int q = 0; q < EPL; ++q) {
       const bool cand = (lane + 32 * q < E) && (!finite || hi[q] >= theta);
-      unsigned m = __ballot_sync(0xffffffffu, cand);
+      mask[q] = __ballot_sync(0xffffffffu, cand);
       if (!cand && lane + 32 * q < E) lg[lane + 32 * q] = -INFINITY;
-      while (m) {
+    }
+    // exact logits, 4 candidates per pass, one call site (instruction cache)
+    int q = 0;
+    unsigned m = mask[0];
+    for (;;) {
+      int ex[4] = {0, 0, 0, 0}, n = 0;
+      while (n < 4) {
+        if (!m) {
+          if (++q >= EPL) break;
+#pragma unroll
+          for (int i = 0; i < EPL; ++i)
+            if (i == q) m = mask[i];  // constant-index select (no local array)
+          continue;
+        }
         const int bit = __ffs(m) - 1;
         m &= m - 1;
         ex[n++] = bit + 32 * q;
-        if (n == 4) {
-          float v[4];
-          exact_logits4(xr, wg, H, ex, 4, v);
-          if (lane < 4) lg[ex[lane]] = v[lane];  // lane 0..3 write their own expert's value
-          n = 0;
-        }
       }
-    }
-    if (n) {
+      if (n == 0) break;
       float v[4];
       exact_logits4(xr, wg, H, ex, n, v);
-      if (lane < n) lg[ex[lane]] = v[lane];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (i < n && lane == i) lg[ex[i]] = v[i];
+      if (q >= EPL) break;
     }
     __syncwarp();
   }
 }
 
 template <int EPL>
-__global__ void __launch_bounds__(kWarps * 32)
+__global__ void __launch_bounds__(kWarps * 32, 3)
 route_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ logits, int T, int E, int K, int BT,
              int32_t* __restrict__ idx_out, float* __restrict__ w_out, int32_t* __restrict__ cnt_out,
              int32_t* __restrict__ slot_out, int32_t* __restrict__ ws, const Placement pl, const DispatchArgs d,
-             const __nv_bfloat16* __restrict__ wg, const float* __restrict__ wnorm, int H) {
+             const __nv_bfloat16* __restrict__ wg, const float* __restrict__ wnorm, int H, int ksplit) {
   extern __shared__ __align__(16) float s_logit[];  // [BT][E]
   pdl_trigger();
   pdl_wait();
@@ -596,7 +605,15 @@ route_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ logi
   const int rows = max(0, min(BT, T - t0));
   const float4* src = reinterpret_cast<const float4*>(logits + (size_t)t0 * E);
   float4* dst = reinterpret_cast<float4*>(s_logit);
-  for (int i = threadIdx.x; i < rows * E / 4; i += blockDim.x) dst[i] = __ldcg(src + i);
+  const size_t plane4 = (size_t)T * E / 4;  // split-K planes of the tensor-core logits, summed here
+  for (int i = threadIdx.x; i < rows * E / 4; i += blockDim.x) {
+    float4 v = __ldcg(src + i);
+    for (int sp = 1; sp < ksplit; ++sp) {
+      const float4 u = __ldcg(src + sp * plane4 + i);
+      v.x += u.x; v.y += u.y; v.z += u.z; v.w += u.w;
+    }
+    dst[i] = v;
+  }
   __syncthreads();
   if (wnorm) {  // tensor-core logits: exact values for the candidates
     exactify<EPL>(x, wg, wnorm, s_logit, t0, rows, E, K, H);
@@ -725,7 +742,7 @@ int launch_split(const void* x, const void* wg, int T, int H, int E, int K, int 
   if (int arc = smem_attr(reinterpret_cast<const void*>(route_kernel<1>), smem)) return arc;
   MSI_CUDA(launch_k(route_kernel<1>, dim3((T + BT - 1) / BT), dim3(kWarps * 32), smem, st,
                     reinterpret_cast<const __nv_bfloat16*>(x), (const float*)logits, T, E, K, BT, idx, w, cnt, slot,
-                    reinterpret_cast<int32_t*>(ws), pl, d, (const __nv_bfloat16*)nullptr, (const float*)nullptr, H));
+                    reinterpret_cast<int32_t*>(ws), pl, d, (const __nv_bfloat16*)nullptr, (const float*)nullptr, H, 1));
   return check_launch("gate_logits_kernel + route_kernel");
 }
 
@@ -733,8 +750,20 @@ int launch_split(const void* x, const void* wg, int T, int H, int E, int K, int 
 // logits on tcgen05 (dense_logits_f32, ~15 us for 4096 x 7168 x 256), then
 // route_kernel recomputes only the candidate experts of every token in the
 // pinned order (exactify) -- routing stays bit-exact with the oracle.
+constexpr int kTcMaxSplit = 16;
 size_t tc_norm_offset(int T, int P, int E) {
-  return split_logits_offset(T, P) + (((size_t)T * E * sizeof(float) + 255) & ~size_t(255));
+  return split_logits_offset(T, P) + (((size_t)kTcMaxSplit * T * E * sizeof(float) + 255) & ~size_t(255));
+}
+
+// split-K factor of the logits GEMM: enough units for the SMs (the N = E
+// dimension is one or two 256-wide tiles), dividing H / 64
+int tc_ksplit(int T, int E, int H) {
+  const int units = ((T + 255) / 256) * (E / 256);  // CTA-pair tiles
+  const int kb = H / 64;
+  int best = 1;
+  for (int sp = 1; sp <= kTcMaxSplit; ++sp)
+    if (kb % sp == 0 && units * sp <= num_sms() / 2) best = sp;
+  return best;
 }
 
 int route_tc(const void* x, const void* wg, int T, int H, int E, int K, int32_t* idx, float* w, int32_t* cnt,
@@ -745,8 +774,12 @@ int route_tc(const void* x, const void* wg, int T, int H, int E, int K, int32_t*
   MSI_CUDA(launch_k(wg_norm_kernel, dim3(E), dim3(256), 0, st, reinterpret_cast<const __nv_bfloat16*>(wg), H, wnorm));
   if (int rc = check_launch("wg_norm_kernel")) return rc;
   // ws word 4: the GEMM's tile counter (0 at rest; the launch's last fetch resets it)
-  if (int rc = dense_logits_f32(x, T, wg, E, H, logits, reinterpret_cast<uint32_t*>(wsb) + 4, st)) return rc;
-  int BT = 16;  // tokens per CTA (warp per token in the candidate pass)
+  const int ksplit = tc_ksplit(T, E, H);
+  if (int rc = dense_logits_f32(x, T, wg, E, H, logits, reinterpret_cast<uint32_t*>(wsb) + 4, st, ksplit)) return rc;
+  // tokens per CTA (one warp per token in the candidate pass): 8 up to
+  // T = 2048, 16 above (scripts/ab_router_tc.py: the candidate recompute is
+  // L2-latency-bound per warp, so more CTAs win until they exceed the SMs)
+  int BT = T <= 2048 ? 8 : 16;
   if (const char* ov = getenv("MSI_ROUTER_TC_BT")) BT = atoi(ov) == 32 ? 32 : (atoi(ov) == 8 ? 8 : 16);
   const size_t smem = tail_smem_bytes(BT, E, pl.P);
   auto kern = E <= 256 ? route_kernel<8> : route_kernel<16>;
@@ -754,17 +787,18 @@ int route_tc(const void* x, const void* wg, int T, int H, int E, int K, int32_t*
   MSI_CUDA(launch_k(kern, dim3((T + BT - 1) / BT), dim3(kWarps * 32), smem, st,
                     reinterpret_cast<const __nv_bfloat16*>(x), (const float*)logits, T, E, K, BT, idx, w, cnt, slot,
                     reinterpret_cast<int32_t*>(ws), pl, d, reinterpret_cast<const __nv_bfloat16*>(wg),
-                    (const float*)wnorm, H));
+                    (const float*)wnorm, H, ksplit));
   return check_launch("route_kernel (tensor-core logits)");
 }
 
 // MSI_ROUTER_TC=1 forces the tensor-core path (when the shape allows), =0
-// disables it; default: on for E % 256 == 0 from T >= 2048 (measured crossover)
+// disables it; default: on for E % 256 == 0 from T >= 1024 (measured crossover:
+// T = 1024 115 vs 164 us, 2048 132 vs 291, 4096 192 vs 484; T = 512 111 vs 106)
 bool tc_enabled(int E, int T, int H) {
   if (E % 256 || E > 512 || H % 64) return false;
   const char* ov = getenv("MSI_ROUTER_TC");
   if (ov) return ov[0] == '1';
-  return T >= 2048;
+  return T >= 1024;
 }
 
 // Split-path tiles: TT tokens per warp tile (TE = 8 experts), BTL tokens x EB

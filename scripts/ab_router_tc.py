@@ -28,7 +28,10 @@ def main():
         outs = {}
         for mode in ("0", "1", "1b32", "1b8"):
             os.environ["MSI_ROUTER_TC"] = mode[0]
-            os.environ["MSI_ROUTER_TC_BT"] = {"1b32": "32", "1b8": "8"}.get(mode, "16")
+            if mode in ("1b32", "1b8"):
+                os.environ["MSI_ROUTER_TC_BT"] = mode[3:]
+            else:
+                os.environ.pop("MSI_ROUTER_TC_BT", None)
             ts = []
             for _ in range(15):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
