@@ -624,8 +624,7 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
                 float r0[2], r1[2];
 #pragma unroll
                 for (int b = 0; b < 2; ++b) {
-                  const int i = c * 32 + 2 * j + b;
-                  const float inv = p.rope.v[i];
+                  const float inv = p.rope.v[c * 32 + 2 * j + b];  // (grid-constant parameter: no local copy)
                   float sn, cs;
                   sincosf(fp * inv, &sn, &cs);
                   const float x0 = __bfloat162float(__float2bfloat16_rn(__uint_as_float(lo[2 * j + b])));

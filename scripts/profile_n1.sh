@@ -15,8 +15,11 @@ NCU=/usr/local/cuda/bin/ncu
 SMALL="--steps 1 --warmup 3 --no-e2e --no-cpu --no-graph --no-m2n"
 timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_n1.csv \
     python bench.py $SMALL > gpurun_out/ncu_launches.log 2>&1 || echo "launch list failed"
-timeout 1200 $NCU --set full --clock-control none --import-source on -k regex:grouped_gemm -s 24 -c 2 \
+# grouped_gemm launches per layer: QKV (+RoPE/append), O projection, GEMM1, GEMM2
+timeout 1200 $NCU --set full --clock-control none --import-source on -k regex:grouped_gemm -s 26 -c 2 \
     -o gpurun_out/full_gemm -f python bench.py $SMALL > gpurun_out/ncu_gemm.log 2>&1 || echo "gemm capture failed"
+timeout 900 $NCU --set full --clock-control none --import-source on -k regex:grouped_gemm -s 24 -c 2 \
+    -o gpurun_out/full_proj -f python bench.py $SMALL > gpurun_out/ncu_proj.log 2>&1 || echo "proj capture failed"
 timeout 900 $NCU --set full --clock-control none --import-source on -k regex:decode_attn -s 12 -c 1 \
     -o gpurun_out/full_attn -f python bench.py $SMALL > gpurun_out/ncu_attn.log 2>&1 || echo "attn capture failed"
 python scripts/summarize_launches.py gpurun_out/launches_n1.csv 4 "N=1 launch list" > gpurun_out/launches_n1_summary.txt 2>&1

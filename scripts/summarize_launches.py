@@ -3,7 +3,10 @@
 `bench.py --steps 1 --warmup W --no-graph ...`: per kernel, launches per step
 (= launches / runs), mean duration and share of the serialised step.
 
-usage: summarize_launches.py launches.csv RUNS [title]"""
+usage: summarize_launches.py launches.csv RUNS [title] [KEY=label1,label2,...]
+The optional KEY=labels splits a kernel that runs several times per layer
+(e.g. grouped_gemm_kernel=QKV+RoPE,O-proj,GEMM1,GEMM2): its i-th launch gets
+label i % len(labels)."""
 
 import csv
 import sys
@@ -13,6 +16,10 @@ from collections import OrderedDict
 def main():
     path, runs = sys.argv[1], int(sys.argv[2])
     title = sys.argv[3] if len(sys.argv) > 3 else ""
+    split_key, split_labels = None, []
+    if len(sys.argv) > 4 and "=" in sys.argv[4]:
+        split_key, lab = sys.argv[4].split("=", 1)
+        split_labels = lab.split(",")
     rows = []
     with open(path) as fh:
         lines = [ln for ln in fh if ln.startswith('"')]
@@ -27,8 +34,12 @@ def main():
             continue  # torch set-up kernels (weights, inputs) and weight packing: not in the step
         rows.append((name, us))
     agg = OrderedDict()
+    seen = 0
     for name, us in rows:
         short = name.split("(")[0].replace("void ", "").replace("msi::", "").replace("(anonymous namespace)::", "")
+        if split_key and split_key in short:
+            short = f"{short} [{split_labels[seen % len(split_labels)]}]"
+            seen += 1
         a = agg.setdefault(short, [0, 0.0])
         a[0] += 1
         a[1] += us
