@@ -43,6 +43,10 @@
 namespace msi {
 namespace {
 
+#ifndef MSI_GEMM_PARAM_QUAL
+#define MSI_GEMM_PARAM_QUAL __grid_constant__  // (A/B builds: -DMSI_GEMM_PARAM_QUAL=)
+#endif
+
 constexpr int BM = 128, BN = 256, BK = 64;
 constexpr int EPI_WARP_BYTES = 32 * 256;  // 32 rows x 128 bf16
 constexpr int kThreads = 256;
@@ -187,7 +191,7 @@ __device__ __forceinline__ bool half_pair_rows(const SegInfo<MAXE>& s, int e, in
 template <int CG, int MAXE>
 __global__ void __launch_bounds__(kThreads, 1)
 grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CUtensorMap tmB,
-                    const __grid_constant__ GemmParams p) {
+                    const MSI_GEMM_PARAM_QUAL GemmParams p) {
   const CUtensorMap& tmA = am.m[0];
   const CUtensorMap& tmA64 = am.m[1];
   using C = Cfg<CG, MAXE>;

@@ -142,3 +142,21 @@ def test_plan_json_round_trip(tmp_path):
     n_a, n_e, colo, src, tp = bench.apply_plan_json(args)
     assert (n_a, n_e, colo, tp, args.m, args.b_a) == (4, 4, True, 1, 1, 1024)
     assert args.shape.name == MIXTRAL.name and src.startswith("--plan-json")
+
+
+def test_search_box_attention_tp_candidates_and_deployment():
+    """Attention TP: the box search evaluates attention nodes of
+    tp_a GPUs (tp_a must divide the KV heads), and to_deployment maps a node's
+    batch onto its GPUs' shards (b_a per GPU = node batch / tp_a)."""
+    from paper_2504_02263_b200.config import DeploymentPlan
+
+    cm = PM.CostModel(k1=3.0956e-07, k2=1.0e-05, k3=4.4384e-07, k4=3.2245e-04,
+                      util_curve=PM.UtilCurve.from_points([(196608, 0.0084), (3145728, 0.12), (50331648, 0.58)]))
+    table = []
+    PL.search_box(MIXTRAL, b200_gpu(), PL.cm_scaled_for_experts(cm, 8), WorkloadSpec(), 8, explain=table)
+    tpa = {r["tp_a"] for r in table if not r["colocated"]}
+    assert {1, 2} <= tpa and 4 not in tpa  # Mixtral-8x22B has 6 KV heads: tp_a in {1, 2} of (1, 2, 4)
+    p = PL.Plan(tp_a=2, tp_e=1, n_a=1, n_e=2, m=2, B=4096, b_a=2048.0, b_e=2048.0, T_a=1e-3, T_e=1e-3, T_c=1e-4,
+                T_f=1e-3, T_iter_upper=0.1, T_total=0.1, tpuc=1.0, gpus=4)
+    d = PL.to_deployment(p)
+    assert d == DeploymentPlan(n_a=2, n_e=2, m=2, b_a=1024, tp_a=2)
