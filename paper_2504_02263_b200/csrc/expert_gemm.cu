@@ -368,6 +368,7 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
     int stage = 0;
     uint32_t phase = 0;
     uint2* pieces = s_pieces;
+    const uint64_t pol_a = l2_policy_evict_last(), pol_b = l2_policy_evict_first();
     int pre[MSI_MAX_RANKS + 1];
     int pre_e = -1;  // expert whose sender prefix is in pre (tiles arrive expert-major)
     for (int it = 0;; ++it) {
@@ -416,12 +417,22 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
           mbar_wait(&empty[stage], phase ^ 1);
           if constexpr (CG == 2) {
             if (leader) mbar_expect_tx(&full[stage], a_bytes_pair + 2 * C::B_BYTES);
-            if (!multi && a_bytes) tma_load_2d_pair(st, mA, (kb0 + kb) * BK, rowA, &full[stage]);
-            tma_load_2d_pair(st + C::A_BYTES, &tmB, (kb0 + kb) * BK, rowB, &full[stage]);
+            if (p.l2hint) {  // A (re-read by every N tile) evict-last, B (streamed) evict-first
+              if (!multi && a_bytes) tma_load_2d_pair_hint(st, mA, (kb0 + kb) * BK, rowA, &full[stage], pol_a);
+              tma_load_2d_pair_hint(st + C::A_BYTES, &tmB, (kb0 + kb) * BK, rowB, &full[stage], pol_b);
+            } else {
+              if (!multi && a_bytes) tma_load_2d_pair(st, mA, (kb0 + kb) * BK, rowA, &full[stage]);
+              tma_load_2d_pair(st + C::A_BYTES, &tmB, (kb0 + kb) * BK, rowB, &full[stage]);
+            }
           } else {
             mbar_expect_tx(&full[stage], a_bytes + C::B_BYTES);
-            if (!multi && a_bytes) tma_load_2d(st, mA, (kb0 + kb) * BK, rowA, &full[stage]);
-            tma_load_2d(st + C::A_BYTES, &tmB, (kb0 + kb) * BK, rowB, &full[stage]);
+            if (p.l2hint) {
+              if (!multi && a_bytes) tma_load_2d_hint(st, mA, (kb0 + kb) * BK, rowA, &full[stage], pol_a);
+              tma_load_2d_hint(st + C::A_BYTES, &tmB, (kb0 + kb) * BK, rowB, &full[stage], pol_b);
+            } else {
+              if (!multi && a_bytes) tma_load_2d(st, mA, (kb0 + kb) * BK, rowA, &full[stage]);
+              tma_load_2d(st + C::A_BYTES, &tmB, (kb0 + kb) * BK, rowB, &full[stage]);
+            }
           }
         }
         if (multi) {
@@ -874,6 +885,13 @@ bool half_pair_box64() {
   return e && e[0] == '1';
 }
 
+// MSI_GEMM_L2HINT=1: TMA loads carry L2 eviction priorities (A evict-last,
+// B evict-first); read per launch for A/B runs
+bool l2_hints() {
+  const char* e = getenv("MSI_GEMM_L2HINT");
+  return e && e[0] == '1';
+}
+
 int num_sms() {
   static int n[64] = {};  // per device (all B200s have 148; no race: idempotent)
   int dev = 0;
@@ -944,6 +962,7 @@ int launch_cg(const GemmLaunch& L, cudaStream_t st) {
   cfg.numAttrs = na;
   GemmParams prm = L.p;
   prm.a64 = half_pair_box64();
+  prm.l2hint = l2_hints();
   MSI_CUDA(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<CG, MAXE>, am, tb, prm));
   return check_launch("grouped_gemm_kernel");
 }

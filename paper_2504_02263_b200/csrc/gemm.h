@@ -46,6 +46,8 @@ struct GemmParams {
   uint32_t* tile_ctr;
   // half-pair tiles load A with the 64-row box (set by the launcher)
   int a64;
+  // TMA loads with L2 eviction priorities (set by the launcher)
+  int l2hint;
   // receive regions (msi_expert_ffn): counts per (sender, expert) from cntab;
   // virtual row v of expert e lives in region (e, s) of cap_s rows at offset
   // v - pre[e][s].  a_runs = 1: GEMM1 loads A by runs of those regions; the
