@@ -1089,6 +1089,9 @@ def measure(args, rank: int, world: int, local: int, layout, full: bool = True, 
 
 def main():
     args = parse()
+    if os.environ.get("MSI_BENCH_STACKDUMP"):  # diagnostics: dump every thread's stack every N s
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["MSI_BENCH_STACKDUMP"]), repeat=True)
     if args.impl == "reference":
         run_reference(args)
         return
