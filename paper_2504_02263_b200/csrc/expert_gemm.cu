@@ -294,6 +294,12 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
       atomicAdd(&seg.total[e], (int)(uint32_t)ld_relaxed_sys64(p.cntab + (size_t)s * p.E + p.e0 + e));
     }
   }
+  // every total complete before thread 0 builds the table: with more than 32
+  // (expert, sender) entries the adds come from several warps, and a CTA
+  // (or the two CTAs of a pair) seeing a partial sum would disagree on the
+  // tile list -- the pair then waits on each other forever (found at
+  // DeepSeek-V3 shape, 64 local experts x 4 senders)
+  __syncthreads();
   if (threadIdx.x == 0) {
     int run_start = 0, run_tile = 0;
     for (int e = 0; e < p.E_l; ++e) {
@@ -1099,8 +1105,11 @@ int grouped_ffn_regions(const void* x_reg, const uint64_t* cntab, int n_src, int
   g1.p.out = reinterpret_cast<__nv_bfloat16*>(hbuf);
   g1.p.out_ld = inter;
   g1.p.tile_ctr = ctrs;
+  const bool dbg = getenv("MSI_DBG_SYNC") != nullptr;  // hang bisection: sync + report after each launch
+  if (dbg) { cudaStreamSynchronize(st); fprintf(stderr, "[dbg] gather/pre-GEMM1 done\n"); }
   int rc = grouped_gemm_launch(g1, st);
   if (rc) return rc;
+  if (dbg) { cudaStreamSynchronize(st); fprintf(stderr, "[dbg] GEMM1 done\n"); }
   GemmLaunch g2{};
   g2.a = hbuf;
   g2.a_rows = hbuf_rows;

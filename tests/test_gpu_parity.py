@@ -702,3 +702,49 @@ def test_router_tensor_core_path_bit_exact(lib, monkeypatch, T, H, E, K, mode):
     fin = np.isfinite(w_r)
     np.testing.assert_array_equal(np.isnan(wgot), np.isnan(w_r))
     np.testing.assert_array_equal(wgot[fin].view(np.uint32), w_r[fin].view(np.uint32))
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("rank", [0, 1, 2, 3])
+def test_expert_ffn_many_experts_many_senders_regression(lib, rank):
+    """Regression: 64 local experts x 4 senders (DeepSeek-V3 shape, co-located
+    4 GPUs, 2048 tokens per rank -- counts captured from that run,
+    tests/golden/hang/).  More than 32 (sender, expert) totals are summed by
+    several warps; the segment table must wait for all of them, or the two
+    CTAs of a pair disagree on the tile list and hang.  Every repetition must
+    finish and give bit-identical rows to the compact layout."""
+    import os
+
+    import torch
+
+    from paper_2504_02263_b200 import ops, runtime
+    from paper_2504_02263_b200.config import MoeModelSpec
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    counts = np.load(os.path.join(here, "golden", "hang", f"dbg_counts_r{rank}.npy"))
+    n_src, E_l = counts.shape
+    cap = int(counts.max()) + 3
+    model = MoeModelSpec("hang", 1, 512, 256, E_l, 1)
+    _, w13, w2 = runtime.synth_device_weights(model, list(range(E_l)), seed=1, device="cuda")
+    x_reg = torch.randn((E_l * n_src * cap, model.hidden), device="cuda").to(torch.bfloat16)
+    tot = counts.sum(0)
+    starts = ops.segment_starts(tot.tolist())
+    rows = starts[-1] + (int(tot[-1]) + 127) // 128 * 128 + 128
+    xc = torch.zeros((rows, model.hidden), dtype=torch.bfloat16, device="cuda")
+    for e in range(E_l):
+        o = starts[e]
+        for s in range(n_src):
+            b = (e * n_src + s) * cap
+            xc[o:o + counts[s, e]] = x_reg[b:b + counts[s, e]]
+            o += counts[s, e]
+    yc = ops.grouped_ffn(xc, torch.tensor(tot, dtype=torch.int32), w13, w2)
+    for rep in range(4):
+        for gather in (True, False):
+            y = ops.grouped_ffn_regions(x_reg, counts, cap, w13, w2, gather=gather)
+            torch.cuda.synchronize()
+            for e in range(0, E_l, 7):
+                o = starts[e]
+                for s in range(n_src):
+                    b = (e * n_src + s) * cap
+                    assert torch.equal(y[b:b + counts[s, e]], yc[o:o + counts[s, e]]), (rep, gather, e, s)
+                    o += counts[s, e]
