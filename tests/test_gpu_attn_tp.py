@@ -129,3 +129,80 @@ def test_attention_tp_vs_oracle(lib, tmp_path, tp, spec, T):
             rows_g = np.stack([k1[bt[t, ctx[t] // 64], :, ctx[t] % 64] for t in range(tp * T)])
             rows_r = np.stack([k[bt[t, ctx[t] // 64], r * kl:(r + 1) * kl, ctx[t] % 64] for t in range(tp * T)])
             assert_close_bf16(rows_g, rows_r, f"appended k rows, shard {r}")
+
+
+def _runner_worker(rank, world, port, outdir):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    from oracle import oracle as O
+    from paper_2504_02263_b200 import attention as A
+    from paper_2504_02263_b200 import ops, runtime
+    from paper_2504_02263_b200.config import DeploymentPlan, MoeModelSpec
+
+    gpu = rank % torch.cuda.device_count()
+    torch.cuda.set_device(gpu)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    model = MoeModelSpec("tpr", 2, 1024, 512, 8, 2, gqa_group=2)
+    T, m, L = 24, 2, 2
+    plan = DeploymentPlan(n_a=2, n_e=1, m=m, b_a=T, tp_a=2)  # one attention node of 2 GPUs + 1 expert GPU
+    g = runtime.M2NGroup(model, plan, rank=rank, device=f"cuda:{gpu}", timeout_s=60)
+    wts = O.synth_weights(model.hidden, model.intermediate, model.experts, seed=0)
+
+    def dev(a):
+        return torch.from_numpy(np.ascontiguousarray(a).view(np.int16).copy()).view(torch.bfloat16).cuda()
+
+    layer_kw = {}
+    stages = None
+    xs = None
+    if g.is_expert:
+        ex = runtime.local_experts(g)
+        layer_kw = dict(w13=ops.pack_w13(dev(wts.w_gate[ex]), dev(wts.w_up[ex])), w2=dev(wts.w_down[ex]))
+    if g.is_attention:
+        w = A.AttentionWeights(model, g.device, seed=0)
+        ctx = np.arange(2 * T, dtype=np.int32) * 7 % 200
+        stages = [A.AttentionTPStage(model, T, L, g, j, w, ctx, seed=3 + j) for j in range(m)]
+        layer_kw = dict(wg=dev(wts.wg))
+        xs = [dev(O.synth_tokens(T, model.hidden, seed=50 * j + g.attn_index)) for j in range(m)]
+    layer = runtime.MoEDecodeLayer(g, **layer_kw)
+    runner = runtime.PingPongRunner(layer, layers=L, chain=False, attn=stages)
+    dist.barrier()
+    runner.run(xs)
+    torch.cuda.synchronize()
+    res = {}
+    if g.is_attention:
+        res["eager"] = np.stack([_u16(runner._out(xs, j)) for j in range(m)])
+    dist.barrier()
+    runner.capture(xs)  # device-tracked epochs for the TP kernels too
+    for _ in range(2):
+        runner.replay()
+    torch.cuda.synchronize()
+    if g.is_attention:
+        res["graph"] = np.stack([_u16(runner._out(xs, j)) for j in range(m)])
+        r = layer._routes[0]
+        h = stages[0].y[:T]
+        idx_r, w_r = O.router(_u16(h), wts.wg, model.topk)
+        res["routing_ok"] = np.array([np.array_equal(r.idx[:T].cpu().numpy(), idx_r)])
+    res["status"] = np.array([g.status()])
+    np.savez(os.path.join(outdir, f"rank{rank}.npz"), **res)
+    dist.barrier()
+    g.close()
+    dist.destroy_process_group()
+
+
+def test_attention_tp_in_pingpong_runner_with_graph(lib, tmp_path):
+    """PingPongRunner on one attention node of 2 GPUs (tp_a = 2) + 1 expert
+    GPU, 2 micro-batches x 2 layers, eager then CUDA-graph replays (the TP
+    kernels' device-tracked epochs): every status 0, the graph replays give
+    the eager step's outputs bit for bit, routing of the TP stage's output
+    bit-exact vs the oracle."""
+    import torch.multiprocessing as mp
+
+    mp.spawn(_runner_worker, args=(3, _free_port(), str(tmp_path)), nprocs=3, join=True)
+    got = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(3)]
+    for r in range(3):
+        assert got[r]["status"][0] == 0, r
+    for r in range(2):  # attention ranks
+        np.testing.assert_array_equal(got[r]["graph"], got[r]["eager"])
+        assert got[r]["routing_ok"][0]
