@@ -180,12 +180,27 @@ __device__ __forceinline__ void route_tail(const __nv_bfloat16* __restrict__ x, 
   for (int p = threadIdx.x; p < P; p += blockDim.x)  // aggregate first (block 0: already inclusive)
     st_volatile64(mine + p, lb_word(b.gen, b.vb == 0 ? kInc : kAgg, __popc(mask[p])));
   for (int p = threadIdx.x; p < P; p += blockDim.x) {
+    // walk back over the predecessors' words LB at a time: the LB loads are
+    // independent (one L2 round trip per batch instead of one per block --
+    // with every block arriving together only block 0 is inclusive at first,
+    // and a one-at-a-time walk cost ~1 us per predecessor); a word not yet
+    // published is re-polled on its own, and the sum stops at the first
+    // inclusive prefix, in block order as before
+    constexpr int LB = 8;
     uint32_t excl = 0;
-    for (int j = b.vb - 1; j >= 0; --j) {
-      uint64_t v;
-      do { v = ld_volatile64(lb + (size_t)j * P + p); } while ((uint32_t)(v >> 32) != b.gen);
-      excl += (uint32_t)v & 0x3fffffffu;
-      if (((uint32_t)v >> 30 & 3u) == kInc) break;
+    for (int j = b.vb - 1; j >= 0; j -= LB) {
+      uint64_t v[LB];
+#pragma unroll
+      for (int q = 0; q < LB; ++q) v[q] = (j - q >= 0) ? ld_volatile64(lb + (size_t)(j - q) * P + p) : 0ull;
+      bool inc = false;
+#pragma unroll
+      for (int q = 0; q < LB; ++q) {
+        if (j - q < 0) break;
+        while ((uint32_t)(v[q] >> 32) != b.gen) v[q] = ld_volatile64(lb + (size_t)(j - q) * P + p);
+        excl += (uint32_t)v[q] & 0x3fffffffu;
+        if (((uint32_t)v[q] >> 30 & 3u) == kInc) { inc = true; break; }
+      }
+      if (inc) break;
     }
     const uint32_t h = __popc(mask[p]);
     if (b.vb > 0) st_volatile64(mine + p, lb_word(b.gen, kInc, excl + h));
