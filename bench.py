@@ -65,12 +65,12 @@ def choose_split(world: int, shape: str, plan_arg: str, split: str = "", colocat
         return world, world, True, "--colocated" if colocated else "1 GPU: co-located", 1
     if plan_arg == "planner":
         import glob
-        cal = None
+        cal, cal_path = None, ""
         for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_calibration_*.json"))):
             with open(path) as fh:
                 c = json.load(fh)
             if str(c.get("shape", "")).lower() == shape.lower():
-                cal = c
+                cal, cal_path = c, os.path.relpath(path, ROOT)
         if cal is not None:
             from paper_2504_02263_b200 import perf_model as PM
             from paper_2504_02263_b200 import planner as PL
@@ -81,7 +81,7 @@ def choose_split(world: int, shape: str, plan_arg: str, split: str = "", colocat
             p = PL.search_box(as_model_spec(shape), b200_gpu(), PL.cm_scaled_for_experts(cm, c["experts_local"]),
                               WorkloadSpec(), world)
             if p:
-                src = "planner.search_box (calibrated B200 costs, profiles/r01_calibration_8x22b.json)"
+                src = f"planner.search_box (calibrated B200 costs, {cal_path})"
                 if p.tp_e > 1:  # expert nodes of tp_e GPUs
                     src += f"; expert TP {p.tp_e}"
                 if p.tp_a > 1:  # attention nodes of tp_a GPUs: the runtime counts attention GPUs
