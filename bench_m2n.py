@@ -69,7 +69,7 @@ def main():
     from paper_2504_02263_b200 import runtime
     from paper_2504_02263_b200.config import DeploymentPlan, as_model_spec
 
-    rank, world, local = runtime.init_distributed_from_env("nccl")
+    rank, world, local = runtime.init_distributed_from_env(os.environ.get("MSI_M2N_BACKEND", "nccl"))
     n_a, n_e, colo = (world, world, True) if args.colocated else SPLITS[world]
     model = as_model_spec(args.shape)
     H, K, E = model.hidden, model.topk, model.experts
