@@ -46,3 +46,22 @@ def test_paged_cache_block_table_is_a_permutation():
     tight = A.PagedKVCache(1, 1, np.array([63], np.int32), layers=1, device="cpu", fill=False)
     with pytest.raises(RuntimeError):
         tight.advance()  # 64 tokens fill the only page; a 65th would need another
+
+
+def test_request_cost_model_and_composed_batches():
+    """Per-request attention cost alpha * seq_len + beta from the KV bytes at the
+    HBM rate and the projection FLOPs at the tensor rate; composed batches
+    over the DP attention GPUs have b_a requests each and near-equal predicted
+    times, identical on every rank for a seed."""
+    m = BENCH_SHAPES["mixtral-8x22b"]
+    cm = A.request_cost_model(m, hbm_gbs=6500.0, tflops=1400.0)
+    nh, nkv = A.head_layout(m)
+    assert cm.alpha == pytest.approx(2 * nkv * 128 * 2 / 6.5e12)
+    assert cm.beta == pytest.approx(2.0 * m.hidden * (nh + 2 * nkv + nh) * 128 / 1.4e15)
+    lens, plan = A.composed_ctx_lens(m, 3, 512, 730, seed=4)
+    assert [len(v) for v in lens] == [512] * 3
+    assert max(plan.predicted) / min(plan.predicted) < 1.001
+    lens2, _ = A.composed_ctx_lens(m, 3, 512, 730, seed=4)
+    assert all((a == b).all() for a, b in zip(lens, lens2))
+    pool = np.sort(A.batch_composition(3 * 512, 730, 4))
+    assert (np.sort(np.concatenate(lens)) == pool).all()  # every request exactly once
