@@ -46,6 +46,9 @@ constexpr int kWarps = 8;
 #ifndef MSI_ROUTER_EP
 #define MSI_ROUTER_EP 1
 #endif
+#ifndef MSI_DISP_U
+#define MSI_DISP_U 12  // measured 73-74 -> 71 us at T = 3072, E = 8 (scripts/r02_ab_dispu.sh)
+#endif
 constexpr uint32_t kTaken = 0x7fc0dead;  // NaN payload marking an already-selected expert
 
 // Shared memory: logits [max(BT,16)][E] fp32 (reused after top-K for the [P]
@@ -240,7 +243,7 @@ __device__ __forceinline__ void route_tail(const __nv_bfloat16* __restrict__ x, 
           my_dst = d.recv[q] + row * row_bytes;
         }
         const char* src = reinterpret_cast<const char*>(x + (size_t)t * d.H) + lane * 16;
-        constexpr int U = 8;
+        constexpr int U = MSI_DISP_U;  // 512-B row chunks loaded per lane before the stores
         for (int j0 = 0; j0 < nchunk; j0 += U) {
           uint4 v[U];
 #pragma unroll
