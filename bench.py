@@ -41,6 +41,7 @@ def apply_plan_json(args):
     bundle, plan = load_plan(args.plan_json)
     args.shape = bundle.model
     args.m, args.b_a = plan.m, plan.b_a
+    args.tp_a = plan.tp_a  # attention nodes of tp_a GPUs
     return plan.n_a, plan.n_e, plan.colocated, f"--plan-json {os.path.basename(args.plan_json)}", plan.tp_e
 
 

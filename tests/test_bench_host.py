@@ -84,3 +84,21 @@ def test_pingpong_summary_keeps_the_comparable_fields():
     out = bench.pingpong_summary(sub, 0.6)
     assert out["value"] == 1.0 and out["expert_ffn"]["achieved"] == 900.0 and out["parity"]["routing_bit_exact"]
     assert "e2e" not in out and bench.pingpong_summary(None, 0.5) is None
+
+
+def test_plan_json_with_attention_tp_reaches_the_bench(tmp_path):
+    """A plan file whose DeploymentPlan has tp_a = 2 round-trips through
+    save_plan / load_plan, and bench.py --plan-json takes tp_a from it."""
+    import argparse
+
+    from paper_2504_02263_b200.config import (Catalog, ConfigBundle, DeploymentPlan, SearchLimits, WorkloadSpec,
+                                               as_model_spec, b200_gpu, load_plan, save_plan)
+
+    bundle = ConfigBundle(Catalog([b200_gpu()]), as_model_spec("mixtral-8x22b"), WorkloadSpec(), SearchLimits())
+    dp = DeploymentPlan(n_a=2, n_e=2, m=2, b_a=512, tp_a=2)
+    out = tmp_path / "plan.json"
+    save_plan(bundle, dp, out)
+    assert load_plan(out)[1] == dp
+    args = argparse.Namespace(plan_json=str(out), shape="dbrx", m=3, b_a=1024, tp_a=1)
+    n_a, n_e, colo, src, tp_e = bench.apply_plan_json(args)
+    assert (n_a, n_e, colo, tp_e, args.tp_a, args.m, args.b_a) == (2, 2, False, 1, 2, 2, 512)
