@@ -215,8 +215,8 @@ class ClockSampler:
 
 def ncu_traffic(name: str, b_a: int, n_a: int, n_e: int, colo: bool) -> dict | None:
     """DRAM bytes per launch of the dominant kernels from the committed ncu
-    capture of this exact configuration (profiles/r01_ncu_traffic.json), or None."""
-    path = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+    capture of this exact configuration (profiles/r02_ncu_traffic.json), or None."""
+    path = os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")
     if not os.path.exists(path):
         return None
     key = f"{name}|{b_a}|{n_a}+{n_e}|{'colo' if colo else 'disagg'}"
@@ -1051,7 +1051,7 @@ def measure(args, rank: int, world: int, local: int, layout, full: bool = True, 
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None,
                      "traffic": traffic.get("ffn_pair") if traffic else None,
-                     "traffic_source": "profiles/r01_ncu_traffic.json (ncu --set full, dram read+write per launch pair)"
+                     "traffic_source": "profiles/r02_ncu_traffic.json (ncu --set full, dram read+write per launch pair)"
                      if traffic else None,
                      "frac_sustained": (achieved / peak_sus) if achieved else None,
                      "frac_nominal_dense": (achieved / 2250.0) if achieved else None,

@@ -50,7 +50,8 @@ def main():
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     if os.environ.get("AB_NCU") == "1":
         for _ in range(3):
-            ops.grouped_ffn_regions(x_reg, counts, cap, w13, w2, y_reg, hb)
+            ops.grouped_ffn_regions(x_reg, counts, cap, w13, w2, y_reg, hb,
+                                    gather=os.environ.get("AB_GATHER") == "1")
         torch.cuda.synchronize()
         return
     res = {"regions_ms": [], "compact_ms": [], "gather_ms": []}
