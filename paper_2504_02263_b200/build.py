@@ -26,6 +26,8 @@ NVCC_FLAGS = [
     "--expt-relaxed-constexpr",
     "-cudart", "static",
 ]
+# tuning experiments only (e.g. -DMSI_EXACT_U=4): extra nvcc flags
+NVCC_FLAGS += os.environ.get("MSI_NVCC_EXTRA", "").split()
 
 
 def sources() -> list[str]:

@@ -91,6 +91,15 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
 // ------------------------------------------------------------------- bf16 --
 __device__ __forceinline__ float bf16lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
+// The same conversion on the ALU pipe: ptxas turns `v << 16` into IMAD.U32,
+// which shares the FMA pipe with the FFMAs it feeds (B300_MICROARCH.md: FMA
+// and ALU pipes each issue every 2nd cycle); a byte permute stays on the ALU
+// pipe.  For FMA-bound dot-product loops (the router's pinned-order logits).
+__device__ __forceinline__ float bf16lo_alu(uint32_t v) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, 0x1044;" : "=r"(r) : "r"(v), "r"(0u));
+  return __uint_as_float(r);
+}
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);  // RNE, matches the oracle

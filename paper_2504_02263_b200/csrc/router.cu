@@ -23,6 +23,7 @@
 // HBM-bound for small E (x read once; the dispatch re-reads the CTA's rows from
 // L2); FMA-bound for E = 256 (logits on CUDA cores because the fixed reduction
 // order is the bit-exactness contract).
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -43,6 +44,12 @@ constexpr int kWarps = 8;
 #ifndef MSI_ROUTER_FFMA2
 #define MSI_ROUTER_FFMA2 1
 #endif
+#ifndef MSI_EXACT_U  // route_tc candidate pass: 256-element chunks loaded ahead per warp
+#define MSI_EXACT_U 2
+#endif
+#ifndef MSI_ROUTE_LB  // route_kernel min CTAs per SM (register budget)
+#define MSI_ROUTE_LB 3
+#endif
 #ifndef MSI_ROUTER_EP
 #define MSI_ROUTER_EP 1
 #endif
@@ -56,6 +63,13 @@ constexpr uint32_t kTaken = 0x7fc0dead;  // NaN payload marking an already-selec
 // the FMA loop reads the gate weights at shared-memory latency.
 __host__ __device__ inline size_t logit_smem_bytes(int BT, int E) {
   return (size_t)(BT > 16 ? BT : 16) * E * sizeof(float) + (size_t)E * sizeof(uint32_t);
+}
+
+// shared memory before the staged W_g: logits, or the [P] masks + [P] bases
+__host__ __device__ inline size_t tail_smem_bytes(int BT, int E, int P) {
+  size_t head = logit_smem_bytes(BT, E);
+  if (head < (size_t)P * 8) head = (size_t)P * 8;
+  return (head + 15) & ~size_t(15);
 }
 
 // Replicated-expert placement: rep[e*(R+1)] = number of
@@ -461,12 +475,12 @@ gate_logits_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __r
 __device__ __noinline__ void exact_logits4(const __nv_bfloat16* __restrict__ xr, const __nv_bfloat16* __restrict__ wg,
                                            int H, const int (&ex)[4], int n, float (&out)[4]) {
   const int lane = threadIdx.x & 31;
-  float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  float2 acc2[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};  // candidates (0,1), (2,3)
   const int nchunk = H >> 8;
   const __nv_bfloat16* wq[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) wq[q] = wg + (size_t)ex[q < n ? q : 0] * H + 8 * lane;
-  constexpr int U = 2;  // chunks whose loads are all issued before the FMAs (L2 latency)
+  constexpr int U = MSI_EXACT_U;  // chunks whose loads are all issued before the FMAs (L2 latency)
   for (int j0 = 0; j0 < nchunk; j0 += U) {
     uint4 xv4[U], wv4[U][4];
 #pragma unroll
@@ -483,16 +497,27 @@ __device__ __noinline__ void exact_logits4(const __nv_bfloat16* __restrict__ xr,
       const uint4 xa = xv4[u];
       const float xv[8] = {bf16lo(xa.x), bf16hi(xa.x), bf16lo(xa.y), bf16hi(xa.y),
                            bf16lo(xa.z), bf16hi(xa.z), bf16lo(xa.w), bf16hi(xa.w)};
+      // candidate pairs on packed FFMA2 (sm_100 fma.rn.f32x2): each half is
+      // the same IEEE fmaf in the same c order as the scalar loop, at half the
+      // FMA issue count; the weights' lo halves of pair 0 convert on the FMA
+      // pipe, the rest on the ALU pipe (the two pipes then carry about the
+      // same count; B300_MICROARCH.md pipe rates)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint4 v = wv4[u][q];
-        const float wv[8] = {bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y),
-                             bf16lo(v.z), bf16hi(v.z), bf16lo(v.w), bf16hi(v.w)};
+      for (int pr = 0; pr < 2; ++pr) {
+        const uint4 v0 = wv4[u][2 * pr], v1 = wv4[u][2 * pr + 1];
+        const uint32_t a0[4] = {v0.x, v0.y, v0.z, v0.w}, a1[4] = {v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
-        for (int c = 0; c < 8; ++c) acc[q] = __fmaf_rn(xv[c], wv[c], acc[q]);  // q >= n: unused
+        for (int h = 0; h < 4; ++h) {
+          const float2 wlo = pr == 0 ? make_float2(bf16lo(a0[h]), bf16lo(a1[h]))
+                                     : make_float2(bf16lo_alu(a0[h]), bf16lo_alu(a1[h]));
+          const float2 whi = make_float2(bf16hi(a0[h]), bf16hi(a1[h]));
+          acc2[pr] = __ffma2_rn(make_float2(xv[2 * h], xv[2 * h]), wlo, acc2[pr]);  // q >= n: unused
+          acc2[pr] = __ffma2_rn(make_float2(xv[2 * h + 1], xv[2 * h + 1]), whi, acc2[pr]);
+        }
       }
     }
   }
+  const float acc[4] = {acc2[0].x, acc2[0].y, acc2[1].x, acc2[1].y};
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     float v = acc[q];
@@ -511,9 +536,15 @@ __device__ __noinline__ void exact_logits4(const __nv_bfloat16* __restrict__ xr,
 // the pinned order (bit-identical), every other expert -inf; non-finite
 // norms or bounds recompute all E.  Top-K, weights and placement then run
 // unchanged on exact values.
+// Two phases so that the recompute is balanced across the CTA's warps (the
+// candidate count varies per token, ~9-30 at the DS-V3 shape): A) one warp
+// per token computes the bounds and writes the token's candidate list to
+// s_cand; B) the CTA's (token, quad of candidates) items are dealt round-robin
+// to the warps.  Each value is still one warp's pinned-order dot product.
 template <int EPL>  // experts per lane (E <= 32 * EPL)
 __device__ void exactify(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
-                         const float* __restrict__ wnorm, float* s_logit, int t0, int rows, int E, int K, int H) {
+                         const float* __restrict__ wnorm, float* s_logit, uint16_t* s_cand, int* s_nc, int t0,
+                         int rows, int E, int K, int H) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float cb = 4.0f * (float)H * 5.9604645e-8f * 1.01f;
   for (int lt = warp; lt < rows; lt += kWarps) {
@@ -528,8 +559,8 @@ __device__ void exactify(const __nv_bfloat16* __restrict__ x, const __nv_bfloat1
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const uint4 v = v4[u];
-        const float f[8] = {bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y),
-                            bf16lo(v.z), bf16hi(v.z), bf16lo(v.w), bf16hi(v.w)};
+        const float f[8] = {bf16lo_alu(v.x), bf16hi(v.x), bf16lo_alu(v.y), bf16hi(v.y),
+                            bf16lo_alu(v.z), bf16hi(v.z), bf16lo_alu(v.w), bf16hi(v.w)};
 #pragma unroll
         for (int c = 0; c < 8; ++c) ss = fmaf(f[c], f[c], ss);
       }
@@ -580,37 +611,37 @@ __device__ void exactify(const __nv_bfloat16* __restrict__ x, const __nv_bfloat1
       mask[q] = __ballot_sync(0xffffffffu, cand);
       if (!cand && lane + 32 * q < E) lg[lane + 32 * q] = -INFINITY;
     }
-    // exact logits, 4 candidates per pass, one call site (instruction cache)
-    int q = 0;
-    unsigned m = mask[0];
-    for (;;) {
-      int ex[4] = {0, 0, 0, 0}, n = 0;
-      while (n < 4) {
-        if (!m) {
-          if (++q >= EPL) break;
+    // the token's candidate list, ascending expert id
+    int base = 0;
 #pragma unroll
-          for (int i = 0; i < EPL; ++i)
-            if (i == q) m = mask[i];  // constant-index select (no local array)
-          continue;
-        }
-        const int bit = __ffs(m) - 1;
-        m &= m - 1;
-        ex[n++] = bit + 32 * q;
-      }
-      if (n == 0) break;
-      float v[4];
-      exact_logits4(xr, wg, H, ex, n, v);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (i < n && lane == i) lg[ex[i]] = v[i];
-      if (q >= EPL) break;
+    for (int q = 0; q < EPL; ++q) {
+      if ((mask[q] >> lane) & 1u) s_cand[lt * E + base + __popc(mask[q] & ((1u << lane) - 1u))] = (uint16_t)(lane + 32 * q);
+      base += __popc(mask[q]);
     }
-    __syncwarp();
+    if (lane == 0) s_nc[lt] = base;
+  }
+  __syncthreads();
+  // B: exact logits of item (token lt, candidates 4 qi .. 4 qi + 3); one call
+  // site of exact_logits4 (instruction cache)
+  int lt = 0, before = 0;  // items before token lt
+  for (int it = warp;; it += kWarps) {
+    while (lt < rows && it >= before + ((s_nc[lt] + 3) >> 2)) before += (s_nc[lt++] + 3) >> 2;
+    if (lt >= rows) break;
+    const int c0 = 4 * (it - before), n = min(4, s_nc[lt] - c0);
+    int ex[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) ex[i] = i < n ? (int)s_cand[lt * E + c0 + i] : 0;
+    float v[4];
+    exact_logits4(x + (size_t)(t0 + lt) * H, wg, H, ex, n, v);
+    float* lg = s_logit + (size_t)lt * E;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i < n && lane == i) lg[ex[i]] = v[i];
   }
 }
 
 template <int EPL>
-__global__ void __launch_bounds__(kWarps * 32, 3)
+__global__ void __launch_bounds__(kWarps * 32, MSI_ROUTE_LB)
 route_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ logits, int T, int E, int K, int BT,
              int32_t* __restrict__ idx_out, float* __restrict__ w_out, int32_t* __restrict__ cnt_out,
              int32_t* __restrict__ slot_out, int32_t* __restrict__ ws, const Placement pl, const DispatchArgs d,
@@ -634,7 +665,10 @@ route_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ logi
   }
   __syncthreads();
   if (wnorm) {  // tensor-core logits: exact values for the candidates
-    exactify<EPL>(x, wg, wnorm, s_logit, t0, rows, E, K, H);
+    // candidate lists after the tail's region (route_tc sizes the launch's smem)
+    uint16_t* s_cand = reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(s_logit) + tail_smem_bytes(BT, E, pl.P));
+    int* s_nc = reinterpret_cast<int*>(s_cand + ((BT * E + 7) & ~7));
+    exactify<EPL>(x, wg, wnorm, s_logit, s_cand, s_nc, t0, rows, E, K, H);
     __syncthreads();
   }
   route_tail(x, s_logit, b, (int)gridDim.x, BT, T, E, K, idx_out, w_out, cnt_out, slot_out, ws, pl, d);
@@ -714,12 +748,6 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __res
 
 constexpr size_t kMaxStagedW = 200 * 1024;  // W_g staged in smem up to this size
 
-// shared memory before the staged W_g: logits, or the [P] masks + [P] bases
-size_t tail_smem_bytes(int BT, int E, int P) {
-  size_t head = logit_smem_bytes(BT, E);
-  if (head < (size_t)P * 8) head = (size_t)P * 8;
-  return (head + 15) & ~size_t(15);
-}
 
 template <int TT, int TE>
 int launch(const void* x, const void* wg, int T, int H, int E, int K, int BT, int32_t* idx,
@@ -798,8 +826,8 @@ int route_tc(const void* x, const void* wg, int T, int H, int E, int K, int32_t*
   // T = 2048, 16 above (scripts/ab_router_tc.py: the candidate recompute is
   // L2-latency-bound per warp, so more CTAs win until they exceed the SMs)
   int BT = T <= 2048 ? 8 : 16;
-  if (const char* ov = getenv("MSI_ROUTER_TC_BT")) BT = atoi(ov) == 32 ? 32 : (atoi(ov) == 8 ? 8 : 16);
-  const size_t smem = tail_smem_bytes(BT, E, pl.P);
+  if (const char* ov = getenv("MSI_ROUTER_TC_BT")) BT = std::max(4, std::min(32, atoi(ov)));
+  const size_t smem = tail_smem_bytes(BT, E, pl.P) + (((size_t)BT * E + 7) & ~size_t(7)) * 2 + 32 * sizeof(int);
   auto kern = E <= 256 ? route_kernel<8> : route_kernel<16>;
   if (int arc = smem_attr(reinterpret_cast<const void*>(kern), smem)) return arc;
   MSI_CUDA(launch_k(kern, dim3((T + BT - 1) / BT), dim3(kWarps * 32), smem, st,
