@@ -45,10 +45,10 @@ constexpr int kWarps = 8;
 #define MSI_ROUTER_FFMA2 1
 #endif
 #ifndef MSI_EXACT_U  // route_tc candidate pass: 256-element chunks loaded ahead per warp
-#define MSI_EXACT_U 2
+#define MSI_EXACT_U 4
 #endif
 #ifndef MSI_ROUTE_LB  // route_kernel min CTAs per SM (register budget)
-#define MSI_ROUTE_LB 3
+#define MSI_ROUTE_LB 2
 #endif
 #ifndef MSI_ROUTER_EP
 #define MSI_ROUTER_EP 1
@@ -822,10 +822,10 @@ int route_tc(const void* x, const void* wg, int T, int H, int E, int K, int32_t*
   // ws word 4: the GEMM's tile counter (0 at rest; the launch's last fetch resets it)
   const int ksplit = tc_ksplit(T, E, H);
   if (int rc = dense_logits_f32(x, T, wg, E, H, logits, reinterpret_cast<uint32_t*>(wsb) + 4, st, ksplit)) return rc;
-  // tokens per CTA (one warp per token in the candidate pass): 8 up to
-  // T = 2048, 16 above (scripts/ab_router_tc.py: the candidate recompute is
-  // L2-latency-bound per warp, so more CTAs win until they exceed the SMs)
-  int BT = T <= 2048 ? 8 : 16;
+  // tokens per CTA: 4 up to T = 1024, 8 up to 2048, 16 above (the candidate
+  // recompute is L2-latency-bound per warp, so more CTAs win until they
+  // exceed 2 per SM; scripts/ab_router_lib.py, profiles/r02_ab_router_*.jsonl)
+  int BT = T <= 1024 ? 4 : (T <= 2048 ? 8 : 16);
   if (const char* ov = getenv("MSI_ROUTER_TC_BT")) BT = std::max(4, std::min(32, atoi(ov)));
   const size_t smem = tail_smem_bytes(BT, E, pl.P) + (((size_t)BT * E + 7) & ~size_t(7)) * 2 + 32 * sizeof(int);
   auto kern = E <= 256 ? route_kernel<8> : route_kernel<16>;
@@ -838,13 +838,14 @@ int route_tc(const void* x, const void* wg, int T, int H, int E, int K, int32_t*
 }
 
 // MSI_ROUTER_TC=1 forces the tensor-core path (when the shape allows), =0
-// disables it; default: on for E % 256 == 0 from T >= 1024 (measured crossover:
-// T = 1024 115 vs 164 us, 2048 132 vs 291, 4096 192 vs 484; T = 512 111 vs 106)
+// disables it; default: on for E % 256 == 0 from T >= 64 (DS-V3 shape, back-to-
+// back medians vs the pinned-order CUDA-core path: T = 64 51 vs 56 us, 256 56
+// vs 83, 1024 69 vs 136, 2048 91 vs 263, 4096 147 vs 454)
 bool tc_enabled(int E, int T, int H) {
   if (E % 256 || E > 512 || H % 64) return false;
   const char* ov = getenv("MSI_ROUTER_TC");
   if (ov) return ov[0] == '1';
-  return T >= 1024;
+  return T >= 64;
 }
 
 // Split-path tiles: TT tokens per warp tile (TE = 8 experts), BTL tokens x EB

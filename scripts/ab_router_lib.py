@@ -43,7 +43,7 @@ def main():
     g = torch.Generator(device="cuda")
     g.manual_seed(0)
     wg = (torch.randn(E, H, generator=g, device="cuda") / H ** 0.5).to(torch.bfloat16)
-    for T in (1024, 2048, 4096):
+    for T in [int(t) for t in os.environ.get("MSI_AB_T", "1024,2048,4096").split(",")]:
         x = torch.randn(T, H, generator=g, device="cuda").to(torch.bfloat16)
         ws = torch.zeros(libs[0][1].msi_gate_topk_workspace(T, E), dtype=torch.uint8, device="cuda")
 
@@ -56,8 +56,18 @@ def main():
         os.environ["MSI_ROUTER_TC"] = "0"
         ref = new_outs()
         run(libs[0][1], x, wg, K, ref, ws)
-        os.environ["MSI_ROUTER_TC"] = "1"
         res = {"T": T}
+        ts, o0 = [], new_outs()
+        for _ in range(7):  # the pinned-order CUDA-core path, last build
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(20):
+                run(libs[-1][1], x, wg, K, o0, ws)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) * 1e3 / 20)
+        res["pinned_cuda_core_us"] = round(statistics.median(ts), 1)
+        os.environ["MSI_ROUTER_TC"] = "1"
         for name, lib in libs:
             for bt in bts:
                 if bt:
