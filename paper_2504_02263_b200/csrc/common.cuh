@@ -413,6 +413,13 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
           smem_u32(bar)), "h"((uint16_t)0x3) : "memory");
 }
+// The same with an explicit CTA mask (a quad of two pairs: the operand-stage
+// release goes to all four CTAs, the accumulator-ready signal to one pair).
+__device__ __forceinline__ void mma_commit_pair_mask(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)), "h"(mask) : "memory");
+}
 // L2 eviction-priority policies for TMA loads (createpolicy): streamed-once
 // operands evict first, operands re-read across tiles evict last.
 __device__ __forceinline__ uint64_t l2_policy_evict_first() {
@@ -441,6 +448,15 @@ __device__ __forceinline__ void tma_load_2d_pair_hint(void* smem_dst, const CUte
 }
 // TMA load into this CTA's smem whose completion bytes land on the leader's
 // barrier (executed by both CTAs of a pair).
+// Pair-mode load multicast to the CTAs in `mask` (same smem offset in each);
+// each destination's bytes complete on its pair leader's barrier.
+__device__ __forceinline__ void tma_load_2d_pair_mc(void* smem_dst, const CUtensorMap* m, int c0, int c1,
+                                                    uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(smem_dst)), "l"(m), "r"(c0), "r"(c1),
+      "r"(smem_u32(bar) & kPeerBitMask), "h"(mask) : "memory");
+}
 __device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const CUtensorMap* m, int c0, int c1,
                                                  uint64_t* bar) {
   asm volatile(

@@ -43,6 +43,14 @@
 namespace msi {
 namespace {
 
+#ifndef MSI_GEMM_PROF  // 1 = MMA-issuer wait profile (diagnostic builds only)
+#define MSI_GEMM_PROF 0
+#endif
+#if MSI_GEMM_PROF
+// [0] cycles waiting for operand stages, [1] waiting for a free accumulator,
+// [2] MMA-issuer loop cycles, [3] tiles, summed over leaders
+__device__ unsigned long long g_gemm_prof[4];
+#endif
 #ifndef MSI_GEMM_PARAM_QUAL
 #define MSI_GEMM_PARAM_QUAL __grid_constant__  // (A/B builds: -DMSI_GEMM_PARAM_QUAL=)
 #endif
@@ -188,7 +196,12 @@ __device__ __forceinline__ bool half_pair_rows(const SegInfo<MAXE>& s, int e, in
   return (mt & 1) && m == s.mtiles[e] - 1;
 }
 
-template <int CG, int MAXE>
+// QD (quad, CG = 2 only): a cluster of two CTA pairs on N tiles 2j and 2j+1
+// of the same (expert, M unit).  Their A slabs are identical, so each CTA
+// loads half of its slab and multicasts it to the same-rank CTA of the other
+// pair: A traffic from L2 halves (the kernel is L2-bandwidth-bound at
+// 256 x 256 pair tiles).  Operand stages are released to all four CTAs.
+template <int CG, int MAXE, bool QD = false>
 __global__ void __launch_bounds__(kThreads, 1)
 grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CUtensorMap tmB,
                     const MSI_GEMM_PARAM_QUAL GemmParams p) {
@@ -214,9 +227,11 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
   __shared__ uint2 s_pieces[kMaxPieces];  // producer: A runs of the current tile
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;  // CTA within the pair
+  const uint32_t crank = CG == 2 ? cluster_ctarank() : 0;  // CTA within the cluster
+  const uint32_t rank = crank & 1;                          // CTA within the pair
+  const int pr = QD ? (int)(crank >> 1) : 0;                // pair within the quad
   const bool leader = rank == 0;
-  const int nunits = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int nunits = QD ? (int)(gridDim.x >> 2) : CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   pdl_trigger();  // the next kernel (GEMM2 / combine) may launch and queue now
   pdl_wait();     // everything earlier on the stream is complete and visible
   uint32_t epoch = p.epoch;
@@ -226,7 +241,7 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
   //      leader waits and both CTAs follow its decision ----------------------
   if (threadIdx.x == 0) {
     bool ok = true;
-    if (leader) {
+    if (crank == 0) {
       if (blockIdx.x == 0 && p.trace && p.wait_ctr) p.trace[p.trace_slot] = globaltimer();
       ok = !(p.epoch_src && epoch == 0);  // epoch mismatch: abort below
       if (ok && p.wait_ctr) ok = wait_geq(p.wait_ctr, epoch * p.wait_mul, p.timeout_ns, p.status);
@@ -241,11 +256,12 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
       tma_prefetch(&am.m[2]); tma_prefetch(&am.m[3]); tma_prefetch(&am.m[4]);
       tma_prefetch(&am.m[5]); tma_prefetch(&am.m[6]); tma_prefetch(&am.m[7]);
     }
-    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], QD ? 2 : 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4 * CG); }
     // ring consumers: MMA thread + 4 epilogue warps (+ the peer's producer
     // and 4 epilogue warps, which arrive on the leader's barrier)
-    for (int i = 0; i < TRING; ++i) { mbar_init(&qfull[i], 1); mbar_init(&qempty[i], CG == 2 ? 10 : 5); }
+    // (quad: 2 MMA threads, 3 producers, 16 epilogue warps on the quad leader's)
+    for (int i = 0; i < TRING; ++i) { mbar_init(&qfull[i], 1); mbar_init(&qempty[i], QD ? 21 : CG == 2 ? 10 : 5); }
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -255,7 +271,7 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
   tc_fence_before();
   if constexpr (CG == 2) {
     cluster_sync();  // barriers of both CTAs initialised, leader's wait done
-    if (!leader) {
+    if (crank != 0) {
       if (threadIdx.x == 0) s_abort = (int)ld_shared_cluster_u32(mapa_shared(smem_u32(&s_abort), 0));
       __syncthreads();
     }
@@ -342,11 +358,13 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
     const int slot = it % TRING;
     if (it >= TRING) mbar_wait_cluster(&qempty[slot], ((it / TRING) - 1) & 1);
     const uint32_t t = atomicAdd(p.tile_ctr, 1u);
-    if (t == (uint32_t)(ntiles + nunits - 1)) *p.tile_ctr = 0;  // the launch's last fetch
+    if (t == (uint32_t)((QD ? ntiles / 2 : ntiles) + nunits - 1)) *p.tile_ctr = 0;  // the launch's last fetch
     s_tau[slot] = (int)t;
     if constexpr (CG == 2) {
-      st_shared_cluster_u32(mapa_shared(smem_u32(&s_tau[slot]), 1), t);
-      mbar_arrive_cluster(mapa_shared(smem_u32(&qfull[slot]), 1));
+      for (uint32_t r = 1; r < (QD ? 4u : 2u); ++r) {
+        st_shared_cluster_u32(mapa_shared(smem_u32(&s_tau[slot]), r), t);
+        mbar_arrive_cluster(mapa_shared(smem_u32(&qfull[slot]), r));
+      }
     }
     mbar_arrive(&qfull[slot]);
     return (int)t;
@@ -357,13 +375,31 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
     const int t = s_tau[slot];
     if (arrive) {
       if constexpr (CG == 2) {
-        if (leader) mbar_arrive(&qempty[slot]);
+        if (crank == 0) mbar_arrive(&qempty[slot]);
         else mbar_arrive_cluster(mapa_shared(smem_u32(&qempty[slot]), 0));
       } else {
         mbar_arrive(&qempty[slot]);
       }
     }
     return t;
+  };
+  // quad: the ring carries quad-tile ids (expert, N-tile pair, M unit); this
+  // pair's tile is N tile 2j + pr (ntiles = the end sentinel)
+  auto pair_tile = [&](int t) -> int {
+    if constexpr (!QD) {
+      return t;
+    } else {
+      if (t >= ntiles / 2) return ntiles;
+      int lo = 0, hi = p.E_l - 1;  // last e with tile0[e] / 2 <= t
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if ((seg.tile0[mid] >> 1) <= t) lo = mid;
+        else hi = mid - 1;
+      }
+      const int local = t - (seg.tile0[lo] >> 1);
+      const int nq = local / seg.mtiles[lo];
+      return seg.tile0[lo] + (2 * nq + pr) * seg.mtiles[lo] + (local - nq * seg.mtiles[lo]);
+    }
   };
 
   if (warp == 0) {
@@ -379,7 +415,7 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
     int pre_e = -1;  // expert whose sender prefix is in pre (tiles arrive expert-major)
     for (int it = 0;; ++it) {
       int tau = 0;
-      if (lane == 0) tau = leader ? publish_tile(it) : take_tile(it, true);
+      if (lane == 0) tau = pair_tile(crank == 0 ? publish_tile(it) : take_tile(it, true));
       tau = __shfl_sync(0xffffffffu, tau, 0);
       if (tau >= ntiles) break;
       const int kb0 = (tau / ntiles1) * kblocks;  // split-K: first k-block of this unit
@@ -427,7 +463,12 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
               if (!multi && a_bytes) tma_load_2d_pair_hint(st, mA, (kb0 + kb) * BK, rowA, &full[stage], pol_a);
               tma_load_2d_pair_hint(st + C::A_BYTES, &tmB, (kb0 + kb) * BK, rowB, &full[stage], pol_b);
             } else {
-              if (!multi && a_bytes) tma_load_2d_pair(st, mA, (kb0 + kb) * BK, rowA, &full[stage]);
+              if (QD && !hp) {  // half of the slab, to this CTA and its twin in the other pair
+                tma_load_2d_pair_mc(st + pr * (C::A_BYTES / 2), &tmA64, (kb0 + kb) * BK, rowA + pr * (BM / 2),
+                                    &full[stage], (uint16_t)((1u << rank) | (4u << rank)));
+              } else if (!multi && a_bytes) {
+                tma_load_2d_pair(st, mA, (kb0 + kb) * BK, rowA, &full[stage]);
+              }
               tma_load_2d_pair(st + C::A_BYTES, &tmB, (kb0 + kb) * BK, rowB, &full[stage]);
             }
           } else {
@@ -458,19 +499,36 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
     constexpr uint32_t idesc_half = umma_idesc_bf16(BM, BN);  // CG = 2 only
     int stage = 0;
     uint32_t phase = 0;
+#if MSI_GEMM_PROF
+    unsigned long long w_full = 0, w_acc = 0, ntile = 0;
+    const long long t_begin = clock64();
+#endif
     for (int it = 0;; ++it) {
-      const int tau = take_tile(it, true);
+      const int tau = pair_tile(take_tile(it, true));
       if (tau >= ntiles) break;
       int e_, n_, m_;
       decode_tile(seg, p.E_l, tau % ntiles1, e_, n_, m_);
       const uint32_t idesc = half_pair(seg, e_, m_) ? idesc_half : idesc_full;
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
+#if MSI_GEMM_PROF
+      long long t0 = clock64();
+#endif
       mbar_wait(&tempty[acc], aph ^ 1);
+#if MSI_GEMM_PROF
+      w_acc += clock64() - t0;
+      ++ntile;
+#endif
       tc_fence_after();
       const uint32_t d = tmem_base + acc * BN;
       for (int kb = 0; kb < kblocks; ++kb) {
+#if MSI_GEMM_PROF
+        t0 = clock64();
+#endif
         mbar_wait(&full[stage], phase);
+#if MSI_GEMM_PROF
+        w_full += clock64() - t0;
+#endif
         tc_fence_after();
         uint8_t* st = sA + stage * C::STAGE_BYTES;
         const uint64_t ad = umma_desc_sw128(st);
@@ -480,13 +538,21 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
           if constexpr (CG == 2) mma_bf16_pair(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
           else mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
         }
-        if constexpr (CG == 2) mma_commit_pair(&empty[stage]);
+        if constexpr (QD) mma_commit_pair_mask(&empty[stage], 0xF);  // both pairs fill every stage
+        else if constexpr (CG == 2) mma_commit_pair(&empty[stage]);
         else mma_commit(&empty[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      if constexpr (CG == 2) mma_commit_pair(&tfull[acc]);
+      if constexpr (QD) mma_commit_pair_mask(&tfull[acc], (uint16_t)(3u << (2 * pr)));
+      else if constexpr (CG == 2) mma_commit_pair(&tfull[acc]);
       else mma_commit(&tfull[acc]);
     }
+#if MSI_GEMM_PROF
+    atomicAdd(&g_gemm_prof[0], w_full);
+    atomicAdd(&g_gemm_prof[1], w_acc);
+    atomicAdd(&g_gemm_prof[2], (unsigned long long)(clock64() - t_begin));
+    atomicAdd(&g_gemm_prof[3], ntile);
+#endif
   } else if (warp >= 4) {
     // ===================== epilogue (both CTAs, own TMEM rows) ============
     // Full tile: warp q owns TMEM lanes [32q, 32q+32) = rows 32q.. of the
@@ -500,13 +566,13 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
     int pre_e = -1;  // receive regions: sender prefix of expert pre_e
     for (int it = 0;; ++it) {
       int tau = 0;
-      if (lane == 0) tau = take_tile(it, false);
+      if (lane == 0) tau = pair_tile(take_tile(it, false));
       tau = __shfl_sync(0xffffffffu, tau, 0);
       __syncwarp();
       if (lane == 0) {  // one ring arrival per epilogue warp
         const int slot = it % TRING;
         if constexpr (CG == 2) {
-          if (leader) mbar_arrive(&qempty[slot]);
+          if (crank == 0) mbar_arrive(&qempty[slot]);
           else mbar_arrive_cluster(mapa_shared(smem_u32(&qempty[slot]), 0));
         } else {
           mbar_arrive(&qempty[slot]);
@@ -690,7 +756,7 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
-            if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+            if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), crank & ~1u));
             else mbar_arrive(&tempty[acc]);
           }
         }
@@ -920,7 +986,7 @@ int gather_regions(const void* recv, const uint64_t* cntab, int E, int e0, int n
   return check_launch("gather_regions_kernel");
 }
 
-template <int CG, int MAXE>
+template <int CG, int MAXE, bool QD = false>
 int launch_cg(const GemmLaunch& L, cudaStream_t st) {
   using C = Cfg<CG, MAXE>;
   AMaps am;
@@ -938,13 +1004,14 @@ int launch_cg(const GemmLaunch& L, cudaStream_t st) {
   if (rc) return rc;
   rc = make_tmap(&tb, L.b, (uint64_t)L.p.kdim, (uint64_t)(L.p.a_shards ? 1 : L.p.E_l) * L.p.n_total, BK, C::B_ROWS);
   if (rc) return rc;
-  if (int arc = smem_attr(reinterpret_cast<const void*>(grouped_gemm_kernel<CG, MAXE>), C::SMEM)) return arc;
+  if (int arc = smem_attr(reinterpret_cast<const void*>(grouped_gemm_kernel<CG, MAXE, QD>), C::SMEM)) return arc;
   int grid = L.grid > 0 ? L.grid : num_sms();
   if (const char* g = getenv("MSI_GEMM_GRID")) {  // A/B: persistent grid on fewer SMs
     const int v = atoi(g);
     if (v >= CG && v < grid) grid = v;
   }
-  grid -= grid % CG;
+  constexpr int kCluster = QD ? 4 : CG;
+  grid -= grid % kCluster;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -954,7 +1021,7 @@ int launch_cg(const GemmLaunch& L, cudaStream_t st) {
   int na = 0;
   if (CG == 2) {
     attrs[na].id = cudaLaunchAttributeClusterDimension;
-    attrs[na].val.clusterDim.x = CG;
+    attrs[na].val.clusterDim.x = kCluster;
     attrs[na].val.clusterDim.y = 1;
     attrs[na].val.clusterDim.z = 1;
     ++na;
@@ -969,7 +1036,7 @@ int launch_cg(const GemmLaunch& L, cudaStream_t st) {
   GemmParams prm = L.p;
   prm.a64 = half_pair_box64();
   prm.l2hint = l2_hints();
-  MSI_CUDA(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<CG, MAXE>, am, tb, prm));
+  MSI_CUDA(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<CG, MAXE, QD>, am, tb, prm));
   return check_launch("grouped_gemm_kernel");
 }
 
@@ -989,11 +1056,20 @@ int default_cg() {
   return cg;
 }
 
+// Quad clusters (two CTA pairs sharing A by multicast): MSI_GEMM_QUAD=1
+bool quad_enabled() {
+  const char* v = getenv("MSI_GEMM_QUAD");
+  return v && v[0] == '1';
+}
+
 int grouped_gemm_launch(const GemmLaunch& L, cudaStream_t st) {
   MSI_REQUIRE(L.p.tile_ctr != nullptr, "grouped_gemm: tile counter required");
   MSI_REQUIRE(L.p.E_l >= 1 && L.p.E_l <= MSI_MAX_LOCAL_EXPERTS, "grouped_gemm: E_l out of range");
   MSI_REQUIRE(L.p.kdim % BK == 0 && L.p.n_total % BN == 0, "grouped_gemm: K %% 64 and N %% 256 required");
   const int cg = L.cta_group ? L.cta_group : default_cg();
+  if (cg == 2 && L.p.E_l <= MSI_SMALL_LOCAL_EXPERTS && quad_enabled() && L.p.nt % 2 == 0 && !L.p.a_runs &&
+      !L.p.a_shards && L.p.ksplit <= 1 && !l2_hints() && half_pair_box64())
+    return launch_cg<2, MSI_SMALL_LOCAL_EXPERTS, true>(L, st);
   if (L.p.E_l > MSI_SMALL_LOCAL_EXPERTS)
     return cg == 1 ? launch_cg<1, MSI_MAX_LOCAL_EXPERTS>(L, st) : launch_cg<2, MSI_MAX_LOCAL_EXPERTS>(L, st);
   return cg == 1 ? launch_cg<1, MSI_SMALL_LOCAL_EXPERTS>(L, st) : launch_cg<2, MSI_SMALL_LOCAL_EXPERTS>(L, st);
@@ -1210,6 +1286,15 @@ int qkv_rope_append(const void* x, int64_t rows, int hidden, const void* wqkv, i
 }
 
 }  // namespace msi
+
+#if MSI_GEMM_PROF
+// read and reset the MMA-issuer wait profile (diagnostic builds only)
+extern "C" int msi_dbg_gemm_prof(unsigned long long* out) {
+  if (cudaMemcpyFromSymbol(out, msi::g_gemm_prof, sizeof(msi::g_gemm_prof)) != cudaSuccess) return -1;
+  const unsigned long long z[4] = {0, 0, 0, 0};
+  return cudaMemcpyToSymbol(msi::g_gemm_prof, z, sizeof(z)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 extern "C" int msi_grouped_ffn_regions(const void* x_reg, const uint64_t* cntab, int n_src, int64_t cap_s, int E_l,
                                        const void* w13, const void* w2, void* hbuf, int64_t hbuf_rows, void* y_reg,
