@@ -57,6 +57,9 @@ __device__ unsigned long long g_gemm_prof[4];
 
 constexpr int BM = 128, BN = 256, BK = 64;
 constexpr int EPI_WARP_BYTES = 32 * 256;  // 32 rows x 128 bf16
+#ifndef MSI_EPI_DIRECT  // 1 = CTA-pair epilogue stores rows from registers (no smem staging: one more operand stage)
+#define MSI_EPI_DIRECT 0
+#endif
 constexpr int kThreads = 256;
 constexpr int TMEM_COLS = 512;
 constexpr int TRING = 4;  // tile ids in flight between the scheduler and the roles
@@ -71,12 +74,14 @@ constexpr int TRING = 4;  // tile ids in flight between the scheduler and the ro
 // to the larger table.
 template <int CG, int MAXE>
 struct Cfg {
-  static constexpr int STAGES = (CG == 1 ? 4 : 6) - (MAXE > MSI_SMALL_LOCAL_EXPERTS ? 1 : 0);
+  static constexpr bool DIRECT = MSI_EPI_DIRECT && CG == 2;
+  static constexpr int STAGES = (CG == 1 ? 4 : 6) - (MAXE > MSI_SMALL_LOCAL_EXPERTS ? 1 : 0) + (DIRECT ? 1 : 0);
+  static constexpr int EPI_BYTES = DIRECT ? 0 : 4 * EPI_WARP_BYTES;
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_ROWS = BN / CG;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr size_t SMEM = 1024 /*align*/ + (size_t)STAGES * STAGE_BYTES + 4 * EPI_WARP_BYTES + 256;
+  static constexpr size_t SMEM = 1024 /*align*/ + (size_t)STAGES * STAGE_BYTES + EPI_BYTES + 256;
 };
 
 template <int MAXE>
@@ -213,7 +218,7 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;                                  // STAGES x (A | B) per stage
   uint8_t* sEpi = smem + STAGES * C::STAGE_BYTES;      // 4 x 8 KB epilogue staging
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + 4 * EPI_WARP_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + C::EPI_BYTES);
   uint64_t* full = bars;                     // [STAGES] (CG=2: the leader's is used)
   uint64_t* empty = bars + STAGES;           // [STAGES]
   uint64_t* tfull = bars + 2 * STAGES;       // [2]
@@ -629,7 +634,16 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
       // or one 128-byte segment (mode 0 half)
       const int segs = (p.mode != 0 && !hp) ? 2 : 1;
       const bool narrow = (p.mode == 0 && hp);
+      char* segdst_l = nullptr;  // DIRECT: this lane's row segment
       auto stage = [&](int cc, const uint32_t (&pk)[16]) {  // 32 bf16 of the lane's row -> swizzled staging
+        if constexpr (C::DIRECT) {  // or straight to the row's destination (64 B per lane)
+          if (segdst_l && lane < valid_rows) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              st_v4(segdst_l + (cc * 4 + j) * 16, make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]));
+          }
+          return;
+        }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int u = cc * 4 + j;
@@ -659,6 +673,7 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
             segdst = rowdst + sgi * 256;
           }
         }
+        segdst_l = segdst;
         const __nv_bfloat16* rsrc = (p.mode == 1 && p.resid && rowdst)
             ? p.resid + (size_t)row_global * p.resid_ld + (size_t)n * BN + colofs + sgi * 128 : nullptr;
         if (valid_rows > 0) {
@@ -761,7 +776,7 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
           }
         }
         __syncwarp();
-        if (p.mode == 4) continue;  // fp32 rows were stored from registers
+        if (p.mode == 4 || C::DIRECT) continue;  // rows already stored from registers
         if (!narrow) {
           // ---- coalesced row stores: 2 rows per instruction, 256 B per row ----
           const int u = lane & 15;
