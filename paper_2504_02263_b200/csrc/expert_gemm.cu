@@ -487,6 +487,9 @@ grouped_gemm_kernel(const __grid_constant__ AMaps am, const __grid_constant__ CU
             }
           }
         }
+        // weights stream from HBM once per N tile: pull the tile p.pfb k-blocks
+        // ahead into L2 so the stage's load meets an L2 hit
+        if (p.pfb && lane == 0 && kb + p.pfb < kblocks) tma_prefetch_l2_2d(&tmB, (kb0 + kb + p.pfb) * BK, rowB);
         if (multi) {
           __syncwarp();  // the stage is free (lane 0 waited for it)
           for (int i = lane; i < npieces; i += 32) {
@@ -1051,6 +1054,10 @@ int launch_cg(const GemmLaunch& L, cudaStream_t st) {
   GemmParams prm = L.p;
   prm.a64 = half_pair_box64();
   prm.l2hint = l2_hints();
+  {
+    const char* v = getenv("MSI_GEMM_PFB");
+    prm.pfb = v ? atoi(v) : 0;
+  }
   MSI_CUDA(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<CG, MAXE, QD>, am, tb, prm));
   return check_launch("grouped_gemm_kernel");
 }

@@ -48,6 +48,7 @@ struct GemmParams {
   int a64;
   // TMA loads with L2 eviction priorities (set by the launcher)
   int l2hint;
+  int pfb;  // > 0: L2 prefetch of the B (weight) tile this many k-blocks ahead (MSI_GEMM_PFB)
   // receive regions (msi_expert_ffn): counts per (sender, expert) from cntab;
   // virtual row v of expert e lives in region (e, s) of cap_s rows at offset
   // v - pre[e][s].  a_runs = 1: GEMM1 loads A by runs of those regions; the
