@@ -454,8 +454,15 @@ cudaError_t launch_combine_kr(const CombineSrc& src, const float* w, const void*
                               const uint32_t* epoch_src, uint64_t timeout_ns, int32_t* status,
                               unsigned long long* trace, cudaStream_t st) {
   const size_t n = (size_t)T * H / 8;
+  // 6 resident CTAs per SM (the 40-register occupancy limit): 36.2 vs 39.5 us
+  // at 4 for the N = 1 bench step (profiles/r02_ab_combine.txt); MSI_COMBINE_CTAS
+  static const int mult = [] {
+    const char* v = getenv("MSI_COMBINE_CTAS");
+    const int m = v ? atoi(v) : 6;
+    return m >= 1 && m <= 8 ? m : 6;
+  }();
   int grid = (int)((n + 255) / 256);
-  grid = grid < 1 ? 1 : (grid > 4 * num_sms() ? 4 * num_sms() : grid);
+  grid = grid < 1 ? 1 : (grid > mult * num_sms() ? mult * num_sms() : grid);
   return launch_k(combine_kernel<KR>, dim3(grid), dim3(256), 0, st, src, w, reinterpret_cast<const uint16_t*>(resid),
                   reinterpret_cast<uint16_t*>(out), reinterpret_cast<uint4*>(gather), T, K, H, wait_ctr, epoch, mul,
                   epoch_src, timeout_ns, status, trace);
