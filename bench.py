@@ -25,6 +25,15 @@ import sys
 import threading
 import time
 
+# --impl reference under torchrun (N > 1): torchrun pins OMP_NUM_THREADS=1 in
+# every rank, which would leave rank 0's CPU arm on one core.  Give it the
+# host threads before numpy / OpenBLAS / the OpenMP oracle read the variable.
+_argv = " ".join(sys.argv[1:])
+if os.environ.get("WORLD_SIZE", "1") != "1" and ("--impl reference" in _argv or "--impl=reference" in _argv):
+    _n = str(len(os.sched_getaffinity(0)))
+    for _k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[_k] = _n
+
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))

@@ -102,3 +102,28 @@ def test_plan_json_with_attention_tp_reaches_the_bench(tmp_path):
     args = argparse.Namespace(plan_json=str(out), shape="dbrx", m=3, b_a=1024, tp_a=1)
     n_a, n_e, colo, src, tp_e = bench.apply_plan_json(args)
     assert (n_a, n_e, colo, tp_e, args.tp_a, args.m, args.b_a) == (2, 2, False, 1, 2, 2, 512)
+
+
+def test_reference_arm_under_torchrun_uses_the_host_threads():
+    """torchrun sets OMP_NUM_THREADS=1 in every rank; the reference arm's
+    rank 0 must still run the CPU oracle on all host threads (else the N > 1
+    reference runs are ~30x slower than the N = 1 one), and the other ranks
+    exit 0 without work."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    probe = ("import os, sys; sys.argv = ['bench.py'] + sys.argv[1:]; "
+             "exec(open('bench.py').read().split('import numpy as np')[0]); print(os.environ['OMP_NUM_THREADS'])")
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", OMP_NUM_THREADS="1")
+    out = subprocess.run([sys.executable, "-c", probe, "--impl", "reference", "--gpus", "2"], env=env, cwd=root,
+                         capture_output=True, text=True, check=True).stdout.strip()
+    assert out == str(len(os.sched_getaffinity(0)))
+    out = subprocess.run([sys.executable, "-c", probe, "--gpus", "2"], env=env, cwd=root,
+                         capture_output=True, text=True, check=True).stdout.strip()
+    assert out == "1"  # the GPU arm is left alone
+    env["RANK"] = "1"
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "2"], env=env, cwd=root,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and not r.stdout.strip()
