@@ -674,9 +674,12 @@ def run_reference(args):
 
 # --------------------------------------------------------------- GPU leg ----
 def disaggregated_layout(args, world: int, expert_share: float):
-    """Best disaggregated split of `world` GPUs for the ping-pong line:
-    n_e = round(world * T_e / (T_a + T_e)) in [1, world - 1] (the balance
-    condition T_a ~ T_e of PAPER.md:296 with the measured per-token costs),
+    """Best disaggregated split of `world` GPUs for the ping-pong line: with
+    s = T_e / (T_a + T_e) the expert share of the measured per-token GPU time,
+    n_a attention and n_e expert GPUs sustain min(n_a / (1 - s), n_e / s)
+    tokens per unit time (the slower stage bounds the pipeline, PAPER.md:296);
+    n_e in [1, world - 1] maximises it (rounding world * s instead picks 1+3
+    over 2+2 at s = 0.63, measured 1.39 M vs 1.59 M layer-tokens/s),
     m = --micro-batches separate micro-batches of --b-a tokens per attention
     GPU.  When n_e does not divide E the experts are spread over slots
     (balance.spread_slots: whole experts plus replicas of the remainder on
@@ -685,11 +688,13 @@ def disaggregated_layout(args, world: int, expert_share: float):
     from paper_2504_02263_b200.config import as_model_spec
 
     model = as_model_spec(args.shape)
-    n_e = int(min(max(round(world * expert_share), 1), world - 1))
+    s = min(max(expert_share, 1e-6), 1 - 1e-6)
+    n_e = max(range(1, world), key=lambda n: (min((world - n) / (1 - s), n / s), -n)) if world > 1 else 1
     n_a = world - n_e
     slots = spread_slots(model.experts, n_e) if model.experts % n_e else None
-    src = (f"disaggregated {n_a}+{n_e}: n_e = round({world} x T_e/(T_a+T_e) = {expert_share:.3f}) from the "
-           "co-located headline's stage times" + (f"; {slots.P} expert slots (spread_slots)" if slots else ""))
+    src = (f"disaggregated {n_a}+{n_e}: n_e maximises min(n_a/(1-s), n_e/s), s = T_e/(T_a+T_e) = "
+           f"{expert_share:.3f} from the co-located headline's stage times"
+           + (f"; {slots.P} expert slots (spread_slots)" if slots else ""))
     return (n_a, n_e, False, src, 1, model, args.m, args.b_a), slots
 
 

@@ -70,7 +70,9 @@ def test_disaggregated_layout_for_the_pingpong_line():
     assert slots is not None and slots.n_e == 5 and slots.P % 5 == 0  # 8 experts over 5 GPUs
     assert "3+5" in src
     (n_a, n_e, *_), slots = bench.disaggregated_layout(args, 4, 0.65)
-    assert (n_a, n_e) == (1, 3) and slots.P == 12
+    assert (n_a, n_e) == (2, 2) and slots is None  # min(2/0.35, 2/0.65) > min(1/0.35, 3/0.65)
+    (n_a, n_e, *_), slots = bench.disaggregated_layout(args, 4, 0.70)
+    assert (n_a, n_e) == (1, 3) and slots.P == 12  # 1+3 wins from s = 2/3
     (n_a, n_e, *_), slots = bench.disaggregated_layout(args, 2, 0.65)
     assert (n_a, n_e) == (1, 1) and slots is None
     (n_a, n_e, *_), slots = bench.disaggregated_layout(args, 8, 0.99)  # at least one attention GPU
